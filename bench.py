@@ -1,0 +1,331 @@
+#!/usr/bin/env python
+"""BFM benchmark: grid-point-iterations/s (float64) on BASELINE.json's C3
+(4096^2, configs[2]) — the headline size the metric is quoted on — or C4
+(384^3) with --config c4.
+
+A "step" is one steady-state back-and-forth iteration (the reference's
+run() loop body: probe + step(), solver.hpp:211-226, i.e. 4 c-transforms, 2
+ascent directions, 4 pair values, 2 axpys). Inputs are seeded synthetic
+densities of the BASELINE shapes (paper_1905_12154_b200/synthetic.py).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c3|c4]
+  python bench.py --impl reference ...   (the reference's own CPU solver,
+        oracle/_ref = unmodified headers + FFTW shim, on the host cores)
+
+Prints ONE JSON line (rank 0)."""
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = "BFM grid-point-iterations/sec (float64) at 4096² and 384³; c-transform HBM GB/s"
+UNIT = "grid-point-iterations/s"
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def workload(cfg):
+    from paper_1905_12154_b200 import synthetic
+
+    if cfg == "c3":
+        mu, nu = synthetic.c3()
+        desc = {"workload": "C3: 2D 4096x4096 quadratic BFM, masked Gaussian mixtures (BASELINE configs[2])",
+                "grid": [4096, 4096]}
+    elif cfg == "c4":
+        mu, nu = synthetic.c4()
+        desc = {"workload": "C4: 3D 384^3 quadratic BFM, Gaussian mixture -> ball (BASELINE configs[3])",
+                "grid": [384, 384, 384]}
+    elif cfg == "c1":
+        mu, nu = synthetic.c1()
+        desc = {"workload": "C1: 2D 256x256 quadratic BFM (BASELINE configs[0])", "grid": [256, 256]}
+    elif cfg == "c2":
+        mu, nu = synthetic.c2()
+        desc = {"workload": "C2: 2D 1024x1024 quadratic BFM (BASELINE configs[1])", "grid": [1024, 1024]}
+    else:
+        raise SystemExit(f"unknown config {cfg}")
+    return mu, nu, desc
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    def __init__(self, index=0):
+        self.samples = []
+        self.index = index
+        self._stop = threading.Event()
+        self._t = None
+
+    def start(self):
+        def run():
+            q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+                 "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_power_cap")
+            while not self._stop.is_set():
+                try:
+                    out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits"],
+                                         capture_output=True, text=True, timeout=5).stdout.strip()
+                    if out:
+                        self.samples.append([x.strip() for x in out.split(",")])
+                except Exception:
+                    pass
+                self._stop.wait(0.2)
+
+        self._t = threading.Thread(target=run, daemon=True)
+        self._t.start()
+
+    def stop(self):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=10)
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4)
+                          if len(s) > i + 2 and s[i + 2].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def reference_arm(args):
+    """--impl reference: the reference's own CPU BFM (oracle/_ref) on the host."""
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import oracle_lib as O
+    from paper_1905_12154_b200 import SolverConfig
+
+    if O.ref_lib() is None:
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libbfmref.so not built"}))
+        return
+    mu, nu, desc = workload(args.config)
+    N = mu.size
+    s = O.RefSolver(mu, nu, SolverConfig(tolerance=-1.0, max_iterations=10 ** 6))
+    s.dual_value()  # first probe (setup)
+    budget = 240.0
+    warm = 0
+    t_start = time.perf_counter()
+    for _ in range(args.warmup):
+        s.step()
+        s.dual_value()
+        warm += 1
+        if time.perf_counter() - t_start > budget / 3:
+            break
+    done = 0
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        s.step()
+        s.dual_value()  # trailing probe = next iteration's run() loop head
+        done += 1
+        if time.perf_counter() - t0 > budget:
+            break
+    dt = time.perf_counter() - t0
+    v = N * done / dt
+    cores = os.cpu_count()
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world,
+        "steps": done, "warmup": warm, "ms_per_step": 1e3 * dt / max(1, done),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded, BASELINE shapes)",
+        "config": dict(desc, parallelism="cpu threads", solver="reference bfm::Solver (oracle/_ref)"),
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "reference",
+                         "sample": f"{done} full BFM iterations (probe+step) of {desc['workload']} on "
+                                   f"{cores} host threads; Poisson via the FFTW-subset shim"},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+
+
+def cpu_baseline(mu, nu, desc):
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    try:
+        import oracle_lib as O
+        from paper_1905_12154_b200 import SolverConfig
+
+        if O.ref_lib() is None:
+            return None
+        s = O.RefSolver(mu, nu, SolverConfig(tolerance=-1.0, max_iterations=10 ** 6))
+        s.dual_value()
+        t0 = time.perf_counter()
+        s.step()
+        s.dual_value()
+        dt = time.perf_counter() - t0
+        cores = os.cpu_count()
+        return {"value": mu.size / dt, "unit": UNIT, "cores": cores, "kind": "reference",
+                "sample": f"1 full BFM iteration (probe+step) of {desc['workload']} with the reference "
+                          f"bfm::Solver (oracle/_ref, FFTW-subset shim) on {cores} host threads, "
+                          f"{dt:.1f} s"}
+    except Exception as e:  # the baseline is reported, never fatal
+        return {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "reference",
+                "sample": f"failed: {e}"}
+
+
+def ctransform_roofline(lib, shape, torch, hbm, hbm_kind, reps=10):
+    """Times the c-transform operator (d kernel launches, one per axis pass)
+    on resident data with CUDA events on its launch stream; L2 flushed
+    between launches. Algorithmic bytes: 16*d per node."""
+    import ctypes as C
+
+    from paper_1905_12154_b200 import synthetic
+
+    d = len(shape)
+    N = int(np.prod(shape))
+    phi = torch.from_numpy(synthetic.c5_potential(tuple(shape))[0]).cuda()
+    out = torch.empty_like(phi)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+    ws = C.c_void_p()
+    ext = (C.c_int * d)(*shape)
+    assert lib.bfm_workspace_create(d, ext, C.byref(ws)) == 0
+    stream = torch.cuda.current_stream()
+    sp = C.c_void_p(stream.cuda_stream)
+    for _ in range(3):
+        assert lib.bfm_ctransform_device(ws, C.c_void_p(phi.data_ptr()), C.c_void_p(out.data_ptr()), sp) == 0
+    launches = lib.bfm_workspace_last_launches(ws)
+    tot = 0.0
+    for _ in range(reps):
+        flush.fill_(1.0)
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        lib.bfm_ctransform_device(ws, C.c_void_p(phi.data_ptr()), C.c_void_p(out.data_ptr()), sp)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        tot += e0.elapsed_time(e1)
+    lib.bfm_workspace_destroy(ws)
+    ms = tot / reps
+    bytes_alg = 16.0 * d * N
+    achieved = bytes_alg / (ms * 1e-3) / 1e9
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "ctransform_dram_bytes.json")
+    if os.path.exists(prof):
+        try:
+            traffic = json.load(open(prof)).get("x".join(map(str, shape)))
+        except Exception:
+            traffic = None
+    return {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+            "frac": achieved / hbm, "traffic": traffic,
+            "kernel": f"c-transform operator ({launches} axis-pass launches) on {'x'.join(map(str, shape))}",
+            "ms_per_launch_group": ms, "algorithmic_bytes": bytes_alg, "peak_kind": hbm_kind}
+
+
+def ours(args):
+    rank, world, local = dist_env()
+    import torch
+
+    import paper_1905_12154_b200 as bfm
+
+    torch.cuda.set_device(local)
+    bfm.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    mu, nu, desc = workload(args.config)
+    N = mu.size
+    cfg = bfm.SolverConfig(tolerance=-1.0, max_iterations=10 ** 6)
+    s = bfm.Solver(mu, nu, cfg)
+    for _ in range(args.warmup):
+        s.step()
+    l0 = s.launches()
+    clocks = ClockSampler(local)
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    ms = s.time_steps(args.steps)
+    torch.cuda.synchronize()
+    ck = clocks.stop()
+    launches = s.launches() - l0
+    t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    if dist:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.barrier()
+    ms_max = float(t.item())
+    value = N * args.steps * world / (ms_max * 1e-3)
+    del s
+
+    # end to end through the public API with host buffers
+    pin_mu = torch.from_numpy(mu).pin_memory().numpy()
+    pin_nu = torch.from_numpy(nu).pin_memory().numpy()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    s2 = bfm.Solver(pin_mu, pin_nu, cfg)
+    for _ in range(args.steps):
+        s2.step()
+    phi_h = s2.phi()
+    psi_h = s2.psi()
+    e2e_s = time.perf_counter() - t0
+    del s2, phi_h, psi_h
+    e2e = {"value": N * args.steps / e2e_s, "unit": UNIT,
+           "h2d_bytes_per_step": int(2 * 8 * N / args.steps),
+           "d2h_bytes_per_step": int(2 * 8 * N / args.steps),
+           "note": "bfm.Solver(mu, nu) from pinned host arrays + K step() + phi()/psi() readback, wall clock"}
+
+    if rank != 0:
+        if dist:
+            dist.destroy_process_group()
+        return
+    hbm, hbm_kind = peaks()
+    lib = bfm.load_library()
+    roof = ctransform_roofline(lib, desc["grid"], torch, hbm, hbm_kind)
+    cpu = cpu_baseline(mu, nu, desc) if world == 1 and not args.no_cpu_baseline else None
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded, BASELINE shapes; no public dataset)",
+        "config": dict(desc, parallelism=("replicas" if world > 1 else "single GPU"),
+                       l2="inputs larger than L2 (about 10 resident float64 fields of 128 MiB)"),
+        "gpu_launches": int(launches),
+        "clocks": ck,
+        "roofline": roof,
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+    }
+    print(json.dumps(line))
+    if dist:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c3", choices=["c1", "c2", "c3", "c4"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        reference_arm(args)
+    else:
+        ours(args)
+
+
+if __name__ == "__main__":
+    main()

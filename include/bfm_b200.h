@@ -1,0 +1,185 @@
+/*
+ * bfm_b200.h — C ABI of the B200-native back-and-forth (BFM) optimal-transport
+ * solver (quadratic cost, float64, cell-centred grids on [0,1]^d, d = 1..3).
+ *
+ * This is the drop-in boundary for the reference's header-only C++ solver API
+ * (/root/reference/proj/include/bfm/<name>.hpp). Every entry point below names the
+ * reference interface it replaces. Plain pointers and sizes only; fields are
+ * row-major float64 with the last axis fastest (grid.hpp:73-75). Host-pointer
+ * entry points copy in/out; *_device entry points take device pointers and a
+ * cudaStream_t passed as void*.
+ *
+ * Errors: every int-returning call returns BFM_OK (0) or a status that maps 1:1
+ * onto the reference exception types (errors.hpp:8-42); bfm_last_error() gives
+ * the message (thread-local). There is no CPU fallback: without a usable CUDA
+ * device every compute call fails with BFM_ERR_CUDA.
+ */
+#ifndef BFM_B200_H
+#define BFM_B200_H
+
+#include <stddef.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Status codes (errors.hpp:8-42). */
+enum {
+  BFM_OK = 0,
+  BFM_ERR_ERROR = 1,            /* bfm::Error */
+  BFM_ERR_INVALID_ARGUMENT = 2, /* bfm::InvalidArgument */
+  BFM_ERR_GRID_MISMATCH = 3,    /* bfm::GridMismatch */
+  BFM_ERR_NEGATIVE_INPUT = 4,   /* bfm::NegativeInput */
+  BFM_ERR_ALL_ZERO_INPUT = 5,   /* bfm::AllZeroInput */
+  BFM_ERR_INFEASIBLE_INPUT = 6, /* bfm::InfeasibleInput */
+  BFM_ERR_NUMERICAL_BLOWUP = 7, /* bfm::NumericalBlowup */
+  BFM_ERR_T_OUT_OF_RANGE = 8,   /* bfm::TOutOfRange */
+  BFM_ERR_IO = 9,               /* bfm::IoError */
+  BFM_ERR_CUDA = 10             /* device failure (surfaces as bfm::Error) */
+};
+
+/* solver.hpp:32 SolverMode */
+enum { BFM_MODE_BACK_AND_FORTH = 0, BFM_MODE_GRADIENT_ASCENT = 1 };
+/* solver.hpp:34 Termination */
+enum {
+  BFM_TERM_TOLERANCE_MET = 0,
+  BFM_TERM_MAX_ITERATIONS = 1,
+  BFM_TERM_DUAL_STALLED = 2,
+  BFM_TERM_COST_TARGET_MET = 3
+};
+/* pushforward.hpp:22 MapSource */
+enum { BFM_MAP_MU_SIDE = 0, BFM_MAP_NU_SIDE = 1 };
+/* Field selectors for bfm_solver_field / bfm_solver_report_field. */
+enum {
+  BFM_FIELD_PHI = 0,
+  BFM_FIELD_PSI = 1,
+  BFM_FIELD_MAP0 = 2, /* displacement along axis 0 (report only) */
+  BFM_FIELD_MAP1 = 3,
+  BFM_FIELD_MAP2 = 4
+};
+
+/* solver.hpp:46-63 SolverConfig. has_exact_cost stands in for std::optional. */
+typedef struct bfm_config {
+  int mode;
+  double tolerance;
+  int max_iterations;
+  int threads; /* accepted for API parity; the device ignores it */
+  double sigma_init;
+  double sigma_min;
+  double beta_1;
+  double beta_2;
+  double alpha_1;
+  double alpha_2;
+  int has_exact_cost;
+  double exact_cost;
+  double exact_tolerance;
+} bfm_config;
+
+/* solver.hpp:78-88 IterationStats */
+typedef struct bfm_iteration_stats {
+  int iteration;
+  double residual;
+  double dual_value;
+  double sigma_first;
+  double sigma_second;
+  double grad_norm_sq_first;
+  double grad_norm_sq_second;
+  double increase_first;
+  double increase_second;
+} bfm_iteration_stats;
+
+/* solver.hpp:90-101 SolveReport (scalars; fields via bfm_solver_report_field,
+ * trace via bfm_solver_trace). */
+typedef struct bfm_report {
+  int termination;
+  int iterations;
+  double dual_value;
+  double primal_cost;
+  double residual;
+  double wall_seconds;
+} bfm_report;
+
+typedef struct bfm_solver bfm_solver;
+
+/* Fills the reference defaults (solver.hpp:46-63). */
+void bfm_config_default(bfm_config* cfg);
+
+/* solver.hpp:68-76 update_sigma. cfg may be NULL (defaults). */
+double bfm_update_sigma(double sigma, double increase, double grad_norm_sq,
+                        const bfm_config* cfg);
+
+/* solver.hpp:148-167 Solver::Solver — validates exactly as
+ * checked_solver_inputs (:132-142) and copies mu, nu (host pointers, N each). */
+int bfm_solver_create(int dim, const int* extents, const double* mu, const double* nu,
+                      const bfm_config* cfg, bfm_solver** out);
+void bfm_solver_destroy(bfm_solver* s);
+
+int bfm_solver_iteration(const bfm_solver* s);                 /* :169 */
+double bfm_solver_sigma(const bfm_solver* s);                  /* :170 */
+int bfm_solver_dual_value(bfm_solver* s, double* out);         /* :178-181 */
+int bfm_solver_residual(bfm_solver* s, double* out);           /* :183-186 */
+int bfm_solver_step(bfm_solver* s, bfm_iteration_stats* out);  /* :189-207 */
+int bfm_solver_run(bfm_solver* s, bfm_report* out);            /* :211-226, finish :330-349 */
+/* Copies up to cap trace entries (:173); *count receives the trace length. */
+int bfm_solver_trace(const bfm_solver* s, bfm_iteration_stats* out, int cap, int* count);
+/* Current iterate phi()/psi() (:171-172) into host memory (N doubles). */
+int bfm_solver_field(bfm_solver* s, int which, double* host_out);
+/* Gauge-fixed report fields of the last run() (:337-344): PHI, PSI, MAP0..2. */
+int bfm_solver_report_field(bfm_solver* s, int which, double* host_out);
+
+/* ---- Operators (host pointers) ------------------------------------------ */
+/* transforms.hpp:396-432 ctransform (quadratic cost, exactly rounded). */
+int bfm_ctransform(int dim, const int* extents, const double* phi, double* out);
+/* pushforward.hpp:70-91 map_from_conjugate: disp is d*N (SoA, axis-major). */
+int bfm_map_from_conjugate(int dim, const int* extents, const double* u, int side,
+                           double* disp);
+/* pushforward.hpp:176-178 pushforward_density (disp d*N, mu N -> rho N). */
+int bfm_pushforward_density(int dim, const int* extents, const double* disp,
+                            const double* mu, double* rho);
+/* interpolation.hpp:18-22 displacement_interpolant: splat at x + t*disp. */
+int bfm_displacement_interpolant(int dim, const int* extents, const double* disp,
+                                 const double* mu, double t, double* rho);
+/* poisson.hpp:87-106 SpectralPlan::solve_neumann. */
+int bfm_solve_neumann(int dim, const int* extents, const double* rhs, double* out);
+/* grid.hpp:171-183 integrate(f, w) (w == NULL: Lebesgue). */
+int bfm_integrate(int dim, const int* extents, const double* f, const double* w,
+                  double* out);
+/* pushforward.hpp:181-196 primal_cost. */
+int bfm_primal_cost(int dim, const int* extents, const double* disp, const double* mu,
+                    double* out);
+
+/* ---- Operators on device memory (C5 sweep, benches) ---------------------- */
+typedef struct bfm_workspace bfm_workspace;
+int bfm_workspace_create(int dim, const int* extents, bfm_workspace** out);
+void bfm_workspace_destroy(bfm_workspace* ws);
+int bfm_ctransform_device(bfm_workspace* ws, const double* d_phi, double* d_out,
+                          void* stream);
+/* Fused map_from_conjugate + pushforward_density + residual (solver.hpp:249-253):
+ * d_r = d_target - T#d_source with T from d_u (side selects mu/nu semantics). */
+int bfm_pushforward_residual_device(bfm_workspace* ws, const double* d_u,
+                                    const double* d_source, const double* d_target,
+                                    double* d_r, void* stream);
+int bfm_solve_neumann_device(bfm_workspace* ws, const double* d_rhs, double* d_out,
+                             void* stream);
+/* Number of device kernels the last *_device call on ws enqueued. */
+int bfm_workspace_last_launches(const bfm_workspace* ws);
+
+/* Total device kernels the solver has enqueued so far (launch evidence). */
+long bfm_solver_launches(const bfm_solver* s);
+
+/* Bench helper: runs k step()s (plus the trailing probe each step() of the
+ * reference also pays, solver.hpp:213) between two CUDA events recorded on the
+ * solver's stream; *ms receives the device-timed duration. */
+int bfm_solver_time_steps(bfm_solver* s, int k, double* ms);
+
+const char* bfm_last_error(void);
+/* Selects the CUDA device for subsequent calls on this thread (one process
+ * per GPU: pass LOCAL_RANK). */
+int bfm_set_device(int device);
+/* 1 if a CUDA device is usable, else 0 (never throws). */
+int bfm_device_available(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BFM_B200_H */

@@ -1,0 +1,671 @@
+// Host-side BFM iterate and the C ABI (include/bfm_b200.h).
+//
+// bfm_solver mirrors the reference's bfm::Solver (solver.hpp:146-368): same
+// validation (checked on the host on the caller's arrays, exactly as
+// solver.hpp:105-142), same probe/step split, stopping-rule order, step-size
+// rule, dual-monotonicity checks and gauge fix. All field work runs on the
+// device through CtPlan / PushforwardPlan / PoissonPlan / Reducer; only
+// scalars cross to the host (one synchronising read per half step).
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <limits>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "../../include/bfm_b200.h"
+#include "common.cuh"
+#include "ctransform.cuh"
+#include "poisson.cuh"
+#include "pushforward.cuh"
+#include "reduce.cuh"
+
+namespace {
+
+using namespace bfmgpu;
+
+thread_local std::string g_err;
+
+struct BfmError {
+  int code;
+  std::string msg;
+};
+
+[[noreturn]] void fail(int code, const std::string& msg) { throw BfmError{code, msg}; }
+
+template <class F>
+int guard(F&& f) {
+  try {
+    f();
+    return BFM_OK;
+  } catch (const BfmError& e) {
+    g_err = e.msg;
+    return e.code;
+  } catch (const CudaError& e) {
+    g_err = e.what();
+    return BFM_ERR_CUDA;
+  } catch (const std::invalid_argument& e) {
+    g_err = e.what();
+    return BFM_ERR_INVALID_ARGUMENT;
+  } catch (const std::bad_alloc& e) {
+    g_err = "out of memory";
+    return BFM_ERR_ERROR;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return BFM_ERR_ERROR;
+  }
+}
+
+// grid.hpp:60-76 validation.
+GridDesc checked_grid(int dim, const int* ext) {
+  if (dim < 1 || dim > 3) fail(BFM_ERR_INVALID_ARGUMENT, "grid dimension must be 1, 2, or 3");
+  for (int a = 0; a < dim; ++a)
+    if (ext[a] < 2) fail(BFM_ERR_INVALID_ARGUMENT, "grid extent must be at least 2");
+  return make_grid(dim, ext);
+}
+
+void require_device() {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) {
+    cudaGetLastError();
+    fail(BFM_ERR_CUDA, "no CUDA device available (the B200 path has no CPU fallback)");
+  }
+}
+
+// grid.hpp:124-133 Kahan accumulator (host-side validation only).
+struct Kahan {
+  double sum = 0.0, carry = 0.0;
+  void add(double v) {
+    const double y = v - carry;
+    const double t = sum + y;
+    carry = (t - sum) - y;
+    sum = t;
+  }
+};
+
+// solver.hpp:105-116
+void check_density(const char* name, const double* f, const GridDesc& g) {
+  for (long i = 0; i < g.size; ++i) {
+    const double v = f[i];
+    if (!std::isfinite(v))
+      fail(BFM_ERR_INFEASIBLE_INPUT, std::string(name) + ": density has a non-finite sample");
+    if (v < 0.0) fail(BFM_ERR_NEGATIVE_INPUT, std::string(name) + ": density has a negative sample");
+  }
+  Kahan k;
+  for (long i = 0; i < g.size; ++i) k.add(f[i]);
+  const double mass = k.sum * g.vol;
+  if (std::abs(mass - 1.0) > 1e-6)
+    fail(BFM_ERR_INFEASIBLE_INPUT, std::string(name) + ": density mass " + std::to_string(mass) +
+                                       " is not 1; normalize inputs first");
+}
+
+// solver.hpp:118-128
+void check_config(const bfm_config& c) {
+  if (c.max_iterations < 0) fail(BFM_ERR_INVALID_ARGUMENT, "solve: max_iterations is negative");
+  if (c.threads < 0) fail(BFM_ERR_INVALID_ARGUMENT, "solve: threads is negative");
+  if (c.sigma_init < 0.0) fail(BFM_ERR_INVALID_ARGUMENT, "solve: sigma_init is negative");
+  if (c.sigma_min <= 0.0) fail(BFM_ERR_INVALID_ARGUMENT, "solve: sigma_min must be positive");
+  if (!(c.beta_1 > 0.0) || !(c.beta_1 < c.beta_2) || !(c.beta_2 < 1.0))
+    fail(BFM_ERR_INVALID_ARGUMENT, "solve: need 0 < beta_1 < beta_2 < 1");
+  if (!(c.alpha_2 < 1.0) || !(c.alpha_2 > 0.0) || !(c.alpha_1 > 1.0))
+    fail(BFM_ERR_INVALID_ARGUMENT, "solve: need 0 < alpha_2 < 1 < alpha_1");
+  if (c.exact_tolerance < 0.0) fail(BFM_ERR_INVALID_ARGUMENT, "solve: exact_tolerance is negative");
+}
+
+void default_config(bfm_config* c) {
+  c->mode = BFM_MODE_BACK_AND_FORTH;
+  c->tolerance = 1e-4;
+  c->max_iterations = 2000;
+  c->threads = 0;
+  c->sigma_init = 0.0;
+  c->sigma_min = 0.01;
+  c->beta_1 = 0.25;
+  c->beta_2 = 0.75;
+  c->alpha_1 = 1.25;
+  c->alpha_2 = 0.8;
+  c->has_exact_cost = 0;
+  c->exact_cost = 0.0;
+  c->exact_tolerance = 0.0;
+}
+
+double update_sigma(double sigma, double increase, double gn, const bfm_config& c) {
+  const double predicted = sigma * gn;  // solver.hpp:68-76
+  if (increase < c.beta_1 * predicted) sigma *= c.alpha_2;
+  else if (increase > c.beta_2 * predicted) sigma *= c.alpha_1;
+  return std::max(sigma, c.sigma_min);
+}
+
+struct DevBuf {
+  double* p = nullptr;
+  DevBuf() = default;
+  explicit DevBuf(long n) { BFM_CUDA(cudaMalloc(&p, n * sizeof(double))); }
+  ~DevBuf() {
+    if (p) cudaFree(p);
+  }
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  void alloc(long n) {
+    if (!p) BFM_CUDA(cudaMalloc(&p, n * sizeof(double)));
+  }
+};
+
+enum { kSlotPair = 0, kSlotGn = 1, kSlotShift = 2, kSlotPrimal = 3 };
+
+}  // namespace
+
+struct bfm_workspace {
+  GridDesc g;
+  std::unique_ptr<CtPlan> ct;
+  std::unique_ptr<PoissonPlan> pois;
+  std::unique_ptr<PushforwardPlan> pf;
+  std::unique_ptr<Reducer> red;
+  LaunchCounter lc;
+  int last_launches = 0;
+  CtPlan& ctp() {
+    if (!ct) {
+      ct.reset(new CtPlan);
+      ct->init(g);
+    }
+    return *ct;
+  }
+  PoissonPlan& poisp() {
+    if (!pois) {
+      pois.reset(new PoissonPlan);
+      pois->init(g);
+    }
+    return *pois;
+  }
+  PushforwardPlan& pfp() {
+    if (!pf) {
+      pf.reset(new PushforwardPlan);
+      pf->init(g);
+    }
+    return *pf;
+  }
+  Reducer& redp() {
+    if (!red) {
+      red.reset(new Reducer);
+      red->init();
+    }
+    return *red;
+  }
+};
+
+struct bfm_solver {
+  GridDesc g;
+  bfm_config cfg;
+  cudaStream_t stream = nullptr;
+  bfm_workspace ws;
+  DevBuf mu, nu, phi, psi, dir, dir2, r;
+  DevBuf rep_phi, rep_psi, rep_map;
+  double sigma = 0.0;
+  double last_pair = 0.0;
+  double prev_dual = std::numeric_limits<double>::quiet_NaN();
+  double probe_dual = 0.0, probe_gn = 0.0;
+  bool fresh = false;
+  int iteration = 0, stall = 0;
+  bool has_report = false;
+  std::vector<bfm_iteration_stats> trace;
+  std::chrono::steady_clock::time_point start;
+
+  ~bfm_solver() {
+    if (stream) cudaStreamDestroy(stream);
+  }
+
+  double fetch1(int slot) {
+    double v[4];
+    ws.redp().fetch(v, slot + 1, stream);
+    return v[slot];
+  }
+
+  void pair_value_async() {  // solver.hpp:240
+    ws.redp().dot(phi.p, nu.p, psi.p, mu.p, g.size, g.vol, kSlotPair, stream, &ws.lc);
+  }
+  void ctransform(const double* in, double* out) { ws.ctp().run(in, out, stream, &ws.lc); }
+
+  // solver.hpp:245-260 (result left in d_dir, gn in kSlotGn)
+  void ascent_direction_async(const double* u, const double* source, const double* target,
+                              double* d_dir) {
+    ws.pfp().from_potential(u, source, target, r.p, nullptr, stream, &ws.lc);
+    ws.poisp().solve(r.p, d_dir, stream, &ws.lc);
+    ws.redp().dot(r.p, d_dir, nullptr, nullptr, g.size, g.vol, kSlotGn, stream, &ws.lc);
+  }
+
+  void ensure_probe() {  // solver.hpp:264-280
+    if (fresh) return;
+    if (cfg.mode == BFM_MODE_BACK_AND_FORTH) {
+      ctransform(phi.p, psi.p);
+      pair_value_async();
+      const double v = fetch1(kSlotPair);
+      if (v < last_pair - 1e-10)
+        fail(BFM_ERR_NUMERICAL_BLOWUP, "solve: conjugation decreased the dual pair value");
+      last_pair = v;
+      probe_dual = v;
+    } else {
+      probe_dual = last_pair;
+    }
+    ascent_direction_async(psi.p, mu.p, nu.p, dir.p);
+    probe_gn = fetch1(kSlotGn);
+    fresh = true;
+  }
+
+  void step_back_and_forth(bfm_iteration_stats& st) {  // solver.hpp:286-310
+    const double v2 = probe_dual;
+    st.sigma_first = sigma;
+    st.grad_norm_sq_first = probe_gn;
+    axpy(phi.p, sigma, dir.p, g.size, stream, &ws.lc);
+    ctransform(phi.p, psi.p);
+    pair_value_async();
+    const double v3 = fetch1(kSlotPair);
+    st.increase_first = v3 - v2;
+    sigma = update_sigma(sigma, st.increase_first, probe_gn, cfg);
+
+    ctransform(psi.p, phi.p);
+    pair_value_async();
+    const double v4 = fetch1(kSlotPair);
+    if (v4 < v3 - 1e-10)
+      fail(BFM_ERR_NUMERICAL_BLOWUP, "solve: conjugation decreased the dual pair value");
+    ascent_direction_async(phi.p, nu.p, mu.p, dir2.p);
+    const double gn2 = fetch1(kSlotGn);
+    st.sigma_second = sigma;
+    st.grad_norm_sq_second = gn2;
+    axpy(psi.p, sigma, dir2.p, g.size, stream, &ws.lc);
+    ctransform(psi.p, phi.p);
+    pair_value_async();
+    const double v5 = fetch1(kSlotPair);
+    st.increase_second = v5 - v4;
+    sigma = update_sigma(sigma, st.increase_second, gn2, cfg);
+    st.dual_value = v5;
+    last_pair = v5;
+  }
+
+  void step_gradient_ascent(bfm_iteration_stats& st) {  // solver.hpp:312-328
+    const double v1 = probe_dual;
+    st.sigma_first = sigma;
+    st.grad_norm_sq_first = probe_gn;
+    axpy(phi.p, sigma, dir.p, g.size, stream, &ws.lc);
+    ctransform(phi.p, psi.p);
+    pair_value_async();
+    const double v2 = fetch1(kSlotPair);
+    st.increase_first = v2 - v1;
+    sigma = update_sigma(sigma, st.increase_first, probe_gn, cfg);
+    ctransform(psi.p, phi.p);
+    pair_value_async();
+    const double v3 = fetch1(kSlotPair);
+    if (v3 < v2 - 1e-10)
+      fail(BFM_ERR_NUMERICAL_BLOWUP, "solve: conjugation decreased the dual pair value");
+    st.dual_value = v3;
+    last_pair = v3;
+  }
+
+  bfm_iteration_stats step() {  // solver.hpp:189-207
+    ensure_probe();
+    bfm_iteration_stats st;
+    std::memset(&st, 0, sizeof(st));
+    st.iteration = iteration + 1;
+    st.residual = std::sqrt(std::max(probe_gn, 0.0));
+    if (cfg.mode == BFM_MODE_BACK_AND_FORTH) step_back_and_forth(st);
+    else step_gradient_ascent(st);
+    fresh = false;
+    ++iteration;
+    if (std::abs(st.dual_value - prev_dual) < 1e-12) ++stall;
+    else stall = 0;
+    prev_dual = st.dual_value;
+    trace.push_back(st);
+    return st;
+  }
+
+  void finish(int term, double residual, bfm_report* rep) {  // solver.hpp:330-349
+    rep->termination = term;
+    rep->iterations = iteration;
+    rep->dual_value = probe_dual;
+    rep->residual = residual;
+    rep_phi.alloc(g.size);
+    rep_psi.alloc(g.size);
+    rep_map.alloc(g.d * g.size);
+    BFM_CUDA(cudaMemcpyAsync(rep_phi.p, phi.p, g.size * sizeof(double), cudaMemcpyDeviceToDevice, stream));
+    BFM_CUDA(cudaMemcpyAsync(rep_psi.p, psi.p, g.size * sizeof(double), cudaMemcpyDeviceToDevice, stream));
+    ws.redp().sum(rep_phi.p, g.size, g.vol, kSlotShift, stream, &ws.lc);
+    const double shift = fetch1(kSlotShift);
+    add_scalar(rep_phi.p, -shift, g.size, stream, &ws.lc);
+    add_scalar(rep_psi.p, shift, g.size, stream, &ws.lc);
+    ws.pfp().map_only(rep_psi.p, rep_map.p, stream, &ws.lc);
+    ws.redp().primal(rep_map.p, mu.p, g.d, g.size, g.vol, kSlotPrimal, stream, &ws.lc);
+    rep->primal_cost = fetch1(kSlotPrimal);
+    rep->wall_seconds =
+        std::chrono::duration<double>(std::chrono::steady_clock::now() - start).count();
+    has_report = true;
+  }
+
+  void run(bfm_report* rep) {  // solver.hpp:211-226
+    while (true) {
+      ensure_probe();
+      const double residual = std::sqrt(std::max(probe_gn, 0.0));
+      if (cfg.tolerance >= 0.0 && residual <= cfg.tolerance)
+        return finish(BFM_TERM_TOLERANCE_MET, residual, rep);
+      if (cfg.has_exact_cost && cfg.exact_tolerance > 0.0 &&
+          std::abs(probe_dual - cfg.exact_cost) <= cfg.exact_tolerance)
+        return finish(BFM_TERM_COST_TARGET_MET, residual, rep);
+      if (iteration >= cfg.max_iterations) return finish(BFM_TERM_MAX_ITERATIONS, residual, rep);
+      if (stall >= 10) return finish(BFM_TERM_DUAL_STALLED, residual, rep);
+      step();
+    }
+  }
+};
+
+namespace {
+
+struct HostOp {
+  GridDesc g;
+  bfm_workspace ws;
+  cudaStream_t s = nullptr;
+  HostOp(int dim, const int* ext) {
+    g = checked_grid(dim, ext);
+    require_device();
+    ws.g = g;
+  }
+  ~HostOp() { release(); }
+  double* up(const double* h, long n) {
+    double* d = nullptr;
+    BFM_CUDA(cudaMalloc(&d, n * sizeof(double)));
+    keep.push_back(d);
+    if (h) BFM_CUDA(cudaMemcpy(d, h, n * sizeof(double), cudaMemcpyHostToDevice));
+    return d;
+  }
+  void down(double* h, const double* d, long n) {
+    BFM_CUDA(cudaDeviceSynchronize());
+    BFM_CUDA(cudaMemcpy(h, d, n * sizeof(double), cudaMemcpyDeviceToHost));
+  }
+  std::vector<double*> keep;
+  void release() {
+    for (double* p : keep) cudaFree(p);
+    keep.clear();
+  }
+};
+
+}  // namespace
+
+extern "C" {
+
+const char* bfm_last_error(void) { return g_err.c_str(); }
+
+int bfm_set_device(int device) {
+  return guard([&] { BFM_CUDA(cudaSetDevice(device)); });
+}
+
+int bfm_device_available(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n > 0 ? 1 : 0;
+}
+
+void bfm_config_default(bfm_config* cfg) { default_config(cfg); }
+
+double bfm_update_sigma(double sigma, double increase, double gn, const bfm_config* cfg) {
+  bfm_config d;
+  default_config(&d);
+  return update_sigma(sigma, increase, gn, cfg ? *cfg : d);
+}
+
+int bfm_solver_create(int dim, const int* extents, const double* mu, const double* nu,
+                      const bfm_config* cfg, bfm_solver** out) {
+  return guard([&] {
+    *out = nullptr;
+    bfm_config c;
+    default_config(&c);
+    if (cfg) c = *cfg;
+    const GridDesc g = checked_grid(dim, extents);
+    check_config(c);
+    check_density("mu", mu, g);
+    check_density("nu", nu, g);
+    require_device();
+    std::unique_ptr<bfm_solver> s(new bfm_solver);
+    s->start = std::chrono::steady_clock::now();
+    s->g = g;
+    s->cfg = c;
+    s->ws.g = g;
+    BFM_CUDA(cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking));
+    const long N = g.size;
+    for (DevBuf* b : {&s->mu, &s->nu, &s->phi, &s->psi, &s->dir, &s->dir2, &s->r}) b->alloc(N);
+    BFM_CUDA(cudaMemcpyAsync(s->mu.p, mu, N * sizeof(double), cudaMemcpyHostToDevice, s->stream));
+    BFM_CUDA(cudaMemcpyAsync(s->nu.p, nu, N * sizeof(double), cudaMemcpyHostToDevice, s->stream));
+    BFM_CUDA(cudaMemsetAsync(s->phi.p, 0, N * sizeof(double), s->stream));
+    BFM_CUDA(cudaMemsetAsync(s->psi.p, 0, N * sizeof(double), s->stream));
+    double sup = 0.0;  // solver.hpp:160-163
+    for (long i = 0; i < N; ++i) sup = std::max(sup, mu[i]);
+    for (long i = 0; i < N; ++i) sup = std::max(sup, nu[i]);
+    s->sigma = c.sigma_init > 0.0 ? c.sigma_init : 8.0 / sup;
+    s->last_pair = 0.0;
+    s->ws.ctp();
+    s->ws.poisp();
+    s->ws.pfp();
+    s->ws.redp();
+    BFM_CUDA(cudaStreamSynchronize(s->stream));
+    *out = s.release();
+  });
+}
+
+void bfm_solver_destroy(bfm_solver* s) { delete s; }
+int bfm_solver_iteration(const bfm_solver* s) { return s->iteration; }
+double bfm_solver_sigma(const bfm_solver* s) { return s->sigma; }
+
+int bfm_solver_dual_value(bfm_solver* s, double* out) {
+  return guard([&] {
+    s->ensure_probe();
+    *out = s->probe_dual;
+  });
+}
+
+int bfm_solver_residual(bfm_solver* s, double* out) {
+  return guard([&] {
+    s->ensure_probe();
+    *out = std::sqrt(std::max(s->probe_gn, 0.0));
+  });
+}
+
+int bfm_solver_step(bfm_solver* s, bfm_iteration_stats* out) {
+  return guard([&] {
+    const bfm_iteration_stats st = s->step();
+    if (out) *out = st;
+  });
+}
+
+int bfm_solver_run(bfm_solver* s, bfm_report* out) {
+  return guard([&] {
+    bfm_report r;
+    std::memset(&r, 0, sizeof(r));
+    s->run(&r);
+    if (out) *out = r;
+  });
+}
+
+int bfm_solver_trace(const bfm_solver* s, bfm_iteration_stats* out, int cap, int* count) {
+  *count = static_cast<int>(s->trace.size());
+  for (int i = 0; i < cap && i < *count; ++i) out[i] = s->trace[i];
+  return BFM_OK;
+}
+
+int bfm_solver_field(bfm_solver* s, int which, double* host_out) {
+  return guard([&] {
+    const double* src = which == BFM_FIELD_PHI ? s->phi.p : which == BFM_FIELD_PSI ? s->psi.p : nullptr;
+    if (!src) fail(BFM_ERR_INVALID_ARGUMENT, "bfm_solver_field: PHI or PSI only");
+    BFM_CUDA(cudaStreamSynchronize(s->stream));
+    BFM_CUDA(cudaMemcpy(host_out, src, s->g.size * sizeof(double), cudaMemcpyDeviceToHost));
+  });
+}
+
+int bfm_solver_report_field(bfm_solver* s, int which, double* host_out) {
+  return guard([&] {
+    if (!s->has_report) fail(BFM_ERR_ERROR, "no report: call bfm_solver_run first");
+    const double* src = nullptr;
+    if (which == BFM_FIELD_PHI) src = s->rep_phi.p;
+    else if (which == BFM_FIELD_PSI) src = s->rep_psi.p;
+    else if (which >= BFM_FIELD_MAP0 && which - BFM_FIELD_MAP0 < s->g.d)
+      src = s->rep_map.p + (which - BFM_FIELD_MAP0) * s->g.size;
+    else fail(BFM_ERR_INVALID_ARGUMENT, "bfm_solver_report_field: bad field");
+    BFM_CUDA(cudaStreamSynchronize(s->stream));
+    BFM_CUDA(cudaMemcpy(host_out, src, s->g.size * sizeof(double), cudaMemcpyDeviceToHost));
+  });
+}
+
+int bfm_ctransform(int dim, const int* extents, const double* phi, double* out) {
+  return guard([&] {
+    HostOp op(dim, extents);
+    double* a = op.up(phi, op.g.size);
+    double* b = op.up(nullptr, op.g.size);
+    op.ws.ctp().run(a, b, nullptr, &op.ws.lc);
+    op.down(out, b, op.g.size);
+    op.release();
+  });
+}
+
+int bfm_map_from_conjugate(int dim, const int* extents, const double* u, int /*side*/,
+                           double* disp) {
+  return guard([&] {
+    HostOp op(dim, extents);
+    double* a = op.up(u, op.g.size);
+    double* m = op.up(nullptr, op.g.d * op.g.size);
+    op.ws.pfp().map_only(a, m, nullptr, &op.ws.lc);
+    op.down(disp, m, op.g.d * op.g.size);
+    op.release();
+  });
+}
+
+int bfm_pushforward_density(int dim, const int* extents, const double* disp, const double* mu,
+                            double* rho) {
+  return guard([&] {
+    HostOp op(dim, extents);
+    double* m = op.up(disp, op.g.d * op.g.size);
+    double* a = op.up(mu, op.g.size);
+    double* b = op.up(nullptr, op.g.size);
+    op.ws.pfp().from_displacement(m, 1.0, a, b, nullptr, &op.ws.lc);
+    op.down(rho, b, op.g.size);
+    op.release();
+  });
+}
+
+int bfm_displacement_interpolant(int dim, const int* extents, const double* disp,
+                                 const double* mu, double t, double* rho) {
+  return guard([&] {
+    if (!(t >= 0.0 && t <= 1.0))  // interpolation.hpp:20-21
+      fail(BFM_ERR_T_OUT_OF_RANGE, "displacement_interpolant: t must lie in [0, 1]");
+    HostOp op(dim, extents);
+    double* m = op.up(disp, op.g.d * op.g.size);
+    double* a = op.up(mu, op.g.size);
+    double* b = op.up(nullptr, op.g.size);
+    op.ws.pfp().from_displacement(m, t, a, b, nullptr, &op.ws.lc);
+    op.down(rho, b, op.g.size);
+    op.release();
+  });
+}
+
+int bfm_solve_neumann(int dim, const int* extents, const double* rhs, double* out) {
+  return guard([&] {
+    HostOp op(dim, extents);
+    double* a = op.up(rhs, op.g.size);
+    double* b = op.up(nullptr, op.g.size);
+    op.ws.poisp().solve(a, b, nullptr, &op.ws.lc);
+    op.down(out, b, op.g.size);
+    op.release();
+  });
+}
+
+int bfm_integrate(int dim, const int* extents, const double* f, const double* w, double* out) {
+  return guard([&] {
+    HostOp op(dim, extents);
+    double* a = op.up(f, op.g.size);
+    if (w) {
+      double* b = op.up(w, op.g.size);
+      op.ws.redp().dot(a, b, nullptr, nullptr, op.g.size, op.g.vol, 0, nullptr, &op.ws.lc);
+    } else {
+      op.ws.redp().sum(a, op.g.size, op.g.vol, 0, nullptr, &op.ws.lc);
+    }
+    double v[1];
+    op.ws.redp().fetch(v, 1, nullptr);
+    *out = v[0];
+    op.release();
+  });
+}
+
+int bfm_primal_cost(int dim, const int* extents, const double* disp, const double* mu,
+                    double* out) {
+  return guard([&] {
+    HostOp op(dim, extents);
+    double* m = op.up(disp, op.g.d * op.g.size);
+    double* a = op.up(mu, op.g.size);
+    op.ws.redp().primal(m, a, op.g.d, op.g.size, op.g.vol, 0, nullptr, &op.ws.lc);
+    double v[1];
+    op.ws.redp().fetch(v, 1, nullptr);
+    *out = v[0];
+    op.release();
+  });
+}
+
+int bfm_workspace_create(int dim, const int* extents, bfm_workspace** out) {
+  return guard([&] {
+    *out = nullptr;
+    const GridDesc g = checked_grid(dim, extents);
+    require_device();
+    std::unique_ptr<bfm_workspace> w(new bfm_workspace);
+    w->g = g;
+    *out = w.release();
+  });
+}
+
+void bfm_workspace_destroy(bfm_workspace* ws) { delete ws; }
+
+int bfm_ctransform_device(bfm_workspace* ws, const double* d_phi, double* d_out, void* stream) {
+  return guard([&] {
+    const long before = ws->lc.count;
+    ws->ctp().run(d_phi, d_out, static_cast<cudaStream_t>(stream), &ws->lc);
+    ws->last_launches = static_cast<int>(ws->lc.count - before);
+  });
+}
+
+int bfm_pushforward_residual_device(bfm_workspace* ws, const double* d_u, const double* d_source,
+                                    const double* d_target, double* d_r, void* stream) {
+  return guard([&] {
+    const long before = ws->lc.count;
+    ws->pfp().from_potential(d_u, d_source, d_target, d_r, nullptr,
+                             static_cast<cudaStream_t>(stream), &ws->lc);
+    ws->last_launches = static_cast<int>(ws->lc.count - before);
+  });
+}
+
+int bfm_solve_neumann_device(bfm_workspace* ws, const double* d_rhs, double* d_out, void* stream) {
+  return guard([&] {
+    const long before = ws->lc.count;
+    ws->poisp().solve(d_rhs, d_out, static_cast<cudaStream_t>(stream), &ws->lc);
+    ws->last_launches = static_cast<int>(ws->lc.count - before);
+  });
+}
+
+int bfm_workspace_last_launches(const bfm_workspace* ws) { return ws->last_launches; }
+
+long bfm_solver_launches(const bfm_solver* s) { return s->ws.lc.count; }
+
+int bfm_solver_time_steps(bfm_solver* s, int k, double* ms) {
+  return guard([&] {
+    s->ensure_probe();
+    cudaEvent_t e0, e1;
+    BFM_CUDA(cudaEventCreate(&e0));
+    BFM_CUDA(cudaEventCreate(&e1));
+    BFM_CUDA(cudaStreamSynchronize(s->stream));
+    BFM_CUDA(cudaEventRecord(e0, s->stream));
+    for (int i = 0; i < k; ++i) s->step();
+    s->ensure_probe();  // the next iteration's probe belongs to this step's work
+    BFM_CUDA(cudaEventRecord(e1, s->stream));
+    BFM_CUDA(cudaEventSynchronize(e1));
+    float f = 0.0f;
+    BFM_CUDA(cudaEventElapsedTime(&f, e0, e1));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    *ms = f;
+  });
+}
+
+}  // extern "C"

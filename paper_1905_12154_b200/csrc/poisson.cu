@@ -1,0 +1,430 @@
+// Neumann Poisson solve on sm_100a: batched DCT-II (REDFT10) along axes
+// d-1..1, one fused kernel for [DCT-II axis 0 -> spectral divide -> DCT-III
+// axis 0], then DCT-III along axes 1..d-1 (reference poisson.hpp:87-106).
+// 2d-1 HBM passes of read+write per solve.
+//
+// Each CTA owns `lpc` grid lines (consecutive along the fastest other axis
+// for strided axes, so global loads/stores are coalesced), stages each line
+// in shared memory, and runs the shared line algorithm of dct_line.h with the
+// butterflies of a stage spread over the line's threads. Every value goes
+// through the same IEEE operations as the CPU shim (bitwise-equal results).
+#include <cstring>
+#include <vector>
+
+#include "poisson.cuh"
+
+namespace bfmgpu {
+namespace {
+
+using bfmdct::cplx;
+constexpr int kMaxItems = 9;
+
+enum { kFwd = 0, kInv = 1, kFused = 2 };
+
+struct PoisArgs {
+  PoisAxisCfg ax;
+  int mode;
+  int d;
+  int n1, n2;  // extents of axes 1, 2 (fused divide)
+  const double* in;
+  double* out;
+  const double* lam0;
+  const double* lam1;
+  const double* lam2;
+  double scale;
+};
+
+__device__ __forceinline__ void gsync(int tpl, int l) {
+  if (tpl <= 32) {
+    __syncwarp();
+  } else {
+    asm volatile("bar.sync %0, %1;" ::"r"(l + 1), "r"(tpl) : "memory");
+  }
+}
+
+__device__ __forceinline__ long line_base(const PoisAxisCfg& ax, long L) {
+  const long inner = L % ax.stride, outer = L / ax.stride;
+  return outer * static_cast<long>(ax.n) * ax.stride + inner;
+}
+
+// Spectral divide for axis-0 wavenumber k of the line with other wavenumbers
+// (k1, k2): poisson.hpp:93-103 (lam summed as (l0 + l1) + l2).
+__device__ __forceinline__ double divide(const PoisArgs& a, double v, int k, double l1v,
+                                         double l2v) {
+  const double l01 = a.lam0[k] + l1v;
+  const double lam = l01 + l2v;
+  return lam == 0.0 ? 0.0 : v / (lam * a.scale);
+}
+
+__global__ void __launch_bounds__(1024) pois_fft_kernel(PoisArgs a) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const PoisAxisCfg& ax = a.ax;
+  const bfmdct::LinePlan& P = ax.plan;
+  const int tpl = ax.tpl, lpc = ax.lpc, n = ax.n, m = P.m;
+  const int l = threadIdx.x / tpl;
+  const int t = threadIdx.x - l * tpl;
+  const long L0 = static_cast<long>(blockIdx.x) * lpc;
+
+  // ---- load (coalesced) ----
+  for (int idx = threadIdx.x; idx < n * lpc; idx += blockDim.x) {
+    int ll, j;
+    if (ax.strided) {
+      ll = idx % lpc;
+      j = idx / lpc;
+    } else {
+      ll = idx / n;
+      j = idx - ll * n;
+    }
+    const long L = L0 + ll;
+    if (L >= ax.nlines) continue;
+    double* zd = reinterpret_cast<double*>(smem + static_cast<long>(ll) * ax.line_bytes);
+    const double v = a.in[line_base(ax, L) + static_cast<long>(j) * ax.stride];
+    if (a.mode == kInv) zd[j] = v;
+    else zd[bfmdct::dct2_vpos(P, j)] = v;
+  }
+  __syncthreads();
+
+  const long L = L0 + l;
+  const bool active = L < ax.nlines;
+  double* zd = reinterpret_cast<double*>(smem + static_cast<long>(l) * ax.line_bytes);
+  cplx* z = reinterpret_cast<cplx*>(zd);
+
+  double l1v = 0.0, l2v = 0.0;
+  if (a.mode == kFused && active) {
+    const long inner = line_base(ax, L);  // axis-0 lines: base == inner offset
+    if (a.d == 2) {
+      l1v = a.lam1[inner];
+    } else if (a.d == 3) {
+      l1v = a.lam1[inner / a.n2];
+      l2v = a.lam2[inner % a.n2];
+    }
+  }
+
+  cplx reg[kMaxItems];
+  cplx reg2[kMaxItems];
+
+  // ---- inverse pre-step: Z_k from V_k, V_{m-k} ----
+  if (a.mode == kInv) {
+#pragma unroll
+    for (int r = 0; r < kMaxItems; ++r) {
+      const int k = t + r * tpl;
+      if (active && k < m) {
+        const cplx A = bfmdct::dct3_V_vals(P, zd[k], k == 0 ? 0.0 : zd[n - k], k);
+        const int km = m - k;
+        const cplx B = bfmdct::dct3_V_vals(P, zd[km], zd[n - km], km);
+        reg[r] = bfmdct::dct3_pre_vals(P, A, B, k);
+      }
+    }
+    gsync(tpl, l);
+#pragma unroll
+    for (int r = 0; r < kMaxItems; ++r) {
+      const int k = t + r * tpl;
+      if (active && k < m) z[k] = reg[r];
+    }
+    gsync(tpl, l);
+  }
+
+  // ---- FFT stages (forward for DCT-II) ----
+  const bool inv_first = a.mode == kInv;
+  for (int s = 0; s < P.nstages; ++s) {
+    const int nb = m / P.radix[s];
+    if (active)
+      for (int b = t; b < nb; b += tpl) bfmdct::fft_butterfly(P, s, b, z, inv_first);
+    gsync(tpl, l);
+  }
+
+  if (a.mode == kFwd) {
+    // unpack k in [0, m] -> y_k, y_{n-k}
+#pragma unroll
+    for (int r = 0; r < kMaxItems; ++r) {
+      const int k = t + r * tpl;
+      if (active && k <= m) {
+        double yk, ynk;
+        bfmdct::dct2_unpack_vals(P, z[P.rev[k == m ? 0 : k]], z[P.rev[k == 0 ? 0 : m - k]], k,
+                                 yk, ynk);
+        reg[r] = cplx{yk, ynk};
+      }
+    }
+    gsync(tpl, l);
+#pragma unroll
+    for (int r = 0; r < kMaxItems; ++r) {
+      const int k = t + r * tpl;
+      if (active && k <= m) {
+        zd[k] = reg[r].re;
+        if (k > 0 && k < m) zd[n - k] = reg[r].im;
+      }
+    }
+  } else {
+    if (a.mode == kFused) {
+      // items k in [0, m/2]: unpack k and m-k, divide, pre-step Z_k, Z_{m-k}
+      const int half = m / 2;
+#pragma unroll
+      for (int r = 0; r < kMaxItems; ++r) {
+        const int k = t + r * tpl;
+        if (active && k <= half) {
+          const int km = m - k;
+          double yk, ynk, ykm, ynkm;
+          bfmdct::dct2_unpack_vals(P, z[P.rev[k == m ? 0 : k]], z[P.rev[k == 0 ? 0 : m - k]], k,
+                                   yk, ynk);
+          bfmdct::dct2_unpack_vals(P, z[P.rev[km == m ? 0 : km]],
+                                   z[P.rev[km == 0 ? 0 : m - km]], km, ykm, ynkm);
+          // values at wavenumbers: k, n-k (0<k<m), km, n-km (0<km<m)
+          const double xk = divide(a, yk, k, l1v, l2v);
+          const double xnk = (k > 0 && k < m) ? divide(a, ynk, n - k, l1v, l2v) : 0.0;
+          const double xkm = divide(a, ykm, km, l1v, l2v);
+          const double xnkm = (km > 0 && km < m) ? divide(a, ynkm, n - km, l1v, l2v) : 0.0;
+          // x_{n-j} for j = k is xnk (j=0 -> 0); for j = km: x_{n-km} = xnkm, but
+          // when km == m, n - km == m so x_{n-m} = x_m = xkm.
+          const double b_k = k == 0 ? 0.0 : xnk;
+          const double b_km = km == m ? xkm : xnkm;
+          const cplx Vk = bfmdct::dct3_V_vals(P, xk, b_k, k);
+          const cplx Vkm = bfmdct::dct3_V_vals(P, xkm, b_km, km);
+          reg[r] = bfmdct::dct3_pre_vals(P, Vk, Vkm, k);
+          if (km < m && km != k) reg2[r] = bfmdct::dct3_pre_vals(P, Vkm, Vk, km);
+        }
+      }
+      gsync(tpl, l);
+#pragma unroll
+      for (int r = 0; r < kMaxItems; ++r) {
+        const int k = t + r * tpl;
+        if (active && k <= half) {
+          const int km = m - k;
+          z[k] = reg[r];
+          if (km < m && km != k) z[km] = reg2[r];
+        }
+      }
+      gsync(tpl, l);
+      for (int s = 0; s < P.nstages; ++s) {
+        const int nb = m / P.radix[s];
+        if (active)
+          for (int b = t; b < nb; b += tpl) bfmdct::fft_butterfly(P, s, b, z, true);
+        gsync(tpl, l);
+      }
+    }
+    // post: y positions of v_{2q}, v_{2q+1}
+#pragma unroll
+    for (int r = 0; r < kMaxItems; ++r) {
+      const int q = t + r * tpl;
+      if (active && q < m) reg[r] = z[P.rev[q]];
+    }
+    gsync(tpl, l);
+#pragma unroll
+    for (int r = 0; r < kMaxItems; ++r) {
+      const int q = t + r * tpl;
+      if (active && q < m) {
+        zd[bfmdct::dct3_ypos(P, 2 * q)] = reg[r].re;
+        zd[bfmdct::dct3_ypos(P, 2 * q + 1)] = reg[r].im;
+      }
+    }
+  }
+  __syncthreads();
+
+  // ---- store (coalesced) ----
+  for (int idx = threadIdx.x; idx < n * lpc; idx += blockDim.x) {
+    int ll, j;
+    if (ax.strided) {
+      ll = idx % lpc;
+      j = idx / lpc;
+    } else {
+      ll = idx / n;
+      j = idx - ll * n;
+    }
+    const long LL = L0 + ll;
+    if (LL >= ax.nlines) continue;
+    const double* zl = reinterpret_cast<const double*>(smem + static_cast<long>(ll) * ax.line_bytes);
+    a.out[line_base(ax, LL) + static_cast<long>(j) * ax.stride] = zl[j];
+  }
+}
+
+// Direct O(n^2) form for extents that are not 2 * 2^a 3^b.
+__global__ void __launch_bounds__(1024) pois_naive_kernel(PoisArgs a) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const PoisAxisCfg& ax = a.ax;
+  const bfmdct::LinePlan& P = ax.plan;
+  const int tpl = ax.tpl, lpc = ax.lpc, n = ax.n;
+  const int l = threadIdx.x / tpl;
+  const int t = threadIdx.x - l * tpl;
+  const long L0 = static_cast<long>(blockIdx.x) * lpc;
+  for (int idx = threadIdx.x; idx < n * lpc; idx += blockDim.x) {
+    int ll, j;
+    if (ax.strided) {
+      ll = idx % lpc;
+      j = idx / lpc;
+    } else {
+      ll = idx / n;
+      j = idx - ll * n;
+    }
+    const long L = L0 + ll;
+    if (L >= ax.nlines) continue;
+    double* xa = reinterpret_cast<double*>(smem + static_cast<long>(ll) * ax.line_bytes);
+    xa[j] = a.in[line_base(ax, L) + static_cast<long>(j) * ax.stride];
+  }
+  __syncthreads();
+  const long L = L0 + l;
+  const bool active = L < ax.nlines;
+  double* xa = reinterpret_cast<double*>(smem + static_cast<long>(l) * ax.line_bytes);
+  double* yb = xa + n;
+  double l1v = 0.0, l2v = 0.0;
+  if (a.mode == kFused && active) {
+    const long inner = line_base(ax, L);
+    if (a.d == 2) {
+      l1v = a.lam1[inner];
+    } else if (a.d == 3) {
+      l1v = a.lam1[inner / a.n2];
+      l2v = a.lam2[inner % a.n2];
+    }
+  }
+  if (active) {
+    for (int k = t; k < n; k += tpl) {
+      double v = a.mode == kInv ? bfmdct::dct3_naive(P, xa, 1, k) : bfmdct::dct2_naive(P, xa, 1, k);
+      if (a.mode == kFused) v = divide(a, v, k, l1v, l2v);
+      yb[k] = v;
+    }
+  }
+  gsync(tpl, l);
+  if (a.mode == kFused && active) {
+    for (int k = t; k < n; k += tpl) xa[k] = bfmdct::dct3_naive(P, yb, 1, k);
+  }
+  __syncthreads();
+  for (int idx = threadIdx.x; idx < n * lpc; idx += blockDim.x) {
+    int ll, j;
+    if (ax.strided) {
+      ll = idx % lpc;
+      j = idx / lpc;
+    } else {
+      ll = idx / n;
+      j = idx - ll * n;
+    }
+    const long LL = L0 + ll;
+    if (LL >= ax.nlines) continue;
+    const double* xl = reinterpret_cast<const double*>(smem + static_cast<long>(ll) * ax.line_bytes);
+    const double* src = a.mode == kFused ? xl : xl + n;
+    a.out[line_base(ax, LL) + static_cast<long>(j) * ax.stride] = src[j];
+  }
+}
+
+template <class T>
+T* upload(const std::vector<T>& v, std::vector<void*>& keep) {
+  if (v.empty()) return nullptr;
+  T* d = nullptr;
+  BFM_CUDA(cudaMalloc(&d, v.size() * sizeof(T)));
+  BFM_CUDA(cudaMemcpy(d, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice));
+  keep.push_back(d);
+  return d;
+}
+
+std::vector<void*>& allocations(void* key) {
+  static thread_local std::vector<std::pair<void*, std::vector<void*>>> reg;
+  for (auto& e : reg)
+    if (e.first == key) return e.second;
+  reg.push_back({key, {}});
+  return reg.back().second;
+}
+
+}  // namespace
+
+PoissonPlan::~PoissonPlan() {
+  for (int a = 0; a < 3; ++a) {
+    if (tables_[a]) {
+      auto* v = static_cast<std::vector<void*>*>(tables_[a]);
+      for (void* p : *v) cudaFree(p);
+      delete v;
+    }
+    if (lam_[a]) cudaFree(lam_[a]);
+  }
+  if (tmp_) cudaFree(tmp_);
+}
+
+void PoissonPlan::init(const GridDesc& g) {
+  constexpr double kPi = 3.14159265358979323846;
+  g_ = g;
+  int dev = 0;
+  BFM_CUDA(cudaGetDevice(&dev));
+  int max_optin = 0;
+  BFM_CUDA(cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+  const int budget = max_optin - 1024;
+  scale_ = 1.0;
+  for (int a = 0; a < g.d; ++a) {
+    const int n = g.n[a];
+    scale_ *= 2.0 * n;
+    host_[a].reset(new bfmdct::HostLinePlan);
+    host_[a]->build(n);
+    const bfmdct::HostLinePlan& H = *host_[a];
+    auto* keep = new std::vector<void*>;
+    tables_[a] = keep;
+    PoisAxisCfg& c = cfg_[a];
+    c.plan = H.plan;
+    c.plan.wm = upload(H.wm, *keep);
+    c.plan.rev = upload(H.rev, *keep);
+    c.plan.cs = upload(H.cs, *keep);
+    c.plan.wn = upload(H.wn, *keep);
+    c.plan.cosmat = upload(H.cosmat, *keep);
+    c.n = n;
+    c.stride = g.stride[a];
+    c.nlines = g.size / n;
+    c.strided = a != g.d - 1;
+    if (H.plan.kind == bfmdct::kFft) {
+      const int m = H.plan.m;
+      int tpl = (m + 7) / 8;
+      tpl = ((tpl + 31) / 32) * 32;
+      if (tpl < 32) tpl = 32;
+      if (tpl > 1024) throw std::invalid_argument("solve_neumann: extent too large");
+      c.tpl = tpl;
+      c.line_bytes = ((8 * n) + 15) & ~15;
+    } else {
+      c.tpl = n >= 256 ? 256 : 32 * ((n + 31) / 32);
+      c.line_bytes = ((16 * n) + 15) & ~15;
+    }
+    if (c.line_bytes > budget) throw std::invalid_argument("solve_neumann: line exceeds shared memory");
+    int lpc = std::min(budget / c.line_bytes, 1024 / c.tpl);
+    lpc = std::min(lpc, c.strided ? 16 : 4);
+    if (c.tpl > 32) lpc = std::min(lpc, 15);
+    lpc = static_cast<int>(std::min<long>(lpc, c.nlines));
+    c.lpc = std::max(1, lpc);
+    std::vector<double> lam(n);
+    const double na = n;
+    for (int k = 0; k < n; ++k) lam[k] = (2.0 - 2.0 * std::cos(kPi * k / na)) * na * na;
+    BFM_CUDA(cudaMalloc(&lam_[a], n * sizeof(double)));
+    BFM_CUDA(cudaMemcpy(lam_[a], lam.data(), n * sizeof(double), cudaMemcpyHostToDevice));
+  }
+  BFM_CUDA(cudaFuncSetAttribute(pois_fft_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, budget));
+  BFM_CUDA(cudaFuncSetAttribute(pois_naive_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, budget));
+}
+
+void PoissonPlan::solve(const double* d_rhs, double* d_out, cudaStream_t stream,
+                        LaunchCounter* lc) {
+  const int d = g_.d;
+  auto launch = [&](int axis, int mode, const double* in, double* out) {
+    PoisArgs A;
+    std::memset(&A, 0, sizeof(A));
+    A.ax = cfg_[axis];
+    A.mode = mode;
+    A.d = d;
+    A.n1 = d > 1 ? g_.n[1] : 1;
+    A.n2 = d > 2 ? g_.n[2] : 1;
+    A.in = in;
+    A.out = out;
+    A.lam0 = lam_[0];
+    A.lam1 = d > 1 ? lam_[1] : nullptr;
+    A.lam2 = d > 2 ? lam_[2] : nullptr;
+    A.scale = scale_;
+    const PoisAxisCfg& c = cfg_[axis];
+    const long blocks = (c.nlines + c.lpc - 1) / c.lpc;
+    const size_t sm = static_cast<size_t>(c.lpc) * c.line_bytes;
+    if (c.plan.kind == bfmdct::kFft)
+      pois_fft_kernel<<<static_cast<unsigned>(blocks), c.lpc * c.tpl, sm, stream>>>(A);
+    else
+      pois_naive_kernel<<<static_cast<unsigned>(blocks), c.lpc * c.tpl, sm, stream>>>(A);
+    BFM_LAUNCH_CHECK("pois kernel");
+    if (lc) lc->add();
+  };
+  const double* cur = d_rhs;
+  for (int a = d - 1; a >= 1; --a) {
+    launch(a, kFwd, cur, d_out);
+    cur = d_out;
+  }
+  launch(0, kFused, cur, d_out);
+  for (int a = 1; a < d; ++a) launch(a, kInv, d_out, d_out);
+}
+
+}  // namespace bfmgpu

@@ -1,0 +1,253 @@
+// Deterministic two-stage double-double reductions + elementwise kernels.
+//
+// The reference sums sequentially with Kahan compensation (grid.hpp:124-133).
+// These reductions accumulate per thread in double-double (two_sum) and
+// combine partials in a fixed tree, so results are run-to-run bitwise
+// deterministic and within an ulp of the exact sum; they only feed scalar
+// decisions (sigma rule, stopping tests), never a field.
+#include <cmath>
+
+#include "exact.cuh"
+#include "reduce.cuh"
+
+namespace bfmgpu {
+namespace {
+
+constexpr int kRedThreads = 256;
+constexpr int kRedBlocks = 148 * 4;
+
+struct DD {
+  double s, c;
+};
+
+__device__ __forceinline__ void dd_add(DD& a, double x) {
+  double s, e;
+  bfmx::two_sum(a.s, x, s, e);
+  a.s = s;
+  a.c += e;
+}
+__device__ __forceinline__ DD dd_merge(DD a, DD b) {
+  double s, e;
+  bfmx::two_sum(a.s, b.s, s, e);
+  return DD{s, (a.c + b.c) + e};
+}
+
+__device__ DD block_reduce(DD v) {
+  __shared__ double ss[kRedThreads / 32], sc[kRedThreads / 32];
+  for (int o = 16; o > 0; o >>= 1) {
+    DD u{__shfl_down_sync(0xffffffffu, v.s, o), __shfl_down_sync(0xffffffffu, v.c, o)};
+    v = dd_merge(v, u);
+  }
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (lane == 0) {
+    ss[w] = v.s;
+    sc[w] = v.c;
+  }
+  __syncthreads();
+  DD r{0.0, 0.0};
+  if (threadIdx.x == 0)
+    for (int i = 0; i < kRedThreads / 32; ++i) r = dd_merge(r, DD{ss[i], sc[i]});
+  __syncthreads();
+  return r;
+}
+
+// mode 0: sum a*b ; 1: sum a ; 2: primal ; partial layout [pair][block][2]
+struct RedArgs {
+  const double* a1;
+  const double* b1;
+  const double* a2;
+  const double* b2;
+  long n;
+  int mode;
+  int d;
+  double* partials;
+};
+
+__global__ void __launch_bounds__(kRedThreads) red_partial_kernel(RedArgs A) {
+  DD acc1{0.0, 0.0}, acc2{0.0, 0.0};
+  for (long i = blockIdx.x * static_cast<long>(kRedThreads) + threadIdx.x; i < A.n;
+       i += static_cast<long>(gridDim.x) * kRedThreads) {
+    if (A.mode == 0) {
+      dd_add(acc1, A.a1[i] * A.b1[i]);
+      if (A.a2) dd_add(acc2, A.a2[i] * A.b2[i]);
+    } else if (A.mode == 1) {
+      dd_add(acc1, A.a1[i]);
+    } else {
+      const double m = A.b1[i];
+      if (m == 0.0) continue;
+      double c = 0.0;
+      for (int a = 0; a < A.d; ++a) {
+        const double dl = A.a1[a * A.n + i];
+        c += 0.5 * dl * dl;
+      }
+      dd_add(acc1, c * m);
+    }
+  }
+  DD r1 = block_reduce(acc1);
+  DD r2 = block_reduce(acc2);
+  if (threadIdx.x == 0) {
+    A.partials[2 * blockIdx.x] = r1.s;
+    A.partials[2 * blockIdx.x + 1] = r1.c;
+    A.partials[2 * (gridDim.x + blockIdx.x)] = r2.s;
+    A.partials[2 * (gridDim.x + blockIdx.x) + 1] = r2.c;
+  }
+}
+
+__global__ void __launch_bounds__(kRedThreads) red_final_kernel(const double* partials, int nb,
+                                                                int two, double vol,
+                                                                double* results, int slot) {
+  DD acc1{0.0, 0.0}, acc2{0.0, 0.0};
+  for (int i = threadIdx.x; i < nb; i += kRedThreads) {
+    acc1 = dd_merge(acc1, DD{partials[2 * i], partials[2 * i + 1]});
+    acc2 = dd_merge(acc2, DD{partials[2 * (nb + i)], partials[2 * (nb + i) + 1]});
+  }
+  DD r1 = block_reduce(acc1);
+  DD r2 = block_reduce(acc2);
+  if (threadIdx.x == 0) {
+    const double s1 = r1.s + r1.c;
+    double v = s1 * vol;
+    if (two) {
+      const double s2 = r2.s + r2.c;
+      v = v + s2 * vol;
+    }
+    results[slot] = v;
+  }
+}
+
+__global__ void __launch_bounds__(kRedThreads) density_scan_kernel(const double* a, long n,
+                                                                   double* partials) {
+  double mx = 0.0;
+  int bad = 0, neg = 0;
+  for (long i = blockIdx.x * static_cast<long>(kRedThreads) + threadIdx.x; i < n;
+       i += static_cast<long>(gridDim.x) * kRedThreads) {
+    const double v = a[i];
+    if (!isfinite(v)) bad = 1;
+    else if (v < 0.0) neg = 1;
+    else mx = fmax(mx, v);
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    mx = fmax(mx, __shfl_down_sync(0xffffffffu, mx, o));
+    bad |= __shfl_down_sync(0xffffffffu, bad, o);
+    neg |= __shfl_down_sync(0xffffffffu, neg, o);
+  }
+  __shared__ double smx[kRedThreads / 32];
+  __shared__ int sbad[kRedThreads / 32], sneg[kRedThreads / 32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (lane == 0) {
+    smx[w] = mx;
+    sbad[w] = bad;
+    sneg[w] = neg;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int i = 1; i < kRedThreads / 32; ++i) {
+      mx = fmax(mx, smx[i]);
+      bad |= sbad[i];
+      neg |= sneg[i];
+    }
+    partials[3 * blockIdx.x] = mx;
+    partials[3 * blockIdx.x + 1] = bad;
+    partials[3 * blockIdx.x + 2] = neg;
+  }
+}
+
+__global__ void density_final_kernel(const double* partials, int nb, double* results, int slot) {
+  if (threadIdx.x != 0) return;
+  double mx = 0.0, bad = 0.0, neg = 0.0;
+  for (int i = 0; i < nb; ++i) {
+    mx = fmax(mx, partials[3 * i]);
+    bad = fmax(bad, partials[3 * i + 1]);
+    neg = fmax(neg, partials[3 * i + 2]);
+  }
+  results[slot] = mx;
+  results[slot + 1] = bad;
+  results[slot + 2] = neg;
+}
+
+__global__ void axpy_kernel(double* u, double s, const double* dir, long n) {
+  for (long i = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<long>(gridDim.x) * blockDim.x)
+    u[i] = u[i] + s * dir[i];  // solver.hpp:283, no contraction (-fmad=false)
+}
+
+__global__ void add_scalar_kernel(double* u, double delta, long n) {
+  for (long i = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<long>(gridDim.x) * blockDim.x)
+    u[i] = u[i] + delta;
+}
+
+unsigned ew_grid(long n) {
+  long b = (n + 255) / 256;
+  if (b > 148L * 16) b = 148L * 16;
+  return static_cast<unsigned>(b < 1 ? 1 : b);
+}
+
+}  // namespace
+
+Reducer::~Reducer() {
+  if (partials_) cudaFree(partials_);
+  if (results_) cudaFree(results_);
+  if (pinned_) cudaFreeHost(pinned_);
+}
+
+void Reducer::init() {
+  blocks_ = kRedBlocks;
+  BFM_CUDA(cudaMalloc(&partials_, 4 * blocks_ * sizeof(double)));
+  BFM_CUDA(cudaMalloc(&results_, kRedSlots * sizeof(double)));
+  BFM_CUDA(cudaMemset(results_, 0, kRedSlots * sizeof(double)));
+  BFM_CUDA(cudaMallocHost(&pinned_, kRedSlots * sizeof(double)));
+}
+
+void Reducer::dot(const double* a1, const double* b1, const double* a2, const double* b2, long n,
+                  double vol, int slot, cudaStream_t s, LaunchCounter* lc) {
+  RedArgs A{a1, b1, a2, b2, n, 0, 0, partials_};
+  red_partial_kernel<<<blocks_, kRedThreads, 0, s>>>(A);
+  red_final_kernel<<<1, kRedThreads, 0, s>>>(partials_, blocks_, a2 ? 1 : 0, vol, results_, slot);
+  BFM_LAUNCH_CHECK("reduce dot");
+  if (lc) lc->add(2);
+}
+
+void Reducer::sum(const double* a, long n, double vol, int slot, cudaStream_t s,
+                  LaunchCounter* lc) {
+  RedArgs A{a, nullptr, nullptr, nullptr, n, 1, 0, partials_};
+  red_partial_kernel<<<blocks_, kRedThreads, 0, s>>>(A);
+  red_final_kernel<<<1, kRedThreads, 0, s>>>(partials_, blocks_, 0, vol, results_, slot);
+  BFM_LAUNCH_CHECK("reduce sum");
+  if (lc) lc->add(2);
+}
+
+void Reducer::primal(const double* disp, const double* mu, int d, long n, double vol, int slot,
+                     cudaStream_t s, LaunchCounter* lc) {
+  RedArgs A{disp, mu, nullptr, nullptr, n, 2, d, partials_};
+  red_partial_kernel<<<blocks_, kRedThreads, 0, s>>>(A);
+  red_final_kernel<<<1, kRedThreads, 0, s>>>(partials_, blocks_, 0, vol, results_, slot);
+  BFM_LAUNCH_CHECK("reduce primal");
+  if (lc) lc->add(2);
+}
+
+void Reducer::scan_density(const double* a, long n, int slot, cudaStream_t s, LaunchCounter* lc) {
+  density_scan_kernel<<<blocks_, kRedThreads, 0, s>>>(a, n, partials_);
+  density_final_kernel<<<1, 32, 0, s>>>(partials_, blocks_, results_, slot);
+  BFM_LAUNCH_CHECK("density scan");
+  if (lc) lc->add(2);
+}
+
+void Reducer::fetch(double* host, int count, cudaStream_t s) {
+  BFM_CUDA(cudaMemcpyAsync(pinned_, results_, count * sizeof(double), cudaMemcpyDeviceToHost, s));
+  BFM_CUDA(cudaStreamSynchronize(s));
+  for (int i = 0; i < count; ++i) host[i] = pinned_[i];
+}
+
+void axpy(double* u, double s, const double* dir, long n, cudaStream_t st, LaunchCounter* lc) {
+  axpy_kernel<<<ew_grid(n), 256, 0, st>>>(u, s, dir, n);
+  BFM_LAUNCH_CHECK("axpy");
+  if (lc) lc->add();
+}
+
+void add_scalar(double* u, double delta, long n, cudaStream_t st, LaunchCounter* lc) {
+  add_scalar_kernel<<<ew_grid(n), 256, 0, st>>>(u, delta, n);
+  BFM_LAUNCH_CHECK("add_scalar");
+  if (lc) lc->add();
+}
+
+}  // namespace bfmgpu

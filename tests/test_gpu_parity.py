@@ -1,0 +1,219 @@
+"""GPU parity: the sm_100a kernels (through the C ABI) against the reference.
+
+Bar: every field-producing operator is BITWISE equal
+to the reference built with the shared DCT (oracle/_ref): c-transform (exactly
+rounded), map, pushforward, Poisson. Scalars from reductions (pair values,
+gn) feed only decisions and are compared with rel tol 1e-12 (they are not
+sequential Kahan sums on the GPU). Goldens in tests/golden/ come from the
+unmodified reference (tests/golden/make_golden.py)."""
+import os
+
+import numpy as np
+import pytest
+
+import oracle_lib as O
+import paper_1905_12154_b200 as bfm
+from paper_1905_12154_b200 import synthetic
+
+pytestmark = pytest.mark.gpu
+GOLD = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+
+
+def load(name):
+    return dict(np.load(os.path.join(GOLD, name)))
+
+
+@pytest.fixture(scope="module", autouse=True)
+def need_gpu():
+    if not bfm.device_available():
+        pytest.skip("no CUDA device")
+
+
+# ------------------------------------------------------------- c-transform
+def test_ctransform_goldens_bitwise():
+    g = load("ctransform.npz")
+    for k in [k for k in g if k.startswith("ct_in_")]:
+        name = k[len("ct_in_"):]
+        out = bfm.ctransform(g[k])
+        assert O.n_bit_diff(out, g["ct_out_" + name]) == 0, name
+
+
+@pytest.mark.parametrize("shape", [(1024,), (256, 256), (512, 512), (384, 96), (96, 384), (48, 48, 48),
+                                   (32, 64, 16), (24, 24, 24), (2, 2), (3, 5), (2, 3, 2)])
+def test_ctransform_random_vs_restatement_or_reference(shape, ref):
+    rng = np.random.default_rng(sum(shape))
+    for kind in range(3):
+        if kind == 0:
+            phi = rng.uniform(-1, 1, shape)
+        elif kind == 1:
+            phi = synthetic.c5_potential(shape)[0]
+        else:
+            g = np.meshgrid(*[(np.arange(n) + 0.5) / n for n in shape], indexing="ij")
+            phi = sum(0.5 * x * x for x in g) + 1e-13 * rng.standard_normal(shape)
+        out = bfm.ctransform(phi)
+        want = ref.ref_ctransform(phi)
+        assert O.n_bit_diff(out, want) == 0, (shape, kind)
+
+
+@pytest.mark.parametrize("shape", [(2048, 2048), (4096, 512), (128, 128, 128)])
+def test_ctransform_large_vs_reference(shape, ref):
+    phi = synthetic.c5_potential(shape)[0]
+    out = bfm.ctransform(phi)
+    want = ref.ref_ctransform(phi)
+    assert O.n_bit_diff(out, want) == 0
+
+
+@pytest.mark.parametrize("shape", [(64,), (24, 24), (8, 8, 8), (33, 17)])
+def test_galois_laws_exact(shape):
+    # test_transforms.cpp:255-283: phi <= phi^cc pointwise, phi^ccc == phi^c bitwise
+    rng = np.random.default_rng(149)
+    for _ in range(20):
+        phi = rng.uniform(0, 1, shape)
+        c = bfm.ctransform(phi)
+        cc = bfm.ctransform(c)
+        assert np.all(phi <= cc)
+        assert O.n_bit_diff(bfm.ctransform(cc), c) == 0
+
+
+def test_ctransform_c5_4096_matches_reference(ref):
+    phi = synthetic.c5_potential((4096, 4096))[0]
+    out = bfm.ctransform(phi)
+    want = ref.ref_ctransform(phi)
+    assert O.n_bit_diff(out, want) == 0
+
+
+# ------------------------------------------------------------- Poisson
+def test_poisson_goldens_bitwise():
+    g = load("poisson.npz")
+    for k in [k for k in g if k.startswith("pois_in_")]:
+        key = k[len("pois_in_"):]
+        out = bfm.solve_neumann(g[k])
+        assert O.n_bit_diff(out, g["pois_out_" + key]) == 0, key
+
+
+@pytest.mark.parametrize("shape", [(4096, 64), (64, 4096), (1024, 1024), (384, 48), (48, 384, 8), (96, 96, 96),
+                                   (30, 50), (130,)])
+def test_poisson_vs_restatement(shape):
+    r = np.random.default_rng(11).uniform(-1, 1, shape)
+    assert O.n_bit_diff(bfm.solve_neumann(r), O.orc_solve_neumann(r)) == 0
+
+
+# ------------------------------------------------------------- pushforward
+def test_pushforward_goldens_bitwise():
+    g = load("pushforward.npz")
+    for k in [k for k in g if k.startswith("pf_u_")]:
+        key = k[len("pf_u_"):]
+        disp = bfm.map_from_conjugate(g[k])
+        assert O.n_bit_diff(disp, g["pf_disp_" + key]) == 0, key
+        rho = bfm.pushforward_density(disp, g["pf_mu_" + key])
+        assert O.n_bit_diff(rho, g["pf_rho_" + key]) == 0, key
+        half = bfm.displacement_interpolant(disp, g["pf_mu_" + key], 0.5)
+        assert O.n_bit_diff(half, g["pf_half_" + key]) == 0, key
+        d2 = bfm.map_from_conjugate(g["pf_u2_" + key])
+        assert O.n_bit_diff(d2, g["pf_disp2_" + key]) == 0, key
+        assert O.n_bit_diff(bfm.pushforward_density(d2, g["pf_mu_" + key]), g["pf_rho2_" + key]) == 0
+
+
+@pytest.mark.parametrize("shape", [(512, 512), (64, 64, 64), (1000, 7)])
+def test_pushforward_vs_restatement(shape):
+    rng = np.random.default_rng(5)
+    u = synthetic.c5_pushforward_potential(shape)
+    mu = rng.uniform(0, 1, shape) * (rng.uniform(0, 1, shape) > 0.4)
+    disp = bfm.map_from_conjugate(u)
+    assert O.n_bit_diff(disp, O.orc_map_from_conjugate(u)) == 0
+    assert O.n_bit_diff(bfm.pushforward_density(disp, mu), O.orc_pushforward_density(disp, mu)) == 0
+
+
+def test_pushforward_concentrated_map():
+    # many sources into few cells: exercises large sorted buckets
+    n = 256
+    x = (np.arange(n) + 0.5) / n
+    X, Y = np.meshgrid(x, x, indexing="ij")
+    u = 0.5 * (X * X + Y * Y) - 0.5 * X - 0.5 * Y  # grad u = x - 0.5 -> everything to the centre
+    mu = np.ones((n, n))
+    disp = bfm.map_from_conjugate(u)
+    rho = bfm.pushforward_density(disp, mu)
+    assert O.n_bit_diff(rho, O.orc_pushforward_density(disp, mu)) == 0
+
+
+def test_pushforward_kats():
+    # test_pushforward.cpp:104-116 fractional split; :137-150 boundary deposits
+    mu = np.zeros(8)
+    mu[2] = 8.0
+    disp = np.zeros((1, 8))
+    disp[0, 2] = 0.7 * (1.0 / 8)
+    rho = bfm.pushforward_density(disp, mu)
+    assert abs(rho[2] - 8 * 0.3) < 1e-13 and abs(rho[3] - 8 * 0.7) < 1e-13
+    mu = np.zeros(8)
+    mu[1] = mu[6] = 4.0
+    disp = np.zeros((1, 8))
+    disp[0, 1] = 0.0 - (1.5 / 8)
+    disp[0, 6] = 1.0 - (6.5 / 8)
+    rho = bfm.pushforward_density(disp, mu)
+    assert rho[0] == 4.0 and rho[7] == 4.0
+
+
+# ------------------------------------------------------------- solver
+def _scal(rep):
+    return np.array([rep.iterations, rep.dual_value, rep.primal_cost, rep.residual])
+
+
+@pytest.mark.parametrize("case,cfg", [
+    ("c1_64", bfm.SolverConfig(tolerance=-1.0, max_iterations=8)),
+    ("discs", bfm.SolverConfig(tolerance=-1.0, max_iterations=40, exact_cost=0.25, exact_tolerance=1e-4)),
+    ("balls", bfm.SolverConfig(tolerance=-1.0, max_iterations=4)),
+])
+def test_solver_goldens(case, cfg):
+    g = load("solver.npz")
+    rep = bfm.Solver(g[case + "_mu"], g[case + "_nu"], cfg).run()
+    want = g[case + "_scalars"]
+    assert rep.iterations == int(want[0])
+    assert abs(rep.dual_value - want[1]) <= 1e-12 * max(1.0, abs(want[1]))
+    assert abs(rep.primal_cost - want[2]) <= 1e-12 * max(1.0, abs(want[2]))
+    assert O.n_bit_diff(rep.phi, g[case + "_phi"]) == 0
+    assert O.n_bit_diff(rep.psi, g[case + "_psi"]) == 0
+    assert O.n_bit_diff(rep.map, g[case + "_map"]) == 0
+
+
+def test_solver_c1_full_vs_reference(ref):
+    """C1: 256^2, 100 iterations, tolerance disabled (BASELINE configs[0])."""
+    mu, nu = synthetic.c1()
+    cfg = bfm.SolverConfig(tolerance=-1.0, max_iterations=100)
+    a = bfm.Solver(mu, nu, cfg).run()
+    b = ref.RefSolver(mu, nu, cfg).run()
+    assert a.iterations == b.iterations == 100 or a.termination == b.termination
+    assert a.termination == b.termination
+    for x, y in [(a.phi, b.phi), (a.psi, b.psi), (a.map, b.map)]:
+        assert O.n_bit_diff(x, y) == 0
+    ta = np.array([t.dual_value for t in a.trace])
+    tb = np.array([t.dual_value for t in b.trace])
+    assert np.abs(ta - tb).max() <= 1e-12 * np.abs(tb).max()
+
+
+def test_solver_deterministic():
+    mu, nu = synthetic.c1(64)
+    cfg = bfm.SolverConfig(tolerance=1e-5, max_iterations=30)
+    a = bfm.Solver(mu, nu, cfg).run()
+    b = bfm.Solver(mu, nu, cfg).run()
+    assert a.iterations == b.iterations and a.dual_value == b.dual_value
+    assert O.n_bit_diff(a.phi, b.phi) == 0
+
+
+def test_identical_marginals_terminate_immediately():
+    # test_solver.cpp:57-70
+    x = (np.arange(32) + 0.5) / 32
+    X, Y = np.meshgrid(x, x, indexing="ij")
+    raw = ((X - 0.5) ** 2 + (Y - 0.5) ** 2 <= 0.04).astype(float)
+    mu = raw / (raw.sum() / 1024)
+    for mode in (bfm.BACK_AND_FORTH, bfm.GRADIENT_ASCENT):
+        rep = bfm.solve(mu, mu, bfm.SolverConfig(mode=mode, tolerance=1e-4))
+        assert rep.termination == "tolerance_met" and rep.iterations == 0
+        assert rep.residual == 0.0 and rep.dual_value == 0.0
+
+
+def test_gradient_ascent_mode_matches_reference(ref):
+    g = load("solver.npz")
+    cfg = bfm.SolverConfig(mode=bfm.GRADIENT_ASCENT, tolerance=-1.0, max_iterations=10)
+    a = bfm.Solver(g["discs_mu"], g["discs_nu"], cfg).run()
+    b = ref.RefSolver(g["discs_mu"], g["discs_nu"], cfg).run()
+    assert O.n_bit_diff(a.phi, b.phi) == 0 and O.n_bit_diff(a.psi, b.psi) == 0

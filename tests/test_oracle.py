@@ -1,0 +1,152 @@
+"""CPU-only: pins the oracles. The restatement (oracle/liboracle.so) must
+reproduce the reference's golden vectors bitwise, the FFTW shim must match
+scipy's DCT conventions, and the reference's own KATs / property tests for the
+path must hold on it (test_poisson.cpp, test_solver.cpp, test_pushforward.cpp)."""
+import os
+
+import numpy as np
+import pytest
+import scipy.fft as sf
+
+import oracle_lib as O
+
+GOLD = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+
+
+def load(name):
+    return dict(np.load(os.path.join(GOLD, name)))
+
+
+def test_restatement_ctransform_matches_reference_goldens_bitwise():
+    g = load("ctransform.npz")
+    names = [k[len("ct_in_"):] for k in g if k.startswith("ct_in_")]
+    assert len(names) >= 10
+    for name in names:
+        out = O.orc_ctransform(g["ct_in_" + name])
+        assert O.n_bit_diff(out, g["ct_out_" + name]) == 0, name
+
+
+def test_restatement_poisson_matches_reference_goldens_bitwise():
+    g = load("poisson.npz")
+    for k in [k for k in g if k.startswith("pois_in_")]:
+        key = k[len("pois_in_"):]
+        out = O.orc_solve_neumann(g[k])
+        assert O.n_bit_diff(out, g["pois_out_" + key]) == 0, key
+
+
+def _scipy_neumann(r):
+    B = sf.dctn(r, type=2)
+    lam = 0
+    for a, n in enumerate(r.shape):
+        k = np.arange(n)
+        l = (2 - 2 * np.cos(np.pi * k / n)) * n * n
+        shp = [1] * r.ndim
+        shp[a] = n
+        lam = lam + l.reshape(shp)
+    scale = np.prod([2.0 * n for n in r.shape])
+    with np.errstate(divide="ignore", invalid="ignore"):
+        B = np.where(lam == 0, 0, B / (lam * scale))
+    return sf.dctn(B, type=3)
+
+
+@pytest.mark.parametrize("shape", [(64,), (384,), (32, 16), (17, 29), (5, 7), (12, 10, 8), (24, 48),
+                                   (6, 9, 11), (96, 12)])
+def test_shim_dct_matches_scipy_conventions(shape):
+    r = np.random.default_rng(3).uniform(-1, 1, shape)
+    out = O.orc_solve_neumann(r)
+    ex = _scipy_neumann(r)
+    assert np.abs(out - ex).max() <= 1e-12 * max(1.0, np.abs(ex).max())
+
+
+def _neg_lap(u):
+    # oracles.hpp:206-233 restated: cell-centred Neumann 5/7-point stencil
+    out = np.zeros_like(u)
+    for a, n in enumerate(u.shape):
+        left = np.concatenate([np.take(u, [0], axis=a), np.take(u, range(0, n - 1), axis=a)], axis=a)
+        right = np.concatenate([np.take(u, range(1, n), axis=a), np.take(u, [n - 1], axis=a)], axis=a)
+        out += (2.0 * u - left - right) * float(n) * n
+    return out
+
+
+@pytest.mark.parametrize("shape", [(33,), (64, 64), (17, 29), (5, 7), (32, 32, 32), (6, 9, 11)])
+def test_stencil_roundtrip_property(shape):
+    # test_poisson.cpp:64-79 / acceptance_main.cpp:272-302 (<= 1e-10)
+    r = np.random.default_rng(1234).uniform(-1, 1, shape)
+    u = O.orc_solve_neumann(r)
+    back = _neg_lap(u)
+    m = r.mean()
+    assert np.abs(back - (r - m)).max() <= 1e-10 * np.abs(r - m).max()
+    assert abs(u.mean()) < 1e-12
+
+
+def test_cosine_eigenmode():
+    # test_poisson.cpp:41-62
+    n = 64
+    x = (np.arange(n) + 0.5) / n
+    rhs = np.cos(np.pi * x)
+    lam = (2 - 2 * np.cos(np.pi / n)) * n * n
+    u = O.orc_solve_neumann(rhs)
+    assert np.abs(u - rhs / lam).max() < 1e-12
+
+
+def test_restatement_pushforward_matches_goldens_bitwise():
+    g = load("pushforward.npz")
+    for k in [k for k in g if k.startswith("pf_u_")]:
+        key = k[len("pf_u_"):]
+        disp = O.orc_map_from_conjugate(g["pf_u_" + key])
+        assert O.n_bit_diff(disp, g["pf_disp_" + key]) == 0, key
+        rho = O.orc_pushforward_density(disp, g["pf_mu_" + key])
+        assert O.n_bit_diff(rho, g["pf_rho_" + key]) == 0, key
+        d2 = O.orc_map_from_conjugate(g["pf_u2_" + key])
+        assert O.n_bit_diff(d2, g["pf_disp2_" + key]) == 0, key
+        assert O.n_bit_diff(O.orc_pushforward_density(d2, g["pf_mu_" + key]), g["pf_rho2_" + key]) == 0
+
+
+def test_restatement_solver_trace_matches_reference_golden():
+    g = load("solver.npz")
+    phi, psi, duals = O.orc_run_steps(g["c1_64_mu"], g["c1_64_nu"], 8)
+    tr = g["c1_64_trace"]
+    assert np.array_equal(O.bits(duals), O.bits(tr[:, 1]))
+    shift = O.orc_integrate(phi)
+    assert O.n_bit_diff(phi - shift, g["c1_64_phi"]) == 0
+    # run() refreshes the probe (psi = phi^c) before finish() (solver.hpp:213)
+    assert O.n_bit_diff(O.orc_ctransform(phi) + shift, g["c1_64_psi"]) == 0
+
+
+def test_sigma_rule_kats():
+    # test_solver.cpp:43-55
+    u = lambda *a: O.orc_lib().orc_update_sigma(*a, None)
+    assert abs(u(1.0, 0.1, 1.0) - 0.8) <= 1e-15
+    assert abs(u(1.0, 0.9, 1.0) - 1.25) <= 1e-15
+    assert u(1.0, 0.5, 1.0) == 1.0
+    assert u(0.012, 0.0, 1.0) == 0.01
+    assert u(0.7, 0.0, 0.0) == 0.7
+
+
+def test_restatement_vs_reference_random_campaign(ref):
+    """Exactly-rounded c-transform: the reference's D&C + expansion rounding and
+    the restatement's brute force + exact round-down agree on every node,
+    including values straddling powers of two and near-collinear lines."""
+    rng = np.random.default_rng(99)
+    mism = tot = 0
+    for trial in range(120):
+        d = int(rng.integers(1, 4))
+        hi = {1: 48, 2: 14, 3: 7}[d]
+        shape = tuple(int(x) for x in rng.integers(2, hi + 1, size=d))
+        kind = trial % 5
+        if kind == 0:
+            phi = rng.uniform(-1, 1, shape)
+        elif kind == 1:
+            phi = np.ldexp(1.0, rng.integers(-6, 2, shape)) * (1 + 1e-15 * rng.standard_normal(shape))
+        elif kind == 2:
+            g = np.meshgrid(*[(np.arange(n) + 0.5) / n for n in shape], indexing="ij")
+            phi = sum(0.5 * x * x for x in g) + 1e-13 * rng.standard_normal(shape)
+        elif kind == 3:
+            phi = rng.uniform(0, 1, shape) * 1e-9
+        else:
+            phi = np.round(rng.uniform(-8, 8, shape)) / 16.0
+        a = ref.ref_ctransform(phi)
+        b = O.orc_ctransform(phi)
+        mism += O.n_bit_diff(a, b)
+        tot += a.size
+    assert mism == 0, f"{mism} of {tot}"
