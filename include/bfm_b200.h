@@ -172,6 +172,10 @@ long bfm_solver_launches(const bfm_solver* s);
  * solver's stream; *ms receives the device-timed duration. */
 int bfm_solver_time_steps(bfm_solver* s, int k, double* ms);
 
+/* Test hook: device evaluation of the exact round-down of `count` sums of m
+ * doubles each (terms row-major). Used by the parity tests only. */
+int bfm_debug_round_down(const double* terms, int m, int count, double* out);
+
 const char* bfm_last_error(void);
 /* Selects the CUDA device for subsequent calls on this thread (one process
  * per GPU: pass LOCAL_RANK). */

@@ -21,6 +21,10 @@
 #include "pushforward.cuh"
 #include "reduce.cuh"
 
+namespace bfmgpu {
+void debug_round_down(const double* h_terms, int m, int count, double* h_out);
+}
+
 namespace {
 
 using namespace bfmgpu;
@@ -326,8 +330,15 @@ struct bfm_solver {
     rep_map.alloc(g.d * g.size);
     BFM_CUDA(cudaMemcpyAsync(rep_phi.p, phi.p, g.size * sizeof(double), cudaMemcpyDeviceToDevice, stream));
     BFM_CUDA(cudaMemcpyAsync(rep_psi.p, psi.p, g.size * sizeof(double), cudaMemcpyDeviceToDevice, stream));
-    ws.redp().sum(rep_phi.p, g.size, g.vol, kSlotShift, stream, &ws.lc);
-    const double shift = fetch1(kSlotShift);
+    // The gauge shift feeds every reported field, so it must be the reference's
+    // exact sequential Kahan sum (grid.hpp:179-183): computed on the host.
+    std::vector<double> hphi(g.size);
+    BFM_CUDA(cudaMemcpyAsync(hphi.data(), rep_phi.p, g.size * sizeof(double), cudaMemcpyDeviceToHost,
+                             stream));
+    BFM_CUDA(cudaStreamSynchronize(stream));
+    Kahan k;
+    for (long i = 0; i < g.size; ++i) k.add(hphi[i]);
+    const double shift = k.sum * g.vol;
     add_scalar(rep_phi.p, -shift, g.size, stream, &ws.lc);
     add_scalar(rep_psi.p, shift, g.size, stream, &ws.lc);
     ws.pfp().map_only(rep_psi.p, rep_map.p, stream, &ws.lc);
@@ -389,6 +400,13 @@ struct HostOp {
 extern "C" {
 
 const char* bfm_last_error(void) { return g_err.c_str(); }
+
+int bfm_debug_round_down(const double* terms, int m, int count, double* out) {
+  return guard([&] {
+    require_device();
+    bfmgpu::debug_round_down(terms, m, count, out);
+  });
+}
 
 int bfm_set_device(int device) {
   return guard([&] { BFM_CUDA(cudaSetDevice(device)); });

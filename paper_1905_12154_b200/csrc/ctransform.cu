@@ -27,6 +27,7 @@
 //    argmin with no exact arithmetic at all; otherwise candidates are
 //    compared with exact expansion arithmetic (exact.cuh).
 //  * The last pass rounds the winner's exact value down once.
+#include <cassert>
 #include <cmath>
 #include <cstring>
 #include <vector>
@@ -38,6 +39,12 @@ namespace bfmgpu {
 namespace {
 
 constexpr double kU = 1.1102230246251565e-16;  // 2^-53
+
+#if defined(BFM_DEBUG_BOUNDS)
+#define BFM_DASSERT(c) assert(c)
+#else
+#define BFM_DASSERT(c) ((void)0)
+#endif
 
 __device__ __forceinline__ int padj(int j) { return j + (j >> 5); }
 
@@ -68,6 +75,7 @@ __device__ __forceinline__ double g_approx(const CtAxis& A, int k, int j) {
     const double dl = coord(A.h, k) - coord(A.h, j);
     return 0.5 * dl * dl;
   }
+  BFM_DASSERT(k >= 0 && k < A.n && j >= 0 && j < A.n);
   return A.G[static_cast<long>(k) * A.n + j].x;
 }
 
@@ -77,14 +85,20 @@ __device__ __forceinline__ int g_terms(const CtAxis& A, int k, int j, double* t)
     t[0] = 0.5 * dl * dl;
     return 1;
   }
-  const double2 v = A.G[static_cast<long>(k) * A.n + j];
-  t[0] = v.x;
-  t[1] = v.y;
-  return 2;
+  BFM_DASSERT(k >= 0 && k < A.n && j >= 0 && j < A.n);
+  const double4 v = A.G[static_cast<long>(k) * A.n + j];
+  int m = 0;
+  t[m++] = v.x;
+  if (v.y != 0.0) t[m++] = v.y;
+  if (v.z != 0.0) t[m++] = v.z;
+  return m;
 }
 
 __device__ __forceinline__ long phi_index(const CtPass& p, const LineGeo& g, uint32_t chain,
                                           int j) {
+  BFM_DASSERT(j >= 0 && j < p.ax[p.a].n);
+  BFM_DASSERT(p.a < 1 || (chain & 0xFFFFu) < static_cast<uint32_t>(p.ax[0].n));
+  BFM_DASSERT(p.a < 2 || (chain >> 16) < static_cast<uint32_t>(p.ax[1].n));
   long idx = g.phi_other + static_cast<long>(j) * p.ax[p.a].stride;
   if (p.a >= 1) idx += static_cast<long>(chain & 0xFFFFu) * p.ax[0].stride;
   if (p.a >= 2) idx += static_cast<long>(chain >> 16) * p.ax[1].stride;
@@ -354,6 +368,7 @@ __global__ void __launch_bounds__(1024) ct_pass_kernel(CtPass p) {
   }
   group_sync(tpl, l);
   const int hsz = static_cast<int>(s.scal[3]);
+  BFM_DASSERT(!active || (hsz >= 1 && hsz <= n));
 
   // ---- 4. suspects: non-corners within tau of their hull edge -----------
   if (active && j0 < j1) {
@@ -442,12 +457,12 @@ __global__ void __launch_bounds__(1024) ct_pass_kernel(CtPass p) {
         const int e1 = R < hsz - 1 ? R + 1 : hsz - 1;
         int best = -1;
         double bestF = 0.0;
-        double bt[8];
+        double bt[12];
         int bm = 0;
         auto consider = [&](int j) {
           const double Fj = Fhat(j, xk);
           if (best >= 0 && Fj - bestF > cmp_margin) return;
-          double ct[8];
+          double ct[12];
           const uint32_t ch = p.a > 0 ? s.chain[j] : 0u;
           const int cm = cand_terms(p, geo, ch, j, k, ct);
           if (best >= 0 && bfmx::sign_diff(ct, cm, bt, bm) >= 0) return;
@@ -471,6 +486,7 @@ __global__ void __launch_bounds__(1024) ct_pass_kernel(CtPass p) {
         }
         win = best;
       }
+      BFM_DASSERT(win >= 0 && win < n);
       res[k] = static_cast<uint16_t>(win);
     }
   }
@@ -498,7 +514,7 @@ __global__ void __launch_bounds__(1024) ct_pass_kernel(CtPass p) {
       p.state_out[node] = p.a == 0 ? static_cast<uint32_t>(win)
                                    : (ch | (static_cast<uint32_t>(win) << 16));
     } else {
-      double tv[8];
+      double tv[12];
       const int m = cand_terms(p, g, ch, win, k, tv);
       double r;
       if (all_dyadic) {
@@ -547,7 +563,7 @@ void CtPlan::init(const GridDesc& g) {
       if (!tables_[a]) {
         if (g.n[a] > 4096) throw std::invalid_argument("ctransform: non-dyadic extent above 4096");
         const int n = g.n[a];
-        std::vector<double2> host(static_cast<size_t>(n) * n);
+        std::vector<double4> host(static_cast<size_t>(n) * n);
         for (int k = 0; k < n; ++k) {
           const double x = coord(g.h[a], k);
           for (int j = 0; j < n; ++j) {
@@ -560,17 +576,18 @@ void CtPlan::init(const GridDesc& g) {
             e.grow(0.5 * y * y);
             e.grow(-pe);
             e.grow(-pr);
-            const double hi = e.approx();
-            bfmx::Exp<9> r;
-            r.clear();
-            for (int i = 0; i < e.n; ++i) r.grow(e.q[i]);
-            r.grow(-hi);
-            if (r.n > 1) throw std::runtime_error("ctransform: g table entry not a double-double");
-            host[static_cast<size_t>(k) * n + j] = make_double2(hi, r.n ? r.q[0] : 0.0);
+            // peel off up to three limbs, largest first; the remainder must vanish
+            double limb[3] = {0.0, 0.0, 0.0};
+            for (int q = 0; q < 3; ++q) {
+              limb[q] = e.approx();
+              e.grow(-limb[q]);
+            }
+            if (e.n != 0) throw std::runtime_error("ctransform: g table entry needs > 3 limbs");
+            host[static_cast<size_t>(k) * n + j] = make_double4(limb[0], limb[1], limb[2], 0.0);
           }
         }
-        BFM_CUDA(cudaMalloc(&tables_[a], host.size() * sizeof(double2)));
-        BFM_CUDA(cudaMemcpy(tables_[a], host.data(), host.size() * sizeof(double2),
+        BFM_CUDA(cudaMalloc(&tables_[a], host.size() * sizeof(double4)));
+        BFM_CUDA(cudaMemcpy(tables_[a], host.data(), host.size() * sizeof(double4),
                             cudaMemcpyHostToDevice));
       }
       A.G = tables_[a];
@@ -651,4 +668,26 @@ unsigned long long CtPlan::slow_query_count() {
   return v;
 }
 
+}  // namespace bfmgpu
+
+// ---- diagnostics (exported through the C ABI for tests) --------------------
+namespace bfmgpu {
+namespace {
+__global__ void debug_rd_kernel(const double* t, int m, int count, double* out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < count) out[i] = bfmx::round_down_sum(t + static_cast<long>(i) * m, m);
+}
+}  // namespace
+
+void debug_round_down(const double* h_terms, int m, int count, double* h_out) {
+  double *dt = nullptr, *dout = nullptr;
+  BFM_CUDA(cudaMalloc(&dt, sizeof(double) * m * count));
+  BFM_CUDA(cudaMalloc(&dout, sizeof(double) * count));
+  BFM_CUDA(cudaMemcpy(dt, h_terms, sizeof(double) * m * count, cudaMemcpyHostToDevice));
+  debug_rd_kernel<<<(count + 127) / 128, 128>>>(dt, m, count, dout);
+  BFM_LAUNCH_CHECK("debug_rd_kernel");
+  BFM_CUDA(cudaMemcpy(h_out, dout, sizeof(double) * count, cudaMemcpyDeviceToHost));
+  cudaFree(dt);
+  cudaFree(dout);
+}
 }  // namespace bfmgpu

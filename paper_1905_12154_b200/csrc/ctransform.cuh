@@ -13,7 +13,7 @@ struct CtAxis {
   long stride;
   double h;
   int dyadic;          // 1: g(k,j) = 0.5 (x_k - y_j)^2 is an exact double
-  const double2* G;    // else: [n*n] exact (hi, lo) of hs(x_k)+hs(y_j)-x_k*y_j
+  const double4* G;    // else: [n*n] exact limbs (hi, mid, lo, 0) of hs(x_k)+hs(y_j)-x_k*y_j
 };
 
 struct CtPass {
@@ -51,7 +51,7 @@ class CtPlan {
  private:
   GridDesc g_;
   CtAxis ax_[3] = {};
-  double2* tables_[3] = {nullptr, nullptr, nullptr};
+  double4* tables_[3] = {nullptr, nullptr, nullptr};
   uint32_t* state_[2] = {nullptr, nullptr};
   unsigned long long* slow_ = nullptr;
   CtPass pass_[3] = {};

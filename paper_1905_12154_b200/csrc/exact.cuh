@@ -33,14 +33,35 @@ BFM_HD void two_prod(double a, double b, double& p, double& e) {
 #endif
 }
 
-BFM_HD double next_down(double x) {
+// Neighbouring doubles by bit manipulation (finite inputs; x == 0 handled).
+BFM_HD double bits_to_double(long long b) {
 #if defined(__CUDA_ARCH__)
-  return nextafter(x, -INFINITY);
+  return __longlong_as_double(b);
 #else
-  return nextafter(x, -INFINITY);
+  double d;
+  __builtin_memcpy(&d, &b, 8);
+  return d;
 #endif
 }
-BFM_HD double next_up(double x) { return nextafter(x, INFINITY); }
+BFM_HD long long double_to_bits(double x) {
+#if defined(__CUDA_ARCH__)
+  return __double_as_longlong(x);
+#else
+  long long b;
+  __builtin_memcpy(&b, &x, 8);
+  return b;
+#endif
+}
+BFM_HD double next_down(double x) {
+  if (x == 0.0) return -4.9406564584124654e-324;
+  const long long b = double_to_bits(x);
+  return bits_to_double(x > 0.0 ? b - 1 : b + 1);
+}
+BFM_HD double next_up(double x) {
+  if (x == 0.0) return 4.9406564584124654e-324;
+  const long long b = double_to_bits(x);
+  return bits_to_double(x > 0.0 ? b + 1 : b - 1);
+}
 
 // Fixed-capacity nonoverlapping expansion (increasing magnitude, zero-free).
 template <int Cap>
@@ -69,9 +90,9 @@ struct Exp {
   }
 };
 
-// Sign of (sum a[0..na) - sum b[0..nb)), exact. na + nb <= 16.
+// Sign of (sum a[0..na) - sum b[0..nb)), exact. na + nb <= 24.
 BFM_HD int sign_diff(const double* a, int na, const double* b, int nb) {
-  Exp<16> e;
+  Exp<24> e;
   e.clear();
   for (int i = 0; i < na; ++i) e.grow(a[i]);
   for (int i = 0; i < nb; ++i) e.grow(-b[i]);
