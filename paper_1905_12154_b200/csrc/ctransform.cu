@@ -127,26 +127,28 @@ __device__ __forceinline__ bool convex3(double ya, double fa, double yb, double 
 }
 
 struct Smem {
-  double* fv;
-  uint32_t* chain;
-  uint16_t* hidx;
-  uint16_t* H;
-  uint8_t* flag;
+  double* fh;          // f~_j (DY: exact high part of f_j)
+  double* fl;          // DY: exact low part (f_j = fh + fl)
+  uint32_t* chain;     // !DY: argmin chain of element j
+  uint16_t* hidx;      // chunk hull stacks, later per-query winners
+  uint16_t* H;         // compacted hull corners
+  uint8_t* dlt;        // per-edge slack code (0: no suspects)
   int* lo;
   int* hi;
   int* off;
-  unsigned long long* scal;  // 0: A bits, 1: Smax bits, 2: dmax bits, 3: hull size
+  unsigned long long* scal;  // 0 A, 1 Smax, 2 Dmax, 3 hull size, 4 #non-convex
   LineGeo* geo;
 };
 
 __device__ __forceinline__ Smem carve(const CtPass& p, unsigned char* base, int l) {
   Smem s;
   unsigned char* b = base + static_cast<long>(l) * p.line_bytes;
-  s.fv = reinterpret_cast<double*>(b + p.off_fv);
+  s.fh = reinterpret_cast<double*>(b + p.off_fv);
+  s.fl = reinterpret_cast<double*>(b + p.off_chain);
   s.chain = reinterpret_cast<uint32_t*>(b + p.off_chain);
   s.hidx = reinterpret_cast<uint16_t*>(b + p.off_hidx);
   s.H = reinterpret_cast<uint16_t*>(b + p.off_H);
-  s.flag = reinterpret_cast<uint8_t*>(b + p.off_flag);
+  s.dlt = reinterpret_cast<uint8_t*>(b + p.off_flag);
   s.lo = reinterpret_cast<int*>(b + p.off_lohi);
   s.hi = s.lo + p.tpl;
   s.off = s.hi + p.tpl;
@@ -155,6 +157,34 @@ __device__ __forceinline__ Smem carve(const CtPass& p, unsigned char* base, int 
   return s;
 }
 
+// Slack codes: Delta <= 2^(code - 128) * sref, code in [1, 255] (conservative).
+__device__ __forceinline__ uint8_t slack_code(double D, double sref) {
+  if (!(D > 0.0)) return 1;
+  int e;
+  frexp(D / sref, &e);  // D/sref < 2^e
+  e += 128;
+  if (e < 1) e = 1;
+  if (e > 255) e = 255;
+  return static_cast<uint8_t>(e);
+}
+__device__ __forceinline__ double slack_value(uint8_t c, double sref) {
+  return ldexp(sref, static_cast<int>(c) - 128);
+}
+__device__ __forceinline__ void slack_max(uint8_t* dlt, int e, uint8_t c) {
+  unsigned* w = reinterpret_cast<unsigned*>(dlt + (e & ~3));
+  const int sh = 8 * (e & 3);
+  unsigned old = *w;
+  while (true) {
+    const unsigned cur = (old >> sh) & 0xffu;
+    if (cur >= c) return;
+    const unsigned nv = (old & ~(0xffu << sh)) | (static_cast<unsigned>(c) << sh);
+    const unsigned prev = atomicCAS(w, old, nv);
+    if (prev == old) return;
+    old = prev;
+  }
+}
+
+template <bool DY>
 __global__ void __launch_bounds__(1024) ct_pass_kernel(CtPass p) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int tpl = p.tpl;
@@ -187,81 +217,60 @@ __global__ void __launch_bounds__(1024) ct_pass_kernel(CtPass p) {
       }
     }
     *s.geo = g;
-    s.scal[0] = 0ull;
-    s.scal[1] = 0ull;
-    s.scal[2] = 0ull;
-    s.scal[3] = 0ull;
+    for (int q = 0; q < 8; ++q) s.scal[q] = 0ull;
   }
   __syncthreads();
 
-  // ---- load: f~_j = fl(-phi + sum_{b<a} g_b + hs(y_j)) -----------------
+  // ---- load (4 independent elements per thread iteration for ILP) --------
   {
     double amax = 0.0, smax = 0.0;
-    int ml;  // the line this thread loads for (fixed per thread)
-    if (p.strided) {
-      ml = threadIdx.x % lpc;
-      const Smem sm = carve(p, smem, ml);
-      const LineGeo g = *sm.geo;
-      for (int idx = threadIdx.x; idx < n * lpc; idx += blockDim.x) {
-        const int j = idx / lpc;
-        sm.flag[j] = 0;
-        if (!g.valid) continue;
-        const long node = g.base + static_cast<long>(j) * A.stride;
-        uint32_t ch = 0;
-        if (p.a > 0) ch = p.state_in[node];
-        const double ph = p.phi[phi_index(p, g, ch, j)];
-        const double y = coord(h, j);
-        const double hy = 0.5 * y * y;
-        double f = -ph;
-        double S = fabs(ph) + hy;
-        if (p.a >= 1) {
-          const double g0 = g_approx(p.ax[0], g.k[0], static_cast<int>(ch & 0xFFFFu));
-          f += g0;
-          S += g0;
+    const int ml = p.strided ? static_cast<int>(threadIdx.x % lpc) : l;
+    const Smem sm = carve(p, smem, ml);
+    const LineGeo g = *sm.geo;
+    const int step = p.strided ? blockDim.x / lpc : tpl;
+    const int first = p.strided ? static_cast<int>(threadIdx.x / lpc) : t;
+    for (int j = first; j < n + 4; j += step) sm.dlt[j] = 0;
+    if (g.valid) {
+      for (int j0 = first; j0 < n; j0 += 4 * step) {
+        uint32_t ch[4] = {0u, 0u, 0u, 0u};
+        double ph[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int j = j0 + u * step;
+          if (p.a > 0 && j < n) ch[u] = p.state_in[g.base + static_cast<long>(j) * A.stride];
         }
-        if (p.a >= 2) {
-          const double g1 = g_approx(p.ax[1], g.k[1], static_cast<int>(ch >> 16));
-          f += g1;
-          S += g1;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int j = j0 + u * step;
+          ph[u] = j < n ? p.phi[phi_index(p, g, ch[u], j)] : 0.0;
         }
-        f += hy;
-        sm.fv[padj(j)] = f;
-        if (p.a > 0) sm.chain[j] = ch;
-        amax = fmax(amax, fabs(f));
-        smax = fmax(smax, S);
-      }
-    } else {
-      ml = l;
-      const LineGeo g = *s.geo;
-      for (int j = t; j < n; j += tpl) {
-        s.flag[j] = 0;
-        if (!g.valid) continue;
-        const long node = g.base + j;
-        uint32_t ch = 0;
-        if (p.a > 0) ch = p.state_in[node];
-        const double ph = p.phi[phi_index(p, g, ch, j)];
-        const double y = coord(h, j);
-        const double hy = 0.5 * y * y;
-        double f = -ph;
-        double S = fabs(ph) + hy;
-        if (p.a >= 1) {
-          const double g0 = g_approx(p.ax[0], g.k[0], static_cast<int>(ch & 0xFFFFu));
-          f += g0;
-          S += g0;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int j = j0 + u * step;
+          if (j >= n) continue;
+          const double y = coord(h, j);
+          const double hy = 0.5 * y * y;
+          double B;
+          double G = 0.0;
+          if (p.a >= 1) G += g_approx(p.ax[0], g.k[0], static_cast<int>(ch[u] & 0xFFFFu));
+          if (p.a >= 2) G += g_approx(p.ax[1], g.k[1], static_cast<int>(ch[u] >> 16));
+          double f;
+          if (DY) {
+            // exact on dyadic grids: f_j = (G + hs(y_j)) - phi_j, G exact
+            B = G + hy;
+            f = B - ph[u];
+            sm.fh[padj(j)] = ph[u];
+            if (p.a > 0) sm.fl[padj(j)] = G;
+          } else {
+            f = (-ph[u] + G) + hy;
+            if (p.a > 0) sm.chain[j] = ch[u];
+            sm.fh[padj(j)] = f;
+          }
+          amax = fmax(amax, fabs(f));
+          smax = fmax(smax, fabs(ph[u]) + G + hy);
         }
-        if (p.a >= 2) {
-          const double g1 = g_approx(p.ax[1], g.k[1], static_cast<int>(ch >> 16));
-          f += g1;
-          S += g1;
-        }
-        f += hy;
-        s.fv[padj(j)] = f;
-        if (p.a > 0) s.chain[j] = ch;
-        amax = fmax(amax, fabs(f));
-        smax = fmax(smax, S);
       }
     }
-    const Smem sm = carve(p, smem, ml);
     atomicMax(&sm.scal[0], dbits(amax));
     atomicMax(&sm.scal[1], dbits(smax));
   }
@@ -271,144 +280,205 @@ __global__ void __launch_bounds__(1024) ct_pass_kernel(CtPass p) {
   const bool active = geo.valid;
   const double Aabs = bitsd(s.scal[0]);
   const double Smax = bitsd(s.scal[1]);
-  const double e_f = 8.0 * kU * Smax;
-  const double e_r = 4.0 * kU * (Aabs + 1.0);
+  const double e_f = DY ? kU * Aabs : 8.0 * kU * Smax;  // |f_j - f~_j|
+  const double e_r = 4.0 * kU * (Aabs + 1.0);           // |F^ - (f~ - x y)|
   const double e_F = e_f + e_r;
-  const double e_d = 32.0 * kU * Aabs;
+  const double e_d = 32.0 * kU * Aabs;                  // chord slack error
   const double tau = 2.0 * e_f + e_d;
+  const double Mc = 4.0 * e_F;
+  const double sref = fmax(Smax, 1e-300);
   const int j0 = t * C;
   const int j1 = min(n, j0 + C);
   uint16_t* st = s.hidx + t * (C + 2);
   auto P_y = [&](int idx) { return coord(h, idx); };
-  auto P_f = [&](int idx) { return s.fv[padj(idx)]; };
-
-  // ---- 1. chunk hulls (Andrew's monotone chain) -------------------------
-  if (active) {
-    int sz = 0;
-    for (int j = j0; j < j1; ++j) {
-      const double yj = P_y(j), fj = P_f(j);
-      while (sz >= 2) {
-        const int ia = st[sz - 2], ib = st[sz - 1];
-        if (convex3(P_y(ia), P_f(ia), P_y(ib), P_f(ib), yj, fj)) break;
-        --sz;
-      }
-      st[sz++] = static_cast<uint16_t>(j);
+  // f~_j: DY recomputes fl((G_j + hs(y_j)) - phi_j) from the stored exact parts
+  auto P_f = [&](int idx) {
+    if (DY) {
+      const double y = coord(h, idx);
+      const double G = p.a > 0 ? s.fl[padj(idx)] : 0.0;
+      return (G + 0.5 * y * y) - s.fh[padj(idx)];
     }
-    s.lo[t] = 0;
-    s.hi[t] = sz;
-  }
+    return s.fh[padj(idx)];
+  };
+  // DY exact value V(k, j) = Gsum + (-phi_j), Gsum = G_j + g_a(k, j) exact.
+  auto dy_gsum = [&](int j, double xk) {
+    const double dl = xk - coord(h, j);
+    const double G = p.a > 0 ? s.fl[padj(j)] : 0.0;
+    return G + 0.5 * dl * dl;
+  };
 
-  // ---- 2. tree merge by bridge walks -------------------------------------
-  for (int lvl = 1; lvl < tpl; lvl <<= 1) {
-    group_sync(tpl, l);
-    if (active && (t % (2 * lvl)) == 0 && t + lvl < tpl) {
-      const int gA = t, gB = t + lvl, gE = min(t + 2 * lvl, tpl);
-      int ca = gB - 1;
-      while (ca >= gA && s.lo[ca] >= s.hi[ca]) --ca;
-      int cb = gB;
-      while (cb < gE && s.lo[cb] >= s.hi[cb]) ++cb;
-      if (ca >= gA && cb < gE) {
-        int pa = s.hi[ca] - 1, pb = s.lo[cb];
-        auto ptidx = [&](int c, int q) { return static_cast<int>(s.hidx[c * (C + 2) + q]); };
-        while (true) {
-          bool moved = false;
-          while (true) {  // retreat a
-            int cp = ca, pp = pa - 1;
-            if (pp < s.lo[cp]) {
-              cp = ca - 1;
-              while (cp >= gA && s.lo[cp] >= s.hi[cp]) --cp;
-              if (cp < gA) break;
-              pp = s.hi[cp] - 1;
-            }
-            const int ip = ptidx(cp, pp), ia = ptidx(ca, pa), ib = ptidx(cb, pb);
-            if (convex3(P_y(ip), P_f(ip), P_y(ia), P_f(ia), P_y(ib), P_f(ib))) break;
-            s.hi[ca] = pa;
-            ca = cp;
-            pa = pp;
-            moved = true;
+  // ---- 0. convex fast path: every interior point a certified strict corner?
+  {
+    int bad = 0;
+    if (active) {
+      const int a0 = max(j0, 1), a1 = min(j1, n - 1);
+      for (int j = a0; j < a1; ++j)
+        if (!convex3(P_y(j - 1), P_f(j - 1), P_y(j), P_f(j), P_y(j + 1), P_f(j + 1))) ++bad;
+    }
+    if (bad) atomicAdd(reinterpret_cast<unsigned int*>(&s.scal[4]), static_cast<unsigned>(bad));
+  }
+  group_sync(tpl, l);
+  const bool convex_line = s.scal[4] == 0ull;
+
+  if (!convex_line) {
+    // ---- 1. chunk hulls (Andrew's monotone chain) -----------------------
+    if (active) {
+      int sz = 0;
+      double ya = 0, fa = 0, yb = 0, fb = 0;  // top two stack points
+      for (int j = j0; j < j1; ++j) {
+        const double yj = P_y(j), fj = P_f(j);
+        while (sz >= 2) {
+          if (convex3(ya, fa, yb, fb, yj, fj)) break;
+          --sz;
+          yb = ya;
+          fb = fa;
+          if (sz >= 2) {
+            const int ia = st[sz - 2];
+            ya = P_y(ia);
+            fa = P_f(ia);
           }
-          while (true) {  // advance b
-            int cq = cb, pq = pb + 1;
-            if (pq >= s.hi[cq]) {
-              cq = cb + 1;
-              while (cq < gE && s.lo[cq] >= s.hi[cq]) ++cq;
-              if (cq >= gE) break;
-              pq = s.lo[cq];
+        }
+        st[sz++] = static_cast<uint16_t>(j);
+        ya = yb;
+        fa = fb;
+        yb = yj;
+        fb = fj;
+      }
+      s.lo[t] = 0;
+      s.hi[t] = sz;
+    }
+    // ---- 2. tree merge by bridge walks ----------------------------------
+    for (int lvl = 1; lvl < tpl; lvl <<= 1) {
+      group_sync(tpl, l);
+      if (active && (t % (2 * lvl)) == 0 && t + lvl < tpl) {
+        const int gA = t, gB = t + lvl, gE = min(t + 2 * lvl, tpl);
+        int ca = gB - 1;
+        while (ca >= gA && s.lo[ca] >= s.hi[ca]) --ca;
+        int cb = gB;
+        while (cb < gE && s.lo[cb] >= s.hi[cb]) ++cb;
+        if (ca >= gA && cb < gE) {
+          int pa = s.hi[ca] - 1, pb = s.lo[cb];
+          auto ptidx = [&](int c, int q) { return static_cast<int>(s.hidx[c * (C + 2) + q]); };
+          while (true) {
+            bool moved = false;
+            while (true) {  // retreat a
+              int cp = ca, pp = pa - 1;
+              if (pp < s.lo[cp]) {
+                cp = ca - 1;
+                while (cp >= gA && s.lo[cp] >= s.hi[cp]) --cp;
+                if (cp < gA) break;
+                pp = s.hi[cp] - 1;
+              }
+              const int ip = ptidx(cp, pp), ia = ptidx(ca, pa), ib = ptidx(cb, pb);
+              if (convex3(P_y(ip), P_f(ip), P_y(ia), P_f(ia), P_y(ib), P_f(ib))) break;
+              s.hi[ca] = pa;
+              ca = cp;
+              pa = pp;
+              moved = true;
             }
-            const int ia = ptidx(ca, pa), ib = ptidx(cb, pb), iq = ptidx(cq, pq);
-            if (convex3(P_y(ia), P_f(ia), P_y(ib), P_f(ib), P_y(iq), P_f(iq))) break;
-            s.lo[cb] = pb + 1;
-            cb = cq;
-            pb = pq;
-            moved = true;
+            while (true) {  // advance b
+              int cq = cb, pq = pb + 1;
+              if (pq >= s.hi[cq]) {
+                cq = cb + 1;
+                while (cq < gE && s.lo[cq] >= s.hi[cq]) ++cq;
+                if (cq >= gE) break;
+                pq = s.lo[cq];
+              }
+              const int ia = ptidx(ca, pa), ib = ptidx(cb, pb), iq = ptidx(cq, pq);
+              if (convex3(P_y(ia), P_f(ia), P_y(ib), P_f(ib), P_y(iq), P_f(iq))) break;
+              s.lo[cb] = pb + 1;
+              cb = cq;
+              pb = pq;
+              moved = true;
+            }
+            if (!moved) break;
           }
-          if (!moved) break;
         }
       }
     }
-  }
-  group_sync(tpl, l);
-
-  // ---- 3. compaction into H ---------------------------------------------
-  {
-    const int cnt = active ? max(0, s.hi[t] - s.lo[t]) : 0;
-    const int lane = t & 31, w = t >> 5;
-    int v = cnt;
-    for (int d = 1; d < 32; d <<= 1) {
-      const int u = __shfl_up_sync(0xffffffffu, v, d);
-      if (lane >= d) v += u;
-    }
-    if (lane == 31) s.off[w] = v;
     group_sync(tpl, l);
-    int pre = 0;
-    for (int ww = 0; ww < w; ++ww) pre += s.off[ww];
-    const int o = pre + v - cnt;
-    for (int i = 0; i < cnt; ++i) s.H[o + i] = st[s.lo[t] + i];
-    if (t == tpl - 1) s.scal[3] = static_cast<unsigned long long>(o + cnt);
-  }
-  group_sync(tpl, l);
-  const int hsz = static_cast<int>(s.scal[3]);
-  BFM_DASSERT(!active || (hsz >= 1 && hsz <= n));
-
-  // ---- 4. suspects: non-corners within tau of their hull edge -----------
-  if (active && j0 < j1) {
-    int lo_e = 0, hi_e = hsz - 1;  // largest e with H[e] <= j0
-    while (lo_e < hi_e) {
-      const int mid = (lo_e + hi_e + 1) >> 1;
-      if (s.H[mid] <= j0) lo_e = mid;
-      else hi_e = mid - 1;
-    }
-    int e = lo_e;
-    double dloc = 0.0;
-    for (int j = j0; j < j1; ++j) {
-      while (e + 1 < hsz && s.H[e + 1] <= j) ++e;
-      const int ca = s.H[e];
-      if (ca == j || e + 1 >= hsz) continue;
-      const int cb = s.H[e + 1];
-      const double ya = P_y(ca), yb = P_y(cb), fa = P_f(ca), fb = P_f(cb);
-      const double tt = (P_y(j) - ya) / (yb - ya);
-      const double Lc = fa + (fb - fa) * tt;
-      const double dt = P_f(j) - Lc;
-      if (dt <= tau) {
-        s.flag[e] = 1;
-        dloc = fmax(dloc, tau - dt);
+    // ---- 3. compaction into H -------------------------------------------
+    {
+      const int cnt = active ? max(0, s.hi[t] - s.lo[t]) : 0;
+      const int lane = t & 31, w = t >> 5;
+      int v = cnt;
+      for (int d = 1; d < 32; d <<= 1) {
+        const int u = __shfl_up_sync(0xffffffffu, v, d);
+        if (lane >= d) v += u;
       }
+      if (lane == 31) s.off[w] = v;
+      group_sync(tpl, l);
+      int pre = 0;
+      for (int ww = 0; ww < w; ++ww) pre += s.off[ww];
+      const int o = pre + v - cnt;
+      for (int i = 0; i < cnt; ++i) s.H[o + i] = st[s.lo[t] + i];
+      if (t == tpl - 1) s.scal[3] = static_cast<unsigned long long>(o + cnt);
     }
-    if (dloc > 0.0) atomicMax(&s.scal[2], dbits(dloc));
+    group_sync(tpl, l);
+    // ---- 4. suspects: per-edge max slack (log-coded, conservative) --------
+    const int hsz0 = static_cast<int>(s.scal[3]);
+    if (active && j0 < j1) {
+      int lo_e = 0, hi_e = hsz0 - 1;  // largest e with H[e] <= j0
+      while (lo_e < hi_e) {
+        const int mid = (lo_e + hi_e + 1) >> 1;
+        if (s.H[mid] <= j0) lo_e = mid;
+        else hi_e = mid - 1;
+      }
+      int e = lo_e;
+      double dloc = 0.0;
+      int ecur = -1;
+      double emax = -1.0;
+      for (int j = j0; j < j1; ++j) {
+        while (e + 1 < hsz0 && s.H[e + 1] <= j) ++e;
+        const int ca = s.H[e];
+        if (ca == j || e + 1 >= hsz0) continue;
+        const int cb = s.H[e + 1];
+        const double ya = P_y(ca), yb = P_y(cb), fa = P_f(ca), fb = P_f(cb);
+        const double tt = (P_y(j) - ya) / (yb - ya);
+        const double Lc = fa + (fb - fa) * tt;
+        const double dt = P_f(j) - Lc;
+        if (dt <= tau) {
+          const double D = tau - dt;
+          dloc = fmax(dloc, D);
+          if (e != ecur) {
+            if (ecur >= 0) slack_max(s.dlt, ecur, slack_code(emax, sref));
+            ecur = e;
+            emax = D;
+          } else {
+            emax = fmax(emax, D);
+          }
+        }
+      }
+      if (ecur >= 0) slack_max(s.dlt, ecur, slack_code(emax, sref));
+      if (dloc > 0.0) atomicMax(&s.scal[2], dbits(dloc));
+    }
+    group_sync(tpl, l);
   }
-  group_sync(tpl, l);
-  const double dmax = bitsd(s.scal[2]);
-  const double Ms = 4.0 * e_F + dmax + 4.0 * e_r;
-  const double cmp_margin = 4.0 * e_F;
+  const int hsz = convex_line ? n : static_cast<int>(s.scal[3]);
+  BFM_DASSERT(!active || (hsz >= 1 && hsz <= n));
+  const double Dmax = convex_line ? 0.0 : bitsd(s.scal[2]);
+  const double Mw = Mc + Dmax;
   uint16_t* res = s.hidx;  // hidx is dead after compaction
+  auto HH = [&](int i) { return convex_line ? i : static_cast<int>(s.H[i]); };
   group_sync(tpl, l);
 
   // ---- 5. queries ---------------------------------------------------------
   if (active && j0 < j1) {
     auto Fhat = [&](int idx, double xk) { return P_f(idx) - xk * P_y(idx); };
     auto slope_ge = [&](int i, double xk) {
-      const int a = s.H[i], b = s.H[i + 1];
+      const int a = HH(i), b = HH(i + 1);
       return (P_f(b) - P_f(a)) >= xk * (P_y(b) - P_y(a));
+    };
+    // exact value V(k, j) rounded down (last pass)
+    auto rd_value = [&](int j, int k, double xk) {
+      if (DY) {
+        return bfmx::round_down2(dy_gsum(j, xk), -s.fh[padj(j)]);
+      } else {
+        double tv[12];
+        const uint32_t ch = p.a > 0 ? s.chain[j] : 0u;
+        const int m = cand_terms(p, geo, ch, j, k, tv);
+        return bfmx::round_down_sum(tv, m);
+      }
     };
     double xk = coord(h, j0);
     int lo_i = 0, hi_i = hsz - 1;
@@ -421,80 +491,105 @@ __global__ void __launch_bounds__(1024) ct_pass_kernel(CtPass p) {
     for (int k = j0; k < j1; ++k) {
       xk = coord(h, k);
       while (i < hsz - 1 && !slope_ge(i, xk)) ++i;
-      // descend to a local minimum of F^ over corners
       int L = i;
-      double Fmin = Fhat(s.H[L], xk);
+      double Fmin = Fhat(HH(L), xk);
       while (L > 0) {
-        const double Fl = Fhat(s.H[L - 1], xk);
+        const double Fl = Fhat(HH(L - 1), xk);
         if (Fl < Fmin) { --L; Fmin = Fl; } else break;
       }
       int R = L;
       if (L == i) {
         while (R < hsz - 1) {
-          const double Fr = Fhat(s.H[R + 1], xk);
+          const double Fr = Fhat(HH(R + 1), xk);
           if (Fr < Fmin) { ++R; Fmin = Fr; } else break;
         }
         L = R;
       }
-      // expand within the certified margin
       while (L > 0) {
-        const double Fl = Fhat(s.H[L - 1], xk);
-        if (Fl <= Fmin + Ms) { --L; Fmin = fmin(Fmin, Fl); } else break;
+        const double Fl = Fhat(HH(L - 1), xk);
+        if (Fl <= Fmin + Mw) { --L; Fmin = fmin(Fmin, Fl); } else break;
       }
       while (R < hsz - 1) {
-        const double Fr = Fhat(s.H[R + 1], xk);
-        if (Fr <= Fmin + Ms) { ++R; Fmin = fmin(Fmin, Fr); } else break;
+        const double Fr = Fhat(HH(R + 1), xk);
+        if (Fr <= Fmin + Mw) { ++R; Fmin = fmin(Fmin, Fr); } else break;
       }
-      const bool sus = (L > 0 && s.flag[L - 1]) || (R < hsz - 1 && s.flag[R]) ||
-                       (L < R);  // interior flags only matter with several corners
-      int win;
-      if (!sus) {
-        win = s.H[L];
-      } else {
-        // exact resolution over corners [L,R] + suspects of edges [L-1, R]
-        if (p.slow_queries) atomicAdd(p.slow_queries, 1ull);
+      int win = HH(L);
+      double outv = 0.0;
+      bool have_out = false;
+      if (!(L == R && convex_line)) {
         const int e0 = L > 0 ? L - 1 : 0;
-        const int e1 = R < hsz - 1 ? R + 1 : hsz - 1;
-        int best = -1;
-        double bestF = 0.0;
-        double bt[12];
-        int bm = 0;
-        auto consider = [&](int j) {
-          const double Fj = Fhat(j, xk);
-          if (best >= 0 && Fj - bestF > cmp_margin) return;
-          double ct[12];
-          const uint32_t ch = p.a > 0 ? s.chain[j] : 0u;
-          const int cm = cand_terms(p, geo, ch, j, k, ct);
-          if (best >= 0 && bfmx::sign_diff(ct, cm, bt, bm) >= 0) return;
-          best = j;
-          bestF = Fj;
-          for (int q = 0; q < cm; ++q) bt[q] = ct[q];
-          bm = cm;
-        };
-        for (int e = e0; e <= e1; ++e) {
-          const int c = s.H[e];
-          if (e >= L && e <= R) consider(c);
-          if (e < e1 && s.flag[e]) {
-            const int cb = s.H[e + 1];
-            const double ya = P_y(c), yb = P_y(cb), fa = P_f(c), fb = P_f(cb);
-            for (int j = c + 1; j < cb; ++j) {
-              const double tt = (P_y(j) - ya) / (yb - ya);
-              const double dt = P_f(j) - (fa + (fb - fa) * tt);
-              if (dt <= tau) consider(j);
-            }
+        const int e1 = R < hsz - 1 ? R : hsz - 2;
+        auto visit = [&](auto&& fn) {
+          for (int c = L; c <= R; ++c) fn(HH(c));
+          if (convex_line) return;
+          for (int e = e0; e <= e1; ++e) {
+            const uint8_t code = s.dlt[e];
+            if (code == 0) continue;
+            const int a = HH(e), b = HH(e + 1);
+            const double Fa = Fhat(a, xk), Fb = Fhat(b, xk);
+            const double slack = slack_value(code, sref) + Mc;
+            if (fmin(Fa, Fb) > Fmin + slack) continue;
+            if (fabs(Fa - Fb) > slack * (1.000001 * (b - a)) + Mc) continue;
+            for (int j = a + 1; j < b; ++j) fn(j);
           }
+        };
+        double Fbest = INFINITY;
+        visit([&](int j) { Fbest = fmin(Fbest, Fhat(j, xk)); });
+        if (p.last) {
+          // RD is monotone: RD(min_j V_j) = min_j RD(V_j); no exact argmin needed.
+          double best = INFINITY;
+          visit([&](int j) {
+            if (Fhat(j, xk) <= Fbest + Mc) best = fmin(best, rd_value(j, k, xk));
+          });
+          outv = best;
+          have_out = true;
+        } else if (DY) {
+          // exact: V_j = two_sum(Gsum_j, -phi_j) normalised; compare lexicographically
+          int bestj = -1;
+          double bh = 0.0, bl = 0.0;
+          visit([&](int j) {
+            if (Fhat(j, xk) > Fbest + Mc) return;
+            double vh, vl;
+            bfmx::two_sum(dy_gsum(j, xk), -s.fh[padj(j)], vh, vl);
+            if (bestj >= 0 && (vh > bh || (vh == bh && vl >= bl))) return;
+            bestj = j;
+            bh = vh;
+            bl = vl;
+          });
+          win = bestj;
+        } else {
+          int bestj = -1;
+          double bt[12];
+          int bm = 0;
+          visit([&](int j) {
+            if (Fhat(j, xk) > Fbest + Mc) return;
+            double ct[12];
+            const uint32_t ch = p.a > 0 ? s.chain[j] : 0u;
+            const int cm = cand_terms(p, geo, ch, j, k, ct);
+            if (bestj >= 0) {
+              if (p.slow_queries) atomicAdd(p.slow_queries, 1ull);
+              if (bfmx::sign_diff(ct, cm, bt, bm) >= 0) return;
+            }
+            bestj = j;
+            for (int q = 0; q < cm; ++q) bt[q] = ct[q];
+            bm = cm;
+          });
+          win = bestj;
         }
-        win = best;
       }
       BFM_DASSERT(win >= 0 && win < n);
-      res[k] = static_cast<uint16_t>(win);
+      if (p.last) {
+        if (!have_out) outv = rd_value(win, k, xk);
+        p.out[geo.base + static_cast<long>(k) * A.stride] = outv;
+      } else {
+        res[k] = static_cast<uint16_t>(win);
+      }
     }
   }
+  if (p.last) return;
   __syncthreads();
 
-  // ---- 6. write-out (coalesced) -------------------------------------------
-  const bool all_dyadic = p.ax[0].dyadic && (p.d < 2 || p.ax[1].dyadic) &&
-                          (p.d < 3 || p.ax[2].dyadic);
+  // ---- 6. intermediate passes: coalesced write of the argmin chain ---------
   for (int idx = threadIdx.x; idx < n * lpc; idx += blockDim.x) {
     int ll, k;
     if (p.strided) {
@@ -509,23 +604,14 @@ __global__ void __launch_bounds__(1024) ct_pass_kernel(CtPass p) {
     if (!g.valid) continue;
     const long node = g.base + static_cast<long>(k) * A.stride;
     const int win = sm.hidx[k];
-    const uint32_t ch = p.a > 0 ? sm.chain[win] : 0u;
-    if (!p.last) {
-      p.state_out[node] = p.a == 0 ? static_cast<uint32_t>(win)
-                                   : (ch | (static_cast<uint32_t>(win) << 16));
+    uint32_t packed;
+    if (p.a == 0) {
+      packed = static_cast<uint32_t>(win);
     } else {
-      double tv[12];
-      const int m = cand_terms(p, g, ch, win, k, tv);
-      double r;
-      if (all_dyadic) {
-        double G = 0.0;
-        for (int q = 1; q < m; ++q) G += tv[q];  // exact on dyadic grids
-        r = bfmx::round_down2(G, tv[0]);
-      } else {
-        r = bfmx::round_down_sum(tv, m);
-      }
-      p.out[node] = r;
+      const uint32_t ch = DY ? p.state_in[g.base + static_cast<long>(win) * A.stride] : sm.chain[win];
+      packed = ch | (static_cast<uint32_t>(win) << 16);
     }
+    p.state_out[node] = packed;
   }
 }
 
@@ -615,20 +701,22 @@ void CtPlan::init(const GridDesc& g) {
     for (int b = 0; b < g.d; ++b) P.ax[b] = ax_[b];
     const int n = g.n[a];
     P.nlines = g.size / n;
-    P.tpl = n <= 1024 ? 32 : (n <= 2048 ? 64 : 128);
+    P.tpl = n <= 512 ? 32 : (n <= 1024 ? 64 : (n <= 2048 ? 128 : 256));
     P.C = (n + P.tpl - 1) / P.tpl;
     P.strided = a != g.d - 1;
+    const bool dy = ax_[0].dyadic && (g.d < 2 || ax_[1].dyadic) && (g.d < 3 || ax_[2].dyadic);
     int o = 0;
     P.off_fv = o;
     o = align16(o + 8 * (n + n / 32 + 1));
-    P.off_chain = o;
-    if (a > 0) o = align16(o + 4 * n);
+    P.off_chain = o;  // DY: fl (double, padded); else chain (uint32)
+    if (dy) o = align16(o + 8 * (n + n / 32 + 1));
+    else if (a > 0) o = align16(o + 4 * n);
     P.off_hidx = o;
     o = align16(o + 2 * std::max(P.tpl * (P.C + 2), n));
     P.off_H = o;
     o = align16(o + 2 * n);
-    P.off_flag = o;
-    o = align16(o + n);
+    P.off_flag = o;  // per-edge slack code (uint8)
+    o = align16(o + n + 4);
     P.off_lohi = o;
     o = align16(o + 12 * P.tpl);
     P.off_scal = o;
@@ -642,8 +730,11 @@ void CtPlan::init(const GridDesc& g) {
     P.lpc = std::max(lpc, 1);
     P.slow_queries = slow_;
   }
-  BFM_CUDA(cudaFuncSetAttribute(ct_pass_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  BFM_CUDA(cudaFuncSetAttribute(ct_pass_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 budget));
+  BFM_CUDA(cudaFuncSetAttribute(ct_pass_kernel<false>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, budget));
+  dyadic_ = ax_[0].dyadic && (g.d < 2 || ax_[1].dyadic) && (g.d < 3 || ax_[2].dyadic);
   ready_ = true;
 }
 
@@ -655,8 +746,12 @@ void CtPlan::run(const double* d_phi, double* d_out, cudaStream_t stream, Launch
     P.state_out = P.last ? nullptr : state_[a & 1];
     P.out = d_out;
     const long blocks = (P.nlines + P.lpc - 1) / P.lpc;
-    ct_pass_kernel<<<static_cast<unsigned>(blocks), P.lpc * P.tpl, P.lpc * P.line_bytes,
-                     stream>>>(P);
+    if (dyadic_)
+      ct_pass_kernel<true><<<static_cast<unsigned>(blocks), P.lpc * P.tpl, P.lpc * P.line_bytes,
+                             stream>>>(P);
+    else
+      ct_pass_kernel<false><<<static_cast<unsigned>(blocks), P.lpc * P.tpl, P.lpc * P.line_bytes,
+                              stream>>>(P);
     BFM_LAUNCH_CHECK("ct_pass_kernel");
     if (lc) lc->add();
   }

@@ -56,6 +56,7 @@ class CtPlan {
   unsigned long long* slow_ = nullptr;
   CtPass pass_[3] = {};
   bool ready_ = false;
+  bool dyadic_ = false;
 };
 
 }  // namespace bfmgpu

@@ -27,6 +27,8 @@ constexpr int kScanItems = 8;
 constexpr int kScanThreads = 1024;
 constexpr int kScanTile = kScanItems * kScanThreads;
 constexpr int kSmallBucket = 64;
+constexpr int kLight = 48;
+constexpr int kChunk = 8192;
 
 struct MapArgs {
   GridDesc g;
@@ -253,14 +255,37 @@ __global__ void pf_sort_small_kernel(long N, const int* cnt, const int* off, int
 // One CTA per large bucket: bitonic sort in shared memory (capacity 32768).
 __global__ void __launch_bounds__(1024) pf_sort_big_kernel(const int* cnt, const int* off,
                                                            int* bucket, const int* big,
-                                                           const int* nbig, int* overflow) {
+                                                           const int* nbig, int* scratch) {
   extern __shared__ int sb[];
   const int nb = *nbig;
   for (int q = blockIdx.x; q < nb; q += gridDim.x) {
     const int c = big[q];
     const int k = cnt[c];
     if (k > 32768) {
-      if (threadIdx.x == 0) atomicExch(overflow, 1);
+      // Huge bucket: bitonic sort in a global scratch window [2*off, 2*off + p2).
+      int p2 = 1;
+      while (p2 < k) p2 <<= 1;
+      int* b = bucket + off[c];
+      int* sc = scratch + 2L * off[c];
+      for (int i = threadIdx.x; i < p2; i += blockDim.x) sc[i] = i < k ? b[i] : INT_MAX;
+      __syncthreads();
+      for (int size = 2; size <= p2; size <<= 1)
+        for (int stride = size >> 1; stride > 0; stride >>= 1) {
+          for (int i = threadIdx.x; i < p2; i += blockDim.x) {
+            const int j = i ^ stride;
+            if (j > i) {
+              const bool up = (i & size) == 0;
+              const int x = sc[i], y = sc[j];
+              if ((x > y) == up) {
+                sc[i] = y;
+                sc[j] = x;
+              }
+            }
+          }
+          __syncthreads();
+        }
+      for (int i = threadIdx.x; i < k; i += blockDim.x) b[i] = sc[i];
+      __syncthreads();
       continue;
     }
     int p2 = 1;
@@ -300,7 +325,19 @@ struct GatherArgs {
   double* out;
 };
 
-__global__ void pf_gather_kernel(GatherArgs A) {
+__device__ __forceinline__ double deposit_weight(const GatherArgs& A, int s, int b) {
+  double wt = A.src[s];
+  for (int a = 0; a < A.g.d; ++a) {
+    const double wh = A.w[a * A.g.size + s];
+    wt *= ((b >> a) & 1) ? wh : 1.0 - wh;
+  }
+  return wt;
+}
+
+// Light targets: merge the <= 2^d sorted neighbouring buckets by source id
+// and fold in place. Targets with more than kLight deposits are deferred to
+// pf_gather_heavy_kernel.
+__global__ void pf_gather_kernel(GatherArgs A, int* heavy, int* nheavy) {
   const GridDesc& g = A.g;
   const int corners = 1 << g.d;
   for (long t = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; t < g.size;
@@ -310,6 +347,7 @@ __global__ void pf_gather_kernel(GatherArgs A) {
     int pos[8], end[8];
     int nl = 0;
     int bits[8];
+    int total = 0;
     for (int b = 0; b < corners; ++b) {
       long c = t;
       bool ok = true;
@@ -324,7 +362,12 @@ __global__ void pf_gather_kernel(GatherArgs A) {
       pos[nl] = A.off[c];
       end[nl] = pos[nl] + k;
       bits[nl] = b;
+      total += k;
       ++nl;
+    }
+    if (total > kLight) {
+      heavy[atomicAdd(nheavy, 1)] = static_cast<int>(t);
+      continue;
     }
     double rho = 0.0;
     while (true) {
@@ -341,14 +384,141 @@ __global__ void pf_gather_kernel(GatherArgs A) {
       ++pos[best];
       const int b = bits[best];
       if (b & A.cmask[bs]) continue;  // clamped axis: upper corner has weight 0
-      double wt = A.src[bs];
-      for (int a = 0; a < g.d; ++a) {
-        const double wh = A.w[a * g.size + bs];
-        wt *= ((b >> a) & 1) ? wh : 1.0 - wh;
-      }
+      const double wt = deposit_weight(A, bs, b);
       if (wt != 0.0) rho += wt;
     }
     A.out[t] = A.target ? A.target[t] - rho : rho;
+  }
+}
+
+// Heavy targets: one CTA each. The merged source order is produced chunk by
+// chunk (source-id ranges holding <= kChunk deposits), sorted in shared
+// memory, weighted in parallel, then folded by one thread in order.
+__global__ void __launch_bounds__(512) pf_gather_heavy_kernel(GatherArgs A, const int* heavy,
+                                                             const int* nheavy) {
+  extern __shared__ __align__(16) unsigned char sm[];
+  unsigned* key = reinterpret_cast<unsigned*>(sm);                 // [kChunk]
+  double* wv = reinterpret_cast<double*>(sm + 4 * kChunk);           // [kChunk]
+  __shared__ int s_pos[8], s_end[8], s_bits[8], s_take[8], s_nl, s_cnt;
+  __shared__ long s_lim;
+  __shared__ double s_rho;
+  const GridDesc& g = A.g;
+  const int corners = 1 << g.d;
+  const int nh = *nheavy;
+  for (int q = blockIdx.x; q < nh; q += gridDim.x) {
+    const long t = heavy[q];
+    if (threadIdx.x == 0) {
+      int id[3] = {0, 0, 0};
+      node_idx(g, t, id);
+      int nl = 0;
+      for (int b = 0; b < corners; ++b) {
+        long c = t;
+        bool ok = true;
+        for (int a = 0; a < g.d; ++a)
+          if ((b >> a) & 1) {
+            if (id[a] == 0) ok = false;
+            c -= g.stride[a];
+          }
+        if (!ok) continue;
+        const int k = A.cnt[c];
+        if (k == 0) continue;
+        s_pos[nl] = A.off[c];
+        s_end[nl] = s_pos[nl] + k;
+        s_bits[nl] = b;
+        ++nl;
+      }
+      s_nl = nl;
+      s_rho = 0.0;
+    }
+    __syncthreads();
+    while (true) {
+      if (threadIdx.x == 0) {
+        // largest source-id bound lim with <= kChunk pending deposits below it
+        long lo = -1, hi = g.size;  // invariant: count(<= lo) <= kChunk
+        int remaining = 0;
+        for (int b = 0; b < s_nl; ++b) remaining += s_end[b] - s_pos[b];
+        if (remaining <= kChunk) {
+          lo = g.size;
+        } else {
+          while (hi - lo > 1) {
+            const long mid = (lo + hi) / 2;
+            int c = 0;
+            for (int b = 0; b < s_nl; ++b) {
+              int l2 = s_pos[b], h2 = s_end[b];  // upper_bound of mid
+              while (l2 < h2) {
+                const int m2 = (l2 + h2) >> 1;
+                if (A.bucket[m2] <= mid) l2 = m2 + 1;
+                else h2 = m2;
+              }
+              c += l2 - s_pos[b];
+            }
+            if (c <= kChunk) lo = mid;
+            else hi = mid;
+          }
+        }
+        s_lim = lo;
+        int c = 0;
+        for (int b = 0; b < s_nl; ++b) {
+          int l2 = s_pos[b], h2 = s_end[b];
+          while (l2 < h2) {
+            const int m2 = (l2 + h2) >> 1;
+            if (A.bucket[m2] <= lo) l2 = m2 + 1;
+            else h2 = m2;
+          }
+          s_take[b] = c;
+          c += l2 - s_pos[b];
+        }
+        s_cnt = c;
+      }
+      __syncthreads();
+      const int cnt = s_cnt;
+      if (cnt == 0) break;
+      int p2 = 1;
+      while (p2 < cnt) p2 <<= 1;
+      // gather (source << 3 | corner) keys of this chunk
+      for (int b = 0; b < s_nl; ++b) {
+        const int nb = (b + 1 < s_nl ? s_take[b + 1] : cnt) - s_take[b];
+        for (int i = threadIdx.x; i < nb; i += blockDim.x)
+          key[s_take[b] + i] = (static_cast<unsigned>(A.bucket[s_pos[b] + i]) << 3) |
+                               static_cast<unsigned>(s_bits[b]);
+      }
+      for (int i = cnt + threadIdx.x; i < p2; i += blockDim.x) key[i] = 0xffffffffu;
+      __syncthreads();
+      for (int size = 2; size <= p2; size <<= 1)
+        for (int stride = size >> 1; stride > 0; stride >>= 1) {
+          for (int i = threadIdx.x; i < p2; i += blockDim.x) {
+            const int j = i ^ stride;
+            if (j > i) {
+              const bool up = (i & size) == 0;
+              const unsigned x = key[i], y = key[j];
+              if ((x > y) == up) {
+                key[i] = y;
+                key[j] = x;
+              }
+            }
+          }
+          __syncthreads();
+        }
+      for (int i = threadIdx.x; i < cnt; i += blockDim.x) {
+        const int src = static_cast<int>(key[i] >> 3);
+        const int b = static_cast<int>(key[i] & 7u);
+        wv[i] = (b & A.cmask[src]) ? 0.0 : deposit_weight(A, src, b);
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        double rho = s_rho;
+        for (int i = 0; i < cnt; ++i) {
+          const double w = wv[i];
+          if (w != 0.0) rho += w;
+        }
+        s_rho = rho;
+        for (int b = 0; b < s_nl; ++b)
+          s_pos[b] += (b + 1 < s_nl ? s_take[b + 1] : cnt) - s_take[b];
+      }
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) A.out[t] = A.target ? A.target[t] - s_rho : s_rho;
+    __syncthreads();
   }
 }
 
@@ -366,7 +536,8 @@ PushforwardPlan::~PushforwardPlan() {
   for (void* p : {static_cast<void*>(key_), static_cast<void*>(cmask_), static_cast<void*>(w_),
                   static_cast<void*>(cnt_), static_cast<void*>(off_), static_cast<void*>(fill_),
                   static_cast<void*>(bucket_), static_cast<void*>(blocksum_),
-                  static_cast<void*>(big_), static_cast<void*>(nbig_)})
+                  static_cast<void*>(big_), static_cast<void*>(nbig_),
+                  static_cast<void*>(scratch_)})
     if (p) cudaFree(p);
 }
 
@@ -384,9 +555,12 @@ void PushforwardPlan::init(const GridDesc& g) {
   scan_blocks_ = (N + kScanTile - 1) / kScanTile;
   BFM_CUDA(cudaMalloc(&blocksum_, (scan_blocks_ + 1) * sizeof(int)));
   BFM_CUDA(cudaMalloc(&big_, N * sizeof(int)));
-  BFM_CUDA(cudaMalloc(&nbig_, 2 * sizeof(int)));
+  BFM_CUDA(cudaMalloc(&scratch_, 2 * (N + 1) * sizeof(int)));
+  BFM_CUDA(cudaMalloc(&nbig_, 4 * sizeof(int)));
   BFM_CUDA(cudaFuncSetAttribute(pf_sort_big_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 32768 * 4));
+  BFM_CUDA(cudaFuncSetAttribute(pf_gather_heavy_kernel,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, kChunk * 12));
 }
 
 void PushforwardPlan::map_only(const double* d_u, double* d_disp, cudaStream_t stream,
@@ -414,7 +588,7 @@ void PushforwardPlan::bin_and_gather(const double* d_source, const double* d_tar
   pf_place_kernel<<<grid_for(N, 256), 256, 0, stream>>>(N, key_, off_, fill_, bucket_);
   pf_sort_small_kernel<<<grid_for(N, 256), 256, 0, stream>>>(N, cnt_, off_, bucket_, big_, nbig_);
   pf_sort_big_kernel<<<148, 1024, 32768 * 4, stream>>>(cnt_, off_, bucket_, big_, nbig_,
-                                                       nbig_ + 1);
+                                                       scratch_);
   GatherArgs G{};
   G.g = g_;
   G.cnt = cnt_;
@@ -425,9 +599,11 @@ void PushforwardPlan::bin_and_gather(const double* d_source, const double* d_tar
   G.src = d_source;
   G.target = d_target;
   G.out = d_out;
-  pf_gather_kernel<<<grid_for(N, 256), 256, 0, stream>>>(G);
+  pf_gather_kernel<<<grid_for(N, 256), 256, 0, stream>>>(G, big_, nbig_ + 2);
   BFM_LAUNCH_CHECK("pf_gather_kernel");
-  if (lc) lc->add(7);
+  pf_gather_heavy_kernel<<<148 * 2, 512, kChunk * 12, stream>>>(G, big_, nbig_ + 2);
+  BFM_LAUNCH_CHECK("pf_gather_heavy_kernel");
+  if (lc) lc->add(8);
 }
 
 void PushforwardPlan::from_potential(const double* d_u, const double* d_source,
@@ -436,7 +612,7 @@ void PushforwardPlan::from_potential(const double* d_u, const double* d_source,
   const long N = g_.size;
   BFM_CUDA(cudaMemsetAsync(cnt_, 0, (N + 1) * sizeof(int), stream));
   BFM_CUDA(cudaMemsetAsync(fill_, 0, N * sizeof(int), stream));
-  BFM_CUDA(cudaMemsetAsync(nbig_, 0, 2 * sizeof(int), stream));
+  BFM_CUDA(cudaMemsetAsync(nbig_, 0, 4 * sizeof(int), stream));
   MapArgs A{};
   A.g = g_;
   A.u = d_u;
@@ -460,7 +636,7 @@ void PushforwardPlan::from_displacement(const double* d_disp, double scale,
   const long N = g_.size;
   BFM_CUDA(cudaMemsetAsync(cnt_, 0, (N + 1) * sizeof(int), stream));
   BFM_CUDA(cudaMemsetAsync(fill_, 0, N * sizeof(int), stream));
-  BFM_CUDA(cudaMemsetAsync(nbig_, 0, 2 * sizeof(int), stream));
+  BFM_CUDA(cudaMemsetAsync(nbig_, 0, 4 * sizeof(int), stream));
   MapArgs A{};
   A.g = g_;
   A.disp = d_disp;

@@ -42,6 +42,7 @@ class PushforwardPlan {
   int* blocksum_ = nullptr;  // scan scratch
   int* big_ = nullptr;       // [N] cells with large buckets
   int* nbig_ = nullptr;
+  int* scratch_ = nullptr;   // [2N+2] huge-bucket sort windows
   long scan_blocks_ = 0;
 };
 
