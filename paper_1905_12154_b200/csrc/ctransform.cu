@@ -48,6 +48,14 @@ constexpr double kU = 1.1102230246251565e-16;  // 2^-53
 
 __device__ __forceinline__ int padj(int j) { return j + (j >> 5); }
 
+__device__ __forceinline__ void cp_async8(void* smem_dst, const void* gmem_src) {
+  const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem_dst));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gmem_src) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.wait_all;\n" ::: "memory");
+}
+
 __device__ __forceinline__ void group_sync(int tpl, int l) {
   if (tpl <= 32) {
     __syncwarp();
@@ -221,9 +229,10 @@ __global__ void __launch_bounds__(1024) ct_pass_kernel(CtPass p) {
   }
   __syncthreads();
 
-  // ---- load (4 independent elements per thread iteration for ILP) --------
+  // ---- load: every element copied asynchronously (cp.async) -------------
+  // DY: fh <- phi_j (exact), fl <- G_j = sum_{b<a} g_b(k_b, j_b*) (exact);
+  // !DY: fh <- f~_j, chain <- chain_j.
   {
-    double amax = 0.0, smax = 0.0;
     const int ml = p.strided ? static_cast<int>(threadIdx.x % lpc) : l;
     const Smem sm = carve(p, smem, ml);
     const LineGeo g = *sm.geo;
@@ -231,48 +240,75 @@ __global__ void __launch_bounds__(1024) ct_pass_kernel(CtPass p) {
     const int first = p.strided ? static_cast<int>(threadIdx.x / lpc) : t;
     for (int j = first; j < n + 4; j += step) sm.dlt[j] = 0;
     if (g.valid) {
-      for (int j0 = first; j0 < n; j0 += 4 * step) {
-        uint32_t ch[4] = {0u, 0u, 0u, 0u};
-        double ph[4];
+      if (p.a == 0 && DY) {
+        for (int j = first; j < n; j += step)
+          cp_async8(&sm.fh[padj(j)], &p.phi[g.phi_other + static_cast<long>(j) * A.stride]);
+      } else {
+        constexpr int kBatch = 8;
+        for (int j0 = first; j0 < n; j0 += kBatch * step) {
+          uint32_t ch[kBatch];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int j = j0 + u * step;
-          if (p.a > 0 && j < n) ch[u] = p.state_in[g.base + static_cast<long>(j) * A.stride];
-        }
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int j = j0 + u * step;
-          ph[u] = j < n ? p.phi[phi_index(p, g, ch[u], j)] : 0.0;
-        }
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int j = j0 + u * step;
-          if (j >= n) continue;
-          const double y = coord(h, j);
-          const double hy = 0.5 * y * y;
-          double B;
-          double G = 0.0;
-          if (p.a >= 1) G += g_approx(p.ax[0], g.k[0], static_cast<int>(ch[u] & 0xFFFFu));
-          if (p.a >= 2) G += g_approx(p.ax[1], g.k[1], static_cast<int>(ch[u] >> 16));
-          double f;
-          if (DY) {
-            // exact on dyadic grids: f_j = (G + hs(y_j)) - phi_j, G exact
-            B = G + hy;
-            f = B - ph[u];
-            sm.fh[padj(j)] = ph[u];
-            if (p.a > 0) sm.fl[padj(j)] = G;
-          } else {
-            f = (-ph[u] + G) + hy;
-            if (p.a > 0) sm.chain[j] = ch[u];
-            sm.fh[padj(j)] = f;
+          for (int u = 0; u < kBatch; ++u) {
+            const int j = j0 + u * step;
+            ch[u] = (p.a > 0 && j < n) ? p.state_in[g.base + static_cast<long>(j) * A.stride] : 0u;
           }
-          amax = fmax(amax, fabs(f));
-          smax = fmax(smax, fabs(ph[u]) + G + hy);
+#pragma unroll
+          for (int u = 0; u < kBatch; ++u) {
+            const int j = j0 + u * step;
+            if (j >= n) continue;
+            double G = 0.0;
+            if (p.a >= 1) G += g_approx(p.ax[0], g.k[0], static_cast<int>(ch[u] & 0xFFFFu));
+            if (p.a >= 2) G += g_approx(p.ax[1], g.k[1], static_cast<int>(ch[u] >> 16));
+            const double* src = &p.phi[phi_index(p, g, ch[u], j)];
+            cp_async8(&sm.fh[padj(j)], src);
+            if (DY) {
+              if (p.a > 0) sm.fl[padj(j)] = G;
+            } else {
+              if (p.a > 0) sm.chain[j] = ch[u];
+            }
+          }
         }
       }
     }
-    atomicMax(&sm.scal[0], dbits(amax));
-    atomicMax(&sm.scal[1], dbits(smax));
+    cp_async_wait_all();
+  }
+  __syncthreads();
+  // line maxima for the rounding bounds (A = max |f~|, Smax = max |phi| + G + hs)
+  {
+    double amax = 0.0, smax = 0.0;
+    const LineGeo g = *s.geo;
+    if (g.valid) {
+      for (int j = t; j < n; j += tpl) {
+        const double y = coord(h, j);
+        const double hy = 0.5 * y * y;
+        double f, S;
+        if (DY) {
+          const double ph = s.fh[padj(j)];
+          const double G = p.a > 0 ? s.fl[padj(j)] : 0.0;
+          f = (G + hy) - ph;
+          S = fabs(ph) + G + hy;
+        } else {
+          const double ph = s.fh[padj(j)];
+          const uint32_t ch = p.a > 0 ? s.chain[j] : 0u;
+          double G = 0.0;
+          if (p.a >= 1) G += g_approx(p.ax[0], g.k[0], static_cast<int>(ch & 0xFFFFu));
+          if (p.a >= 2) G += g_approx(p.ax[1], g.k[1], static_cast<int>(ch >> 16));
+          f = (-ph + G) + hy;
+          s.fh[padj(j)] = f;
+          S = fabs(ph) + G + hy;
+        }
+        amax = fmax(amax, fabs(f));
+        smax = fmax(smax, S);
+      }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      amax = fmax(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+      smax = fmax(smax, __shfl_xor_sync(0xffffffffu, smax, o));
+    }
+    if ((threadIdx.x & 31) == 0) {
+      atomicMax(&s.scal[0], dbits(amax));
+      atomicMax(&s.scal[1], dbits(smax));
+    }
   }
   __syncthreads();
 
@@ -709,8 +745,8 @@ void CtPlan::init(const GridDesc& g) {
     P.off_fv = o;
     o = align16(o + 8 * (n + n / 32 + 1));
     P.off_chain = o;  // DY: fl (double, padded); else chain (uint32)
-    if (dy) o = align16(o + 8 * (n + n / 32 + 1));
-    else if (a > 0) o = align16(o + 4 * n);
+    if (dy && a > 0) o = align16(o + 8 * (n + n / 32 + 1));
+    else if (!dy && a > 0) o = align16(o + 4 * n);
     P.off_hidx = o;
     o = align16(o + 2 * std::max(P.tpl * (P.C + 2), n));
     P.off_H = o;

@@ -19,6 +19,7 @@
 #include <climits>
 
 #include "pushforward.cuh"
+#include <cmath>
 
 namespace bfmgpu {
 namespace {
@@ -26,9 +27,9 @@ namespace {
 constexpr int kScanItems = 8;
 constexpr int kScanThreads = 1024;
 constexpr int kScanTile = kScanItems * kScanThreads;
-constexpr int kSmallBucket = 64;
 constexpr int kLight = 48;
-constexpr int kChunk = 8192;
+constexpr int kFoldChunk = 8192;
+constexpr int kMedium = 4096;
 
 struct MapArgs {
   GridDesc g;
@@ -36,11 +37,11 @@ struct MapArgs {
   const double* disp;   // displacement (mode 1)
   double scale;
   const double* src;    // source density
-  int* key;
+  uint32_t* key;        // cell of the lo corner; sentinel = N for massless sources
   uint8_t* cmask;
   double* w;
   double* disp_out;     // optional
-  int* cnt;             // optional (null: map only)
+  int binning;          // 0: map only
   double diam;          // sqrt(d)
 };
 
@@ -111,10 +112,10 @@ __global__ void pf_map_kernel(MapArgs A) {
         dsp[a] = A.disp[a * g.size + s];
       }
     }
-    if (!A.cnt) continue;
+    if (!A.binning) continue;
     const double m = A.src[s];
     if (m == 0.0) {
-      A.key[s] = -1;
+      A.key[s] = static_cast<uint32_t>(g.size);
       continue;
     }
     long key = 0;
@@ -130,192 +131,25 @@ __global__ void pf_map_kernel(MapArgs A) {
       if (cl) mask |= static_cast<uint8_t>(1u << a);
       A.w[a * g.size + s] = whi;
     }
-    A.key[s] = static_cast<int>(key);
+    A.key[s] = static_cast<uint32_t>(key);
     A.cmask[s] = mask;
-    atomicAdd(&A.cnt[key], 1);
   }
 }
 
-// ---- exclusive scan of int counts (3 kernels) ----
-__global__ void __launch_bounds__(kScanThreads) scan_reduce_kernel(const int* in, long n, int* bsum) {
-  __shared__ int warp_tot[32];
-  const long base = static_cast<long>(blockIdx.x) * kScanTile;
-  int v = 0;
-  for (int i = 0; i < kScanItems; ++i) {
-    const long idx = base + static_cast<long>(i) * kScanThreads + threadIdx.x;
-    if (idx < n) v += in[idx];
-  }
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
-  if ((threadIdx.x & 31) == 0) warp_tot[threadIdx.x >> 5] = v;
-  __syncthreads();
-  if (threadIdx.x < 32) {
-    int w = warp_tot[threadIdx.x];
-    for (int o = 16; o > 0; o >>= 1) w += __shfl_down_sync(0xffffffffu, w, o);
-    if (threadIdx.x == 0) bsum[blockIdx.x] = w;
-  }
-}
-
-__device__ int block_exclusive_scan(int v, int* total) {
-  __shared__ int warp_tot[32];
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  int incl = v;
-  for (int d = 1; d < 32; d <<= 1) {
-    const int u = __shfl_up_sync(0xffffffffu, incl, d);
-    if (lane >= d) incl += u;
-  }
-  if (lane == 31) warp_tot[w] = incl;
-  __syncthreads();
-  if (w == 0) {
-    int t = lane < (blockDim.x >> 5) ? warp_tot[lane] : 0;
-    int ti = t;
-    for (int d = 1; d < 32; d <<= 1) {
-      const int u = __shfl_up_sync(0xffffffffu, ti, d);
-      if (lane >= d) ti += u;
-    }
-    warp_tot[lane] = ti - t;
-    if (lane == 31) *total = ti;
-  }
-  __syncthreads();
-  const int r = warp_tot[w] + incl - v;
-  __syncthreads();
-  return r;
-}
-
-__global__ void __launch_bounds__(kScanThreads) scan_blocks_kernel(int* bsum, long nb) {
-  __shared__ int carry_s;
-  __shared__ int tot_s;
-  if (threadIdx.x == 0) carry_s = 0;
-  __syncthreads();
-  for (long base = 0; base < nb; base += kScanThreads) {
-    const long idx = base + threadIdx.x;
-    const int v = idx < nb ? bsum[idx] : 0;
-    const int ex = block_exclusive_scan(v, &tot_s);
-    if (idx < nb) bsum[idx] = carry_s + ex;
-    __syncthreads();
-    if (threadIdx.x == 0) carry_s += tot_s;
-    __syncthreads();
-  }
-}
-
-__global__ void __launch_bounds__(kScanThreads) scan_apply_kernel(const int* in, int* out, long n,
-                                                                  const int* bsum) {
-  __shared__ int tot_s;
-  const long base = static_cast<long>(blockIdx.x) * kScanTile;
-  int carry = bsum[blockIdx.x];
-  // each thread owns kScanItems consecutive elements
-  const long mine = base + static_cast<long>(threadIdx.x) * kScanItems;
-  int vals[kScanItems];
-  int sum = 0;
-  for (int i = 0; i < kScanItems; ++i) {
-    const long idx = mine + i;
-    vals[i] = idx < n ? in[idx] : 0;
-    sum += vals[i];
-  }
-  int ex = block_exclusive_scan(sum, &tot_s) + carry;
-  for (int i = 0; i < kScanItems; ++i) {
-    const long idx = mine + i;
-    if (idx < n) out[idx] = ex;
-    ex += vals[i];
-  }
-}
-
-__global__ void pf_place_kernel(long N, const int* key, const int* off, int* fill, int* bucket) {
-  for (long s = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; s < N;
-       s += static_cast<long>(gridDim.x) * blockDim.x) {
-    const int k = key[s];
-    if (k < 0) continue;
-    const int slot = off[k] + atomicAdd(&fill[k], 1);
-    bucket[slot] = static_cast<int>(s);
-  }
-}
-
-__global__ void pf_sort_small_kernel(long N, const int* cnt, const int* off, int* bucket,
-                                     int* big, int* nbig) {
-  for (long c = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; c < N;
-       c += static_cast<long>(gridDim.x) * blockDim.x) {
-    const int k = cnt[c];
-    if (k < 2) continue;
-    if (k > kSmallBucket) {
-      big[atomicAdd(nbig, 1)] = static_cast<int>(c);
-      continue;
-    }
-    int* b = bucket + off[c];
-    for (int i = 1; i < k; ++i) {
-      const int v = b[i];
-      int j = i - 1;
-      while (j >= 0 && b[j] > v) {
-        b[j + 1] = b[j];
-        --j;
-      }
-      b[j + 1] = v;
-    }
-  }
-}
-
-// One CTA per large bucket: bitonic sort in shared memory (capacity 32768).
-__global__ void __launch_bounds__(1024) pf_sort_big_kernel(const int* cnt, const int* off,
-                                                           int* bucket, const int* big,
-                                                           const int* nbig, int* scratch) {
-  extern __shared__ int sb[];
-  const int nb = *nbig;
-  for (int q = blockIdx.x; q < nb; q += gridDim.x) {
-    const int c = big[q];
-    const int k = cnt[c];
-    if (k > 32768) {
-      // Huge bucket: bitonic sort in a global scratch window [2*off, 2*off + p2).
-      int p2 = 1;
-      while (p2 < k) p2 <<= 1;
-      int* b = bucket + off[c];
-      int* sc = scratch + 2L * off[c];
-      for (int i = threadIdx.x; i < p2; i += blockDim.x) sc[i] = i < k ? b[i] : INT_MAX;
-      __syncthreads();
-      for (int size = 2; size <= p2; size <<= 1)
-        for (int stride = size >> 1; stride > 0; stride >>= 1) {
-          for (int i = threadIdx.x; i < p2; i += blockDim.x) {
-            const int j = i ^ stride;
-            if (j > i) {
-              const bool up = (i & size) == 0;
-              const int x = sc[i], y = sc[j];
-              if ((x > y) == up) {
-                sc[i] = y;
-                sc[j] = x;
-              }
-            }
-          }
-          __syncthreads();
-        }
-      for (int i = threadIdx.x; i < k; i += blockDim.x) b[i] = sc[i];
-      __syncthreads();
-      continue;
-    }
-    int p2 = 1;
-    while (p2 < k) p2 <<= 1;
-    int* b = bucket + off[c];
-    for (int i = threadIdx.x; i < p2; i += blockDim.x) sb[i] = i < k ? b[i] : INT_MAX;
-    __syncthreads();
-    for (int size = 2; size <= p2; size <<= 1)
-      for (int stride = size >> 1; stride > 0; stride >>= 1) {
-        for (int i = threadIdx.x; i < p2; i += blockDim.x) {
-          const int j = i ^ stride;
-          if (j > i) {
-            const bool up = (i & size) == 0;
-            const int x = sb[i], y = sb[j];
-            if ((x > y) == up) {
-              sb[i] = y;
-              sb[j] = x;
-            }
-          }
-        }
-        __syncthreads();
-      }
-    for (int i = threadIdx.x; i < k; i += blockDim.x) b[i] = sb[i];
-    __syncthreads();
+// Bucket boundaries of the sorted (cell, source) pairs: off[c] = first, end[c] = one past last.
+__global__ void pf_bounds_kernel(const uint32_t* keys, long n, uint32_t sentinel, int* off, int* end) {
+  for (long i = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<long>(gridDim.x) * blockDim.x) {
+    const uint32_t k = keys[i];
+    if (k == sentinel) continue;
+    if (i == 0 || keys[i - 1] != k) off[k] = static_cast<int>(i);
+    if (i == n - 1 || keys[i + 1] != k) end[k] = static_cast<int>(i + 1);
   }
 }
 
 struct GatherArgs {
   GridDesc g;
-  const int* cnt;
+  const int* end;
   const int* off;
   const int* bucket;
   const uint8_t* cmask;
@@ -357,8 +191,8 @@ __global__ void pf_gather_kernel(GatherArgs A, int* heavy, int* nheavy) {
           c -= g.stride[a];
         }
       if (!ok) continue;
-      const int k = A.cnt[c];
-      if (k == 0) continue;
+      const int k = A.end[c] - A.off[c];
+      if (k <= 0) continue;
       pos[nl] = A.off[c];
       end[nl] = pos[nl] + k;
       bits[nl] = b;
@@ -366,7 +200,8 @@ __global__ void pf_gather_kernel(GatherArgs A, int* heavy, int* nheavy) {
       ++nl;
     }
     if (total > kLight) {
-      heavy[atomicAdd(nheavy, 1)] = static_cast<int>(t);
+      if (total <= kMedium) heavy[atomicAdd(nheavy, 1)] = static_cast<int>(t);
+      else heavy[g.size - 1 - atomicAdd(nheavy + 1, 1)] = static_cast<int>(t);  // huge: from the top
       continue;
     }
     double rho = 0.0;
@@ -391,26 +226,98 @@ __global__ void pf_gather_kernel(GatherArgs A, int* heavy, int* nheavy) {
   }
 }
 
-// Heavy targets: one CTA each. The merged source order is produced chunk by
-// chunk (source-id ranges holding <= kChunk deposits), sorted in shared
-// memory, weighted in parallel, then folded by one thread in order.
-__global__ void __launch_bounds__(512) pf_gather_heavy_kernel(GatherArgs A, const int* heavy,
-                                                             const int* nheavy) {
-  extern __shared__ __align__(16) unsigned char sm[];
-  unsigned* key = reinterpret_cast<unsigned*>(sm);                 // [kChunk]
-  double* wv = reinterpret_cast<double*>(sm + 4 * kChunk);           // [kChunk]
-  __shared__ int s_pos[8], s_end[8], s_bits[8], s_take[8], s_nl, s_cnt;
-  __shared__ long s_lim;
-  __shared__ double s_rho;
+// Medium targets (kLight < K <= kMedium): one warp each; lanes rank and weight
+// the deposits into the global buffer, then lane 0 folds them in order while
+// the warp streams 32 at a time through shuffles.
+__global__ void __launch_bounds__(256) pf_gather_medium_kernel(GatherArgs A, const int* heavy,
+                                                              const int* nheavy, double* hbuf,
+                                                              unsigned long long* hfill) {
   const GridDesc& g = A.g;
   const int corners = 1 << g.d;
-  const int nh = *nheavy;
-  for (int q = blockIdx.x; q < nh; q += gridDim.x) {
+  const int nh = nheavy[0];
+  const int lane = threadIdx.x & 31;
+  const long warp0 = (static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const long nwarps = (static_cast<long>(gridDim.x) * blockDim.x) >> 5;
+  for (long q = warp0; q < nh; q += nwarps) {
     const long t = heavy[q];
+    int id[3] = {0, 0, 0};
+    node_idx(g, t, id);
+    int pos[8], endp[8], bits[8];
+    int nl = 0, K = 0;
+    for (int b = 0; b < corners; ++b) {
+      long c = t;
+      bool ok = true;
+      for (int a = 0; a < g.d; ++a)
+        if ((b >> a) & 1) {
+          if (id[a] == 0) ok = false;
+          c -= g.stride[a];
+        }
+      if (!ok) continue;
+      const int k = A.end[c] - A.off[c];
+      if (k <= 0) continue;
+      pos[nl] = A.off[c];
+      endp[nl] = A.end[c];
+      bits[nl] = b;
+      K += k;
+      ++nl;
+    }
+    unsigned long long base = 0;
+    if (lane == 0) base = atomicAdd(hfill, static_cast<unsigned long long>(K));
+    base = __shfl_sync(0xffffffffu, base, 0);
+    double* buf = hbuf + base;
+    for (int qq = 0; qq < nl; ++qq) {
+      for (int i = pos[qq] + lane; i < endp[qq]; i += 32) {
+        const int src = A.bucket[i];
+        int fin = i - pos[qq];
+        for (int o = 0; o < nl; ++o) {
+          if (o == qq) continue;
+          int lo = pos[o], hi = endp[o];
+          while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (A.bucket[mid] < src) lo = mid + 1;
+            else hi = mid;
+          }
+          fin += lo - pos[o];
+        }
+        buf[fin] = (bits[qq] & A.cmask[src]) ? 0.0 : deposit_weight(A, src, bits[qq]);
+      }
+    }
+    __syncwarp();
+    double rho = 0.0;
+    for (int c = 0; c < K; c += 32) {
+      const double v = c + lane < K ? buf[c + lane] : 0.0;
+      const int m = min(32, K - c);
+      for (int i = 0; i < m; ++i) {
+        const double w = __shfl_sync(0xffffffffu, v, i);
+        if (w != 0.0) rho += w;
+      }
+    }
+    if (lane == 0) A.out[t] = A.target ? A.target[t] - rho : rho;
+  }
+}
+
+// Heavy targets: one CTA each. Every deposit's position in the source-ordered
+// merge of the <= 2^d sorted neighbouring buckets is its index in its own
+// bucket plus its rank (lower_bound) in each other bucket (a source lives in
+// exactly one bucket, so there are no ties). Weights are written to those
+// positions in a global buffer in parallel; one thread then folds them in
+// order from 0.0 exactly like the reference's sequential +=.
+__global__ void __launch_bounds__(512) pf_gather_heavy_kernel(GatherArgs A, const int* heavy,
+                                                             const int* nheavy, double* hbuf,
+                                                             unsigned long long* hfill) {
+  __shared__ int s_pos[8], s_end[8], s_bits[8], s_nl, s_K;
+  __shared__ unsigned long long s_base;
+  extern __shared__ __align__(16) unsigned char fold_raw[];
+  double* fold = reinterpret_cast<double*>(fold_raw);  // [2 * kFoldChunk]
+  const GridDesc& g = A.g;
+  const int corners = 1 << g.d;
+  const int nh = nheavy[1];
+  for (int q = blockIdx.x; q < nh; q += gridDim.x) {
+    const long t = heavy[g.size - 1 - q];
     if (threadIdx.x == 0) {
       int id[3] = {0, 0, 0};
       node_idx(g, t, id);
-      int nl = 0;
+      int nl = 0, K = 0;
       for (int b = 0; b < corners; ++b) {
         long c = t;
         bool ok = true;
@@ -420,104 +327,65 @@ __global__ void __launch_bounds__(512) pf_gather_heavy_kernel(GatherArgs A, cons
             c -= g.stride[a];
           }
         if (!ok) continue;
-        const int k = A.cnt[c];
-        if (k == 0) continue;
+        const int k = A.end[c] - A.off[c];
+        if (k <= 0) continue;
         s_pos[nl] = A.off[c];
-        s_end[nl] = s_pos[nl] + k;
+        s_end[nl] = A.end[c];
         s_bits[nl] = b;
+        K += k;
         ++nl;
       }
       s_nl = nl;
-      s_rho = 0.0;
+      s_K = K;
+      s_base = atomicAdd(hfill, static_cast<unsigned long long>(K));
     }
     __syncthreads();
-    while (true) {
-      if (threadIdx.x == 0) {
-        // largest source-id bound lim with <= kChunk pending deposits below it
-        long lo = -1, hi = g.size;  // invariant: count(<= lo) <= kChunk
-        int remaining = 0;
-        for (int b = 0; b < s_nl; ++b) remaining += s_end[b] - s_pos[b];
-        if (remaining <= kChunk) {
-          lo = g.size;
-        } else {
-          while (hi - lo > 1) {
-            const long mid = (lo + hi) / 2;
-            int c = 0;
-            for (int b = 0; b < s_nl; ++b) {
-              int l2 = s_pos[b], h2 = s_end[b];  // upper_bound of mid
-              while (l2 < h2) {
-                const int m2 = (l2 + h2) >> 1;
-                if (A.bucket[m2] <= mid) l2 = m2 + 1;
-                else h2 = m2;
-              }
-              c += l2 - s_pos[b];
-            }
-            if (c <= kChunk) lo = mid;
+    const int nl = s_nl;
+    double* buf = hbuf + s_base;
+    for (int qq = 0; qq < nl; ++qq) {
+      const int p0 = s_pos[qq], p1 = s_end[qq], b = s_bits[qq];
+      for (int i = p0 + threadIdx.x; i < p1; i += blockDim.x) {
+        const int src = A.bucket[i];
+        int fin = i - p0;
+        for (int o = 0; o < nl; ++o) {
+          if (o == qq) continue;
+          int lo = s_pos[o], hi = s_end[o];
+          while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (A.bucket[mid] < src) lo = mid + 1;
             else hi = mid;
           }
+          fin += lo - s_pos[o];
         }
-        s_lim = lo;
-        int c = 0;
-        for (int b = 0; b < s_nl; ++b) {
-          int l2 = s_pos[b], h2 = s_end[b];
-          while (l2 < h2) {
-            const int m2 = (l2 + h2) >> 1;
-            if (A.bucket[m2] <= lo) l2 = m2 + 1;
-            else h2 = m2;
-          }
-          s_take[b] = c;
-          c += l2 - s_pos[b];
-        }
-        s_cnt = c;
+        buf[fin] = (b & A.cmask[src]) ? 0.0 : deposit_weight(A, src, b);
       }
-      __syncthreads();
-      const int cnt = s_cnt;
-      if (cnt == 0) break;
-      int p2 = 1;
-      while (p2 < cnt) p2 <<= 1;
-      // gather (source << 3 | corner) keys of this chunk
-      for (int b = 0; b < s_nl; ++b) {
-        const int nb = (b + 1 < s_nl ? s_take[b + 1] : cnt) - s_take[b];
-        for (int i = threadIdx.x; i < nb; i += blockDim.x)
-          key[s_take[b] + i] = (static_cast<unsigned>(A.bucket[s_pos[b] + i]) << 3) |
-                               static_cast<unsigned>(s_bits[b]);
-      }
-      for (int i = cnt + threadIdx.x; i < p2; i += blockDim.x) key[i] = 0xffffffffu;
-      __syncthreads();
-      for (int size = 2; size <= p2; size <<= 1)
-        for (int stride = size >> 1; stride > 0; stride >>= 1) {
-          for (int i = threadIdx.x; i < p2; i += blockDim.x) {
-            const int j = i ^ stride;
-            if (j > i) {
-              const bool up = (i & size) == 0;
-              const unsigned x = key[i], y = key[j];
-              if ((x > y) == up) {
-                key[i] = y;
-                key[j] = x;
-              }
-            }
-          }
-          __syncthreads();
-        }
-      for (int i = threadIdx.x; i < cnt; i += blockDim.x) {
-        const int src = static_cast<int>(key[i] >> 3);
-        const int b = static_cast<int>(key[i] & 7u);
-        wv[i] = (b & A.cmask[src]) ? 0.0 : deposit_weight(A, src, b);
-      }
-      __syncthreads();
+    }
+    __syncthreads();
+    // Sequential fold from shared memory, double-buffered: thread 0 folds
+    // chunk c while the other threads stage chunk c+1.
+    const int K = s_K;
+    const int nch = (K + kFoldChunk - 1) / kFoldChunk;
+    double rho = 0.0;
+    for (int i = threadIdx.x; i < min(K, kFoldChunk); i += blockDim.x) fold[i] = buf[i];
+    __syncthreads();
+    for (int c = 0; c < nch; ++c) {
+      const double* cur = fold + (c & 1) * kFoldChunk;
+      double* nxt = fold + ((c + 1) & 1) * kFoldChunk;
+      const int len = min(kFoldChunk, K - c * kFoldChunk);
       if (threadIdx.x == 0) {
-        double rho = s_rho;
-        for (int i = 0; i < cnt; ++i) {
-          const double w = wv[i];
+#pragma unroll 8
+        for (int i = 0; i < len; ++i) {
+          const double w = cur[i];
           if (w != 0.0) rho += w;
         }
-        s_rho = rho;
-        for (int b = 0; b < s_nl; ++b)
-          s_pos[b] += (b + 1 < s_nl ? s_take[b + 1] : cnt) - s_take[b];
+      } else if (c + 1 < nch) {
+        const int base = (c + 1) * kFoldChunk;
+        const int len2 = min(kFoldChunk, K - base);
+        for (int i = threadIdx.x - 1; i < len2; i += blockDim.x - 1) nxt[i] = buf[base + i];
       }
       __syncthreads();
     }
-    if (threadIdx.x == 0) A.out[t] = A.target ? A.target[t] - s_rho : s_rho;
+    if (threadIdx.x == 0) A.out[t] = A.target ? A.target[t] - rho : rho;
     __syncthreads();
   }
 }
@@ -534,33 +402,28 @@ unsigned grid_for(long n, int threads) {
 
 PushforwardPlan::~PushforwardPlan() {
   for (void* p : {static_cast<void*>(key_), static_cast<void*>(cmask_), static_cast<void*>(w_),
-                  static_cast<void*>(cnt_), static_cast<void*>(off_), static_cast<void*>(fill_),
-                  static_cast<void*>(bucket_), static_cast<void*>(blocksum_),
-                  static_cast<void*>(big_), static_cast<void*>(nbig_),
-                  static_cast<void*>(scratch_)})
+                  static_cast<void*>(off_), static_cast<void*>(end_), static_cast<void*>(heavy_),
+                  static_cast<void*>(nheavy_), static_cast<void*>(hbuf_)})
     if (p) cudaFree(p);
 }
 
 void PushforwardPlan::init(const GridDesc& g) {
   g_ = g;
   const long N = g.size;
-  if (N >= INT_MAX) throw std::invalid_argument("pushforward: grid too large");
-  BFM_CUDA(cudaMalloc(&key_, N * sizeof(int)));
+  if (N >= (1L << 29)) throw std::invalid_argument("pushforward: grid too large");
+  BFM_CUDA(cudaMalloc(&key_, N * sizeof(uint32_t)));
   BFM_CUDA(cudaMalloc(&cmask_, N));
   BFM_CUDA(cudaMalloc(&w_, g.d * N * sizeof(double)));
-  BFM_CUDA(cudaMalloc(&cnt_, (N + 1) * sizeof(int)));
   BFM_CUDA(cudaMalloc(&off_, (N + 1) * sizeof(int)));
-  BFM_CUDA(cudaMalloc(&fill_, N * sizeof(int)));
-  BFM_CUDA(cudaMalloc(&bucket_, N * sizeof(int)));
-  scan_blocks_ = (N + kScanTile - 1) / kScanTile;
-  BFM_CUDA(cudaMalloc(&blocksum_, (scan_blocks_ + 1) * sizeof(int)));
-  BFM_CUDA(cudaMalloc(&big_, N * sizeof(int)));
-  BFM_CUDA(cudaMalloc(&scratch_, 2 * (N + 1) * sizeof(int)));
-  BFM_CUDA(cudaMalloc(&nbig_, 4 * sizeof(int)));
-  BFM_CUDA(cudaFuncSetAttribute(pf_sort_big_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                32768 * 4));
-  BFM_CUDA(cudaFuncSetAttribute(pf_gather_heavy_kernel,
-                                cudaFuncAttributeMaxDynamicSharedMemorySize, kChunk * 12));
+  BFM_CUDA(cudaMalloc(&end_, (N + 1) * sizeof(int)));
+  BFM_CUDA(cudaMalloc(&heavy_, (N + 1) * sizeof(int)));
+  BFM_CUDA(cudaMalloc(&nheavy_, 4 * sizeof(unsigned long long)));
+  BFM_CUDA(cudaMalloc(&hbuf_, (static_cast<long>(1) << g.d) * N * sizeof(double)));
+  sorter_.init(N);
+  BFM_CUDA(cudaFuncSetAttribute(pf_gather_heavy_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                2 * kFoldChunk * static_cast<int>(sizeof(double))));
+  key_bits_ = 1;
+  while ((1L << key_bits_) <= N) ++key_bits_;  // cells 0..N-1 plus sentinel N
 }
 
 void PushforwardPlan::map_only(const double* d_u, double* d_disp, cudaStream_t stream,
@@ -579,40 +442,37 @@ void PushforwardPlan::map_only(const double* d_u, double* d_disp, cudaStream_t s
 void PushforwardPlan::bin_and_gather(const double* d_source, const double* d_target,
                                      double* d_out, cudaStream_t stream, LaunchCounter* lc) {
   const long N = g_.size;
-  scan_reduce_kernel<<<static_cast<unsigned>(scan_blocks_), kScanThreads, 0, stream>>>(cnt_, N,
-                                                                                      blocksum_);
-  scan_blocks_kernel<<<1, kScanThreads, 0, stream>>>(blocksum_, scan_blocks_);
-  scan_apply_kernel<<<static_cast<unsigned>(scan_blocks_), kScanThreads, 0, stream>>>(
-      cnt_, off_, N, blocksum_);
-  BFM_LAUNCH_CHECK("scan");
-  pf_place_kernel<<<grid_for(N, 256), 256, 0, stream>>>(N, key_, off_, fill_, bucket_);
-  pf_sort_small_kernel<<<grid_for(N, 256), 256, 0, stream>>>(N, cnt_, off_, bucket_, big_, nbig_);
-  pf_sort_big_kernel<<<148, 1024, 32768 * 4, stream>>>(cnt_, off_, bucket_, big_, nbig_,
-                                                       scratch_);
+  const uint32_t* skeys = nullptr;
+  const int* svals = nullptr;
+  sorter_.sort(key_, nullptr, N, key_bits_, stream, lc, &skeys, &svals);
+  BFM_CUDA(cudaMemsetAsync(off_, 0, (N + 1) * sizeof(int), stream));
+  BFM_CUDA(cudaMemsetAsync(end_, 0, (N + 1) * sizeof(int), stream));
+  BFM_CUDA(cudaMemsetAsync(nheavy_, 0, 4 * sizeof(unsigned long long), stream));
+  pf_bounds_kernel<<<grid_for(N, 256), 256, 0, stream>>>(skeys, N, static_cast<uint32_t>(N), off_,
+                                                         end_);
   GatherArgs G{};
   G.g = g_;
-  G.cnt = cnt_;
+  G.end = end_;
   G.off = off_;
-  G.bucket = bucket_;
+  G.bucket = svals;
   G.cmask = cmask_;
   G.w = w_;
   G.src = d_source;
   G.target = d_target;
   G.out = d_out;
-  pf_gather_kernel<<<grid_for(N, 256), 256, 0, stream>>>(G, big_, nbig_ + 2);
+  int* nheavy = reinterpret_cast<int*>(nheavy_);
+  pf_gather_kernel<<<grid_for(N, 256), 256, 0, stream>>>(G, heavy_, nheavy);
   BFM_LAUNCH_CHECK("pf_gather_kernel");
-  pf_gather_heavy_kernel<<<148 * 2, 512, kChunk * 12, stream>>>(G, big_, nbig_ + 2);
+  pf_gather_medium_kernel<<<148 * 8, 256, 0, stream>>>(G, heavy_, nheavy, hbuf_, nheavy_ + 1);
+  BFM_LAUNCH_CHECK("pf_gather_medium_kernel");
+  pf_gather_heavy_kernel<<<148, 512, 2 * kFoldChunk * sizeof(double), stream>>>(G, heavy_, nheavy, hbuf_, nheavy_ + 1);
   BFM_LAUNCH_CHECK("pf_gather_heavy_kernel");
-  if (lc) lc->add(8);
+  if (lc) lc->add(4);
 }
 
 void PushforwardPlan::from_potential(const double* d_u, const double* d_source,
                                      const double* d_target, double* d_out, double* d_disp_out,
                                      cudaStream_t stream, LaunchCounter* lc) {
-  const long N = g_.size;
-  BFM_CUDA(cudaMemsetAsync(cnt_, 0, (N + 1) * sizeof(int), stream));
-  BFM_CUDA(cudaMemsetAsync(fill_, 0, N * sizeof(int), stream));
-  BFM_CUDA(cudaMemsetAsync(nbig_, 0, 4 * sizeof(int), stream));
   MapArgs A{};
   A.g = g_;
   A.u = d_u;
@@ -622,9 +482,9 @@ void PushforwardPlan::from_potential(const double* d_u, const double* d_source,
   A.cmask = cmask_;
   A.w = w_;
   A.disp_out = d_disp_out;
-  A.cnt = cnt_;
+  A.binning = 1;
   A.diam = std::sqrt(static_cast<double>(g_.d));
-  pf_map_kernel<<<grid_for(N, 256), 256, 0, stream>>>(A);
+  pf_map_kernel<<<grid_for(g_.size, 256), 256, 0, stream>>>(A);
   BFM_LAUNCH_CHECK("pf_map_kernel");
   if (lc) lc->add();
   bin_and_gather(d_source, d_target, d_out, stream, lc);
@@ -633,10 +493,6 @@ void PushforwardPlan::from_potential(const double* d_u, const double* d_source,
 void PushforwardPlan::from_displacement(const double* d_disp, double scale,
                                         const double* d_source, double* d_rho,
                                         cudaStream_t stream, LaunchCounter* lc) {
-  const long N = g_.size;
-  BFM_CUDA(cudaMemsetAsync(cnt_, 0, (N + 1) * sizeof(int), stream));
-  BFM_CUDA(cudaMemsetAsync(fill_, 0, N * sizeof(int), stream));
-  BFM_CUDA(cudaMemsetAsync(nbig_, 0, 4 * sizeof(int), stream));
   MapArgs A{};
   A.g = g_;
   A.disp = d_disp;
@@ -645,9 +501,9 @@ void PushforwardPlan::from_displacement(const double* d_disp, double scale,
   A.key = key_;
   A.cmask = cmask_;
   A.w = w_;
-  A.cnt = cnt_;
+  A.binning = 1;
   A.diam = std::sqrt(static_cast<double>(g_.d));
-  pf_map_kernel<<<grid_for(N, 256), 256, 0, stream>>>(A);
+  pf_map_kernel<<<grid_for(g_.size, 256), 256, 0, stream>>>(A);
   BFM_LAUNCH_CHECK("pf_map_kernel");
   if (lc) lc->add();
   bin_and_gather(d_source, nullptr, d_rho, stream, lc);

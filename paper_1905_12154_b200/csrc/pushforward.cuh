@@ -5,6 +5,7 @@
 #include <stdint.h>
 
 #include "common.cuh"
+#include "radix_sort.cuh"
 
 namespace bfmgpu {
 
@@ -32,18 +33,16 @@ class PushforwardPlan {
   void bin_and_gather(const double* d_source, const double* d_target, double* d_out,
                       cudaStream_t stream, LaunchCounter* lc);
   GridDesc g_;
-  int* key_ = nullptr;       // [N] lo-corner cell of each source, -1 if no mass
+  uint32_t* key_ = nullptr;  // [N] lo-corner cell of each source (N = no mass)
   uint8_t* cmask_ = nullptr; // [N] axes on which the source is clamped (lo == hi)
   double* w_ = nullptr;      // [d*N] upper-node weight per axis
-  int* cnt_ = nullptr;       // [N+1] per-cell counts
-  int* off_ = nullptr;       // [N+1] exclusive scan
-  int* fill_ = nullptr;      // [N]
-  int* bucket_ = nullptr;    // [N] source indices grouped by cell
-  int* blocksum_ = nullptr;  // scan scratch
-  int* big_ = nullptr;       // [N] cells with large buckets
-  int* nbig_ = nullptr;
-  int* scratch_ = nullptr;   // [2N+2] huge-bucket sort windows
-  long scan_blocks_ = 0;
+  int* off_ = nullptr;       // [N+1] first sorted position of each cell
+  int* end_ = nullptr;       // [N+1] one past the last
+  int* heavy_ = nullptr;     // [N] targets with long deposit lists
+  unsigned long long* nheavy_ = nullptr;  // [0] heavy count, [1] buffer fill
+  double* hbuf_ = nullptr;   // [2^d * N] merged heavy deposits
+  RadixSorter sorter_;
+  int key_bits_ = 0;
 };
 
 }  // namespace bfmgpu

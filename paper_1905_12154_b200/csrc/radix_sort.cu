@@ -1,0 +1,201 @@
+// Stable LSD radix sort (8-bit digits) of (key, value) pairs.
+//
+// Per pass: (1) per-tile digit histograms (digit-major), (2) exclusive scan
+// of the histograms, (3) stable scatter: each tile walks its elements in
+// input order in rounds of 256; within a round the rank of an element among
+// equal digits is (warp-local rank via __match_any_sync) + (counts of the same
+// digit in lower warps) + (running per-tile digit count), so equal keys keep
+// their input order. Deterministic by construction.
+#include "radix_sort.cuh"
+
+namespace bfmgpu {
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kItems = 16;
+constexpr int kTile = kThreads * kItems;
+constexpr int kWarps = kThreads / 32;
+
+__global__ void __launch_bounds__(kThreads) rs_hist_kernel(const uint32_t* keys, long n, int shift,
+                                                         long nblocks, int* hist) {
+  __shared__ int h[256];
+  h[threadIdx.x] = 0;
+  __syncthreads();
+  const long base = static_cast<long>(blockIdx.x) * kTile;
+  const unsigned lane = threadIdx.x & 31u;
+  for (int r = 0; r < kItems; ++r) {
+    const long i = base + static_cast<long>(r) * kThreads + threadIdx.x;
+    const bool ok = i < n;
+    const unsigned d = ok ? (keys[i] >> shift) & 255u : 256u;
+    const unsigned act = __ballot_sync(0xffffffffu, ok);
+    if (ok) {
+      const unsigned m = __match_any_sync(act, d);
+      if ((__ffs(m) - 1) == static_cast<int>(lane)) atomicAdd(&h[d], __popc(m));
+    }
+  }
+  __syncthreads();
+  hist[static_cast<long>(threadIdx.x) * nblocks + blockIdx.x] = h[threadIdx.x];
+}
+
+__device__ int block_exscan(int v, int* total) {
+  __shared__ int wt[32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  int incl = v;
+  for (int d = 1; d < 32; d <<= 1) {
+    const int u = __shfl_up_sync(0xffffffffu, incl, d);
+    if (lane >= d) incl += u;
+  }
+  if (lane == 31) wt[w] = incl;
+  __syncthreads();
+  if (w == 0) {
+    const int t = lane < static_cast<int>(blockDim.x >> 5) ? wt[lane] : 0;
+    int ti = t;
+    for (int d = 1; d < 32; d <<= 1) {
+      const int u = __shfl_up_sync(0xffffffffu, ti, d);
+      if (lane >= d) ti += u;
+    }
+    wt[lane] = ti - t;
+    if (lane == 31) *total = ti;
+  }
+  __syncthreads();
+  const int r = wt[w] + incl - v;
+  __syncthreads();
+  return r;
+}
+
+// In-place exclusive scan of m ints (m up to a few million), two levels.
+constexpr int kScanTile = 1024 * 8;
+__global__ void __launch_bounds__(1024) rs_scan_reduce(const int* a, long m, int* bsum) {
+  __shared__ int tot;
+  const long base = static_cast<long>(blockIdx.x) * kScanTile + threadIdx.x * 8;
+  int s = 0;
+  for (int i = 0; i < 8; ++i)
+    if (base + i < m) s += a[base + i];
+  block_exscan(s, &tot);
+  if (threadIdx.x == 0) bsum[blockIdx.x] = tot;
+}
+__global__ void __launch_bounds__(1024) rs_scan_top(int* bsum, long nb) {
+  __shared__ int carry, tot;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (long b0 = 0; b0 < nb; b0 += 1024) {
+    const long i = b0 + threadIdx.x;
+    const int v = i < nb ? bsum[i] : 0;
+    const int ex = block_exscan(v, &tot);
+    if (i < nb) bsum[i] = carry + ex;
+    __syncthreads();
+    if (threadIdx.x == 0) carry += tot;
+    __syncthreads();
+  }
+}
+__global__ void __launch_bounds__(1024) rs_scan_apply(int* a, long m, const int* bsum) {
+  __shared__ int tot;
+  const long base = static_cast<long>(blockIdx.x) * kScanTile + threadIdx.x * 8;
+  int v[8];
+  int s = 0;
+  for (int i = 0; i < 8; ++i) {
+    v[i] = base + i < m ? a[base + i] : 0;
+    s += v[i];
+  }
+  int ex = block_exscan(s, &tot) + bsum[blockIdx.x];
+  for (int i = 0; i < 8; ++i) {
+    if (base + i < m) a[base + i] = ex;
+    ex += v[i];
+  }
+}
+
+__global__ void __launch_bounds__(kThreads) rs_scatter_kernel(const uint32_t* kin, const int* vin,
+                                                            long n, int shift, long nblocks,
+                                                            const int* hist, uint32_t* kout,
+                                                            int* vout) {
+  __shared__ int gbase[256];
+  __shared__ int run[256];
+  __shared__ int wcnt[kWarps][256];
+  gbase[threadIdx.x] = hist[static_cast<long>(threadIdx.x) * nblocks + blockIdx.x];
+  run[threadIdx.x] = 0;
+  for (int w = 0; w < kWarps; ++w) wcnt[w][threadIdx.x] = 0;
+  __syncthreads();
+  const long base = static_cast<long>(blockIdx.x) * kTile;
+  const unsigned lane = threadIdx.x & 31u;
+  const int warp = threadIdx.x >> 5;
+  const unsigned lt = (1u << lane) - 1u;
+  for (int r = 0; r < kItems; ++r) {
+    const long i = base + static_cast<long>(r) * kThreads + threadIdx.x;
+    const bool ok = i < n;
+    uint32_t k = 0;
+    int v = 0;
+    unsigned d = 256u, m = 0u;
+    const unsigned act = __ballot_sync(0xffffffffu, ok);
+    if (ok) {
+      k = kin[i];
+      v = vin ? vin[i] : static_cast<int>(i);
+      d = (k >> shift) & 255u;
+      m = __match_any_sync(act, d);
+      if ((__ffs(m) - 1) == static_cast<int>(lane)) wcnt[warp][d] = __popc(m);
+    }
+    __syncthreads();
+    if (ok) {
+      int pre = 0;
+      for (int w = 0; w < warp; ++w) pre += wcnt[w][d];
+      const long pos = static_cast<long>(gbase[d]) + run[d] + pre + __popc(m & lt);
+      kout[pos] = k;
+      vout[pos] = v;
+    }
+    __syncthreads();
+    if (ok && (__ffs(m) - 1) == static_cast<int>(lane)) {
+      atomicAdd(&run[d], __popc(m));
+      wcnt[warp][d] = 0;
+    }
+    __syncthreads();
+  }
+}
+
+}  // namespace
+
+RadixSorter::~RadixSorter() {
+  for (int i = 0; i < 2; ++i) {
+    if (kbuf_[i]) cudaFree(kbuf_[i]);
+    if (vbuf_[i]) cudaFree(vbuf_[i]);
+  }
+  if (hist_) cudaFree(hist_);
+  if (bsum_) cudaFree(bsum_);
+}
+
+void RadixSorter::init(long n) {
+  cap_ = n;
+  blocks_ = (n + kTile - 1) / kTile;
+  for (int i = 0; i < 2; ++i) {
+    BFM_CUDA(cudaMalloc(&kbuf_[i], (n + 1) * sizeof(uint32_t)));
+    BFM_CUDA(cudaMalloc(&vbuf_[i], (n + 1) * sizeof(int)));
+  }
+  const long m = 256 * blocks_;
+  BFM_CUDA(cudaMalloc(&hist_, (m + 1) * sizeof(int)));
+  BFM_CUDA(cudaMalloc(&bsum_, ((m + kScanTile - 1) / kScanTile + 1) * sizeof(int)));
+}
+
+void RadixSorter::sort(const uint32_t* keys_in, const int* vals_in, long n, int bits, cudaStream_t s,
+                       LaunchCounter* lc, const uint32_t** keys_out, const int** vals_out) {
+  const long nb = (n + kTile - 1) / kTile;
+  const long m = 256 * nb;
+  const long sb = (m + kScanTile - 1) / kScanTile;
+  const uint32_t* kin = keys_in;
+  const int* vin = vals_in;
+  int cur = 0;
+  for (int shift = 0; shift < bits; shift += 8) {
+    rs_hist_kernel<<<static_cast<unsigned>(nb), kThreads, 0, s>>>(kin, n, shift, nb, hist_);
+    rs_scan_reduce<<<static_cast<unsigned>(sb), 1024, 0, s>>>(hist_, m, bsum_);
+    rs_scan_top<<<1, 1024, 0, s>>>(bsum_, sb);
+    rs_scan_apply<<<static_cast<unsigned>(sb), 1024, 0, s>>>(hist_, m, bsum_);
+    rs_scatter_kernel<<<static_cast<unsigned>(nb), kThreads, 0, s>>>(kin, vin, n, shift, nb, hist_,
+                                                                     kbuf_[cur], vbuf_[cur]);
+    BFM_LAUNCH_CHECK("radix sort pass");
+    if (lc) lc->add(5);
+    kin = kbuf_[cur];
+    vin = vbuf_[cur];
+    cur ^= 1;
+  }
+  *keys_out = kin;
+  *vals_out = vin;
+}
+
+}  // namespace bfmgpu
