@@ -71,22 +71,18 @@ BFM_HD cplx csub(cplx a, cplx b) { return cplx{a.re - b.re, a.im - b.im}; }
 // Number of butterflies in stage s.
 BFM_HD int stage_butterflies(const LinePlan& p, int s) { return p.m / p.radix[s]; }
 
-// One DIF butterfly of stage s on the complex buffer z (in place).
-// inverse = true uses e^{+2 pi i / m}.
-BFM_HD void fft_butterfly(const LinePlan& p, int s, int b, cplx* z, bool inverse) {
-  const int r = p.radix[s];
-  const int L = p.span[s];
-  const int q = L / r;
-  const int blk = b / q;
-  const int j = b - blk * q;
-  const int base = blk * L + j;
-  const int tw_step = (p.m / L) * j;  // twiddle exponent for output digit 1
+// Arithmetic of one DIF butterfly (radix r, elements base + t*q, twiddle
+// exponent tw for output digit 1). Index math is left to the caller so the
+// GPU can use cheaper integer arithmetic; the double operations are shared.
+BFM_HD void butterfly_core(const LinePlan& p, int r, int base, int q, int tw, cplx* z,
+                           bool inverse) {
+  const int m = p.m;
   if (r == 2) {
     const cplx a = z[base];
     const cplx c = z[base + q];
     z[base] = cadd(a, c);
     const cplx d = csub(a, c);
-    const cplx w = p.wm[tw_step];
+    const cplx w = p.wm[tw];
     z[base + q] = inverse ? cmulc(d, w) : cmul(d, w);
   } else if (r == 4) {
     const cplx x0 = z[base], x1 = z[base + q], x2 = z[base + 2 * q], x3 = z[base + 3 * q];
@@ -99,10 +95,13 @@ BFM_HD void fft_butterfly(const LinePlan& p, int s, int b, cplx* z, bool inverse
     const cplx y1 = inverse ? cadd(a1, ib1) : csub(a1, ib1);
     const cplx y3 = inverse ? csub(a1, ib1) : cadd(a1, ib1);
     z[base] = y0;
-    const int m = p.m;
-    const cplx w1 = p.wm[tw_step % m];
-    const cplx w2 = p.wm[(2 * tw_step) % m];
-    const cplx w3 = p.wm[(3 * tw_step) % m];
+    int t2 = 2 * tw;
+    if (t2 >= m) t2 -= m;
+    int t3 = t2 + tw;
+    if (t3 >= m) t3 -= m;
+    const cplx w1 = p.wm[tw];
+    const cplx w2 = p.wm[t2];
+    const cplx w3 = p.wm[t3];
     if (inverse) {
       z[base + q] = cmulc(y1, w1);
       z[base + 2 * q] = cmulc(y2, w2);
@@ -116,18 +115,19 @@ BFM_HD void fft_butterfly(const LinePlan& p, int s, int b, cplx* z, bool inverse
     const cplx x0 = z[base], x1 = z[base + q], x2 = z[base + 2 * q];
     const cplx t1 = cadd(x1, x2);
     const cplx y0 = cadd(x0, t1);
-    const cplx t2{x0.re - 0.5 * t1.re, x0.im - 0.5 * t1.im};
+    const cplx t2c{x0.re - 0.5 * t1.re, x0.im - 0.5 * t1.im};
     const cplx d = csub(x1, x2);
     const double h3 = 0.86602540378443864676;  // sqrt(3)/2
     const cplx u{h3 * d.re, h3 * d.im};
     const cplx iu{-u.im, u.re};
     // forward: y1 = t2 - i u, y2 = t2 + i u.
-    const cplx y1 = inverse ? cadd(t2, iu) : csub(t2, iu);
-    const cplx y2 = inverse ? csub(t2, iu) : cadd(t2, iu);
+    const cplx y1 = inverse ? cadd(t2c, iu) : csub(t2c, iu);
+    const cplx y2 = inverse ? csub(t2c, iu) : cadd(t2c, iu);
     z[base] = y0;
-    const int m = p.m;
-    const cplx w1 = p.wm[tw_step % m];
-    const cplx w2 = p.wm[(2 * tw_step) % m];
+    int t2 = 2 * tw;
+    if (t2 >= m) t2 -= m;
+    const cplx w1 = p.wm[tw];
+    const cplx w2 = p.wm[t2];
     if (inverse) {
       z[base + q] = cmulc(y1, w1);
       z[base + 2 * q] = cmulc(y2, w2);
@@ -136,6 +136,17 @@ BFM_HD void fft_butterfly(const LinePlan& p, int s, int b, cplx* z, bool inverse
       z[base + 2 * q] = cmul(y2, w2);
     }
   }
+}
+
+// One DIF butterfly of stage s on the complex buffer z (in place).
+// inverse = true uses e^{+2 pi i / m}.
+BFM_HD void fft_butterfly(const LinePlan& p, int s, int b, cplx* z, bool inverse) {
+  const int r = p.radix[s];
+  const int L = p.span[s];
+  const int q = L / r;
+  const int blk = b / q;
+  const int j = b - blk * q;
+  butterfly_core(p, r, blk * L + j, q, (p.m / L) * j, z, inverse);
 }
 
 // ---- DCT-II (REDFT10) ----------------------------------------------------

@@ -32,6 +32,7 @@ struct PoisArgs {
   const double* lam1;
   const double* lam2;
   double scale;
+  unsigned qmagic[bfmdct::kMaxStages];
 };
 
 __device__ __forceinline__ void gsync(int tpl, int l) {
@@ -56,7 +57,29 @@ __device__ __forceinline__ double divide(const PoisArgs& a, double v, int k, dou
   return lam == 0.0 ? 0.0 : v / (lam * a.scale);
 }
 
-__global__ void __launch_bounds__(1024) pois_fft_kernel(PoisArgs a) {
+// Stage loop with division by q through a precomputed 32-bit magic number.
+__device__ __forceinline__ void fft_stages(const PoisArgs& a, cplx* z, bool inverse, int t,
+                                           int tpl, int l) {
+  const bfmdct::LinePlan& P = a.ax.plan;
+  for (int s = 0; s < P.nstages; ++s) {
+    const int r = P.radix[s];
+    const int L = P.span[s];
+    const int q = L / r;
+    const unsigned magic = a.qmagic[s];
+    const int twmul = P.m / L;
+    const int nb = P.m / r;
+    for (int b = t; b < nb; b += tpl) {
+      const int blk = magic ? static_cast<int>(__umulhi(static_cast<unsigned>(b), magic)) : b;
+      const int j = b - blk * q;
+      bfmdct::butterfly_core(P, r, blk * L + j, q, twmul * j, z, inverse);
+    }
+    gsync(tpl, l);
+  }
+}
+
+// Two shared buffers per line (zA, zB): phases read one and write the other,
+// so no register staging is needed; butterflies run in place.
+__global__ void __launch_bounds__(512) pois_fft_kernel(PoisArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   const PoisAxisCfg& ax = a.ax;
   const bfmdct::LinePlan& P = ax.plan;
@@ -64,180 +87,120 @@ __global__ void __launch_bounds__(1024) pois_fft_kernel(PoisArgs a) {
   const int l = threadIdx.x / tpl;
   const int t = threadIdx.x - l * tpl;
   const long L0 = static_cast<long>(blockIdx.x) * lpc;
-
-  // ---- load (coalesced) ----
-  for (int idx = threadIdx.x; idx < n * lpc; idx += blockDim.x) {
-    int ll, j;
-    if (ax.strided) {
-      ll = idx % lpc;
-      j = idx / lpc;
-    } else {
-      ll = idx / n;
-      j = idx - ll * n;
-    }
-    const long L = L0 + ll;
-    if (L >= ax.nlines) continue;
-    double* zd = reinterpret_cast<double*>(smem + static_cast<long>(ll) * ax.line_bytes);
-    const double v = a.in[line_base(ax, L) + static_cast<long>(j) * ax.stride];
-    if (a.mode == kInv) zd[j] = v;
-    else zd[bfmdct::dct2_vpos(P, j)] = v;
+  __shared__ long s_base[16];
+  if (threadIdx.x < lpc) {
+    const long L = L0 + threadIdx.x;
+    s_base[threadIdx.x] = L < ax.nlines ? line_base(ax, L) : -1;
   }
   __syncthreads();
-
-  const long L = L0 + l;
-  const bool active = L < ax.nlines;
-  double* zd = reinterpret_cast<double*>(smem + static_cast<long>(l) * ax.line_bytes);
-  cplx* z = reinterpret_cast<cplx*>(zd);
-
+  // load (coalesced): thread's line is fixed, no per-element division
+  const int ml = ax.strided ? static_cast<int>(threadIdx.x % lpc) : l;
+  const int step = ax.strided ? blockDim.x / lpc : tpl;
+  const int first = ax.strided ? static_cast<int>(threadIdx.x / lpc) : t;
+  {
+    const long base = s_base[ml];
+    double* zA = reinterpret_cast<double*>(smem + static_cast<long>(ml) * ax.line_bytes);
+    if (base >= 0)
+      for (int j = first; j < n; j += step) {
+        const double v = a.in[base + static_cast<long>(j) * ax.stride];
+        if (a.mode == kInv) zA[j] = v;
+        else zA[bfmdct::dct2_vpos(P, j)] = v;
+      }
+  }
+  __syncthreads();
+  const long lbase = s_base[l];
+  const bool active = lbase >= 0;
+  double* zAd = reinterpret_cast<double*>(smem + static_cast<long>(l) * ax.line_bytes);
+  double* zBd = zAd + n;
+  cplx* zA = reinterpret_cast<cplx*>(zAd);
+  cplx* zB = reinterpret_cast<cplx*>(zBd);
   double l1v = 0.0, l2v = 0.0;
   if (a.mode == kFused && active) {
-    const long inner = line_base(ax, L);  // axis-0 lines: base == inner offset
     if (a.d == 2) {
-      l1v = a.lam1[inner];
+      l1v = a.lam1[lbase];
     } else if (a.d == 3) {
-      l1v = a.lam1[inner / a.n2];
-      l2v = a.lam2[inner % a.n2];
+      l1v = a.lam1[lbase / a.n2];
+      l2v = a.lam2[lbase % a.n2];
     }
   }
-
-  cplx reg[kMaxItems];
-  cplx reg2[kMaxItems];
-
-  // ---- inverse pre-step: Z_k from V_k, V_{m-k} ----
+  double* outbuf = zAd;  // where the line's final values end up
   if (a.mode == kInv) {
-#pragma unroll
-    for (int r = 0; r < kMaxItems; ++r) {
-      const int k = t + r * tpl;
-      if (active && k < m) {
-        const cplx A = bfmdct::dct3_V_vals(P, zd[k], k == 0 ? 0.0 : zd[n - k], k);
-        const int km = m - k;
-        const cplx B = bfmdct::dct3_V_vals(P, zd[km], zd[n - km], km);
-        reg[r] = bfmdct::dct3_pre_vals(P, A, B, k);
-      }
-    }
-    gsync(tpl, l);
-#pragma unroll
-    for (int r = 0; r < kMaxItems; ++r) {
-      const int k = t + r * tpl;
-      if (active && k < m) z[k] = reg[r];
-    }
-    gsync(tpl, l);
-  }
-
-  // ---- FFT stages (forward for DCT-II) ----
-  const bool inv_first = a.mode == kInv;
-  for (int s = 0; s < P.nstages; ++s) {
-    const int nb = m / P.radix[s];
     if (active)
-      for (int b = t; b < nb; b += tpl) bfmdct::fft_butterfly(P, s, b, z, inv_first);
-    gsync(tpl, l);
-  }
-
-  if (a.mode == kFwd) {
-    // unpack k in [0, m] -> y_k, y_{n-k}
-#pragma unroll
-    for (int r = 0; r < kMaxItems; ++r) {
-      const int k = t + r * tpl;
-      if (active && k <= m) {
-        double yk, ynk;
-        bfmdct::dct2_unpack_vals(P, z[P.rev[k == m ? 0 : k]], z[P.rev[k == 0 ? 0 : m - k]], k,
-                                 yk, ynk);
-        reg[r] = cplx{yk, ynk};
+      for (int k = t; k < m; k += tpl) {
+        const cplx A = bfmdct::dct3_V_vals(P, zAd[k], k == 0 ? 0.0 : zAd[n - k], k);
+        const int km = m - k;
+        const cplx B = bfmdct::dct3_V_vals(P, zAd[km], zAd[n - km], km);
+        zB[k] = bfmdct::dct3_pre_vals(P, A, B, k);
       }
-    }
     gsync(tpl, l);
-#pragma unroll
-    for (int r = 0; r < kMaxItems; ++r) {
-      const int k = t + r * tpl;
-      if (active && k <= m) {
-        zd[k] = reg[r].re;
-        if (k > 0 && k < m) zd[n - k] = reg[r].im;
+    if (active) fft_stages(a, zB, true, t, tpl, l);
+    else for (int s = 0; s < P.nstages; ++s) gsync(tpl, l);
+    if (active)
+      for (int q = t; q < m; q += tpl) {
+        const cplx v = zB[P.rev[q]];
+        zAd[bfmdct::dct3_ypos(P, 2 * q)] = v.re;
+        zAd[bfmdct::dct3_ypos(P, 2 * q + 1)] = v.im;
       }
-    }
+    outbuf = zAd;
   } else {
-    if (a.mode == kFused) {
-      // items k in [0, m/2]: unpack k and m-k, divide, pre-step Z_k, Z_{m-k}
+    if (active) fft_stages(a, zA, false, t, tpl, l);
+    else for (int s = 0; s < P.nstages; ++s) gsync(tpl, l);
+    if (a.mode == kFwd) {
+      if (active)
+        for (int k = t; k <= m; k += tpl) {
+          double yk, ynk;
+          bfmdct::dct2_unpack_vals(P, zA[P.rev[k == m ? 0 : k]], zA[P.rev[k == 0 ? 0 : m - k]], k,
+                                   yk, ynk);
+          zBd[k] = yk;
+          if (k > 0 && k < m) zBd[n - k] = ynk;
+        }
+      outbuf = zBd;
+    } else {
       const int half = m / 2;
-#pragma unroll
-      for (int r = 0; r < kMaxItems; ++r) {
-        const int k = t + r * tpl;
-        if (active && k <= half) {
+      if (active)
+        for (int k = t; k <= half; k += tpl) {
           const int km = m - k;
           double yk, ynk, ykm, ynkm;
-          bfmdct::dct2_unpack_vals(P, z[P.rev[k == m ? 0 : k]], z[P.rev[k == 0 ? 0 : m - k]], k,
+          bfmdct::dct2_unpack_vals(P, zA[P.rev[k == m ? 0 : k]], zA[P.rev[k == 0 ? 0 : m - k]], k,
                                    yk, ynk);
-          bfmdct::dct2_unpack_vals(P, z[P.rev[km == m ? 0 : km]],
-                                   z[P.rev[km == 0 ? 0 : m - km]], km, ykm, ynkm);
-          // values at wavenumbers: k, n-k (0<k<m), km, n-km (0<km<m)
+          bfmdct::dct2_unpack_vals(P, zA[P.rev[km == m ? 0 : km]],
+                                   zA[P.rev[km == 0 ? 0 : m - km]], km, ykm, ynkm);
           const double xk = divide(a, yk, k, l1v, l2v);
           const double xnk = (k > 0 && k < m) ? divide(a, ynk, n - k, l1v, l2v) : 0.0;
           const double xkm = divide(a, ykm, km, l1v, l2v);
           const double xnkm = (km > 0 && km < m) ? divide(a, ynkm, n - km, l1v, l2v) : 0.0;
-          // x_{n-j} for j = k is xnk (j=0 -> 0); for j = km: x_{n-km} = xnkm, but
-          // when km == m, n - km == m so x_{n-m} = x_m = xkm.
           const double b_k = k == 0 ? 0.0 : xnk;
           const double b_km = km == m ? xkm : xnkm;
           const cplx Vk = bfmdct::dct3_V_vals(P, xk, b_k, k);
           const cplx Vkm = bfmdct::dct3_V_vals(P, xkm, b_km, km);
-          reg[r] = bfmdct::dct3_pre_vals(P, Vk, Vkm, k);
-          if (km < m && km != k) reg2[r] = bfmdct::dct3_pre_vals(P, Vkm, Vk, km);
+          zB[k] = bfmdct::dct3_pre_vals(P, Vk, Vkm, k);
+          if (km < m && km != k) zB[km] = bfmdct::dct3_pre_vals(P, Vkm, Vk, km);
         }
-      }
       gsync(tpl, l);
-#pragma unroll
-      for (int r = 0; r < kMaxItems; ++r) {
-        const int k = t + r * tpl;
-        if (active && k <= half) {
-          const int km = m - k;
-          z[k] = reg[r];
-          if (km < m && km != k) z[km] = reg2[r];
+      if (active) fft_stages(a, zB, true, t, tpl, l);
+      else for (int s = 0; s < P.nstages; ++s) gsync(tpl, l);
+      if (active)
+        for (int q = t; q < m; q += tpl) {
+          const cplx v = zB[P.rev[q]];
+          zAd[bfmdct::dct3_ypos(P, 2 * q)] = v.re;
+          zAd[bfmdct::dct3_ypos(P, 2 * q + 1)] = v.im;
         }
-      }
-      gsync(tpl, l);
-      for (int s = 0; s < P.nstages; ++s) {
-        const int nb = m / P.radix[s];
-        if (active)
-          for (int b = t; b < nb; b += tpl) bfmdct::fft_butterfly(P, s, b, z, true);
-        gsync(tpl, l);
-      }
-    }
-    // post: y positions of v_{2q}, v_{2q+1}
-#pragma unroll
-    for (int r = 0; r < kMaxItems; ++r) {
-      const int q = t + r * tpl;
-      if (active && q < m) reg[r] = z[P.rev[q]];
-    }
-    gsync(tpl, l);
-#pragma unroll
-    for (int r = 0; r < kMaxItems; ++r) {
-      const int q = t + r * tpl;
-      if (active && q < m) {
-        zd[bfmdct::dct3_ypos(P, 2 * q)] = reg[r].re;
-        zd[bfmdct::dct3_ypos(P, 2 * q + 1)] = reg[r].im;
-      }
+      outbuf = zAd;
     }
   }
   __syncthreads();
-
-  // ---- store (coalesced) ----
-  for (int idx = threadIdx.x; idx < n * lpc; idx += blockDim.x) {
-    int ll, j;
-    if (ax.strided) {
-      ll = idx % lpc;
-      j = idx / lpc;
-    } else {
-      ll = idx / n;
-      j = idx - ll * n;
-    }
-    const long LL = L0 + ll;
-    if (LL >= ax.nlines) continue;
-    const double* zl = reinterpret_cast<const double*>(smem + static_cast<long>(ll) * ax.line_bytes);
-    a.out[line_base(ax, LL) + static_cast<long>(j) * ax.stride] = zl[j];
+  // store (coalesced)
+  {
+    const long base = s_base[ml];
+    const double* src = reinterpret_cast<const double*>(smem + static_cast<long>(ml) * ax.line_bytes) +
+                        (outbuf == zAd ? 0 : n);
+    if (base >= 0)
+      for (int j = first; j < n; j += step) a.out[base + static_cast<long>(j) * ax.stride] = src[j];
   }
 }
 
 // Direct O(n^2) form for extents that are not 2 * 2^a 3^b.
-__global__ void __launch_bounds__(1024) pois_naive_kernel(PoisArgs a) {
+__global__ void __launch_bounds__(512) pois_naive_kernel(PoisArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   const PoisAxisCfg& ax = a.ax;
   const bfmdct::LinePlan& P = ax.plan;
@@ -313,14 +276,6 @@ T* upload(const std::vector<T>& v, std::vector<void*>& keep) {
   return d;
 }
 
-std::vector<void*>& allocations(void* key) {
-  static thread_local std::vector<std::pair<void*, std::vector<void*>>> reg;
-  for (auto& e : reg)
-    if (e.first == key) return e.second;
-  reg.push_back({key, {}});
-  return reg.back().second;
-}
-
 }  // namespace
 
 PoissonPlan::~PoissonPlan() {
@@ -368,15 +323,15 @@ void PoissonPlan::init(const GridDesc& g) {
       int tpl = (m + 7) / 8;
       tpl = ((tpl + 31) / 32) * 32;
       if (tpl < 32) tpl = 32;
-      if (tpl > 1024) throw std::invalid_argument("solve_neumann: extent too large");
+      if (tpl > 256) tpl = 256;
       c.tpl = tpl;
-      c.line_bytes = ((8 * n) + 15) & ~15;
+      c.line_bytes = ((16 * n) + 15) & ~15;
     } else {
       c.tpl = n >= 256 ? 256 : 32 * ((n + 31) / 32);
       c.line_bytes = ((16 * n) + 15) & ~15;
     }
     if (c.line_bytes > budget) throw std::invalid_argument("solve_neumann: line exceeds shared memory");
-    int lpc = std::min(budget / c.line_bytes, 1024 / c.tpl);
+    int lpc = std::min(budget / c.line_bytes, 512 / c.tpl);
     lpc = std::min(lpc, c.strided ? 16 : 4);
     if (c.tpl > 32) lpc = std::min(lpc, 15);
     lpc = static_cast<int>(std::min<long>(lpc, c.nlines));
@@ -409,6 +364,10 @@ void PoissonPlan::solve(const double* d_rhs, double* d_out, cudaStream_t stream,
     A.lam2 = d > 2 ? lam_[2] : nullptr;
     A.scale = scale_;
     const PoisAxisCfg& c = cfg_[axis];
+    for (int st = 0; st < c.plan.nstages; ++st) {
+      const unsigned q = static_cast<unsigned>(c.plan.span[st] / c.plan.radix[st]);
+      A.qmagic[st] = q == 1 ? 0u : static_cast<unsigned>((0x100000000ULL + q - 1) / q);
+    }
     const long blocks = (c.nlines + c.lpc - 1) / c.lpc;
     const size_t sm = static_cast<size_t>(c.lpc) * c.line_bytes;
     if (c.plan.kind == bfmdct::kFft)
