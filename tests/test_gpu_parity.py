@@ -217,3 +217,20 @@ def test_gradient_ascent_mode_matches_reference(ref):
     a = bfm.Solver(g["discs_mu"], g["discs_nu"], cfg).run()
     b = ref.RefSolver(g["discs_mu"], g["discs_nu"], cfg).run()
     assert O.n_bit_diff(a.phi, b.phi) == 0 and O.n_bit_diff(a.psi, b.psi) == 0
+
+
+def test_cpp_facade_driver_runs_on_gpu(tmp_path):
+    """A driver written against the reference's C++ API compiles unchanged
+    against include/bfm_b200/bfm.hpp and passes the reference's own checks."""
+    import subprocess
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    exe = tmp_path / "facade_drive"
+    libdir = os.path.join(root, "paper_1905_12154_b200")
+    r = subprocess.run(["g++", "-std=c++17", "-O2", "-I" + os.path.join(root, "include"),
+                        os.path.join(root, "tests", "cxx", "facade_drive.cpp"), "-L" + libdir,
+                        "-l:libbfm_b200.so", "-Wl,-rpath," + libdir, "-o", str(exe)],
+                       capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    run = subprocess.run([str(exe)], capture_output=True, text=True, timeout=300)
+    assert run.returncode == 0, run.stdout + run.stderr
