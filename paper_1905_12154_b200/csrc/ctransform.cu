@@ -261,11 +261,7 @@ __global__ void __launch_bounds__(1024) ct_pass_kernel(CtPass p) {
             if (p.a >= 2) G += g_approx(p.ax[1], g.k[1], static_cast<int>(ch[u] >> 16));
             const double* src = &p.phi[phi_index(p, g, ch[u], j)];
             cp_async8(&sm.fh[padj(j)], src);
-            if (DY) {
-              if (p.a > 0) sm.fl[padj(j)] = G;
-            } else {
-              if (p.a > 0) sm.chain[j] = ch[u];
-            }
+            if (!DY && p.a > 0) sm.chain[j] = ch[u];
           }
         }
       }
@@ -283,9 +279,16 @@ __global__ void __launch_bounds__(1024) ct_pass_kernel(CtPass p) {
         const double hy = 0.5 * y * y;
         double f, S;
         if (DY) {
+          // f~_j = fl((G_j + hs(y_j)) - phi_j) in place of phi_j (G exact)
           const double ph = s.fh[padj(j)];
-          const double G = p.a > 0 ? s.fl[padj(j)] : 0.0;
+          double G = 0.0;
+          if (p.a > 0) {
+            const uint32_t ch = p.state_in[g.base + static_cast<long>(j) * A.stride];
+            G = g_approx(p.ax[0], g.k[0], static_cast<int>(ch & 0xFFFFu));
+            if (p.a >= 2) G += g_approx(p.ax[1], g.k[1], static_cast<int>(ch >> 16));
+          }
           f = (G + hy) - ph;
+          s.fh[padj(j)] = f;
           S = fabs(ph) + G + hy;
         } else {
           const double ph = s.fh[padj(j)];
@@ -328,19 +331,15 @@ __global__ void __launch_bounds__(1024) ct_pass_kernel(CtPass p) {
   uint16_t* st = s.hidx + t * (C + 2);
   auto P_y = [&](int idx) { return coord(h, idx); };
   // f~_j: DY recomputes fl((G_j + hs(y_j)) - phi_j) from the stored exact parts
-  auto P_f = [&](int idx) {
-    if (DY) {
-      const double y = coord(h, idx);
-      const double G = p.a > 0 ? s.fl[padj(idx)] : 0.0;
-      return (G + 0.5 * y * y) - s.fh[padj(idx)];
-    }
-    return s.fh[padj(idx)];
-  };
-  // DY exact value V(k, j) = Gsum + (-phi_j), Gsum = G_j + g_a(k, j) exact.
-  auto dy_gsum = [&](int j, double xk) {
-    const double dl = xk - coord(h, j);
-    const double G = p.a > 0 ? s.fl[padj(j)] : 0.0;
-    return G + 0.5 * dl * dl;
+  auto P_f = [&](int idx) { return s.fh[padj(idx)]; };
+  // DY exact parts of candidate j, re-read from L2: G_j (exact) and phi_j.
+  auto dy_parts = [&](int j, double& G, double& ph) {
+    uint32_t ch = 0u;
+    if (p.a > 0) ch = p.state_in[geo.base + static_cast<long>(j) * A.stride];
+    G = 0.0;
+    if (p.a >= 1) G += g_approx(p.ax[0], geo.k[0], static_cast<int>(ch & 0xFFFFu));
+    if (p.a >= 2) G += g_approx(p.ax[1], geo.k[1], static_cast<int>(ch >> 16));
+    ph = p.phi[phi_index(p, geo, ch, j)];
   };
 
   // ---- 0. convex fast path: every interior point a certified strict corner?
@@ -508,7 +507,10 @@ __global__ void __launch_bounds__(1024) ct_pass_kernel(CtPass p) {
     // exact value V(k, j) rounded down (last pass)
     auto rd_value = [&](int j, int k, double xk) {
       if (DY) {
-        return bfmx::round_down2(dy_gsum(j, xk), -s.fh[padj(j)]);
+        double G, ph;
+        dy_parts(j, G, ph);
+        const double dl = xk - coord(h, j);
+        return bfmx::round_down2(G + 0.5 * dl * dl, -ph);
       } else {
         double tv[12];
         const uint32_t ch = p.a > 0 ? s.chain[j] : 0u;
@@ -552,7 +554,10 @@ __global__ void __launch_bounds__(1024) ct_pass_kernel(CtPass p) {
       int win = HH(L);
       double outv = 0.0;
       bool have_out = false;
-      if (!(L == R && convex_line)) {
+      // Single corner and no suspects on its two edges: it is the only candidate.
+      const bool lone = L == R && (convex_line || ((L == 0 || s.dlt[L - 1] == 0) &&
+                                                   (R >= hsz - 1 || s.dlt[R] == 0)));
+      if (!lone) {
         const int e0 = L > 0 ? L - 1 : 0;
         const int e1 = R < hsz - 1 ? R : hsz - 2;
         auto visit = [&](auto&& fn) {
@@ -585,8 +590,10 @@ __global__ void __launch_bounds__(1024) ct_pass_kernel(CtPass p) {
           double bh = 0.0, bl = 0.0;
           visit([&](int j) {
             if (Fhat(j, xk) > Fbest + Mc) return;
-            double vh, vl;
-            bfmx::two_sum(dy_gsum(j, xk), -s.fh[padj(j)], vh, vl);
+            double vh, vl, G, ph;
+            dy_parts(j, G, ph);
+            const double dl = xk - coord(h, j);
+            bfmx::two_sum(G + 0.5 * dl * dl, -ph, vh, vl);
             if (bestj >= 0 && (vh > bh || (vh == bh && vl >= bl))) return;
             bestj = j;
             bh = vh;
@@ -615,10 +622,41 @@ __global__ void __launch_bounds__(1024) ct_pass_kernel(CtPass p) {
       }
       BFM_DASSERT(win >= 0 && win < n);
       if (p.last) {
-        if (!have_out) outv = rd_value(win, k, xk);
-        p.out[geo.base + static_cast<long>(k) * A.stride] = outv;
+        if (have_out) {
+          p.out[geo.base + static_cast<long>(k) * A.stride] = outv;
+          res[k] = 0xffffu;  // done
+        } else if (DY) {
+          res[k] = static_cast<uint16_t>(win);  // batched below
+        } else {
+          p.out[geo.base + static_cast<long>(k) * A.stride] = rd_value(win, k, xk);
+          res[k] = 0xffffu;
+        }
       } else {
         res[k] = static_cast<uint16_t>(win);
+      }
+    }
+    if (DY && p.last) {
+      // batched final round-downs: independent L2 loads in flight
+      constexpr int kB = 8;
+      for (int k0 = j0; k0 < j1; k0 += kB) {
+        double G[kB], ph[kB];
+        int wv[kB];
+#pragma unroll
+        for (int u = 0; u < kB; ++u) {
+          const int k = k0 + u;
+          wv[u] = (k < j1) ? static_cast<int>(res[k]) : 0xffff;
+          G[u] = 0.0;
+          ph[u] = 0.0;
+          if (wv[u] != 0xffff) dy_parts(wv[u], G[u], ph[u]);
+        }
+#pragma unroll
+        for (int u = 0; u < kB; ++u) {
+          const int k = k0 + u;
+          if (wv[u] == 0xffff) continue;
+          const double dl = coord(h, k) - coord(h, wv[u]);
+          p.out[geo.base + static_cast<long>(k) * A.stride] =
+              bfmx::round_down2(G[u] + 0.5 * dl * dl, -ph[u]);
+        }
       }
     }
   }
@@ -745,8 +783,7 @@ void CtPlan::init(const GridDesc& g) {
     P.off_fv = o;
     o = align16(o + 8 * (n + n / 32 + 1));
     P.off_chain = o;  // DY: fl (double, padded); else chain (uint32)
-    if (dy && a > 0) o = align16(o + 8 * (n + n / 32 + 1));
-    else if (!dy && a > 0) o = align16(o + 4 * n);
+    if (!dy && a > 0) o = align16(o + 4 * n);
     P.off_hidx = o;
     o = align16(o + 2 * std::max(P.tpl * (P.C + 2), n));
     P.off_H = o;
