@@ -174,6 +174,8 @@ int bfm_solver_time_steps(bfm_solver* s, int k, double* ms);
 
 /* Test hook: device evaluation of the exact round-down of `count` sums of m
  * doubles each (terms row-major). Used by the parity tests only. */
+/* Test hook: c-transform diagnostic counters (needs env BFM_CT_STATS=1). */
+int bfm_debug_ct_stats(bfm_solver* s, unsigned long long* out8);
 int bfm_debug_round_down(const double* terms, int m, int count, double* out);
 
 const char* bfm_last_error(void);

@@ -666,6 +666,10 @@ int bfm_workspace_last_launches(const bfm_workspace* ws) { return ws->last_launc
 
 long bfm_solver_launches(const bfm_solver* s) { return s->ws.lc.count; }
 
+int bfm_debug_ct_stats(bfm_solver* s, unsigned long long* out8) {
+  return guard([&] { s->ws.ctp().stats(out8); });
+}
+
 int bfm_solver_time_steps(bfm_solver* s, int k, double* ms) {
   return guard([&] {
     s->ensure_probe();

@@ -29,6 +29,7 @@
 //  * The last pass rounds the winner's exact value down once.
 #include <cassert>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -498,7 +499,7 @@ __global__ void __launch_bounds__(1024) ct_pass_kernel(CtPass p) {
   group_sync(tpl, l);
 
   // ---- 5. queries ---------------------------------------------------------
-  if (active && j0 < j1) {
+  if (active) {
     auto Fhat = [&](int idx, double xk) { return P_f(idx) - xk * P_y(idx); };
     auto slope_ge = [&](int i, double xk) {
       const int a = HH(i), b = HH(i + 1);
@@ -518,17 +519,77 @@ __global__ void __launch_bounds__(1024) ct_pass_kernel(CtPass p) {
         return bfmx::round_down_sum(tv, m);
       }
     };
-    double xk = coord(h, j0);
-    int lo_i = 0, hi_i = hsz - 1;
-    while (lo_i < hi_i) {
-      const int mid = (lo_i + hi_i) >> 1;
-      if (slope_ge(mid, xk)) hi_i = mid;
-      else lo_i = mid + 1;
+    // ---- 5a. tangent corner of every query: balanced merge path of the
+    //          query slopes x_k against the hull-edge slopes (ties: query first)
+    {
+      const int E = hsz - 1;
+      const int total = n + E;
+      const int per = (total + tpl - 1) / tpl;
+      const int d0 = min(total, t * per), d1 = min(total, d0 + per);
+      if (d0 < d1) {
+        int lo = max(0, d0 - E), hi = min(d0, n);
+        while (lo < hi) {
+          const int q = (lo + hi) >> 1;
+          if (slope_ge(d0 - q - 1, coord(h, q))) lo = q + 1;
+          else hi = q;
+        }
+        int k = lo, i = d0 - lo;
+        for (int d = d0; d < d1; ++d) {
+          if (k < n && (i >= E || slope_ge(i, coord(h, k)))) {
+            res[k] = static_cast<uint16_t>(i);
+            ++k;
+          } else {
+            ++i;
+          }
+        }
+      }
     }
-    int i = lo_i;
-    for (int k = j0; k < j1; ++k) {
-      xk = coord(h, k);
-      while (i < hsz - 1 && !slope_ge(i, xk)) ++i;
+  }
+  group_sync(tpl, l);
+  // ---- 5b. uniform certification: the tangent corner is the only candidate
+  //          if both neighbours are beyond the walk margin and neither
+  //          adjacent edge holds suspects. Others are flagged (bit 15).
+  if (active) {
+    auto Fhat = [&](int idx, double xk) { return P_f(idx) - xk * P_y(idx); };
+    for (int k = t; k < n; k += tpl) {
+      const int i = res[k];
+      const double xk = coord(h, k);
+      const double F0 = Fhat(HH(i), xk);
+      const double Fl = i > 0 ? Fhat(HH(i - 1), xk) : INFINITY;
+      const double Fr = i < hsz - 1 ? Fhat(HH(i + 1), xk) : INFINITY;
+      const bool lone = Fl > F0 + Mw && Fr > F0 + Mw &&
+                        (convex_line || ((i == 0 || s.dlt[i - 1] == 0) &&
+                                         (i >= hsz - 1 || s.dlt[i] == 0)));
+      if (p.stats) {
+        atomicAdd(p.stats + 0, 1ull);
+        if (!lone) atomicAdd(p.stats + 1, 1ull);
+      }
+      res[k] = lone ? static_cast<uint16_t>(HH(i)) : static_cast<uint16_t>(i | 0x8000);
+    }
+  }
+  group_sync(tpl, l);
+  // ---- 5c. flagged queries: full resolution from their tangent corner
+  if (active) {
+    auto Fhat = [&](int idx, double xk) { return P_f(idx) - xk * P_y(idx); };
+    // exact value V(k, j) rounded down (last pass)
+    auto rd_value = [&](int j, int k, double xk) {
+      if (DY) {
+        double G, ph;
+        dy_parts(j, G, ph);
+        const double dl = xk - coord(h, j);
+        return bfmx::round_down2(G + 0.5 * dl * dl, -ph);
+      } else {
+        double tv[12];
+        const uint32_t ch = p.a > 0 ? s.chain[j] : 0u;
+        const int m = cand_terms(p, geo, ch, j, k, tv);
+        return bfmx::round_down_sum(tv, m);
+      }
+    };
+    for (int k = t; k < n; k += tpl) {
+      const int rv = res[k];
+      if (!(rv & 0x8000)) continue;
+      const int i = rv & 0x7fff;
+      const double xk = coord(h, k);
       int L = i;
       double Fmin = Fhat(HH(L), xk);
       while (L > 0) {
@@ -554,7 +615,6 @@ __global__ void __launch_bounds__(1024) ct_pass_kernel(CtPass p) {
       int win = HH(L);
       double outv = 0.0;
       bool have_out = false;
-      // Single corner and no suspects on its two edges: it is the only candidate.
       const bool lone = L == R && (convex_line || ((L == 0 || s.dlt[L - 1] == 0) &&
                                                    (R >= hsz - 1 || s.dlt[R] == 0)));
       if (!lone) {
@@ -565,12 +625,17 @@ __global__ void __launch_bounds__(1024) ct_pass_kernel(CtPass p) {
           if (convex_line) return;
           for (int e = e0; e <= e1; ++e) {
             const uint8_t code = s.dlt[e];
+            if (p.stats) atomicAdd(p.stats + 3, 1ull);
             if (code == 0) continue;
             const int a = HH(e), b = HH(e + 1);
             const double Fa = Fhat(a, xk), Fb = Fhat(b, xk);
             const double slack = slack_value(code, sref) + Mc;
             if (fmin(Fa, Fb) > Fmin + slack) continue;
             if (fabs(Fa - Fb) > slack * (1.000001 * (b - a)) + Mc) continue;
+            if (p.stats) {
+              atomicAdd(p.stats + 4, 1ull);
+              atomicAdd(p.stats + 5, static_cast<unsigned long long>(b - a - 1));
+            }
             for (int j = a + 1; j < b; ++j) fn(j);
           }
         };
@@ -622,41 +687,44 @@ __global__ void __launch_bounds__(1024) ct_pass_kernel(CtPass p) {
       }
       BFM_DASSERT(win >= 0 && win < n);
       if (p.last) {
-        if (have_out) {
-          p.out[geo.base + static_cast<long>(k) * A.stride] = outv;
-          res[k] = 0xffffu;  // done
-        } else if (DY) {
-          res[k] = static_cast<uint16_t>(win);  // batched below
-        } else {
-          p.out[geo.base + static_cast<long>(k) * A.stride] = rd_value(win, k, xk);
-          res[k] = 0xffffu;
-        }
+        if (!have_out) outv = rd_value(win, k, xk);
+        p.out[geo.base + static_cast<long>(k) * A.stride] = outv;
+        res[k] = 0xffffu;  // done
       } else {
         res[k] = static_cast<uint16_t>(win);
       }
     }
-    if (DY && p.last) {
-      // batched final round-downs: independent L2 loads in flight
-      constexpr int kB = 8;
-      for (int k0 = j0; k0 < j1; k0 += kB) {
-        double G[kB], ph[kB];
-        int wv[kB];
+  }
+  if (p.last && active) {
+    // lone queries: final round-downs, batched so the L2 loads overlap
+    constexpr int kB = 8;
+    for (int kk = t; kk < n; kk += kB * tpl) {
+      double G[kB], ph[kB];
+      int wv[kB];
 #pragma unroll
-        for (int u = 0; u < kB; ++u) {
-          const int k = k0 + u;
-          wv[u] = (k < j1) ? static_cast<int>(res[k]) : 0xffff;
-          G[u] = 0.0;
-          ph[u] = 0.0;
-          if (wv[u] != 0xffff) dy_parts(wv[u], G[u], ph[u]);
-        }
+      for (int u = 0; u < kB; ++u) {
+        const int k = kk + u * tpl;
+        wv[u] = (k < n) ? static_cast<int>(res[k]) : 0xffff;
+        G[u] = 0.0;
+        ph[u] = 0.0;
+        if (DY && wv[u] != 0xffff) dy_parts(wv[u], G[u], ph[u]);
+      }
 #pragma unroll
-        for (int u = 0; u < kB; ++u) {
-          const int k = k0 + u;
-          if (wv[u] == 0xffff) continue;
-          const double dl = coord(h, k) - coord(h, wv[u]);
-          p.out[geo.base + static_cast<long>(k) * A.stride] =
-              bfmx::round_down2(G[u] + 0.5 * dl * dl, -ph[u]);
+      for (int u = 0; u < kB; ++u) {
+        const int k = kk + u * tpl;
+        if (wv[u] == 0xffff) continue;
+        const double xk = coord(h, k);
+        double v;
+        if (DY) {
+          const double dl = xk - coord(h, wv[u]);
+          v = bfmx::round_down2(G[u] + 0.5 * dl * dl, -ph[u]);
+        } else {
+          double tv[12];
+          const uint32_t ch = p.a > 0 ? s.chain[wv[u]] : 0u;
+          const int m = cand_terms(p, geo, ch, wv[u], k, tv);
+          v = bfmx::round_down_sum(tv, m);
         }
+        p.out[geo.base + static_cast<long>(k) * A.stride] = v;
       }
     }
   }
@@ -705,6 +773,7 @@ CtPlan::~CtPlan() {
   for (auto* p : state_)
     if (p) cudaFree(p);
   if (slow_) cudaFree(slow_);
+  if (stats_) cudaFree(stats_);
 }
 
 void CtPlan::init(const GridDesc& g) {
@@ -759,6 +828,10 @@ void CtPlan::init(const GridDesc& g) {
   }
   BFM_CUDA(cudaMalloc(&slow_, sizeof(unsigned long long)));
   BFM_CUDA(cudaMemset(slow_, 0, sizeof(unsigned long long)));
+  if (getenv("BFM_CT_STATS")) {
+    BFM_CUDA(cudaMalloc(&stats_, 8 * sizeof(unsigned long long)));
+    BFM_CUDA(cudaMemset(stats_, 0, 8 * sizeof(unsigned long long)));
+  }
 
   int dev = 0;
   BFM_CUDA(cudaGetDevice(&dev));
@@ -802,6 +875,7 @@ void CtPlan::init(const GridDesc& g) {
     lpc = static_cast<int>(std::min<long>(lpc, P.nlines));
     P.lpc = std::max(lpc, 1);
     P.slow_queries = slow_;
+    P.stats = stats_;
   }
   BFM_CUDA(cudaFuncSetAttribute(ct_pass_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 budget));
@@ -828,6 +902,11 @@ void CtPlan::run(const double* d_phi, double* d_out, cudaStream_t stream, Launch
     BFM_LAUNCH_CHECK("ct_pass_kernel");
     if (lc) lc->add();
   }
+}
+
+void CtPlan::stats(unsigned long long* out8) {
+  for (int i = 0; i < 8; ++i) out8[i] = 0;
+  if (stats_) BFM_CUDA(cudaMemcpy(out8, stats_, 8 * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
 }
 
 unsigned long long CtPlan::slow_query_count() {

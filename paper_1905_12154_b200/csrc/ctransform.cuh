@@ -32,6 +32,7 @@ struct CtPass {
   int off_fv, off_chain, off_hidx, off_H, off_flag, off_lohi, off_scal, line_bytes;
   // statistics (device counters, may be null): lines that needed exact resolution
   unsigned long long* slow_queries;
+  unsigned long long* stats;  // optional diagnostics (env BFM_CT_STATS=1)
 };
 
 class CtPlan {
@@ -46,6 +47,7 @@ class CtPlan {
   // (may not alias). Enqueues g.d kernels on stream.
   void run(const double* d_phi, double* d_out, cudaStream_t stream, LaunchCounter* lc);
   unsigned long long slow_query_count();  // diagnostic (synchronous)
+  void stats(unsigned long long* out8);     // diagnostic counters (synchronous)
   const GridDesc& grid() const { return g_; }
 
  private:
@@ -54,6 +56,7 @@ class CtPlan {
   double4* tables_[3] = {nullptr, nullptr, nullptr};
   uint32_t* state_[2] = {nullptr, nullptr};
   unsigned long long* slow_ = nullptr;
+  unsigned long long* stats_ = nullptr;
   CtPass pass_[3] = {};
   bool ready_ = false;
   bool dyadic_ = false;
