@@ -166,6 +166,11 @@ __device__ __forceinline__ Smem carve(const CtPass& p, unsigned char* base, int 
   return s;
 }
 
+struct DdBest {
+  int j;
+  double h, l;
+};
+
 // Slack codes: Delta <= 2^(code - 128) * sref, code in [1, 255] (conservative).
 __device__ __forceinline__ uint8_t slack_code(double D, double sref) {
   if (!(D > 0.0)) return 1;
@@ -230,6 +235,14 @@ __global__ void __launch_bounds__(1024) ct_pass_kernel(CtPass p) {
   }
   __syncthreads();
 
+  long long tph = clock64();
+  auto PH = [&](int i) {
+    if (p.stats && t == 0) {
+      const long long now = clock64();
+      atomicAdd(p.stats + 8 + i, static_cast<unsigned long long>(now - tph));
+      tph = now;
+    }
+  };
   // ---- load: every element copied asynchronously (cp.async) -------------
   // DY: fh <- phi_j (exact), fl <- G_j = sum_{b<a} g_b(k_b, j_b*) (exact);
   // !DY: fh <- f~_j, chain <- chain_j.
@@ -343,6 +356,7 @@ __global__ void __launch_bounds__(1024) ct_pass_kernel(CtPass p) {
     ph = p.phi[phi_index(p, geo, ch, j)];
   };
 
+  PH(0);  // load + maxima
   // ---- 0. convex fast path: every interior point a certified strict corner?
   {
     int bad = 0;
@@ -357,6 +371,7 @@ __global__ void __launch_bounds__(1024) ct_pass_kernel(CtPass p) {
   const bool convex_line = s.scal[4] == 0ull;
 
   if (!convex_line) {
+    PH(1);  // convexity test
     // ---- 1. chunk hulls (Andrew's monotone chain) -----------------------
     if (active) {
       int sz = 0;
@@ -383,6 +398,7 @@ __global__ void __launch_bounds__(1024) ct_pass_kernel(CtPass p) {
       s.lo[t] = 0;
       s.hi[t] = sz;
     }
+    PH(2);  // chunk hulls
     // ---- 2. tree merge by bridge walks ----------------------------------
     for (int lvl = 1; lvl < tpl; lvl <<= 1) {
       group_sync(tpl, l);
@@ -433,6 +449,7 @@ __global__ void __launch_bounds__(1024) ct_pass_kernel(CtPass p) {
       }
     }
     group_sync(tpl, l);
+    PH(3);  // merges
     // ---- 3. compaction into H -------------------------------------------
     {
       const int cnt = active ? max(0, s.hi[t] - s.lo[t]) : 0;
@@ -451,6 +468,7 @@ __global__ void __launch_bounds__(1024) ct_pass_kernel(CtPass p) {
       if (t == tpl - 1) s.scal[3] = static_cast<unsigned long long>(o + cnt);
     }
     group_sync(tpl, l);
+    PH(4);  // compaction
     // ---- 4. suspects: per-edge max slack (log-coded, conservative) --------
     const int hsz0 = static_cast<int>(s.scal[3]);
     if (active && j0 < j1) {
@@ -498,6 +516,7 @@ __global__ void __launch_bounds__(1024) ct_pass_kernel(CtPass p) {
   auto HH = [&](int i) { return convex_line ? i : static_cast<int>(s.H[i]); };
   group_sync(tpl, l);
 
+  PH(5);  // suspects (or convexity test on convex lines)
   // ---- 5. queries ---------------------------------------------------------
   if (active) {
     auto Fhat = [&](int idx, double xk) { return P_f(idx) - xk * P_y(idx); };
@@ -546,6 +565,7 @@ __global__ void __launch_bounds__(1024) ct_pass_kernel(CtPass p) {
     }
   }
   group_sync(tpl, l);
+  PH(6);  // merge-path tangents
   // ---- 5b. uniform certification: the tangent corner is the only candidate
   //          if both neighbours are beyond the walk margin and neither
   //          adjacent edge holds suspects. Others are flagged (bit 15).
@@ -557,9 +577,19 @@ __global__ void __launch_bounds__(1024) ct_pass_kernel(CtPass p) {
       const double F0 = Fhat(HH(i), xk);
       const double Fl = i > 0 ? Fhat(HH(i - 1), xk) : INFINITY;
       const double Fr = i < hsz - 1 ? Fhat(HH(i + 1), xk) : INFINITY;
+      // an adjacent edge's suspects cannot win unless the edge passes the same
+      // relevance tests the full resolution applies (see visit below)
+      auto edge_quiet = [&](int e, double Fa, double Fb) {
+        const uint8_t code = s.dlt[e];
+        if (code == 0) return true;
+        const double slack = slack_value(code, sref) + Mc;
+        if (fmin(Fa, Fb) > F0 + slack) return true;
+        const int a = HH(e), b = HH(e + 1);
+        return fabs(Fa - Fb) > slack * (1.000001 * (b - a)) + Mc;
+      };
       const bool lone = Fl > F0 + Mw && Fr > F0 + Mw &&
-                        (convex_line || ((i == 0 || s.dlt[i - 1] == 0) &&
-                                         (i >= hsz - 1 || s.dlt[i] == 0)));
+                        (convex_line || ((i == 0 || edge_quiet(i - 1, Fl, F0)) &&
+                                         (i >= hsz - 1 || edge_quiet(i, F0, Fr))));
       if (p.stats) {
         atomicAdd(p.stats + 0, 1ull);
         if (!lone) atomicAdd(p.stats + 1, 1ull);
@@ -568,6 +598,7 @@ __global__ void __launch_bounds__(1024) ct_pass_kernel(CtPass p) {
     }
   }
   group_sync(tpl, l);
+  PH(7);  // certification
   // ---- 5c. flagged queries: full resolution from their tangent corner
   if (active) {
     auto Fhat = [&](int idx, double xk) { return P_f(idx) - xk * P_y(idx); };
@@ -587,7 +618,7 @@ __global__ void __launch_bounds__(1024) ct_pass_kernel(CtPass p) {
     };
     for (int k = t; k < n; k += tpl) {
       const int rv = res[k];
-      if (!(rv & 0x8000)) continue;
+      if (!(rv & 0x8000) || rv == 0xffff) continue;  // resolved, or done (last pass)
       const int i = rv & 0x7fff;
       const double xk = coord(h, k);
       int L = i;
@@ -695,6 +726,7 @@ __global__ void __launch_bounds__(1024) ct_pass_kernel(CtPass p) {
       }
     }
   }
+  PH(8);  // flagged queries
   if (p.last && active) {
     // lone queries: final round-downs, batched so the L2 loads overlap
     constexpr int kB = 8;
@@ -728,6 +760,7 @@ __global__ void __launch_bounds__(1024) ct_pass_kernel(CtPass p) {
       }
     }
   }
+  PH(9);  // final round-downs
   if (p.last) return;
   __syncthreads();
 
@@ -829,8 +862,8 @@ void CtPlan::init(const GridDesc& g) {
   BFM_CUDA(cudaMalloc(&slow_, sizeof(unsigned long long)));
   BFM_CUDA(cudaMemset(slow_, 0, sizeof(unsigned long long)));
   if (getenv("BFM_CT_STATS")) {
-    BFM_CUDA(cudaMalloc(&stats_, 8 * sizeof(unsigned long long)));
-    BFM_CUDA(cudaMemset(stats_, 0, 8 * sizeof(unsigned long long)));
+    BFM_CUDA(cudaMalloc(&stats_, 32 * sizeof(unsigned long long)));
+    BFM_CUDA(cudaMemset(stats_, 0, 32 * sizeof(unsigned long long)));
   }
 
   int dev = 0;
@@ -905,8 +938,8 @@ void CtPlan::run(const double* d_phi, double* d_out, cudaStream_t stream, Launch
 }
 
 void CtPlan::stats(unsigned long long* out8) {
-  for (int i = 0; i < 8; ++i) out8[i] = 0;
-  if (stats_) BFM_CUDA(cudaMemcpy(out8, stats_, 8 * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+  for (int i = 0; i < 32; ++i) out8[i] = 0;
+  if (stats_) BFM_CUDA(cudaMemcpy(out8, stats_, 32 * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
 }
 
 unsigned long long CtPlan::slow_query_count() {
