@@ -71,21 +71,21 @@ BFM_HD cplx csub(cplx a, cplx b) { return cplx{a.re - b.re, a.im - b.im}; }
 // Number of butterflies in stage s.
 BFM_HD int stage_butterflies(const LinePlan& p, int s) { return p.m / p.radix[s]; }
 
-// Arithmetic of one DIF butterfly (radix r, elements base + t*q, twiddle
-// exponent tw for output digit 1). Index math is left to the caller so the
-// GPU can use cheaper integer arithmetic; the double operations are shared.
-BFM_HD void butterfly_core(const LinePlan& p, int r, int base, int q, int tw, cplx* z,
-                           bool inverse) {
+// Arithmetic of one DIF butterfly of radix r on x[0..r) (in place), twiddle
+// exponent tw for output digit 1. Shared verbatim by the CPU shim (through
+// butterfly_core) and the GPU's register-resident fused stages, so both
+// evaluate the same IEEE operations.
+BFM_HD void butterfly_regs(const LinePlan& p, int r, cplx* x, int tw, bool inverse) {
   const int m = p.m;
   if (r == 2) {
-    const cplx a = z[base];
-    const cplx c = z[base + q];
-    z[base] = cadd(a, c);
+    const cplx a = x[0];
+    const cplx c = x[1];
+    x[0] = cadd(a, c);
     const cplx d = csub(a, c);
     const cplx w = p.wm[tw];
-    z[base + q] = inverse ? cmulc(d, w) : cmul(d, w);
+    x[1] = inverse ? cmulc(d, w) : cmul(d, w);
   } else if (r == 4) {
-    const cplx x0 = z[base], x1 = z[base + q], x2 = z[base + 2 * q], x3 = z[base + 3 * q];
+    const cplx x0 = x[0], x1 = x[1], x2 = x[2], x3 = x[3];
     const cplx a0 = cadd(x0, x2), a1 = csub(x0, x2);
     const cplx b0 = cadd(x1, x3), b1 = csub(x1, x3);
     // forward: y1 = a1 - i b1, y3 = a1 + i b1; inverse swaps the rotation.
@@ -94,7 +94,7 @@ BFM_HD void butterfly_core(const LinePlan& p, int r, int base, int q, int tw, cp
     const cplx y2 = csub(a0, b0);
     const cplx y1 = inverse ? cadd(a1, ib1) : csub(a1, ib1);
     const cplx y3 = inverse ? csub(a1, ib1) : cadd(a1, ib1);
-    z[base] = y0;
+    x[0] = y0;
     int t2 = 2 * tw;
     if (t2 >= m) t2 -= m;
     int t3 = t2 + tw;
@@ -103,16 +103,16 @@ BFM_HD void butterfly_core(const LinePlan& p, int r, int base, int q, int tw, cp
     const cplx w2 = p.wm[t2];
     const cplx w3 = p.wm[t3];
     if (inverse) {
-      z[base + q] = cmulc(y1, w1);
-      z[base + 2 * q] = cmulc(y2, w2);
-      z[base + 3 * q] = cmulc(y3, w3);
+      x[1] = cmulc(y1, w1);
+      x[2] = cmulc(y2, w2);
+      x[3] = cmulc(y3, w3);
     } else {
-      z[base + q] = cmul(y1, w1);
-      z[base + 2 * q] = cmul(y2, w2);
-      z[base + 3 * q] = cmul(y3, w3);
+      x[1] = cmul(y1, w1);
+      x[2] = cmul(y2, w2);
+      x[3] = cmul(y3, w3);
     }
   } else {  // r == 3
-    const cplx x0 = z[base], x1 = z[base + q], x2 = z[base + 2 * q];
+    const cplx x0 = x[0], x1 = x[1], x2 = x[2];
     const cplx t1 = cadd(x1, x2);
     const cplx y0 = cadd(x0, t1);
     const cplx t2c{x0.re - 0.5 * t1.re, x0.im - 0.5 * t1.im};
@@ -123,19 +123,28 @@ BFM_HD void butterfly_core(const LinePlan& p, int r, int base, int q, int tw, cp
     // forward: y1 = t2 - i u, y2 = t2 + i u.
     const cplx y1 = inverse ? cadd(t2c, iu) : csub(t2c, iu);
     const cplx y2 = inverse ? csub(t2c, iu) : cadd(t2c, iu);
-    z[base] = y0;
+    x[0] = y0;
     int t2 = 2 * tw;
     if (t2 >= m) t2 -= m;
     const cplx w1 = p.wm[tw];
     const cplx w2 = p.wm[t2];
     if (inverse) {
-      z[base + q] = cmulc(y1, w1);
-      z[base + 2 * q] = cmulc(y2, w2);
+      x[1] = cmulc(y1, w1);
+      x[2] = cmulc(y2, w2);
     } else {
-      z[base + q] = cmul(y1, w1);
-      z[base + 2 * q] = cmul(y2, w2);
+      x[1] = cmul(y1, w1);
+      x[2] = cmul(y2, w2);
     }
   }
+}
+
+// One DIF butterfly on z[base + t*q], t < r (in place).
+BFM_HD void butterfly_core(const LinePlan& p, int r, int base, int q, int tw, cplx* z,
+                           bool inverse) {
+  cplx x[4];
+  for (int t = 0; t < r; ++t) x[t] = z[base + t * q];
+  butterfly_regs(p, r, x, tw, inverse);
+  for (int t = 0; t < r; ++t) z[base + t * q] = x[t];
 }
 
 // One DIF butterfly of stage s on the complex buffer z (in place).

@@ -32,7 +32,10 @@ struct PoisArgs {
   const double* lam1;
   const double* lam2;
   double scale;
-  unsigned qmagic[bfmdct::kMaxStages];
+  int npass;
+  int pstage[bfmdct::kMaxStages];
+  int pfused[bfmdct::kMaxStages];
+  unsigned pmagic[bfmdct::kMaxStages];  // division by q1 (fused) or q (single)
 };
 
 __device__ __forceinline__ void gsync(int tpl, int l) {
@@ -57,21 +60,85 @@ __device__ __forceinline__ double divide(const PoisArgs& a, double v, int k, dou
   return lam == 0.0 ? 0.0 : v / (lam * a.scale);
 }
 
-// Stage loop with division by q through a precomputed 32-bit magic number.
+// FFT passes: pairs of consecutive DIF stages are fused so a thread keeps
+// R0*R1 points in registers across both stages (one shared-memory round trip
+// per pass instead of per stage). Each butterfly is butterfly_regs, the same
+// arithmetic the CPU shim runs stage by stage.
+template <int R0, int R1>
+__device__ __forceinline__ void fused_pass(const PoisArgs& a, cplx* z, int s, int pi, bool inverse,
+                                           int t, int tpl) {
+  const bfmdct::LinePlan& P = a.ax.plan;
+  const int L0 = P.span[s];
+  const int q0 = L0 / R0, q1 = q0 / R1;
+  const int twm0 = P.m / L0, twm1 = P.m / q0;
+  const int ng = P.m / (R0 * R1);
+  const unsigned magic = a.pmagic[pi];
+  for (int g = t; g < ng; g += tpl) {
+    const int blk = magic ? static_cast<int>(__umulhi(static_cast<unsigned>(g), magic)) : g;
+    const int jpp = g - blk * q1;
+    const int base = blk * L0 + jpp;
+    cplx x[R0 * R1];
+#pragma unroll
+    for (int aa = 0; aa < R0; ++aa)
+#pragma unroll
+      for (int bb = 0; bb < R1; ++bb) x[aa * R1 + bb] = z[base + aa * q0 + bb * q1];
+#pragma unroll
+    for (int bb = 0; bb < R1; ++bb) {
+      cplx col[R0];
+#pragma unroll
+      for (int aa = 0; aa < R0; ++aa) col[aa] = x[aa * R1 + bb];
+      bfmdct::butterfly_regs(P, R0, col, twm0 * (jpp + bb * q1), inverse);
+#pragma unroll
+      for (int aa = 0; aa < R0; ++aa) x[aa * R1 + bb] = col[aa];
+    }
+#pragma unroll
+    for (int aa = 0; aa < R0; ++aa) bfmdct::butterfly_regs(P, R1, x + aa * R1, twm1 * jpp, inverse);
+#pragma unroll
+    for (int aa = 0; aa < R0; ++aa)
+#pragma unroll
+      for (int bb = 0; bb < R1; ++bb) z[base + aa * q0 + bb * q1] = x[aa * R1 + bb];
+  }
+}
+
+template <int R>
+__device__ __forceinline__ void single_pass(const PoisArgs& a, cplx* z, int s, int pi, bool inverse,
+                                            int t, int tpl) {
+  const bfmdct::LinePlan& P = a.ax.plan;
+  const int L = P.span[s];
+  const int q = L / R;
+  const int twm = P.m / L;
+  const int nb = P.m / R;
+  const unsigned magic = a.pmagic[pi];
+  for (int b = t; b < nb; b += tpl) {
+    const int blk = magic ? static_cast<int>(__umulhi(static_cast<unsigned>(b), magic)) : b;
+    const int j = b - blk * q;
+    const int base = blk * L + j;
+    cplx x[R];
+#pragma unroll
+    for (int u = 0; u < R; ++u) x[u] = z[base + u * q];
+    bfmdct::butterfly_regs(P, R, x, twm * j, inverse);
+#pragma unroll
+    for (int u = 0; u < R; ++u) z[base + u * q] = x[u];
+  }
+}
+
 __device__ __forceinline__ void fft_stages(const PoisArgs& a, cplx* z, bool inverse, int t,
                                            int tpl, int l) {
   const bfmdct::LinePlan& P = a.ax.plan;
-  for (int s = 0; s < P.nstages; ++s) {
-    const int r = P.radix[s];
-    const int L = P.span[s];
-    const int q = L / r;
-    const unsigned magic = a.qmagic[s];
-    const int twmul = P.m / L;
-    const int nb = P.m / r;
-    for (int b = t; b < nb; b += tpl) {
-      const int blk = magic ? static_cast<int>(__umulhi(static_cast<unsigned>(b), magic)) : b;
-      const int j = b - blk * q;
-      bfmdct::butterfly_core(P, r, blk * L + j, q, twmul * j, z, inverse);
+  for (int pi = 0; pi < a.npass; ++pi) {
+    const int s = a.pstage[pi];
+    const int r0 = P.radix[s];
+    if (a.pfused[pi]) {
+      const int r1 = P.radix[s + 1];
+      if (r0 == 4 && r1 == 4) fused_pass<4, 4>(a, z, s, pi, inverse, t, tpl);
+      else if (r0 == 4 && r1 == 2) fused_pass<4, 2>(a, z, s, pi, inverse, t, tpl);
+      else if (r0 == 4 && r1 == 3) fused_pass<4, 3>(a, z, s, pi, inverse, t, tpl);
+      else if (r0 == 2 && r1 == 3) fused_pass<2, 3>(a, z, s, pi, inverse, t, tpl);
+      else fused_pass<3, 3>(a, z, s, pi, inverse, t, tpl);
+    } else {
+      if (r0 == 4) single_pass<4>(a, z, s, pi, inverse, t, tpl);
+      else if (r0 == 2) single_pass<2>(a, z, s, pi, inverse, t, tpl);
+      else single_pass<3>(a, z, s, pi, inverse, t, tpl);
     }
     gsync(tpl, l);
   }
@@ -134,7 +201,7 @@ __global__ void __launch_bounds__(512) pois_fft_kernel(PoisArgs a) {
       }
     gsync(tpl, l);
     if (active) fft_stages(a, zB, true, t, tpl, l);
-    else for (int s = 0; s < P.nstages; ++s) gsync(tpl, l);
+    else for (int s = 0; s < a.npass; ++s) gsync(tpl, l);
     if (active)
       for (int q = t; q < m; q += tpl) {
         const cplx v = zB[P.rev[q]];
@@ -144,7 +211,7 @@ __global__ void __launch_bounds__(512) pois_fft_kernel(PoisArgs a) {
     outbuf = zAd;
   } else {
     if (active) fft_stages(a, zA, false, t, tpl, l);
-    else for (int s = 0; s < P.nstages; ++s) gsync(tpl, l);
+    else for (int s = 0; s < a.npass; ++s) gsync(tpl, l);
     if (a.mode == kFwd) {
       if (active)
         for (int k = t; k <= m; k += tpl) {
@@ -178,7 +245,7 @@ __global__ void __launch_bounds__(512) pois_fft_kernel(PoisArgs a) {
         }
       gsync(tpl, l);
       if (active) fft_stages(a, zB, true, t, tpl, l);
-      else for (int s = 0; s < P.nstages; ++s) gsync(tpl, l);
+      else for (int s = 0; s < a.npass; ++s) gsync(tpl, l);
       if (active)
         for (int q = t; q < m; q += tpl) {
           const cplx v = zB[P.rev[q]];
@@ -320,7 +387,7 @@ void PoissonPlan::init(const GridDesc& g) {
     c.strided = a != g.d - 1;
     if (H.plan.kind == bfmdct::kFft) {
       const int m = H.plan.m;
-      int tpl = (m + 7) / 8;
+      int tpl = (m + 15) / 16;
       tpl = ((tpl + 31) / 32) * 32;
       if (tpl < 32) tpl = 32;
       if (tpl > 256) tpl = 256;
@@ -364,9 +431,16 @@ void PoissonPlan::solve(const double* d_rhs, double* d_out, cudaStream_t stream,
     A.lam2 = d > 2 ? lam_[2] : nullptr;
     A.scale = scale_;
     const PoisAxisCfg& c = cfg_[axis];
-    for (int st = 0; st < c.plan.nstages; ++st) {
-      const unsigned q = static_cast<unsigned>(c.plan.span[st] / c.plan.radix[st]);
-      A.qmagic[st] = q == 1 ? 0u : static_cast<unsigned>((0x100000000ULL + q - 1) / q);
+    A.npass = 0;
+    for (int st = 0; st < c.plan.nstages;) {
+      const bool fuse = st + 1 < c.plan.nstages;
+      const int q0 = c.plan.span[st] / c.plan.radix[st];
+      const unsigned q = static_cast<unsigned>(fuse ? q0 / c.plan.radix[st + 1] : q0);
+      A.pstage[A.npass] = st;
+      A.pfused[A.npass] = fuse ? 1 : 0;
+      A.pmagic[A.npass] = q == 1 ? 0u : static_cast<unsigned>((0x100000000ULL + q - 1) / q);
+      ++A.npass;
+      st += fuse ? 2 : 1;
     }
     const long blocks = (c.nlines + c.lpc - 1) / c.lpc;
     const size_t sm = static_cast<size_t>(c.lpc) * c.line_bytes;
