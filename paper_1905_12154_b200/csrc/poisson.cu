@@ -38,6 +38,16 @@ struct PoisArgs {
   unsigned pmagic[bfmdct::kMaxStages];  // division by q1 (fused) or q (single)
 };
 
+// Shared-memory layout of a line: complex slot i lives at sw(i), an XOR
+// swizzle of the low three bits (8 complex = 128 B = all 32 banks) with
+// higher index bits. It makes the strided butterfly groups of the late FFT
+// stages and the digit-reversed gathers of the unpack/post phases (nearly)
+// conflict-free for 2^a 3^b line lengths. The double view of the same
+// buffer keeps the two halves of a complex slot adjacent.
+__device__ __forceinline__ int sw(int i) { return i ^ (((i >> 4) ^ (i >> 5) ^ (i >> 8)) & 7); }
+__device__ __forceinline__ double& dref(double* zd, int j) { return zd[2 * sw(j >> 1) + (j & 1)]; }
+__device__ __forceinline__ cplx& cref(cplx* z, int i) { return z[sw(i)]; }
+
 __device__ __forceinline__ void gsync(int tpl, int l) {
   if (tpl <= 32) {
     __syncwarp();
@@ -81,7 +91,7 @@ __device__ __forceinline__ void fused_pass(const PoisArgs& a, cplx* z, int s, in
 #pragma unroll
     for (int aa = 0; aa < R0; ++aa)
 #pragma unroll
-      for (int bb = 0; bb < R1; ++bb) x[aa * R1 + bb] = z[base + aa * q0 + bb * q1];
+      for (int bb = 0; bb < R1; ++bb) x[aa * R1 + bb] = cref(z, base + aa * q0 + bb * q1);
 #pragma unroll
     for (int bb = 0; bb < R1; ++bb) {
       cplx col[R0];
@@ -96,7 +106,7 @@ __device__ __forceinline__ void fused_pass(const PoisArgs& a, cplx* z, int s, in
 #pragma unroll
     for (int aa = 0; aa < R0; ++aa)
 #pragma unroll
-      for (int bb = 0; bb < R1; ++bb) z[base + aa * q0 + bb * q1] = x[aa * R1 + bb];
+      for (int bb = 0; bb < R1; ++bb) cref(z, base + aa * q0 + bb * q1) = x[aa * R1 + bb];
   }
 }
 
@@ -115,10 +125,10 @@ __device__ __forceinline__ void single_pass(const PoisArgs& a, cplx* z, int s, i
     const int base = blk * L + j;
     cplx x[R];
 #pragma unroll
-    for (int u = 0; u < R; ++u) x[u] = z[base + u * q];
+    for (int u = 0; u < R; ++u) x[u] = cref(z, base + u * q);
     bfmdct::butterfly_regs(P, R, x, twm * j, inverse);
 #pragma unroll
-    for (int u = 0; u < R; ++u) z[base + u * q] = x[u];
+    for (int u = 0; u < R; ++u) cref(z, base + u * q) = x[u];
   }
 }
 
@@ -167,18 +177,32 @@ __global__ void __launch_bounds__(512) pois_fft_kernel(PoisArgs a) {
   {
     const long base = s_base[ml];
     double* zA = reinterpret_cast<double*>(smem + static_cast<long>(ml) * ax.line_bytes);
+    // batches of kLoadBatch independent loads per thread keep enough bytes in
+    // flight to cover HBM latency with one CTA per SM
+    constexpr int kLoadBatch = 8;
     if (base >= 0)
-      for (int j = first; j < n; j += step) {
-        const double v = a.in[base + static_cast<long>(j) * ax.stride];
-        if (a.mode == kInv) zA[j] = v;
-        else zA[bfmdct::dct2_vpos(P, j)] = v;
+      for (int j0 = first; j0 < n; j0 += kLoadBatch * step) {
+        double v[kLoadBatch];
+#pragma unroll
+        for (int u = 0; u < kLoadBatch; ++u) {
+          const int j = j0 + u * step;
+          v[u] = j < n ? a.in[base + static_cast<long>(j) * ax.stride] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < kLoadBatch; ++u) {
+          const int j = j0 + u * step;
+          if (j < n) {
+            if (a.mode == kInv) dref(zA, j) = v[u];
+            else dref(zA, bfmdct::dct2_vpos(P, j)) = v[u];
+          }
+        }
       }
   }
   __syncthreads();
   const long lbase = s_base[l];
   const bool active = lbase >= 0;
   double* zAd = reinterpret_cast<double*>(smem + static_cast<long>(l) * ax.line_bytes);
-  double* zBd = zAd + n;
+  double* zBd = zAd + 2 * ax.cslots;
   cplx* zA = reinterpret_cast<cplx*>(zAd);
   cplx* zB = reinterpret_cast<cplx*>(zBd);
   double l1v = 0.0, l2v = 0.0;
@@ -194,19 +218,19 @@ __global__ void __launch_bounds__(512) pois_fft_kernel(PoisArgs a) {
   if (a.mode == kInv) {
     if (active)
       for (int k = t; k < m; k += tpl) {
-        const cplx A = bfmdct::dct3_V_vals(P, zAd[k], k == 0 ? 0.0 : zAd[n - k], k);
+        const cplx A = bfmdct::dct3_V_vals(P, dref(zAd, k), k == 0 ? 0.0 : dref(zAd, n - k), k);
         const int km = m - k;
-        const cplx B = bfmdct::dct3_V_vals(P, zAd[km], zAd[n - km], km);
-        zB[k] = bfmdct::dct3_pre_vals(P, A, B, k);
+        const cplx B = bfmdct::dct3_V_vals(P, dref(zAd, km), dref(zAd, n - km), km);
+        cref(zB, k) = bfmdct::dct3_pre_vals(P, A, B, k);
       }
     gsync(tpl, l);
     if (active) fft_stages(a, zB, true, t, tpl, l);
     else for (int s = 0; s < a.npass; ++s) gsync(tpl, l);
     if (active)
       for (int q = t; q < m; q += tpl) {
-        const cplx v = zB[P.rev[q]];
-        zAd[bfmdct::dct3_ypos(P, 2 * q)] = v.re;
-        zAd[bfmdct::dct3_ypos(P, 2 * q + 1)] = v.im;
+        const cplx v = cref(zB, P.rev[q]);
+        dref(zAd, bfmdct::dct3_ypos(P, 2 * q)) = v.re;
+        dref(zAd, bfmdct::dct3_ypos(P, 2 * q + 1)) = v.im;
       }
     outbuf = zAd;
   } else {
@@ -216,10 +240,10 @@ __global__ void __launch_bounds__(512) pois_fft_kernel(PoisArgs a) {
       if (active)
         for (int k = t; k <= m; k += tpl) {
           double yk, ynk;
-          bfmdct::dct2_unpack_vals(P, zA[P.rev[k == m ? 0 : k]], zA[P.rev[k == 0 ? 0 : m - k]], k,
-                                   yk, ynk);
-          zBd[k] = yk;
-          if (k > 0 && k < m) zBd[n - k] = ynk;
+          bfmdct::dct2_unpack_vals(P, cref(zA, P.rev[k == m ? 0 : k]),
+                                   cref(zA, P.rev[k == 0 ? 0 : m - k]), k, yk, ynk);
+          dref(zBd, k) = yk;
+          if (k > 0 && k < m) dref(zBd, n - k) = ynk;
         }
       outbuf = zBd;
     } else {
@@ -228,10 +252,10 @@ __global__ void __launch_bounds__(512) pois_fft_kernel(PoisArgs a) {
         for (int k = t; k <= half; k += tpl) {
           const int km = m - k;
           double yk, ynk, ykm, ynkm;
-          bfmdct::dct2_unpack_vals(P, zA[P.rev[k == m ? 0 : k]], zA[P.rev[k == 0 ? 0 : m - k]], k,
-                                   yk, ynk);
-          bfmdct::dct2_unpack_vals(P, zA[P.rev[km == m ? 0 : km]],
-                                   zA[P.rev[km == 0 ? 0 : m - km]], km, ykm, ynkm);
+          bfmdct::dct2_unpack_vals(P, cref(zA, P.rev[k == m ? 0 : k]),
+                                   cref(zA, P.rev[k == 0 ? 0 : m - k]), k, yk, ynk);
+          bfmdct::dct2_unpack_vals(P, cref(zA, P.rev[km == m ? 0 : km]),
+                                   cref(zA, P.rev[km == 0 ? 0 : m - km]), km, ykm, ynkm);
           const double xk = divide(a, yk, k, l1v, l2v);
           const double xnk = (k > 0 && k < m) ? divide(a, ynk, n - k, l1v, l2v) : 0.0;
           const double xkm = divide(a, ykm, km, l1v, l2v);
@@ -240,17 +264,17 @@ __global__ void __launch_bounds__(512) pois_fft_kernel(PoisArgs a) {
           const double b_km = km == m ? xkm : xnkm;
           const cplx Vk = bfmdct::dct3_V_vals(P, xk, b_k, k);
           const cplx Vkm = bfmdct::dct3_V_vals(P, xkm, b_km, km);
-          zB[k] = bfmdct::dct3_pre_vals(P, Vk, Vkm, k);
-          if (km < m && km != k) zB[km] = bfmdct::dct3_pre_vals(P, Vkm, Vk, km);
+          cref(zB, k) = bfmdct::dct3_pre_vals(P, Vk, Vkm, k);
+          if (km < m && km != k) cref(zB, km) = bfmdct::dct3_pre_vals(P, Vkm, Vk, km);
         }
       gsync(tpl, l);
       if (active) fft_stages(a, zB, true, t, tpl, l);
       else for (int s = 0; s < a.npass; ++s) gsync(tpl, l);
       if (active)
         for (int q = t; q < m; q += tpl) {
-          const cplx v = zB[P.rev[q]];
-          zAd[bfmdct::dct3_ypos(P, 2 * q)] = v.re;
-          zAd[bfmdct::dct3_ypos(P, 2 * q + 1)] = v.im;
+          const cplx v = cref(zB, P.rev[q]);
+          dref(zAd, bfmdct::dct3_ypos(P, 2 * q)) = v.re;
+          dref(zAd, bfmdct::dct3_ypos(P, 2 * q + 1)) = v.im;
         }
       outbuf = zAd;
     }
@@ -259,10 +283,10 @@ __global__ void __launch_bounds__(512) pois_fft_kernel(PoisArgs a) {
   // store (coalesced)
   {
     const long base = s_base[ml];
-    const double* src = reinterpret_cast<const double*>(smem + static_cast<long>(ml) * ax.line_bytes) +
-                        (outbuf == zAd ? 0 : n);
+    double* src = reinterpret_cast<double*>(smem + static_cast<long>(ml) * ax.line_bytes) +
+                  (outbuf == zAd ? 0 : 2 * ax.cslots);
     if (base >= 0)
-      for (int j = first; j < n; j += step) a.out[base + static_cast<long>(j) * ax.stride] = src[j];
+      for (int j = first; j < n; j += step) a.out[base + static_cast<long>(j) * ax.stride] = dref(src, j);
   }
 }
 
@@ -392,7 +416,8 @@ void PoissonPlan::init(const GridDesc& g) {
       if (tpl < 32) tpl = 32;
       if (tpl > 256) tpl = 256;
       c.tpl = tpl;
-      c.line_bytes = ((16 * n) + 15) & ~15;
+      c.cslots = (m + 7) & ~7;
+      c.line_bytes = 2 * 16 * c.cslots;
     } else {
       c.tpl = n >= 256 ? 256 : 32 * ((n + 31) / 32);
       c.line_bytes = ((16 * n) + 15) & ~15;

@@ -14,6 +14,7 @@ namespace bfmgpu {
 struct PoisAxisCfg {
   bfmdct::LinePlan plan;  // device table pointers
   int n, tpl, lpc, strided, line_bytes;
+  int cslots;  // complex slots per line buffer (m rounded up to 8 for the swizzle)
   long stride, nlines;
 };
 
