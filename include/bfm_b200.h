@@ -172,11 +172,15 @@ long bfm_solver_launches(const bfm_solver* s);
  * solver's stream; *ms receives the device-timed duration. */
 int bfm_solver_time_steps(bfm_solver* s, int k, double* ms);
 
-/* Test hook: device evaluation of the exact round-down of `count` sums of m
- * doubles each (terms row-major). Used by the parity tests only. */
 /* Test hook: c-transform diagnostic counters (needs env BFM_CT_STATS=1). */
 int bfm_debug_ct_stats(bfm_solver* s, unsigned long long* out8);
+/* Test hook: device evaluation of the exact round-down of `count` sums of m
+ * doubles each (terms row-major). Used by the parity tests only. */
 int bfm_debug_round_down(const double* terms, int m, int count, double* out);
+/* Test hook: the pushforward's parallel evaluation of the sequential fold
+ * rho = ((0 + w_0) + w_1) + ... of each sequence w[offsets[i] .. offsets[i+1])
+ * (exact_fold.cuh), by a 512-thread CTA (mode 0) or one warp (mode 1). */
+int bfm_debug_fold(const double* w, const long* offsets, int nseq, int mode, double* out);
 
 const char* bfm_last_error(void);
 /* Selects the CUDA device for subsequent calls on this thread (one process

@@ -23,6 +23,7 @@
 
 namespace bfmgpu {
 void debug_round_down(const double* h_terms, int m, int count, double* h_out);
+void debug_fold(const double* h_w, const long* h_off, int nseq, int mode, double* h_out);
 }
 
 namespace {
@@ -405,6 +406,15 @@ int bfm_debug_round_down(const double* terms, int m, int count, double* out) {
   return guard([&] {
     require_device();
     bfmgpu::debug_round_down(terms, m, count, out);
+  });
+}
+
+int bfm_debug_fold(const double* w, const long* offsets, int nseq, int mode, double* out) {
+  return guard([&] {
+    require_device();
+    if (nseq < 0 || (mode != 0 && mode != 1) || (nseq > 0 && (!w || !offsets || !out)))
+      throw std::invalid_argument("debug_fold: bad arguments");
+    bfmgpu::debug_fold(w, offsets, nseq, mode, out);
   });
 }
 

@@ -142,10 +142,11 @@ struct Smem {
   uint16_t* hidx;      // chunk hull stacks, later per-query winners
   uint16_t* H;         // compacted hull corners
   uint8_t* dlt;        // per-edge slack code (0: no suspects)
+  uint16_t* flist;     // compacted list of flagged queries
   int* lo;
   int* hi;
   int* off;
-  unsigned long long* scal;  // 0 A, 1 Smax, 2 Dmax, 3 hull size, 4 #non-convex
+  unsigned long long* scal;  // 0 A, 1 Smax, 2 Dmax, 3 hull size, 4 #non-convex, 5 #flagged
   LineGeo* geo;
 };
 
@@ -158,6 +159,7 @@ __device__ __forceinline__ Smem carve(const CtPass& p, unsigned char* base, int 
   s.hidx = reinterpret_cast<uint16_t*>(b + p.off_hidx);
   s.H = reinterpret_cast<uint16_t*>(b + p.off_H);
   s.dlt = reinterpret_cast<uint8_t*>(b + p.off_flag);
+  s.flist = reinterpret_cast<uint16_t*>(b + p.off_list);
   s.lo = reinterpret_cast<int*>(b + p.off_lohi);
   s.hi = s.lo + p.tpl;
   s.off = s.hi + p.tpl;
@@ -571,30 +573,47 @@ __global__ void __launch_bounds__(1024) ct_pass_kernel(CtPass p) {
   //          adjacent edge holds suspects. Others are flagged (bit 15).
   if (active) {
     auto Fhat = [&](int idx, double xk) { return P_f(idx) - xk * P_y(idx); };
-    for (int k = t; k < n; k += tpl) {
-      const int i = res[k];
-      const double xk = coord(h, k);
-      const double F0 = Fhat(HH(i), xk);
-      const double Fl = i > 0 ? Fhat(HH(i - 1), xk) : INFINITY;
-      const double Fr = i < hsz - 1 ? Fhat(HH(i + 1), xk) : INFINITY;
-      // an adjacent edge's suspects cannot win unless the edge passes the same
-      // relevance tests the full resolution applies (see visit below)
-      auto edge_quiet = [&](int e, double Fa, double Fb) {
-        const uint8_t code = s.dlt[e];
-        if (code == 0) return true;
-        const double slack = slack_value(code, sref) + Mc;
-        if (fmin(Fa, Fb) > F0 + slack) return true;
-        const int a = HH(e), b = HH(e + 1);
-        return fabs(Fa - Fb) > slack * (1.000001 * (b - a)) + Mc;
-      };
-      const bool lone = Fl > F0 + Mw && Fr > F0 + Mw &&
-                        (convex_line || ((i == 0 || edge_quiet(i - 1, Fl, F0)) &&
-                                         (i >= hsz - 1 || edge_quiet(i, F0, Fr))));
-      if (p.stats) {
-        atomicAdd(p.stats + 0, 1ull);
-        if (!lone) atomicAdd(p.stats + 1, 1ull);
+    unsigned* nflag = reinterpret_cast<unsigned*>(&s.scal[5]);
+    const unsigned lane = threadIdx.x & 31u;
+    // tpl is a multiple of 32: every warp belongs to one line and runs the
+    // same number of iterations (needed by the ballot below)
+    for (int kb = t - static_cast<int>(lane); kb < n; kb += tpl) {
+      const int k = kb + static_cast<int>(lane);
+      const bool in = k < n;
+      bool lone = true;
+      if (in) {
+        const int i = res[k];
+        const double xk = coord(h, k);
+        const double F0 = Fhat(HH(i), xk);
+        const double Fl = i > 0 ? Fhat(HH(i - 1), xk) : INFINITY;
+        const double Fr = i < hsz - 1 ? Fhat(HH(i + 1), xk) : INFINITY;
+        // an adjacent edge's suspects cannot win unless the edge passes the same
+        // relevance tests the full resolution applies (see visit below)
+        auto edge_quiet = [&](int e, double Fa, double Fb) {
+          const uint8_t code = s.dlt[e];
+          if (code == 0) return true;
+          const double slack = slack_value(code, sref) + Mc;
+          if (fmin(Fa, Fb) > F0 + slack) return true;
+          const int a = HH(e), b = HH(e + 1);
+          return fabs(Fa - Fb) > slack * (1.000001 * (b - a)) + Mc;
+        };
+        lone = Fl > F0 + Mw && Fr > F0 + Mw &&
+               (convex_line || ((i == 0 || edge_quiet(i - 1, Fl, F0)) &&
+                                (i >= hsz - 1 || edge_quiet(i, F0, Fr))));
+        if (p.stats) {
+          atomicAdd(p.stats + 0, 1ull);
+          if (!lone) atomicAdd(p.stats + 1, 1ull);
       }
       res[k] = lone ? static_cast<uint16_t>(HH(i)) : static_cast<uint16_t>(i | 0x8000);
+      }
+      // flagged queries are appended to the line's list (warp-aggregated)
+      const unsigned fm = __ballot_sync(0xffffffffu, in && !lone);
+      if (fm) {
+        unsigned b0 = 0;
+        if (lane == static_cast<unsigned>(__ffs(fm) - 1)) b0 = atomicAdd(nflag, __popc(fm));
+        b0 = __shfl_sync(0xffffffffu, b0, __ffs(fm) - 1);
+        if (in && !lone) s.flist[b0 + __popc(fm & ((1u << lane) - 1u))] = static_cast<uint16_t>(k);
+      }
     }
   }
   group_sync(tpl, l);
@@ -616,9 +635,10 @@ __global__ void __launch_bounds__(1024) ct_pass_kernel(CtPass p) {
         return bfmx::round_down_sum(tv, m);
       }
     };
-    for (int k = t; k < n; k += tpl) {
+    const int nfl = static_cast<int>(*reinterpret_cast<const unsigned*>(&s.scal[5]));
+    for (int fi = t; fi < nfl; fi += tpl) {
+      const int k = s.flist[fi];
       const int rv = res[k];
-      if (!(rv & 0x8000) || rv == 0xffff) continue;  // resolved, or done (last pass)
       const int i = rv & 0x7fff;
       const double xk = coord(h, k);
       int L = i;
@@ -727,6 +747,7 @@ __global__ void __launch_bounds__(1024) ct_pass_kernel(CtPass p) {
     }
   }
   PH(8);  // flagged queries
+  if (p.last) group_sync(tpl, l);  // flagged queries were resolved by any thread of the line
   if (p.last && active) {
     // lone queries: final round-downs, batched so the L2 loads overlap
     constexpr int kB = 8;
@@ -896,6 +917,8 @@ void CtPlan::init(const GridDesc& g) {
     o = align16(o + 2 * n);
     P.off_flag = o;  // per-edge slack code (uint8)
     o = align16(o + n + 4);
+    P.off_list = o;  // flagged query list (uint16)
+    o = align16(o + 2 * n);
     P.off_lohi = o;
     o = align16(o + 12 * P.tpl);
     P.off_scal = o;

@@ -29,7 +29,7 @@ struct CtPass {
   uint32_t* state_out;       // non-last passes
   double* out;               // last pass
   // shared-memory carve-up (bytes, per line)
-  int off_fv, off_chain, off_hidx, off_H, off_flag, off_lohi, off_scal, line_bytes;
+  int off_fv, off_chain, off_hidx, off_H, off_flag, off_list, off_lohi, off_scal, line_bytes;
   // statistics (device counters, may be null): lines that needed exact resolution
   unsigned long long* slow_queries;
   unsigned long long* stats;  // optional diagnostics (env BFM_CT_STATS=1)

@@ -17,7 +17,6 @@ namespace bfmgpu {
 namespace {
 
 using bfmdct::cplx;
-constexpr int kMaxItems = 9;
 
 enum { kFwd = 0, kInv = 1, kFused = 2 };
 

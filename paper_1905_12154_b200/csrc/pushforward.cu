@@ -16,20 +16,25 @@
 //      neighbouring cells by source id and folds the nonzero corner weights
 //      from 0.0 in increasing source order — exactly the order in which the
 //      reference adds them — then writes target - rho.
+#include <algorithm>
 #include <climits>
 
-#include "pushforward.cuh"
 #include <cmath>
+#include <vector>
+
+#include "exact_fold.cuh"
+#include "pushforward.cuh"
 
 namespace bfmgpu {
 namespace {
 
-constexpr int kScanItems = 8;
-constexpr int kScanThreads = 1024;
-constexpr int kScanTile = kScanItems * kScanThreads;
 constexpr int kLight = 48;
-constexpr int kFoldChunk = 8192;
-constexpr int kMedium = 4096;
+constexpr int kMedium = 2048;
+constexpr int kMedWarps = 8;
+constexpr int kHeavyIds = 24576;
+constexpr int kMedSmem = kMedWarps * kMedium * 4;
+constexpr int kMedBlocks = 148 * 3;  // each warp owns kMedium doubles of hbuf
+constexpr int kHeavySmem = kHeavyIds * 4;
 
 struct MapArgs {
   GridDesc g;
@@ -226,165 +231,164 @@ __global__ void pf_gather_kernel(GatherArgs A, int* heavy, int* nheavy) {
   }
 }
 
-// Medium targets (kLight < K <= kMedium): one warp each; lanes rank and weight
-// the deposits into the global buffer, then lane 0 folds them in order while
-// the warp streams 32 at a time through shuffles.
-__global__ void __launch_bounds__(256) pf_gather_medium_kernel(GatherArgs A, const int* heavy,
-                                                              const int* nheavy, double* hbuf,
-                                                              unsigned long long* hfill) {
+// The <= 2^d neighbouring cells of target t whose buckets are non-empty.
+struct TargetBuckets {
+  int pos[8], end[8], bits[8];
+  int nl, K;
+};
+__device__ __forceinline__ void target_buckets(const GatherArgs& A, long t, TargetBuckets& tb) {
   const GridDesc& g = A.g;
-  const int corners = 1 << g.d;
+  int id[3] = {0, 0, 0};
+  node_idx(g, t, id);
+  tb.nl = 0;
+  tb.K = 0;
+  for (int b = 0; b < (1 << g.d); ++b) {
+    long c = t;
+    bool ok = true;
+    for (int a = 0; a < g.d; ++a)
+      if ((b >> a) & 1) {
+        if (id[a] == 0) ok = false;
+        c -= g.stride[a];
+      }
+    if (!ok) continue;
+    const int k = A.end[c] - A.off[c];
+    if (k <= 0) continue;
+    tb.pos[tb.nl] = A.off[c];
+    tb.end[tb.nl] = A.end[c];
+    tb.bits[tb.nl] = b;
+    tb.K += k;
+    ++tb.nl;
+  }
+}
+
+__device__ __forceinline__ int lower_bound_ids(const int* v, int len, int key) {
+  int lo = 0, hi = len;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (v[mid] < key) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo;
+}
+
+// Medium targets (kLight < K <= kMedium): one warp each. The source ids of
+// the neighbouring buckets are staged in shared memory; every deposit's
+// position in the source-ordered merge is its index in its own bucket plus
+// its rank (lower_bound) in each other bucket (a source lives in exactly one
+// bucket, so there are no ties). Lanes write the weights to those positions
+// in the warp's private slice of a global buffer, then fold them in order.
+__global__ void __launch_bounds__(kMedWarps * 32) pf_gather_medium_kernel(GatherArgs A,
+                                                                         const int* heavy,
+                                                                         const int* nheavy,
+                                                                         double* hbuf) {
+  extern __shared__ int med_ids[];  // [kMedWarps][kMedium]
   const int nh = nheavy[0];
   const int lane = threadIdx.x & 31;
+  int* ids = med_ids + (threadIdx.x >> 5) * kMedium;
   const long warp0 = (static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const long nwarps = (static_cast<long>(gridDim.x) * blockDim.x) >> 5;
   for (long q = warp0; q < nh; q += nwarps) {
     const long t = heavy[q];
-    int id[3] = {0, 0, 0};
-    node_idx(g, t, id);
-    int pos[8], endp[8], bits[8];
-    int nl = 0, K = 0;
-    for (int b = 0; b < corners; ++b) {
-      long c = t;
-      bool ok = true;
-      for (int a = 0; a < g.d; ++a)
-        if ((b >> a) & 1) {
-          if (id[a] == 0) ok = false;
-          c -= g.stride[a];
-        }
-      if (!ok) continue;
-      const int k = A.end[c] - A.off[c];
-      if (k <= 0) continue;
-      pos[nl] = A.off[c];
-      endp[nl] = A.end[c];
-      bits[nl] = b;
-      K += k;
-      ++nl;
+    TargetBuckets tb;
+    target_buckets(A, t, tb);
+    const int K = tb.K;
+    int cat[8];
+    for (int qq = 0, o = 0; qq < tb.nl; ++qq) {
+      cat[qq] = o;
+      o += tb.end[qq] - tb.pos[qq];
     }
-    unsigned long long base = 0;
-    if (lane == 0) base = atomicAdd(hfill, static_cast<unsigned long long>(K));
-    base = __shfl_sync(0xffffffffu, base, 0);
-    double* buf = hbuf + base;
-    for (int qq = 0; qq < nl; ++qq) {
-      for (int i = pos[qq] + lane; i < endp[qq]; i += 32) {
-        const int src = A.bucket[i];
-        int fin = i - pos[qq];
-        for (int o = 0; o < nl; ++o) {
-          if (o == qq) continue;
-          int lo = pos[o], hi = endp[o];
-          while (lo < hi) {
-            const int mid = (lo + hi) >> 1;
-            if (A.bucket[mid] < src) lo = mid + 1;
-            else hi = mid;
-          }
-          fin += lo - pos[o];
-        }
-        buf[fin] = (bits[qq] & A.cmask[src]) ? 0.0 : deposit_weight(A, src, bits[qq]);
+    for (int qq = 0; qq < tb.nl; ++qq)
+      for (int i = lane; i < tb.end[qq] - tb.pos[qq]; i += 32) ids[cat[qq] + i] = A.bucket[tb.pos[qq] + i];
+    double* buf = hbuf + warp0 * kMedium;  // the warp's private slice (K <= kMedium)
+    __syncwarp();
+    for (int qq = 0; qq < tb.nl; ++qq) {
+      const int len = tb.end[qq] - tb.pos[qq];
+      for (int i = lane; i < len; i += 32) {
+        const int src = ids[cat[qq] + i];
+        int fin = i;
+        for (int o = 0; o < tb.nl; ++o)
+          if (o != qq) fin += lower_bound_ids(ids + cat[o], tb.end[o] - tb.pos[o], src);
+        buf[fin] = (tb.bits[qq] & A.cmask[src]) ? 0.0 : deposit_weight(A, src, tb.bits[qq]);
       }
     }
     __syncwarp();
+    // Starting from +0.0, rho can never become -0.0, so adding a zero weight
+    // leaves it unchanged: folding every weight equals the reference's skip
+    // of zero weights bit for bit. K is small here: a sequential chain of
+    // adds fed by shuffles (all 32 issued ahead of the chain when unrolled).
     double rho = 0.0;
-    for (int c = 0; c < K; c += 32) {
+    int c = 0;
+    for (; c + 32 <= K; c += 32) {
+      const double v = buf[c + lane];
+      double x[32];
+#pragma unroll
+      for (int i = 0; i < 32; ++i) x[i] = __shfl_sync(0xffffffffu, v, i);
+#pragma unroll
+      for (int i = 0; i < 32; ++i) rho += x[i];
+    }
+    if (c < K) {
       const double v = c + lane < K ? buf[c + lane] : 0.0;
-      const int m = min(32, K - c);
-      for (int i = 0; i < m; ++i) {
-        const double w = __shfl_sync(0xffffffffu, v, i);
-        if (w != 0.0) rho += w;
-      }
+      for (int i = 0; i < K - c; ++i) rho += __shfl_sync(0xffffffffu, v, i);
     }
     if (lane == 0) A.out[t] = A.target ? A.target[t] - rho : rho;
+    __syncwarp();
   }
 }
 
-// Heavy targets: one CTA each. Every deposit's position in the source-ordered
-// merge of the <= 2^d sorted neighbouring buckets is its index in its own
-// bucket plus its rank (lower_bound) in each other bucket (a source lives in
-// exactly one bucket, so there are no ties). Weights are written to those
-// positions in a global buffer in parallel; one thread then folds them in
-// order from 0.0 exactly like the reference's sequential +=.
+// Heavy targets (K > kMedium): one CTA each, same merge-rank scheme with the
+// ids in shared memory when they fit (else ranked against global memory),
+// weights to the global buffer, then the CTA folds them (exact_fold.cuh).
 __global__ void __launch_bounds__(512) pf_gather_heavy_kernel(GatherArgs A, const int* heavy,
                                                              const int* nheavy, double* hbuf,
                                                              unsigned long long* hfill) {
-  __shared__ int s_pos[8], s_end[8], s_bits[8], s_nl, s_K;
+  __shared__ int s_pos[8], s_end[8], s_bits[8], s_cat[8], s_nl, s_K;
   __shared__ unsigned long long s_base;
-  extern __shared__ __align__(16) unsigned char fold_raw[];
-  double* fold = reinterpret_cast<double*>(fold_raw);  // [2 * kFoldChunk]
+  __shared__ FoldTr fold_scr[512 / 32 + 1];
+  __shared__ int fold_iscr[512 / 32];
+  extern __shared__ int ids[];  // [kHeavyIds]
   const GridDesc& g = A.g;
-  const int corners = 1 << g.d;
   const int nh = nheavy[1];
   for (int q = blockIdx.x; q < nh; q += gridDim.x) {
     const long t = heavy[g.size - 1 - q];
     if (threadIdx.x == 0) {
-      int id[3] = {0, 0, 0};
-      node_idx(g, t, id);
-      int nl = 0, K = 0;
-      for (int b = 0; b < corners; ++b) {
-        long c = t;
-        bool ok = true;
-        for (int a = 0; a < g.d; ++a)
-          if ((b >> a) & 1) {
-            if (id[a] == 0) ok = false;
-            c -= g.stride[a];
-          }
-        if (!ok) continue;
-        const int k = A.end[c] - A.off[c];
-        if (k <= 0) continue;
-        s_pos[nl] = A.off[c];
-        s_end[nl] = A.end[c];
-        s_bits[nl] = b;
-        K += k;
-        ++nl;
+      TargetBuckets tb;
+      target_buckets(A, t, tb);
+      for (int qq = 0, o = 0; qq < tb.nl; ++qq) {
+        s_pos[qq] = tb.pos[qq];
+        s_end[qq] = tb.end[qq];
+        s_bits[qq] = tb.bits[qq];
+        s_cat[qq] = o;
+        o += tb.end[qq] - tb.pos[qq];
       }
-      s_nl = nl;
-      s_K = K;
-      s_base = atomicAdd(hfill, static_cast<unsigned long long>(K));
+      s_nl = tb.nl;
+      s_K = tb.K;
+      s_base = atomicAdd(hfill, static_cast<unsigned long long>(tb.K));
     }
     __syncthreads();
     const int nl = s_nl;
+    const int K = s_K;
+    const bool staged = K <= kHeavyIds;
+    if (staged)
+      for (int qq = 0; qq < nl; ++qq)
+        for (int i = threadIdx.x; i < s_end[qq] - s_pos[qq]; i += blockDim.x)
+          ids[s_cat[qq] + i] = A.bucket[s_pos[qq] + i];
+    __syncthreads();
     double* buf = hbuf + s_base;
     for (int qq = 0; qq < nl; ++qq) {
-      const int p0 = s_pos[qq], p1 = s_end[qq], b = s_bits[qq];
-      for (int i = p0 + threadIdx.x; i < p1; i += blockDim.x) {
-        const int src = A.bucket[i];
-        int fin = i - p0;
+      const int p0 = s_pos[qq], len = s_end[qq] - p0, b = s_bits[qq];
+      for (int i = threadIdx.x; i < len; i += blockDim.x) {
+        const int src = staged ? ids[s_cat[qq] + i] : A.bucket[p0 + i];
+        int fin = i;
         for (int o = 0; o < nl; ++o) {
           if (o == qq) continue;
-          int lo = s_pos[o], hi = s_end[o];
-          while (lo < hi) {
-            const int mid = (lo + hi) >> 1;
-            if (A.bucket[mid] < src) lo = mid + 1;
-            else hi = mid;
-          }
-          fin += lo - s_pos[o];
+          fin += staged ? lower_bound_ids(ids + s_cat[o], s_end[o] - s_pos[o], src)
+                        : lower_bound_ids(A.bucket + s_pos[o], s_end[o] - s_pos[o], src);
         }
         buf[fin] = (b & A.cmask[src]) ? 0.0 : deposit_weight(A, src, b);
       }
     }
     __syncthreads();
-    // Sequential fold from shared memory, double-buffered: thread 0 folds
-    // chunk c while the other threads stage chunk c+1.
-    const int K = s_K;
-    const int nch = (K + kFoldChunk - 1) / kFoldChunk;
-    double rho = 0.0;
-    for (int i = threadIdx.x; i < min(K, kFoldChunk); i += blockDim.x) fold[i] = buf[i];
-    __syncthreads();
-    for (int c = 0; c < nch; ++c) {
-      const double* cur = fold + (c & 1) * kFoldChunk;
-      double* nxt = fold + ((c + 1) & 1) * kFoldChunk;
-      const int len = min(kFoldChunk, K - c * kFoldChunk);
-      if (threadIdx.x == 0) {
-#pragma unroll 8
-        for (int i = 0; i < len; ++i) {
-          const double w = cur[i];
-          if (w != 0.0) rho += w;
-        }
-      } else if (c + 1 < nch) {
-        const int base = (c + 1) * kFoldChunk;
-        const int len2 = min(kFoldChunk, K - base);
-        for (int i = threadIdx.x - 1; i < len2; i += blockDim.x - 1) nxt[i] = buf[base + i];
-      }
-      __syncthreads();
-    }
+    const double rho = exact_fold<512, 8>(buf, K, fold_scr, fold_iscr, [] { __syncthreads(); });
     if (threadIdx.x == 0) A.out[t] = A.target ? A.target[t] - rho : rho;
     __syncthreads();
   }
@@ -418,10 +422,15 @@ void PushforwardPlan::init(const GridDesc& g) {
   BFM_CUDA(cudaMalloc(&end_, (N + 1) * sizeof(int)));
   BFM_CUDA(cudaMalloc(&heavy_, (N + 1) * sizeof(int)));
   BFM_CUDA(cudaMalloc(&nheavy_, 4 * sizeof(unsigned long long)));
-  BFM_CUDA(cudaMalloc(&hbuf_, (static_cast<long>(1) << g.d) * N * sizeof(double)));
+  const long deposits = (static_cast<long>(1) << g.d) * N;
+  med_blocks_ = static_cast<int>(std::max<long>(1, std::min<long>(kMedBlocks, deposits / (kMedWarps * kMedium))));
+  const long hcap = std::max<long>(deposits, static_cast<long>(med_blocks_) * kMedWarps * kMedium);
+  BFM_CUDA(cudaMalloc(&hbuf_, hcap * sizeof(double)));
   sorter_.init(N);
   BFM_CUDA(cudaFuncSetAttribute(pf_gather_heavy_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                2 * kFoldChunk * static_cast<int>(sizeof(double))));
+                                kHeavySmem));
+  BFM_CUDA(cudaFuncSetAttribute(pf_gather_medium_kernel,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, kMedSmem));
   key_bits_ = 1;
   while ((1L << key_bits_) <= N) ++key_bits_;  // cells 0..N-1 plus sentinel N
 }
@@ -463,9 +472,9 @@ void PushforwardPlan::bin_and_gather(const double* d_source, const double* d_tar
   int* nheavy = reinterpret_cast<int*>(nheavy_);
   pf_gather_kernel<<<grid_for(N, 256), 256, 0, stream>>>(G, heavy_, nheavy);
   BFM_LAUNCH_CHECK("pf_gather_kernel");
-  pf_gather_medium_kernel<<<148 * 8, 256, 0, stream>>>(G, heavy_, nheavy, hbuf_, nheavy_ + 1);
+  pf_gather_medium_kernel<<<med_blocks_, kMedWarps * 32, kMedSmem, stream>>>(G, heavy_, nheavy, hbuf_);
   BFM_LAUNCH_CHECK("pf_gather_medium_kernel");
-  pf_gather_heavy_kernel<<<148, 512, 2 * kFoldChunk * sizeof(double), stream>>>(G, heavy_, nheavy, hbuf_, nheavy_ + 1);
+  pf_gather_heavy_kernel<<<2 * 148, 512, kHeavySmem, stream>>>(G, heavy_, nheavy, hbuf_, nheavy_ + 1);
   BFM_LAUNCH_CHECK("pf_gather_heavy_kernel");
   if (lc) lc->add(4);
 }
@@ -509,4 +518,43 @@ void PushforwardPlan::from_displacement(const double* d_disp, double scale,
   bin_and_gather(d_source, nullptr, d_rho, stream, lc);
 }
 
+}  // namespace bfmgpu
+
+// ---- test hook: the parallel sequential-fold on given sequences ------------
+namespace bfmgpu {
+namespace {
+__global__ void __launch_bounds__(512) debug_fold_kernel(const double* w, const long* off, int mode,
+                                                        double* out) {
+  __shared__ FoldTr scr[2 * 16 + 2];
+  __shared__ int iscr[16];
+  const long b = off[blockIdx.x];
+  const int K = static_cast<int>(off[blockIdx.x + 1] - b);
+  double r;
+  if (mode == 0) {
+    r = exact_fold<512, 8>(w + b, K, scr, iscr, [] { __syncthreads(); });
+  } else {
+    if (threadIdx.x >= 32) return;
+    r = exact_fold<32, 8>(w + b, K, scr, iscr, [] { __syncwarp(); });
+  }
+  if (threadIdx.x == 0) out[blockIdx.x] = r;
+}
+}  // namespace
+
+void debug_fold(const double* h_w, const long* h_off, int nseq, int mode, double* h_out) {
+  if (nseq == 0) return;
+  const long total = h_off[nseq];
+  double *dw = nullptr, *dout = nullptr;
+  long* doff = nullptr;
+  BFM_CUDA(cudaMalloc(&dw, sizeof(double) * (total + 1)));
+  BFM_CUDA(cudaMalloc(&doff, sizeof(long) * (nseq + 1)));
+  BFM_CUDA(cudaMalloc(&dout, sizeof(double) * nseq));
+  BFM_CUDA(cudaMemcpy(dw, h_w, sizeof(double) * total, cudaMemcpyHostToDevice));
+  BFM_CUDA(cudaMemcpy(doff, h_off, sizeof(long) * (nseq + 1), cudaMemcpyHostToDevice));
+  debug_fold_kernel<<<nseq, mode == 0 ? 512 : 32>>>(dw, doff, mode, dout);
+  BFM_LAUNCH_CHECK("debug_fold_kernel");
+  BFM_CUDA(cudaMemcpy(h_out, dout, sizeof(double) * nseq, cudaMemcpyDeviceToHost));
+  cudaFree(dw);
+  cudaFree(doff);
+  cudaFree(dout);
+}
 }  // namespace bfmgpu

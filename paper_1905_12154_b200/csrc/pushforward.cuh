@@ -43,6 +43,7 @@ class PushforwardPlan {
   double* hbuf_ = nullptr;   // [2^d * N] merged heavy deposits
   RadixSorter sorter_;
   int key_bits_ = 0;
+  int med_blocks_ = 1;       // medium-gather CTAs (each warp owns a kMedium slice of hbuf_)
 };
 
 }  // namespace bfmgpu

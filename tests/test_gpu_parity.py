@@ -136,6 +136,74 @@ def test_pushforward_concentrated_map():
     assert O.n_bit_diff(rho, O.orc_pushforward_density(disp, mu)) == 0
 
 
+@pytest.mark.parametrize("n", [40, 128, 300])
+def test_pushforward_concentrated_random_mass(n):
+    # medium (K <= 2048), heavy with shared-memory ranks, heavy with global ranks
+    rng = np.random.default_rng(n)
+    x = (np.arange(n) + 0.5) / n
+    X, Y = np.meshgrid(x, x, indexing="ij")
+    u = 0.5 * (X * X + Y * Y) - 0.31 * X - 0.67 * Y
+    mu = rng.lognormal(0.0, 2.0, (n, n)) * (rng.uniform(0, 1, (n, n)) > 0.1)
+    disp = bfm.map_from_conjugate(u)
+    rho = bfm.pushforward_density(disp, mu)
+    assert O.n_bit_diff(rho, O.orc_pushforward_density(disp, mu)) == 0
+
+
+def _seq_fold(w):
+    r = 0.0
+    for x in w.tolist():
+        r = r + x
+    return r
+
+
+def _fold_cases():
+    rng = np.random.default_rng(11)
+    cases = []
+    for K in [0, 1, 2, 31, 32, 33, 255, 256, 257, 4095, 4096, 4097, 20000]:
+        cases.append(rng.lognormal(0.0, 3.0, K))
+    cases.append(np.zeros(5000))
+    w = rng.uniform(0, 1, 9000)
+    w[:3000] = 0.0
+    w[rng.uniform(0, 1, 9000) < 0.3] = 0.0
+    cases.append(w)
+    # ties: half-ulp and odd multiples of half-ulps around 1.0 (round half to even)
+    ulp = 2.0 ** -52
+    t = rng.integers(0, 4, 6000) * (ulp / 2)
+    t[0] = 1.0
+    cases.append(t)
+    t2 = rng.integers(0, 8, 6000) * (ulp / 4) + (rng.uniform(0, 1, 6000) < 0.5) * ulp * 3.5
+    t2[0] = 1.0 + 3 * ulp
+    cases.append(t2)
+    cases.append(2.0 ** np.arange(0, 700, 0.5))                   # a binade crossing per step
+    cases.append(np.concatenate([[1.0], np.full(5000, 2.0 ** -53)]))  # ties that never round up
+    cases.append(np.concatenate([[1.0 + ulp], np.full(5000, 2.0 ** -53)]))  # ties that round up
+    cases.append(rng.uniform(0, 1, 3000) * 1e-310)                # subnormal weights
+    cases.append(np.concatenate([rng.uniform(0, 1, 100), [np.inf], rng.uniform(0, 1, 100)]))
+    cases.append(np.concatenate([rng.uniform(0, 1, 100), [np.nan], rng.uniform(0, 1, 100)]))
+    cases.append(rng.uniform(-1, 1, 3000))                        # negative weights (not produced, still exact)
+    cases.append(rng.uniform(0, 1, 5000) * 2.0 ** rng.integers(-60, 60, 5000))
+    return cases
+
+
+@pytest.mark.parametrize("mode", [0, 1])
+def test_exact_fold_matches_sequential(mode):
+    import ctypes as C
+    lib = bfm.load_library()
+    cases = _fold_cases()
+    off = np.zeros(len(cases) + 1, dtype=np.int64)
+    off[1:] = np.cumsum([len(c) for c in cases])
+    w = np.ascontiguousarray(np.concatenate(cases).astype(np.float64)) if off[-1] else np.zeros(1)
+    out = np.empty(len(cases))
+    rc = lib.bfm_debug_fold(w.ctypes.data_as(C.c_void_p), off.ctypes.data_as(C.c_void_p),
+                            C.c_int(len(cases)), C.c_int(mode), out.ctypes.data_as(C.c_void_p))
+    assert rc == 0, lib.bfm_last_error()
+    for i, c in enumerate(cases):
+        want = _seq_fold(c)
+        got = float(out[i])
+        same = (np.isnan(want) and np.isnan(got)) or np.float64(want).view(np.int64) == np.float64(got).view(np.int64)
+        assert same, (i, len(c), want.hex() if not np.isnan(want) else "nan", got.hex() if not np.isnan(got) else "nan")
+
+
 def test_pushforward_kats():
     # test_pushforward.cpp:104-116 fractional split; :137-150 boundary deposits
     mu = np.zeros(8)
