@@ -786,28 +786,27 @@ __global__ void __launch_bounds__(1024) ct_pass_kernel(CtPass p) {
   __syncthreads();
 
   // ---- 6. intermediate passes: coalesced write of the argmin chain ---------
-  for (int idx = threadIdx.x; idx < n * lpc; idx += blockDim.x) {
-    int ll, k;
-    if (p.strided) {
-      ll = idx % lpc;
-      k = idx / lpc;
-    } else {
-      ll = idx / n;
-      k = idx - ll * n;
-    }
-    const Smem sm = carve(p, smem, ll);
+  // (same fixed thread -> line mapping as the load: no per-element division)
+  {
+    const int ml = p.strided ? static_cast<int>(threadIdx.x % lpc) : l;
+    const int step = p.strided ? blockDim.x / lpc : tpl;
+    const int first = p.strided ? static_cast<int>(threadIdx.x / lpc) : t;
+    const Smem sm = carve(p, smem, ml);
     const LineGeo g = *sm.geo;
-    if (!g.valid) continue;
-    const long node = g.base + static_cast<long>(k) * A.stride;
-    const int win = sm.hidx[k];
-    uint32_t packed;
-    if (p.a == 0) {
-      packed = static_cast<uint32_t>(win);
-    } else {
-      const uint32_t ch = DY ? p.state_in[g.base + static_cast<long>(win) * A.stride] : sm.chain[win];
-      packed = ch | (static_cast<uint32_t>(win) << 16);
-    }
-    p.state_out[node] = packed;
+    if (g.valid)
+      for (int k = first; k < n; k += step) {
+        const long node = g.base + static_cast<long>(k) * A.stride;
+        const int win = sm.hidx[k];
+        uint32_t packed;
+        if (p.a == 0) {
+          packed = static_cast<uint32_t>(win);
+        } else {
+          const uint32_t ch =
+              DY ? p.state_in[g.base + static_cast<long>(win) * A.stride] : sm.chain[win];
+          packed = ch | (static_cast<uint32_t>(win) << 16);
+        }
+        p.state_out[node] = packed;
+      }
   }
 }
 
