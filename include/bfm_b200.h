@@ -18,6 +18,7 @@
 #define BFM_B200_H
 
 #include <stddef.h>
+#include <stdint.h>
 
 #ifdef __cplusplus
 extern "C" {
@@ -163,6 +164,56 @@ int bfm_solve_neumann_device(bfm_workspace* ws, const double* d_rhs, double* d_o
                              void* stream);
 /* Number of device kernels the last *_device call on ws enqueued. */
 int bfm_workspace_last_launches(const bfm_workspace* ws);
+
+/* ---- Multi-GPU building blocks (one process per GPU) ---------
+ * The reference has no distributed mode; these are the rank-local halves of
+ * its operators under an axis-0 slab decomposition, driven by
+ * paper_1905_12154_b200/dist.py over torch.distributed (NCCL). A rank owns
+ * rows [row0, row0+nrows) of the grid and, for axis-0 work, the flattened
+ * columns [col0, col0+ncols) of the n1*n2 non-axis-0 index. All pointers are
+ * device pointers; `stream` is a cudaStream_t. Results equal the single-GPU
+ * operators bit for bit once the exchanges in dist.py are applied. */
+typedef struct bfm_slab bfm_slab;
+/* Host-only: the validation of bfm_solver_create (solver.hpp:105-142,148-167)
+ * without creating a solver (every rank of the multi-GPU driver runs it). */
+int bfm_validate_inputs(int dim, const int* extents, const double* mu, const double* nu,
+                        const bfm_config* cfg);
+int bfm_slab_create(int dim, const int* extents, int row0, int nrows, long col0, int ncols,
+                    bfm_slab** out);
+void bfm_slab_destroy(bfm_slab* s);
+/* c-transform (transforms.hpp:396-432): pass 0 on the (n0 x ncols) column
+ * slab -> argmin chain j0* (uint32) and Q = phi(j0*, column); passes 1..d-1
+ * on the row slab from (chain, Q) of its rows -> phi^c. */
+int bfm_slab_ct_cols(bfm_slab* s, const double* d_phi_cols, uint32_t* d_chain, double* d_q,
+                     void* stream);
+int bfm_slab_ct_rows(bfm_slab* s, const uint32_t* d_chain, const double* d_q, double* d_out,
+                     void* stream);
+/* solve_neumann (poisson.hpp:87-106): DCT-II along axes d-1..1 (rows), the
+ * fused axis-0 [DCT-II, divide, DCT-III] (columns), DCT-III along 1..d-1. */
+int bfm_slab_poisson_rows_forward(bfm_slab* s, const double* d_in, double* d_out, void* stream);
+int bfm_slab_poisson_cols(bfm_slab* s, const double* d_in, double* d_out, void* stream);
+int bfm_slab_poisson_rows_inverse(bfm_slab* s, double* d_inout, void* stream);
+/* pushforward (pushforward.hpp:70-91,141-172): deposit records of the rank's
+ * sources from u with one halo row above and below ((nrows+2) rows): global
+ * lo-corner cell (massless: global N), upper weights (d x nrows*M SoA), clamp
+ * mask, optional displacement (d x nrows*M). Gather: records from all ranks
+ * in global source order, keys relative to the rank's cells (global cell -
+ * (row0-1)*M; sentinel bfm_slab_pf_num_cells) -> target - rho (or rho). */
+int bfm_slab_pf_map(bfm_slab* s, const double* d_u_halo, const double* d_source, uint32_t* d_key,
+                    double* d_w, uint8_t* d_cmask, double* d_disp, void* stream);
+long bfm_slab_pf_num_cells(const bfm_slab* s);
+int bfm_slab_pf_gather(bfm_slab* s, long nrec, const uint32_t* d_keys, const double* d_mass,
+                       const double* d_w, const uint8_t* d_cmask, const double* d_target,
+                       double* d_out, void* stream);
+/* Scalars: unscaled double-double partial sums of the rank's rows
+ * (out4 = hi1, lo1, hi2, lo2 of sum a1*b1, sum a2*b2; a2/b2 may be null),
+ * combined in rank order by the driver; primal (pushforward.hpp:181-196). */
+int bfm_slab_dot(bfm_slab* s, const double* d_a1, const double* d_b1, const double* d_a2,
+                 const double* d_b2, double* out4, void* stream);
+int bfm_slab_primal(bfm_slab* s, const double* d_disp, const double* d_mu, double* out2,
+                    void* stream);
+int bfm_slab_axpy(bfm_slab* s, double* d_u, double sigma, const double* d_dir, void* stream);
+int bfm_slab_last_launches(const bfm_slab* s);
 
 /* Total device kernels the solver has enqueued so far (launch evidence). */
 long bfm_solver_launches(const bfm_solver* s);

@@ -197,6 +197,20 @@ struct bfm_workspace {
   }
 };
 
+// Rank-local plans of the multi-GPU slab decomposition.
+struct bfm_slab {
+  GridDesc g;  // global grid
+  int row0 = 0, nrows = 0;
+  long col0 = 0;
+  int ncols = 0;
+  LaunchCounter lc;
+  int last_launches = 0;
+  CtPlan ct_cols, ct_rows;
+  PoissonPlan pois_rows, pois_cols;
+  PushforwardPlan pf;
+  Reducer red;
+};
+
 struct bfm_solver {
   GridDesc g;
   bfm_config cfg;
@@ -396,6 +410,18 @@ struct HostOp {
   }
 };
 
+}  // namespace
+
+namespace {
+template <class F>
+int slab_op(bfm_slab* s, F&& f) {
+  return guard([&] {
+    if (!s) fail(BFM_ERR_INVALID_ARGUMENT, "slab: null handle");
+    const long before = s->lc.count;
+    f();
+    s->last_launches = static_cast<int>(s->lc.count - before);
+  });
+}
 }  // namespace
 
 extern "C" {
@@ -673,6 +699,131 @@ int bfm_solve_neumann_device(bfm_workspace* ws, const double* d_rhs, double* d_o
 }
 
 int bfm_workspace_last_launches(const bfm_workspace* ws) { return ws->last_launches; }
+
+// ---- multi-GPU slabs -------------------------------------------------------
+int bfm_validate_inputs(int dim, const int* extents, const double* mu, const double* nu,
+                        const bfm_config* cfg) {
+  return guard([&] {
+    bfm_config c;
+    default_config(&c);
+    if (cfg) c = *cfg;
+    const GridDesc g = checked_grid(dim, extents);
+    check_config(c);
+    check_density("mu", mu, g);
+    check_density("nu", nu, g);
+  });
+}
+
+int bfm_slab_create(int dim, const int* extents, int row0, int nrows, long col0, int ncols,
+                    bfm_slab** out) {
+  return guard([&] {
+    *out = nullptr;
+    const GridDesc g = checked_grid(dim, extents);
+    if (dim < 2) fail(BFM_ERR_INVALID_ARGUMENT, "slab: the decomposition needs d >= 2");
+    const long M = g.size / g.n[0];
+    if (row0 < 0 || nrows < 1 || row0 + nrows > g.n[0])
+      fail(BFM_ERR_INVALID_ARGUMENT, "slab: row range outside the grid");
+    if (col0 < 0 || ncols < 1 || col0 + ncols > M)
+      fail(BFM_ERR_INVALID_ARGUMENT, "slab: column range outside the grid");
+    require_device();
+    std::unique_ptr<bfm_slab> s(new bfm_slab);
+    s->g = g;
+    s->row0 = row0;
+    s->nrows = nrows;
+    s->col0 = col0;
+    s->ncols = ncols;
+    s->ct_cols.init_slab_cols(g, ncols);
+    s->ct_rows.init_slab_rows(g, row0, nrows);
+    s->pois_rows.init_slab_rows(g, nrows);
+    s->pois_cols.init_slab_cols(g, col0, ncols);
+    s->pf.init_slab(g, row0, nrows);
+    s->red.init();
+    *out = s.release();
+  });
+}
+
+void bfm_slab_destroy(bfm_slab* s) { delete s; }
+
+int bfm_slab_ct_cols(bfm_slab* s, const double* d_phi_cols, uint32_t* d_chain, double* d_q,
+                     void* stream) {
+  return slab_op(s, [&] {
+    s->ct_cols.run_cols(d_phi_cols, d_chain, d_q, static_cast<cudaStream_t>(stream), &s->lc);
+  });
+}
+
+int bfm_slab_ct_rows(bfm_slab* s, const uint32_t* d_chain, const double* d_q, double* d_out,
+                     void* stream) {
+  return slab_op(s, [&] {
+    s->ct_rows.run_rows(d_chain, d_q, d_out, static_cast<cudaStream_t>(stream), &s->lc);
+  });
+}
+
+int bfm_slab_poisson_rows_forward(bfm_slab* s, const double* d_in, double* d_out, void* stream) {
+  return slab_op(s, [&] {
+    s->pois_rows.rows_forward(d_in, d_out, static_cast<cudaStream_t>(stream), &s->lc);
+  });
+}
+
+int bfm_slab_poisson_cols(bfm_slab* s, const double* d_in, double* d_out, void* stream) {
+  return slab_op(s, [&] {
+    s->pois_cols.cols_fused(d_in, d_out, static_cast<cudaStream_t>(stream), &s->lc);
+  });
+}
+
+int bfm_slab_poisson_rows_inverse(bfm_slab* s, double* d_inout, void* stream) {
+  return slab_op(s, [&] {
+    s->pois_rows.rows_inverse(d_inout, static_cast<cudaStream_t>(stream), &s->lc);
+  });
+}
+
+int bfm_slab_pf_map(bfm_slab* s, const double* d_u_halo, const double* d_source, uint32_t* d_key,
+                    double* d_w, uint8_t* d_cmask, double* d_disp, void* stream) {
+  return slab_op(s, [&] {
+    s->pf.map_records(d_u_halo, d_source, d_key, d_w, d_cmask, d_disp,
+                      static_cast<cudaStream_t>(stream), &s->lc);
+  });
+}
+
+long bfm_slab_pf_num_cells(const bfm_slab* s) { return s ? s->pf.num_cells() : -1; }
+
+int bfm_slab_pf_gather(bfm_slab* s, long nrec, const uint32_t* d_keys, const double* d_mass,
+                       const double* d_w, const uint8_t* d_cmask, const double* d_target,
+                       double* d_out, void* stream) {
+  return slab_op(s, [&] {
+    if (nrec < 0) fail(BFM_ERR_INVALID_ARGUMENT, "slab: negative record count");
+    s->pf.gather(nrec, d_keys, d_mass, d_w, d_cmask, d_target, d_out,
+                 static_cast<cudaStream_t>(stream), &s->lc);
+  });
+}
+
+int bfm_slab_dot(bfm_slab* s, const double* d_a1, const double* d_b1, const double* d_a2,
+                 const double* d_b2, double* out4, void* stream) {
+  return slab_op(s, [&] {
+    const cudaStream_t st = static_cast<cudaStream_t>(stream);
+    s->red.dot_raw(d_a1, d_b1, d_a2, d_b2, static_cast<long>(s->nrows) * (s->g.size / s->g.n[0]),
+                   0, st, &s->lc);
+    s->red.fetch(out4, 4, st);
+  });
+}
+
+int bfm_slab_primal(bfm_slab* s, const double* d_disp, const double* d_mu, double* out2,
+                    void* stream) {
+  return slab_op(s, [&] {
+    const cudaStream_t st = static_cast<cudaStream_t>(stream);
+    s->red.primal_raw(d_disp, d_mu, s->g.d, static_cast<long>(s->nrows) * (s->g.size / s->g.n[0]),
+                      0, st, &s->lc);
+    s->red.fetch(out2, 2, st);
+  });
+}
+
+int bfm_slab_axpy(bfm_slab* s, double* d_u, double sigma, const double* d_dir, void* stream) {
+  return slab_op(s, [&] {
+    axpy(d_u, sigma, d_dir, static_cast<long>(s->nrows) * (s->g.size / s->g.n[0]),
+         static_cast<cudaStream_t>(stream), &s->lc);
+  });
+}
+
+int bfm_slab_last_launches(const bfm_slab* s) { return s ? s->last_launches : 0; }
 
 long bfm_solver_launches(const bfm_solver* s) { return s->ws.lc.count; }
 

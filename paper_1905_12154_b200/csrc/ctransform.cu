@@ -75,7 +75,8 @@ __device__ __forceinline__ double bitsd(unsigned long long v) {
 struct LineGeo {
   long base;
   long phi_other;
-  int k[3];
+  int k[3];  // coordinate indices (k[0] global: local + p.k0_off)
+  int k0l;   // local index along axis 0 (row within a slab)
   int valid;
 };
 
@@ -109,7 +110,9 @@ __device__ __forceinline__ long phi_index(const CtPass& p, const LineGeo& g, uin
   BFM_DASSERT(p.a < 1 || (chain & 0xFFFFu) < static_cast<uint32_t>(p.ax[0].n));
   BFM_DASSERT(p.a < 2 || (chain >> 16) < static_cast<uint32_t>(p.ax[1].n));
   long idx = g.phi_other + static_cast<long>(j) * p.ax[p.a].stride;
-  if (p.a >= 1) idx += static_cast<long>(chain & 0xFFFFu) * p.ax[0].stride;
+  // pregathered (row slab of the multi-GPU path): phi already holds
+  // Q = phi(j0*, .) at the line's own row, so axis 0 is the local row
+  if (p.a >= 1) idx += static_cast<long>(p.pregathered ? g.k0l : static_cast<int>(chain & 0xFFFFu)) * p.ax[0].stride;
   if (p.a >= 2) idx += static_cast<long>(chain >> 16) * p.ax[1].stride;
   return idx;
 }
@@ -232,6 +235,8 @@ __global__ void __launch_bounds__(1024) ct_pass_kernel(CtPass p) {
         if (b > p.a) g.phi_other += static_cast<long>(c) * p.ax[b].stride;
       }
     }
+    g.k0l = g.k[0];
+    g.k[0] += p.k0_off;
     *s.geo = g;
     for (int q = 0; q < 8; ++q) s.scal[q] = 0ull;
   }
@@ -800,6 +805,8 @@ __global__ void __launch_bounds__(1024) ct_pass_kernel(CtPass p) {
         uint32_t packed;
         if (p.a == 0) {
           packed = static_cast<uint32_t>(win);
+          // multi-GPU column slab: also hand phi(j0*, column) to the row owner
+          if (p.q_out) p.q_out[node] = p.phi[g.phi_other + static_cast<long>(win) * A.stride];
         } else {
           const uint32_t ch =
               DY ? p.state_in[g.base + static_cast<long>(win) * A.stride] : sm.chain[win];
@@ -829,34 +836,64 @@ CtPlan::~CtPlan() {
   if (stats_) cudaFree(stats_);
 }
 
-void CtPlan::init(const GridDesc& g) {
-  g_ = g;
-  for (int a = 0; a < g.d; ++a) {
-    if (g.n[a] > 65535) throw std::invalid_argument("ctransform: extent above 65535");
+void CtPlan::init(const GridDesc& g) { setup(g, g, 0, g.d, 0, false, false); }
+
+void CtPlan::init_slab_rows(const GridDesc& global, int row0, int nrows) {
+  if (global.d < 2) throw std::invalid_argument("ctransform: slabs need d >= 2");
+  int ext[3] = {nrows, global.n[1], global.d > 2 ? global.n[2] : 1};
+  setup(make_grid(global.d, ext), global, 1, global.d, row0, true, false);
+}
+
+void CtPlan::init_slab_cols(const GridDesc& global, int ncols) {
+  if (global.d < 2) throw std::invalid_argument("ctransform: slabs need d >= 2");
+  int ext[2] = {global.n[0], ncols};
+  setup(make_grid(2, ext), global, 0, 1, 0, false, true);
+}
+
+// loc: the grid the kernels walk (the whole grid, a row slab, or the
+// (n0 x ncols) column slab whose second axis is virtual); global: the
+// problem's grid (coordinates, dyadic tables). Passes [pb, pe) of loc.
+void CtPlan::setup(const GridDesc& loc, const GridDesc& global, int pb, int pe, int k0_off,
+                   bool pregathered, bool virtual_cols) {
+  g_ = loc;
+  pb_ = pb;
+  pe_ = pe;
+  k0_off_ = k0_off;
+  // real axes share the global grid's extent and coordinates; the column
+  // slab's second axis is virtual (a flattened block of columns)
+  const int nreal = virtual_cols ? 1 : loc.d;
+  for (int a = 0; a < loc.d; ++a) {
     CtAxis& A = ax_[a];
-    A.n = g.n[a];
-    A.stride = g.stride[a];
-    A.h = g.h[a];
-    A.dyadic = is_dyadic(g.n[a]) ? 1 : 0;
+    A.stride = loc.stride[a];
     A.G = nullptr;
+    if (a >= nreal) {  // virtual column axis
+      A.n = loc.n[a];
+      A.h = 1.0;
+      A.dyadic = 1;
+      continue;
+    }
+    if (global.n[a] > 65535) throw std::invalid_argument("ctransform: extent above 65535");
+    A.n = global.n[a];
+    A.h = global.h[a];
+    A.dyadic = is_dyadic(global.n[a]) ? 1 : 0;
     if (!A.dyadic) {
       for (int b = 0; b < a; ++b)
-        if (!ax_[b].dyadic && g.n[b] == g.n[a]) tables_[a] = tables_[b];
+        if (!ax_[b].dyadic && global.n[b] == global.n[a]) tables_[a] = tables_[b];
       if (!tables_[a]) {
-        if (g.n[a] > 4096) throw std::invalid_argument("ctransform: non-dyadic extent above 4096");
-        const int n = g.n[a];
+        if (global.n[a] > 4096) throw std::invalid_argument("ctransform: non-dyadic extent above 4096");
+        const int n = global.n[a];
         std::vector<double4> host(static_cast<size_t>(n) * n);
         for (int k = 0; k < n; ++k) {
-          const double x = coord(g.h[a], k);
+          const double x = coord(global.h[a], k);
           for (int j = 0; j < n; ++j) {
-            const double y = coord(g.h[a], j);
-            double pr, pe;
-            bfmx::two_prod(x, y, pr, pe);
+            const double y = coord(global.h[a], j);
+            double pr, pe2;
+            bfmx::two_prod(x, y, pr, pe2);
             bfmx::Exp<8> e;
             e.clear();
             e.grow(0.5 * x * x);
             e.grow(0.5 * y * y);
-            e.grow(-pe);
+            e.grow(-pe2);
             e.grow(-pr);
             // peel off up to three limbs, largest first; the remainder must vanish
             double limb[3] = {0.0, 0.0, 0.0};
@@ -875,9 +912,11 @@ void CtPlan::init(const GridDesc& g) {
       A.G = tables_[a];
     }
   }
-  if (g.d > 1) {
-    BFM_CUDA(cudaMalloc(&state_[0], g.size * sizeof(uint32_t)));
-    if (g.d > 2) BFM_CUDA(cudaMalloc(&state_[1], g.size * sizeof(uint32_t)));
+  dyadic_ = true;
+  for (int a = 0; a < global.d; ++a) dyadic_ = dyadic_ && is_dyadic(global.n[a]);
+  if (loc.d > 1 && pe - pb > 1) {
+    BFM_CUDA(cudaMalloc(&state_[0], loc.size * sizeof(uint32_t)));
+    if (pe - pb > 2) BFM_CUDA(cudaMalloc(&state_[1], loc.size * sizeof(uint32_t)));
   }
   BFM_CUDA(cudaMalloc(&slow_, sizeof(unsigned long long)));
   BFM_CUDA(cudaMemset(slow_, 0, sizeof(unsigned long long)));
@@ -892,19 +931,21 @@ void CtPlan::init(const GridDesc& g) {
   BFM_CUDA(cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
   const int budget = max_optin - 1024;
 
-  for (int a = 0; a < g.d; ++a) {
+  for (int a = pb; a < pe; ++a) {
     CtPass& P = pass_[a];
     std::memset(&P, 0, sizeof(P));
-    P.d = g.d;
+    P.d = loc.d;
     P.a = a;
-    P.last = a == g.d - 1;
-    for (int b = 0; b < g.d; ++b) P.ax[b] = ax_[b];
-    const int n = g.n[a];
-    P.nlines = g.size / n;
+    P.last = a == global.d - 1;
+    P.k0_off = k0_off;
+    P.pregathered = pregathered ? 1 : 0;
+    for (int b = 0; b < loc.d; ++b) P.ax[b] = ax_[b];
+    const int n = loc.n[a];
+    P.nlines = loc.size / n;
     P.tpl = n <= 512 ? 32 : (n <= 1024 ? 64 : (n <= 2048 ? 128 : 256));
     P.C = (n + P.tpl - 1) / P.tpl;
-    P.strided = a != g.d - 1;
-    const bool dy = ax_[0].dyadic && (g.d < 2 || ax_[1].dyadic) && (g.d < 3 || ax_[2].dyadic);
+    P.strided = a != loc.d - 1;
+    const bool dy = dyadic_;
     int o = 0;
     P.off_fv = o;
     o = align16(o + 8 * (n + n / 32 + 1));
@@ -936,8 +977,40 @@ void CtPlan::init(const GridDesc& g) {
                                 budget));
   BFM_CUDA(cudaFuncSetAttribute(ct_pass_kernel<false>,
                                 cudaFuncAttributeMaxDynamicSharedMemorySize, budget));
-  dyadic_ = ax_[0].dyadic && (g.d < 2 || ax_[1].dyadic) && (g.d < 3 || ax_[2].dyadic);
   ready_ = true;
+}
+
+void CtPlan::launch(const CtPass& P, cudaStream_t stream, LaunchCounter* lc) {
+  const long blocks = (P.nlines + P.lpc - 1) / P.lpc;
+  if (dyadic_)
+    ct_pass_kernel<true><<<static_cast<unsigned>(blocks), P.lpc * P.tpl, P.lpc * P.line_bytes,
+                           stream>>>(P);
+  else
+    ct_pass_kernel<false><<<static_cast<unsigned>(blocks), P.lpc * P.tpl, P.lpc * P.line_bytes,
+                            stream>>>(P);
+  BFM_LAUNCH_CHECK("ct_pass_kernel");
+  if (lc) lc->add();
+}
+
+void CtPlan::run_cols(const double* d_phi_cols, uint32_t* d_chain, double* d_q, cudaStream_t stream,
+                      LaunchCounter* lc) {
+  CtPass P = pass_[0];
+  P.phi = d_phi_cols;
+  P.state_out = d_chain;
+  P.q_out = d_q;
+  launch(P, stream, lc);
+}
+
+void CtPlan::run_rows(const uint32_t* d_chain0, const double* d_q, double* d_out,
+                      cudaStream_t stream, LaunchCounter* lc) {
+  for (int a = 1; a < g_.d; ++a) {
+    CtPass P = pass_[a];
+    P.phi = d_q;
+    P.state_in = a == 1 ? d_chain0 : state_[0];
+    P.state_out = P.last ? nullptr : state_[0];
+    P.out = d_out;
+    launch(P, stream, lc);
+  }
 }
 
 void CtPlan::run(const double* d_phi, double* d_out, cudaStream_t stream, LaunchCounter* lc) {
@@ -947,15 +1020,7 @@ void CtPlan::run(const double* d_phi, double* d_out, cudaStream_t stream, Launch
     P.state_in = a > 0 ? state_[(a - 1) & 1] : nullptr;
     P.state_out = P.last ? nullptr : state_[a & 1];
     P.out = d_out;
-    const long blocks = (P.nlines + P.lpc - 1) / P.lpc;
-    if (dyadic_)
-      ct_pass_kernel<true><<<static_cast<unsigned>(blocks), P.lpc * P.tpl, P.lpc * P.line_bytes,
-                             stream>>>(P);
-    else
-      ct_pass_kernel<false><<<static_cast<unsigned>(blocks), P.lpc * P.tpl, P.lpc * P.line_bytes,
-                              stream>>>(P);
-    BFM_LAUNCH_CHECK("ct_pass_kernel");
-    if (lc) lc->add();
+    launch(P, stream, lc);
   }
 }
 

@@ -28,6 +28,11 @@ struct CtPass {
   const uint32_t* state_in;  // argmin chain of previous passes (a > 0)
   uint32_t* state_out;       // non-last passes
   double* out;               // last pass
+  // multi-GPU slabs (0 / null on a whole grid): global row of local row 0;
+  // phi holds Q = phi(j0*, .) per node (row-slab passes); pass-0 output of Q
+  int k0_off;
+  int pregathered;
+  double* q_out;
   // shared-memory carve-up (bytes, per line)
   int off_fv, off_chain, off_hidx, off_H, off_flag, off_list, off_lohi, off_scal, line_bytes;
   // statistics (device counters, may be null): lines that needed exact resolution
@@ -46,11 +51,27 @@ class CtPlan {
   // out = phi^c (exactly rounded toward -inf). phi and out are device pointers
   // (may not alias). Enqueues g.d kernels on stream.
   void run(const double* d_phi, double* d_out, cudaStream_t stream, LaunchCounter* lc);
+
+  // Multi-GPU slab decomposition along axis 0. Column slab:
+  // the (n0 x ncols) block of the flattened non-axis-0 columns; pass 0 writes
+  // the argmin j0* and Q = phi(j0*, column) per node. Row slab: rows
+  // [row0, row0 + nrows) of the global grid; passes 1..d-1 read the chain and
+  // Q of their own rows (after the transpose) and write phi^c.
+  void init_slab_cols(const GridDesc& global, int ncols);
+  void init_slab_rows(const GridDesc& global, int row0, int nrows);
+  void run_cols(const double* d_phi_cols, uint32_t* d_chain, double* d_q, cudaStream_t stream,
+                LaunchCounter* lc);
+  void run_rows(const uint32_t* d_chain0, const double* d_q, double* d_out, cudaStream_t stream,
+                LaunchCounter* lc);
   unsigned long long slow_query_count();  // diagnostic (synchronous)
   void stats(unsigned long long* out8);     // diagnostic counters (synchronous)
   const GridDesc& grid() const { return g_; }
 
  private:
+  void setup(const GridDesc& loc, const GridDesc& global, int pb, int pe, int k0_off,
+             bool pregathered, bool virtual_cols);
+  void launch(const CtPass& P, cudaStream_t stream, LaunchCounter* lc);
+  int pb_ = 0, pe_ = 0, k0_off_ = 0;
   GridDesc g_;
   CtAxis ax_[3] = {};
   double4* tables_[3] = {nullptr, nullptr, nullptr};

@@ -31,6 +31,7 @@ struct PoisArgs {
   const double* lam1;
   const double* lam2;
   double scale;
+  long col_off;  // multi-GPU column slab: global index of local column 0
   int npass;
   int pstage[bfmdct::kMaxStages];
   int pfused[bfmdct::kMaxStages];
@@ -206,11 +207,12 @@ __global__ void __launch_bounds__(512) pois_fft_kernel(PoisArgs a) {
   cplx* zB = reinterpret_cast<cplx*>(zBd);
   double l1v = 0.0, l2v = 0.0;
   if (a.mode == kFused && active) {
+    const long c = lbase + a.col_off;
     if (a.d == 2) {
-      l1v = a.lam1[lbase];
+      l1v = a.lam1[c];
     } else if (a.d == 3) {
-      l1v = a.lam1[lbase / a.n2];
-      l2v = a.lam2[lbase % a.n2];
+      l1v = a.lam1[c / a.n2];
+      l2v = a.lam2[c % a.n2];
     }
   }
   double* outbuf = zAd;  // where the line's final values end up
@@ -319,7 +321,7 @@ __global__ void __launch_bounds__(512) pois_naive_kernel(PoisArgs a) {
   double* yb = xa + n;
   double l1v = 0.0, l2v = 0.0;
   if (a.mode == kFused && active) {
-    const long inner = line_base(ax, L);
+    const long inner = line_base(ax, L) + a.col_off;
     if (a.d == 2) {
       l1v = a.lam1[inner];
     } else if (a.d == 3) {
@@ -380,18 +382,45 @@ PoissonPlan::~PoissonPlan() {
   if (tmp_) cudaFree(tmp_);
 }
 
-void PoissonPlan::init(const GridDesc& g) {
+void PoissonPlan::init(const GridDesc& g) { setup(g, g, 0, 0, g.d); }
+
+void PoissonPlan::init_slab_rows(const GridDesc& global, int nrows) {
+  if (global.d < 2) throw std::invalid_argument("solve_neumann: slabs need d >= 2");
+  int ext[3] = {nrows, global.n[1], global.d > 2 ? global.n[2] : 1};
+  setup(make_grid(global.d, ext), global, 0, 1, global.d);
+}
+
+void PoissonPlan::init_slab_cols(const GridDesc& global, long col0, int ncols) {
+  if (global.d < 2) throw std::invalid_argument("solve_neumann: slabs need d >= 2");
+  int ext[2] = {global.n[0], ncols};
+  setup(make_grid(2, ext), global, col0, 0, 1);
+}
+
+// loc: the grid the kernels walk; global: the problem grid (spectrum,
+// normalisation). A column slab is (n0 x ncols) with a virtual second axis.
+void PoissonPlan::setup(const GridDesc& loc, const GridDesc& global, long col0, int ab, int ae) {
   constexpr double kPi = 3.14159265358979323846;
-  g_ = g;
+  g_ = loc;
+  gg_ = global;
+  col_off_ = col0;
+  scale_ = 1.0;
+  for (int a = 0; a < global.d; ++a) scale_ *= 2.0 * global.n[a];
+  for (int a = 0; a < global.d; ++a) {
+    const int n = global.n[a];
+    std::vector<double> lam(n);
+    const double na = n;
+    for (int k = 0; k < n; ++k) lam[k] = (2.0 - 2.0 * std::cos(kPi * k / na)) * na * na;
+    BFM_CUDA(cudaMalloc(&lam_[a], n * sizeof(double)));
+    BFM_CUDA(cudaMemcpy(lam_[a], lam.data(), n * sizeof(double), cudaMemcpyHostToDevice));
+  }
+  const GridDesc& g = loc;
   int dev = 0;
   BFM_CUDA(cudaGetDevice(&dev));
   int max_optin = 0;
   BFM_CUDA(cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
   const int budget = max_optin - 1024;
-  scale_ = 1.0;
-  for (int a = 0; a < g.d; ++a) {
+  for (int a = ab; a < ae; ++a) {  // axes whose line transforms this plan runs
     const int n = g.n[a];
-    scale_ *= 2.0 * n;
     host_[a].reset(new bfmdct::HostLinePlan);
     host_[a]->build(n);
     const bfmdct::HostLinePlan& H = *host_[a];
@@ -427,33 +456,29 @@ void PoissonPlan::init(const GridDesc& g) {
     if (c.tpl > 32) lpc = std::min(lpc, 15);
     lpc = static_cast<int>(std::min<long>(lpc, c.nlines));
     c.lpc = std::max(1, lpc);
-    std::vector<double> lam(n);
-    const double na = n;
-    for (int k = 0; k < n; ++k) lam[k] = (2.0 - 2.0 * std::cos(kPi * k / na)) * na * na;
-    BFM_CUDA(cudaMalloc(&lam_[a], n * sizeof(double)));
-    BFM_CUDA(cudaMemcpy(lam_[a], lam.data(), n * sizeof(double), cudaMemcpyHostToDevice));
   }
   BFM_CUDA(cudaFuncSetAttribute(pois_fft_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, budget));
   BFM_CUDA(cudaFuncSetAttribute(pois_naive_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, budget));
 }
 
-void PoissonPlan::solve(const double* d_rhs, double* d_out, cudaStream_t stream,
-                        LaunchCounter* lc) {
-  const int d = g_.d;
-  auto launch = [&](int axis, int mode, const double* in, double* out) {
+void PoissonPlan::launch(int axis, int mode, const double* in, double* out, cudaStream_t stream,
+                         LaunchCounter* lc) {
+  {
+    const int d = gg_.d;
     PoisArgs A;
     std::memset(&A, 0, sizeof(A));
     A.ax = cfg_[axis];
     A.mode = mode;
     A.d = d;
-    A.n1 = d > 1 ? g_.n[1] : 1;
-    A.n2 = d > 2 ? g_.n[2] : 1;
+    A.n1 = d > 1 ? gg_.n[1] : 1;
+    A.n2 = d > 2 ? gg_.n[2] : 1;
     A.in = in;
     A.out = out;
     A.lam0 = lam_[0];
     A.lam1 = d > 1 ? lam_[1] : nullptr;
     A.lam2 = d > 2 ? lam_[2] : nullptr;
     A.scale = scale_;
+    A.col_off = col_off_;
     const PoisAxisCfg& c = cfg_[axis];
     A.npass = 0;
     for (int st = 0; st < c.plan.nstages;) {
@@ -474,14 +499,37 @@ void PoissonPlan::solve(const double* d_rhs, double* d_out, cudaStream_t stream,
       pois_naive_kernel<<<static_cast<unsigned>(blocks), c.lpc * c.tpl, sm, stream>>>(A);
     BFM_LAUNCH_CHECK("pois kernel");
     if (lc) lc->add();
-  };
+  }
+}
+
+void PoissonPlan::solve(const double* d_rhs, double* d_out, cudaStream_t stream,
+                        LaunchCounter* lc) {
+  const int d = g_.d;
   const double* cur = d_rhs;
   for (int a = d - 1; a >= 1; --a) {
-    launch(a, kFwd, cur, d_out);
+    launch(a, kFwd, cur, d_out, stream, lc);
     cur = d_out;
   }
-  launch(0, kFused, cur, d_out);
-  for (int a = 1; a < d; ++a) launch(a, kInv, d_out, d_out);
+  launch(0, kFused, cur, d_out, stream, lc);
+  for (int a = 1; a < d; ++a) launch(a, kInv, d_out, d_out, stream, lc);
+}
+
+void PoissonPlan::rows_forward(const double* d_in, double* d_out, cudaStream_t stream,
+                               LaunchCounter* lc) {
+  const double* cur = d_in;
+  for (int a = g_.d - 1; a >= 1; --a) {
+    launch(a, kFwd, cur, d_out, stream, lc);
+    cur = d_out;
+  }
+}
+
+void PoissonPlan::cols_fused(const double* d_in, double* d_out, cudaStream_t stream,
+                             LaunchCounter* lc) {
+  launch(0, kFused, d_in, d_out, stream, lc);
+}
+
+void PoissonPlan::rows_inverse(double* d_inout, cudaStream_t stream, LaunchCounter* lc) {
+  for (int a = 1; a < g_.d; ++a) launch(a, kInv, d_inout, d_inout, stream, lc);
 }
 
 }  // namespace bfmgpu

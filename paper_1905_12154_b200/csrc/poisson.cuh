@@ -30,8 +30,23 @@ class PoissonPlan {
   // the shared DCT (bitwise equal to oracle/_ref). rhs and out may alias.
   void solve(const double* d_rhs, double* d_out, cudaStream_t stream, LaunchCounter* lc);
 
+  // Multi-GPU slab decomposition along axis 0: DCT-II along
+  // axes d-1..1 on a row slab, transpose, [DCT-II axis 0, divide, DCT-III
+  // axis 0] on a column slab (global columns col0 .. col0+ncols of the
+  // flattened non-axis-0 index), transpose back, DCT-III axes 1..d-1.
+  void init_slab_rows(const GridDesc& global, int nrows);
+  void init_slab_cols(const GridDesc& global, long col0, int ncols);
+  void rows_forward(const double* d_in, double* d_out, cudaStream_t stream, LaunchCounter* lc);
+  void cols_fused(const double* d_in, double* d_out, cudaStream_t stream, LaunchCounter* lc);
+  void rows_inverse(double* d_inout, cudaStream_t stream, LaunchCounter* lc);
+
  private:
-  GridDesc g_;
+  void setup(const GridDesc& loc, const GridDesc& global, long col0, int ab, int ae);
+  void launch(int axis, int mode, const double* in, double* out, cudaStream_t stream,
+              LaunchCounter* lc);
+  GridDesc g_;   // grid the kernels walk
+  GridDesc gg_;  // problem grid
+  long col_off_ = 0;
   std::unique_ptr<bfmdct::HostLinePlan> host_[3];
   PoisAxisCfg cfg_[3] = {};
   void* tables_[3] = {nullptr, nullptr, nullptr};

@@ -37,12 +37,15 @@ constexpr int kMedBlocks = 148 * 3;  // each warp owns kMedium doubles of hbuf
 constexpr int kHeavySmem = kHeavyIds * 4;
 
 struct MapArgs {
-  GridDesc g;
+  GridDesc g;           // the nodes this launch maps (whole grid or a row slab)
+  GridDesc gg;          // the problem grid (coordinates, boundaries, cell keys)
+  int row_off;          // global row of local row 0 (row slab), else 0
+  long u_shift;         // u index of local node 0 (one halo row above a slab)
   const double* u;      // potential (mode 0) or nullptr
   const double* disp;   // displacement (mode 1)
   double scale;
   const double* src;    // source density
-  uint32_t* key;        // cell of the lo corner; sentinel = N for massless sources
+  uint32_t* key;        // global cell of the lo corner; sentinel = N (global) for massless sources
   uint8_t* cmask;
   double* w;
   double* disp_out;     // optional
@@ -88,23 +91,26 @@ __device__ __forceinline__ void locate(int n, double h, double x, int& lo, bool&
 
 __global__ void pf_map_kernel(MapArgs A) {
   const GridDesc& g = A.g;
+  const GridDesc& gg = A.gg;
   for (long s = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; s < g.size;
        s += static_cast<long>(gridDim.x) * blockDim.x) {
     int id[3] = {0, 0, 0};
     node_idx(g, s, id);
+    id[0] += A.row_off;  // global indices from here on
     double dsp[3] = {0.0, 0.0, 0.0};
     for (int a = 0; a < g.d; ++a) {
-      const double x = coord(g.h[a], id[a]);
+      const double x = coord(gg.h[a], id[a]);
       if (A.u) {
         const long st = g.stride[a];
-        const int n = g.n[a];
+        const int n = gg.n[a];
         const int j = id[a];
+        const long su = s + A.u_shift;
         const double inv_h = static_cast<double>(n);
         const double inv_2h = 0.5 * inv_h;
         double gr;
-        if (j == 0) gr = (A.u[s + st] - A.u[s]) * inv_h;
-        else if (j == n - 1) gr = (A.u[s] - A.u[s - st]) * inv_h;
-        else gr = (A.u[s + st] - A.u[s - st]) * inv_2h;
+        if (j == 0) gr = (A.u[su + st] - A.u[su]) * inv_h;
+        else if (j == n - 1) gr = (A.u[su] - A.u[su - st]) * inv_h;
+        else gr = (A.u[su + st] - A.u[su - st]) * inv_2h;
         double mag = fabs(gr);
         if (!(mag < A.diam)) mag = A.diam;
         const double v = gr < 0.0 ? -mag : mag;
@@ -120,19 +126,19 @@ __global__ void pf_map_kernel(MapArgs A) {
     if (!A.binning) continue;
     const double m = A.src[s];
     if (m == 0.0) {
-      A.key[s] = static_cast<uint32_t>(g.size);
+      A.key[s] = static_cast<uint32_t>(gg.size);
       continue;
     }
     long key = 0;
     uint8_t mask = 0;
     for (int a = 0; a < g.d; ++a) {
-      const double x = coord(g.h[a], id[a]);
+      const double x = coord(gg.h[a], id[a]);
       const double xp = x + A.scale * dsp[a];
       int lo;
       bool cl;
       double whi;
-      locate(g.n[a], g.h[a], xp, lo, cl, whi);
-      key += static_cast<long>(lo) * g.stride[a];
+      locate(gg.n[a], gg.h[a], xp, lo, cl, whi);
+      key += static_cast<long>(lo) * gg.stride[a];
       if (cl) mask |= static_cast<uint8_t>(1u << a);
       A.w[a * g.size + s] = whi;
     }
@@ -153,13 +159,16 @@ __global__ void pf_bounds_kernel(const uint32_t* keys, long n, uint32_t sentinel
 }
 
 struct GatherArgs {
-  GridDesc g;
+  GridDesc g;        // target nodes (whole grid or a row slab)
+  int row_off;       // global row of local target row 0
+  long cell_shift;   // cell index of target t's own cell is t + cell_shift
+  long nrec;         // deposit records (sources): stride of w
   const int* end;
   const int* off;
-  const int* bucket;
+  const int* bucket;  // record ids sorted by (cell, record id)
   const uint8_t* cmask;
   const double* w;
-  const double* src;
+  const double* src;  // record mass
   const double* target;  // may be null: output rho
   double* out;
 };
@@ -167,7 +176,7 @@ struct GatherArgs {
 __device__ __forceinline__ double deposit_weight(const GatherArgs& A, int s, int b) {
   double wt = A.src[s];
   for (int a = 0; a < A.g.d; ++a) {
-    const double wh = A.w[a * A.g.size + s];
+    const double wh = A.w[a * A.nrec + s];
     wt *= ((b >> a) & 1) ? wh : 1.0 - wh;
   }
   return wt;
@@ -183,12 +192,13 @@ __global__ void pf_gather_kernel(GatherArgs A, int* heavy, int* nheavy) {
        t += static_cast<long>(gridDim.x) * blockDim.x) {
     int id[3] = {0, 0, 0};
     node_idx(g, t, id);
+    id[0] += A.row_off;
     int pos[8], end[8];
     int nl = 0;
     int bits[8];
     int total = 0;
     for (int b = 0; b < corners; ++b) {
-      long c = t;
+      long c = t + A.cell_shift;
       bool ok = true;
       for (int a = 0; a < g.d; ++a)
         if ((b >> a) & 1) {
@@ -240,10 +250,11 @@ __device__ __forceinline__ void target_buckets(const GatherArgs& A, long t, Targ
   const GridDesc& g = A.g;
   int id[3] = {0, 0, 0};
   node_idx(g, t, id);
+  id[0] += A.row_off;
   tb.nl = 0;
   tb.K = 0;
   for (int b = 0; b < (1 << g.d); ++b) {
-    long c = t;
+    long c = t + A.cell_shift;
     bool ok = true;
     for (int a = 0; a < g.d; ++a)
       if ((b >> a) & 1) {
@@ -411,62 +422,121 @@ PushforwardPlan::~PushforwardPlan() {
     if (p) cudaFree(p);
 }
 
-void PushforwardPlan::init(const GridDesc& g) {
-  g_ = g;
-  const long N = g.size;
-  if (N >= (1L << 29)) throw std::invalid_argument("pushforward: grid too large");
+void PushforwardPlan::init(const GridDesc& g) { setup(g, g, 0, false); }
+
+void PushforwardPlan::init_slab(const GridDesc& global, int row0, int nrows) {
+  if (global.d < 2) throw std::invalid_argument("pushforward: slabs need d >= 2");
+  int ext[3] = {nrows, global.n[1], global.d > 2 ? global.n[2] : 1};
+  setup(make_grid(global.d, ext), global, row0, true);
+}
+
+// loc: target/source nodes of this plan (the grid, or rows [row0, row0 +
+// nrows) of it); global: the problem grid. A slab's cells start one row above
+// its first row (deposits from the cell row above reach its first row).
+void PushforwardPlan::setup(const GridDesc& loc, const GridDesc& global, int row0, bool slab) {
+  g_ = loc;
+  gg_ = global;
+  row_off_ = row0;
+  cell_shift_ = slab ? loc.stride[0] : 0;
+  ncells_ = slab ? loc.size + loc.stride[0] : loc.size;
+  if (global.size >= (1L << 29)) throw std::invalid_argument("pushforward: grid too large");
+  const long N = loc.size;
   BFM_CUDA(cudaMalloc(&key_, N * sizeof(uint32_t)));
   BFM_CUDA(cudaMalloc(&cmask_, N));
-  BFM_CUDA(cudaMalloc(&w_, g.d * N * sizeof(double)));
-  BFM_CUDA(cudaMalloc(&off_, (N + 1) * sizeof(int)));
-  BFM_CUDA(cudaMalloc(&end_, (N + 1) * sizeof(int)));
+  BFM_CUDA(cudaMalloc(&w_, g_.d * N * sizeof(double)));
+  BFM_CUDA(cudaMalloc(&off_, (ncells_ + 1) * sizeof(int)));
+  BFM_CUDA(cudaMalloc(&end_, (ncells_ + 1) * sizeof(int)));
   BFM_CUDA(cudaMalloc(&heavy_, (N + 1) * sizeof(int)));
   BFM_CUDA(cudaMalloc(&nheavy_, 4 * sizeof(unsigned long long)));
-  const long deposits = (static_cast<long>(1) << g.d) * N;
-  med_blocks_ = static_cast<int>(std::max<long>(1, std::min<long>(kMedBlocks, deposits / (kMedWarps * kMedium))));
-  const long hcap = std::max<long>(deposits, static_cast<long>(med_blocks_) * kMedWarps * kMedium);
-  BFM_CUDA(cudaMalloc(&hbuf_, hcap * sizeof(double)));
-  sorter_.init(N);
+  ensure_records(N);
   BFM_CUDA(cudaFuncSetAttribute(pf_gather_heavy_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 kHeavySmem));
   BFM_CUDA(cudaFuncSetAttribute(pf_gather_medium_kernel,
                                 cudaFuncAttributeMaxDynamicSharedMemorySize, kMedSmem));
   key_bits_ = 1;
-  while ((1L << key_bits_) <= N) ++key_bits_;  // cells 0..N-1 plus sentinel N
+  while ((1L << key_bits_) <= ncells_) ++key_bits_;  // cells 0..ncells-1 plus the sentinel
 }
+
+void PushforwardPlan::ensure_records(long nrec) {
+  if (nrec <= rec_cap_ && hbuf_) return;
+  const long cap = std::max<long>(nrec, 1);
+  if (hbuf_) {
+    cudaFree(hbuf_);
+    hbuf_ = nullptr;
+  }
+  const long deposits = (static_cast<long>(1) << g_.d) * cap;
+  med_blocks_ = static_cast<int>(std::max<long>(1, std::min<long>(kMedBlocks, deposits / (kMedWarps * kMedium))));
+  const long hcap = std::max<long>(deposits, static_cast<long>(med_blocks_) * kMedWarps * kMedium);
+  BFM_CUDA(cudaMalloc(&hbuf_, hcap * sizeof(double)));
+  sorter_.init(cap);
+  rec_cap_ = cap;
+}
+
+namespace {
+MapArgs map_args(const GridDesc& g, const GridDesc& gg, int row_off, long cell_shift) {
+  MapArgs A{};
+  A.g = g;
+  A.gg = gg;
+  A.row_off = row_off;
+  A.u_shift = cell_shift;  // a slab's u carries one halo row on each side
+  A.scale = 1.0;
+  A.diam = std::sqrt(static_cast<double>(g.d));
+  return A;
+}
+}  // namespace
 
 void PushforwardPlan::map_only(const double* d_u, double* d_disp, cudaStream_t stream,
                                LaunchCounter* lc) {
-  MapArgs A{};
-  A.g = g_;
+  MapArgs A = map_args(g_, gg_, row_off_, cell_shift_);
   A.u = d_u;
-  A.scale = 1.0;
   A.disp_out = d_disp;
-  A.diam = std::sqrt(static_cast<double>(g_.d));
   pf_map_kernel<<<grid_for(g_.size, 256), 256, 0, stream>>>(A);
   BFM_LAUNCH_CHECK("pf_map_kernel");
   if (lc) lc->add();
 }
 
-void PushforwardPlan::bin_and_gather(const double* d_source, const double* d_target,
-                                     double* d_out, cudaStream_t stream, LaunchCounter* lc) {
+void PushforwardPlan::map_records(const double* d_u_ext, const double* d_source, uint32_t* d_key,
+                                  double* d_w, uint8_t* d_cmask, double* d_disp_out,
+                                  cudaStream_t stream, LaunchCounter* lc) {
+  MapArgs A = map_args(g_, gg_, row_off_, cell_shift_);
+  A.u = d_u_ext;
+  A.src = d_source;
+  A.key = d_key;
+  A.cmask = d_cmask;
+  A.w = d_w;
+  A.disp_out = d_disp_out;
+  A.binning = 1;
+  pf_map_kernel<<<grid_for(g_.size, 256), 256, 0, stream>>>(A);
+  BFM_LAUNCH_CHECK("pf_map_kernel");
+  if (lc) lc->add();
+}
+
+void PushforwardPlan::gather(long nrec, const uint32_t* d_keys, const double* d_mass,
+                             const double* d_w, const uint8_t* d_cmask, const double* d_target,
+                             double* d_out, cudaStream_t stream, LaunchCounter* lc) {
+  ensure_records(nrec);
   const long N = g_.size;
-  const uint32_t* skeys = nullptr;
-  const int* svals = nullptr;
-  sorter_.sort(key_, nullptr, N, key_bits_, stream, lc, &skeys, &svals);
-  BFM_CUDA(cudaMemsetAsync(off_, 0, (N + 1) * sizeof(int), stream));
-  BFM_CUDA(cudaMemsetAsync(end_, 0, (N + 1) * sizeof(int), stream));
+  BFM_CUDA(cudaMemsetAsync(off_, 0, (ncells_ + 1) * sizeof(int), stream));
+  BFM_CUDA(cudaMemsetAsync(end_, 0, (ncells_ + 1) * sizeof(int), stream));
   BFM_CUDA(cudaMemsetAsync(nheavy_, 0, 4 * sizeof(unsigned long long), stream));
-  pf_bounds_kernel<<<grid_for(N, 256), 256, 0, stream>>>(skeys, N, static_cast<uint32_t>(N), off_,
-                                                         end_);
+  const int* svals = nullptr;
+  if (nrec > 0) {
+    const uint32_t* skeys = nullptr;
+    sorter_.sort(d_keys, nullptr, nrec, key_bits_, stream, lc, &skeys, &svals);
+    pf_bounds_kernel<<<grid_for(nrec, 256), 256, 0, stream>>>(
+        skeys, nrec, static_cast<uint32_t>(ncells_), off_, end_);
+  }
   GatherArgs G{};
   G.g = g_;
+  G.row_off = row_off_;
+  G.cell_shift = cell_shift_;
+  G.nrec = nrec;
   G.end = end_;
   G.off = off_;
   G.bucket = svals;
-  G.cmask = cmask_;
-  G.w = w_;
-  G.src = d_source;
+  G.cmask = d_cmask;
+  G.w = d_w;
+  G.src = d_mass;
   G.target = d_target;
   G.out = d_out;
   int* nheavy = reinterpret_cast<int*>(nheavy_);
@@ -476,34 +546,20 @@ void PushforwardPlan::bin_and_gather(const double* d_source, const double* d_tar
   BFM_LAUNCH_CHECK("pf_gather_medium_kernel");
   pf_gather_heavy_kernel<<<2 * 148, 512, kHeavySmem, stream>>>(G, heavy_, nheavy, hbuf_, nheavy_ + 1);
   BFM_LAUNCH_CHECK("pf_gather_heavy_kernel");
-  if (lc) lc->add(4);
+  if (lc) lc->add(nrec > 0 ? 4 : 3);
 }
 
 void PushforwardPlan::from_potential(const double* d_u, const double* d_source,
                                      const double* d_target, double* d_out, double* d_disp_out,
                                      cudaStream_t stream, LaunchCounter* lc) {
-  MapArgs A{};
-  A.g = g_;
-  A.u = d_u;
-  A.scale = 1.0;
-  A.src = d_source;
-  A.key = key_;
-  A.cmask = cmask_;
-  A.w = w_;
-  A.disp_out = d_disp_out;
-  A.binning = 1;
-  A.diam = std::sqrt(static_cast<double>(g_.d));
-  pf_map_kernel<<<grid_for(g_.size, 256), 256, 0, stream>>>(A);
-  BFM_LAUNCH_CHECK("pf_map_kernel");
-  if (lc) lc->add();
-  bin_and_gather(d_source, d_target, d_out, stream, lc);
+  map_records(d_u, d_source, key_, w_, cmask_, d_disp_out, stream, lc);
+  gather(g_.size, key_, d_source, w_, cmask_, d_target, d_out, stream, lc);
 }
 
 void PushforwardPlan::from_displacement(const double* d_disp, double scale,
                                         const double* d_source, double* d_rho,
                                         cudaStream_t stream, LaunchCounter* lc) {
-  MapArgs A{};
-  A.g = g_;
+  MapArgs A = map_args(g_, gg_, row_off_, cell_shift_);
   A.disp = d_disp;
   A.scale = scale;
   A.src = d_source;
@@ -511,11 +567,10 @@ void PushforwardPlan::from_displacement(const double* d_disp, double scale,
   A.cmask = cmask_;
   A.w = w_;
   A.binning = 1;
-  A.diam = std::sqrt(static_cast<double>(g_.d));
   pf_map_kernel<<<grid_for(g_.size, 256), 256, 0, stream>>>(A);
   BFM_LAUNCH_CHECK("pf_map_kernel");
   if (lc) lc->add();
-  bin_and_gather(d_source, nullptr, d_rho, stream, lc);
+  gather(g_.size, key_, d_source, w_, cmask_, nullptr, d_rho, stream, lc);
 }
 
 }  // namespace bfmgpu

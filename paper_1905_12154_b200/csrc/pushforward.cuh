@@ -17,6 +17,10 @@ class PushforwardPlan {
   PushforwardPlan& operator=(const PushforwardPlan&) = delete;
 
   void init(const GridDesc& g);
+  // Multi-GPU row slab: sources and targets are rows
+  // [row0, row0 + nrows) of `global`; u arrays carry one halo row above and
+  // below; deposit records arrive from every rank (see map_records/gather).
+  void init_slab(const GridDesc& global, int row0, int nrows);
 
   // out = target - T#source with T = x - grad(u) (map_from_conjugate,
   // pushforward.hpp:70-91) — or, if target == nullptr, out = T#source.
@@ -28,11 +32,27 @@ class PushforwardPlan {
                          double* d_rho, cudaStream_t stream, LaunchCounter* lc);
   // Map only (displacements), no splat.
   void map_only(const double* d_u, double* d_disp, cudaStream_t stream, LaunchCounter* lc);
+  // Deposit records of this plan's sources: global lo-corner cell (sentinel:
+  // global N for massless sources), upper weights w (d x N SoA), clamp mask.
+  void map_records(const double* d_u, const double* d_source, uint32_t* d_key, double* d_w,
+                   uint8_t* d_cmask, double* d_disp_out, cudaStream_t stream, LaunchCounter* lc);
+  // out = target - rho (or rho) for this plan's targets from nrec records in
+  // global source order: keys are cells of this plan (slab: global cell minus
+  // (row0 - 1) * row stride; sentinel num_cells()), mass, w (d x nrec), mask.
+  void gather(long nrec, const uint32_t* d_keys, const double* d_mass, const double* d_w,
+              const uint8_t* d_cmask, const double* d_target, double* d_out, cudaStream_t stream,
+              LaunchCounter* lc);
+  long num_cells() const { return ncells_; }
 
  private:
-  void bin_and_gather(const double* d_source, const double* d_target, double* d_out,
-                      cudaStream_t stream, LaunchCounter* lc);
-  GridDesc g_;
+  void setup(const GridDesc& loc, const GridDesc& global, int row0, bool slab);
+  void ensure_records(long nrec);
+  GridDesc g_;    // this plan's nodes
+  GridDesc gg_;   // problem grid
+  int row_off_ = 0;
+  long cell_shift_ = 0;
+  long ncells_ = 0;
+  long rec_cap_ = 0;
   uint32_t* key_ = nullptr;  // [N] lo-corner cell of each source (N = no mass)
   uint8_t* cmask_ = nullptr; // [N] axes on which the source is clamped (lo == hi)
   double* w_ = nullptr;      // [d*N] upper-node weight per axis

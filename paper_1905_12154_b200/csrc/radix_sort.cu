@@ -162,6 +162,16 @@ RadixSorter::~RadixSorter() {
 }
 
 void RadixSorter::init(long n) {
+  for (int i = 0; i < 2; ++i) {  // re-init (capacity growth) releases the old buffers
+    if (kbuf_[i]) cudaFree(kbuf_[i]);
+    if (vbuf_[i]) cudaFree(vbuf_[i]);
+    kbuf_[i] = nullptr;
+    vbuf_[i] = nullptr;
+  }
+  if (hist_) cudaFree(hist_);
+  if (bsum_) cudaFree(bsum_);
+  hist_ = nullptr;
+  bsum_ = nullptr;
   cap_ = n;
   blocks_ = (n + kTile - 1) / kTile;
   for (int i = 0; i < 2; ++i) {

@@ -103,6 +103,13 @@ __global__ void __launch_bounds__(kRedThreads) red_final_kernel(const double* pa
   }
   DD r1 = block_reduce(acc1);
   DD r2 = block_reduce(acc2);
+  if (threadIdx.x == 0 && two < 0) {  // raw double-double partial sums (multi-GPU ranks)
+    results[slot] = r1.s;
+    results[slot + 1] = r1.c;
+    results[slot + 2] = r2.s;
+    results[slot + 3] = r2.c;
+    return;
+  }
   if (threadIdx.x == 0) {
     const double s1 = r1.s + r1.c;
     double v = s1 * vol;
@@ -204,6 +211,24 @@ void Reducer::dot(const double* a1, const double* b1, const double* a2, const do
   red_partial_kernel<<<blocks_, kRedThreads, 0, s>>>(A);
   red_final_kernel<<<1, kRedThreads, 0, s>>>(partials_, blocks_, a2 ? 1 : 0, vol, results_, slot);
   BFM_LAUNCH_CHECK("reduce dot");
+  if (lc) lc->add(2);
+}
+
+void Reducer::dot_raw(const double* a1, const double* b1, const double* a2, const double* b2,
+                      long n, int slot, cudaStream_t s, LaunchCounter* lc) {
+  RedArgs A{a1, b1, a2, b2, n, 0, 0, partials_};
+  red_partial_kernel<<<blocks_, kRedThreads, 0, s>>>(A);
+  red_final_kernel<<<1, kRedThreads, 0, s>>>(partials_, blocks_, -1, 1.0, results_, slot);
+  BFM_LAUNCH_CHECK("reduce dot_raw");
+  if (lc) lc->add(2);
+}
+
+void Reducer::primal_raw(const double* disp, const double* mu, int d, long n, int slot,
+                         cudaStream_t s, LaunchCounter* lc) {
+  RedArgs A{disp, mu, nullptr, nullptr, n, 2, d, partials_};
+  red_partial_kernel<<<blocks_, kRedThreads, 0, s>>>(A);
+  red_final_kernel<<<1, kRedThreads, 0, s>>>(partials_, blocks_, -1, 1.0, results_, slot);
+  BFM_LAUNCH_CHECK("reduce primal_raw");
   if (lc) lc->add(2);
 }
 

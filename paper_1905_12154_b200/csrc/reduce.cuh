@@ -22,6 +22,13 @@ class Reducer {
   // (a2 may be null). Sums are double-double accurate (one final rounding).
   void dot(const double* a1, const double* b1, const double* a2, const double* b2, long n,
            double vol, int slot, cudaStream_t s, LaunchCounter* lc);
+  // Unscaled double-double partial sums for a multi-GPU rank:
+  // results[slot..slot+3] = (hi1, lo1, hi2, lo2) of sum fl(a1*b1), sum fl(a2*b2).
+  void dot_raw(const double* a1, const double* b1, const double* a2, const double* b2, long n,
+               int slot, cudaStream_t s, LaunchCounter* lc);
+  // results[slot..slot+1] = (hi, lo) of sum_{m != 0} fl(c * m) (see primal).
+  void primal_raw(const double* disp, const double* mu, int d, long n, int slot, cudaStream_t s,
+                  LaunchCounter* lc);
   // results[slot] = (sum_i a_i) * vol
   void sum(const double* a, long n, double vol, int slot, cudaStream_t s, LaunchCounter* lc);
   // results[slot] = max_i a_i (a_i >= 0 expected); results[slot+1] = 1 if any

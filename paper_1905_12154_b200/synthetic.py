@@ -66,6 +66,20 @@ def c1(n: int = 256, seed: int = 1) -> Tuple[np.ndarray, np.ndarray]:
     return mu, nu
 
 
+def c1_like(shape, seed: int = 1) -> Tuple[np.ndarray, np.ndarray]:
+    """C1's recipe on any 2-D/3-D grid: 3 Gaussians vs a centred disc/ball
+    (test-sized instances, e.g. the multi-GPU decomposition checks)."""
+    d = len(shape)
+    rng = np.random.default_rng(seed)
+    cs, ss = [], []
+    for _ in range(3):
+        cs.append(rng.uniform(0.2, 0.8, size=d))
+        ss.append(rng.uniform(0.05, 0.15))
+    mu = _normalize(_gauss(tuple(shape), cs, ss))
+    nu = _normalize(_ball(tuple(shape), (0.5,) * d, 0.3))
+    return mu, nu
+
+
 def c2(n: int = 1024, seed: int = 2) -> Tuple[np.ndarray, np.ndarray]:
     rng = np.random.default_rng(seed)
     x = axis_coords(n)
