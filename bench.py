@@ -232,8 +232,102 @@ def ctransform_roofline(lib, shape, torch, hbm, hbm_kind, reps=10):
             "ms_per_launch_group": ms, "algorithmic_bytes": bytes_alg, "peak_kind": hbm_kind}
 
 
+def ours_dist(args):
+    """N > 1: the axis-0 slab decomposition (paper_1905_12154_b200/dist.py):
+    one problem split over N GPUs (strong scaling), NCCL all-to-alls for the
+    transposes and deposit records, rank-ordered scalar merges."""
+    rank, world, local = dist_env()
+    import torch
+    import torch.distributed as tdist
+
+    import paper_1905_12154_b200 as bfm
+    from paper_1905_12154_b200 import dist as D
+
+    torch.cuda.set_device(local)
+    bfm.set_device(local)
+    dev = torch.device("cuda", local)
+    tdist.init_process_group("nccl", device_id=dev)
+    comm = D.TorchComm()
+    mu, nu, desc = workload(args.config)
+    N = mu.size
+    L = D.SlabLayout(mu.shape, world)
+    r0, nr = L.rows(rank)
+    cfg = bfm.SolverConfig(tolerance=-1.0, max_iterations=10 ** 6)
+    ops = D.CudaSlabOps(L, rank, dev)
+    s = D.DistSolver(L, comm, ops, mu[r0:r0 + nr], nu[r0:r0 + nr], cfg, mu_full=mu, nu_full=nu,
+                     device=dev)
+    for _ in range(args.warmup):
+        s.step()
+    s.ensure_probe()
+    l0 = ops.launches
+    clocks = ClockSampler(local)
+    tdist.barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    stream = torch.cuda.current_stream()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        s.step()
+    s.ensure_probe()  # the next iteration's probe belongs to this step's work
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ck = clocks.stop()
+    launches = ops.launches - l0
+    t = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
+    tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+    tdist.barrier()
+    ms_max = float(t.item())
+    value = N * args.steps / (ms_max * 1e-3)
+    del s
+
+    # end to end: pinned host slabs in, K iterations, phi/psi slabs back
+    pin_mu = torch.from_numpy(np.ascontiguousarray(mu[r0:r0 + nr])).pin_memory()
+    pin_nu = torch.from_numpy(np.ascontiguousarray(nu[r0:r0 + nr])).pin_memory()
+    tdist.barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    s2 = D.DistSolver(L, comm, ops, pin_mu.numpy(), pin_nu.numpy(), cfg, device=dev)
+    for _ in range(args.steps):
+        s2.step()
+    phi_h = s2.phi.cpu()
+    psi_h = s2.psi.cpu()
+    e2e_local = time.perf_counter() - t0
+    te = torch.tensor([e2e_local], dtype=torch.float64, device=dev)
+    tdist.all_reduce(te, op=tdist.ReduceOp.MAX)
+    e2e_s = float(te.item())
+    del s2, phi_h, psi_h
+    e2e = {"value": N * args.steps / e2e_s, "unit": UNIT,
+           "h2d_bytes_per_step": int(2 * 8 * N / args.steps),
+           "d2h_bytes_per_step": int(2 * 8 * N / args.steps),
+           "note": "DistSolver from pinned host slabs + K step() + phi/psi slab readback, wall clock, max over ranks"}
+    if rank == 0:
+        hbm, hbm_kind = peaks()
+        lib = bfm.load_library()
+        roof = ctransform_roofline(lib, desc["grid"], torch, hbm, hbm_kind)
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded, BASELINE shapes; no public dataset)",
+            "config": dict(desc, parallelism=f"axis-0 slabs x{world} (NCCL all-to-all transposes)",
+                           l2="inputs larger than L2 (about 10 resident float64 fields of 128 MiB)"),
+            "gpu_launches": int(launches),
+            "clocks": ck,
+            "roofline": roof,
+            "cpu_baseline": None,
+            "e2e": e2e,
+        }
+        print(json.dumps(line))
+    ops.close()
+    tdist.destroy_process_group()
+
+
 def ours(args):
     rank, world, local = dist_env()
+    if (world > 1 and not args.replicas) or args.slabs:
+        return ours_dist(args)
     import torch
 
     import paper_1905_12154_b200 as bfm
@@ -299,7 +393,7 @@ def ours(args):
         "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded, BASELINE shapes; no public dataset)",
-        "config": dict(desc, parallelism=("replicas" if world > 1 else "single GPU"),
+        "config": dict(desc, parallelism=("independent replicas" if world > 1 else "single GPU"),
                        l2="inputs larger than L2 (about 10 resident float64 fields of 128 MiB)"),
         "gpu_launches": int(launches),
         "clocks": ck,
@@ -320,6 +414,10 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c3", choices=["c1", "c2", "c3", "c4"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--slabs", action="store_true",
+                    help="use the slab-decomposition driver even at N = 1 (checks the NCCL path)")
+    ap.add_argument("--replicas", action="store_true",
+                    help="N > 1: independent single-GPU replicas instead of the slab decomposition")
     args = ap.parse_args()
     if args.impl == "reference":
         reference_arm(args)

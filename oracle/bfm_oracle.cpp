@@ -514,6 +514,54 @@ int orc_solve_neumann(int dim, const int* ext, const double* rhs, double* out) {
   })
 }
 
+// Multi-GPU slab checks (tests/test_dist_cpu.py): one DCT axis of an array,
+// and the column-slab axis-0 step [DCT-II, divide, DCT-III] of poisson.hpp
+// for global flattened columns col0 .. col0 + ncols (d >= 2).
+int orc_dct_axis(int dim, const int* ext, int axis, int inverse, double* data) {
+  OGUARD({
+    check_grid(dim, ext);
+    if (axis < 0 || axis >= dim) throw std::invalid_argument("orc_dct_axis: bad axis");
+    Grid g(dim, ext);
+    bfmdct::HostLinePlan plan;
+    plan.build(g.n[axis]);
+    std::vector<bfmdct::cplx> scratch(g.n[axis] + 1);
+    const long st = g.stride[axis];
+    const long len = g.n[axis];
+    const long outer = g.size / (len * st);
+    for (long o = 0; o < outer; ++o)
+      for (long i = 0; i < st; ++i) {
+        double* line = data + o * len * st + i;
+        if (inverse) bfmdct::dct3_line_cpu(plan.plan, line, st, scratch.data());
+        else bfmdct::dct2_line_cpu(plan.plan, line, st, scratch.data());
+      }
+  })
+}
+
+int orc_poisson_cols(int dim, const int* ext, long col0, int ncols, const double* in,
+                     double* out) {
+  OGUARD({
+    check_grid(dim, ext);
+    if (dim < 2) throw std::invalid_argument("orc_poisson_cols: d >= 2");
+    Poisson p{Grid(dim, ext)};
+    const int n0 = ext[0];
+    const int n2 = dim > 2 ? ext[2] : 1;
+    std::vector<double> col(n0);
+    for (int c = 0; c < ncols; ++c) {
+      for (int k = 0; k < n0; ++k) col[k] = in[static_cast<long>(k) * ncols + c];
+      bfmdct::dct2_line_cpu(p.plan[0]->plan, col.data(), 1, p.scratch.data());
+      const long gc = col0 + c;
+      const double l1 = p.lam[1][dim > 2 ? gc / n2 : gc];
+      const double l2 = dim > 2 ? p.lam[2][gc % n2] : p.lam[2][0];
+      for (int k = 0; k < n0; ++k) {
+        const double l = (p.lam[0][k] + l1) + l2;
+        col[k] = l == 0.0 ? 0.0 : col[k] / (l * p.scale);
+      }
+      bfmdct::dct3_line_cpu(p.plan[0]->plan, col.data(), 1, p.scratch.data());
+      for (int k = 0; k < n0; ++k) out[static_cast<long>(k) * ncols + c] = col[k];
+    }
+  })
+}
+
 int orc_integrate(int dim, const int* ext, const double* f, const double* w, double* out) {
   OGUARD({
     check_grid(dim, ext);

@@ -76,7 +76,6 @@ struct LineGeo {
   long base;
   long phi_other;
   int k[3];  // coordinate indices (k[0] global: local + p.k0_off)
-  int k0l;   // local index along axis 0 (row within a slab)
   int valid;
 };
 
@@ -109,10 +108,12 @@ __device__ __forceinline__ long phi_index(const CtPass& p, const LineGeo& g, uin
   BFM_DASSERT(j >= 0 && j < p.ax[p.a].n);
   BFM_DASSERT(p.a < 1 || (chain & 0xFFFFu) < static_cast<uint32_t>(p.ax[0].n));
   BFM_DASSERT(p.a < 2 || (chain >> 16) < static_cast<uint32_t>(p.ax[1].n));
+  // pregathered: the previous pass already stored phi(chain*, y) at every
+  // node y (its q output), so candidate j reads its own node — a coalesced
+  // line read instead of a gather along the chain
+  if (p.pregathered) return g.base + static_cast<long>(j) * p.ax[p.a].stride;
   long idx = g.phi_other + static_cast<long>(j) * p.ax[p.a].stride;
-  // pregathered (row slab of the multi-GPU path): phi already holds
-  // Q = phi(j0*, .) at the line's own row, so axis 0 is the local row
-  if (p.a >= 1) idx += static_cast<long>(p.pregathered ? g.k0l : static_cast<int>(chain & 0xFFFFu)) * p.ax[0].stride;
+  if (p.a >= 1) idx += static_cast<long>(chain & 0xFFFFu) * p.ax[0].stride;
   if (p.a >= 2) idx += static_cast<long>(chain >> 16) * p.ax[1].stride;
   return idx;
 }
@@ -235,7 +236,6 @@ __global__ void __launch_bounds__(1024) ct_pass_kernel(CtPass p) {
         if (b > p.a) g.phi_other += static_cast<long>(c) * p.ax[b].stride;
       }
     }
-    g.k0l = g.k[0];
     g.k[0] += p.k0_off;
     *s.geo = g;
     for (int q = 0; q < 8; ++q) s.scal[q] = 0ull;
@@ -803,16 +803,16 @@ __global__ void __launch_bounds__(1024) ct_pass_kernel(CtPass p) {
         const long node = g.base + static_cast<long>(k) * A.stride;
         const int win = sm.hidx[k];
         uint32_t packed;
+        uint32_t ch = 0u;
         if (p.a == 0) {
           packed = static_cast<uint32_t>(win);
-          // multi-GPU column slab: also hand phi(j0*, column) to the row owner
-          if (p.q_out) p.q_out[node] = p.phi[g.phi_other + static_cast<long>(win) * A.stride];
         } else {
-          const uint32_t ch =
-              DY ? p.state_in[g.base + static_cast<long>(win) * A.stride] : sm.chain[win];
+          ch = DY ? p.state_in[g.base + static_cast<long>(win) * A.stride] : sm.chain[win];
           packed = ch | (static_cast<uint32_t>(win) << 16);
         }
         p.state_out[node] = packed;
+        // phi at the winner's full chain, for the next pass (or the row owner)
+        if (p.q_out) p.q_out[node] = p.phi[phi_index(p, g, ch, win)];
       }
   }
 }
@@ -831,6 +831,8 @@ CtPlan::~CtPlan() {
       if (!shared) cudaFree(tables_[a]);
     }
   for (auto* p : state_)
+    if (p) cudaFree(p);
+  for (auto* p : qbuf_)
     if (p) cudaFree(p);
   if (slow_) cudaFree(slow_);
   if (stats_) cudaFree(stats_);
@@ -916,7 +918,11 @@ void CtPlan::setup(const GridDesc& loc, const GridDesc& global, int pb, int pe, 
   for (int a = 0; a < global.d; ++a) dyadic_ = dyadic_ && is_dyadic(global.n[a]);
   if (loc.d > 1 && pe - pb > 1) {
     BFM_CUDA(cudaMalloc(&state_[0], loc.size * sizeof(uint32_t)));
-    if (pe - pb > 2) BFM_CUDA(cudaMalloc(&state_[1], loc.size * sizeof(uint32_t)));
+    BFM_CUDA(cudaMalloc(&qbuf_[0], loc.size * sizeof(double)));
+    if (pe - pb > 2) {
+      BFM_CUDA(cudaMalloc(&state_[1], loc.size * sizeof(uint32_t)));
+      BFM_CUDA(cudaMalloc(&qbuf_[1], loc.size * sizeof(double)));
+    }
   }
   BFM_CUDA(cudaMalloc(&slow_, sizeof(unsigned long long)));
   BFM_CUDA(cudaMemset(slow_, 0, sizeof(unsigned long long)));
@@ -1005,20 +1011,26 @@ void CtPlan::run_rows(const uint32_t* d_chain0, const double* d_q, double* d_out
                       cudaStream_t stream, LaunchCounter* lc) {
   for (int a = 1; a < g_.d; ++a) {
     CtPass P = pass_[a];
-    P.phi = d_q;
+    P.phi = a == 1 ? d_q : qbuf_[0];
+    P.pregathered = 1;
     P.state_in = a == 1 ? d_chain0 : state_[0];
     P.state_out = P.last ? nullptr : state_[0];
+    P.q_out = P.last ? nullptr : qbuf_[0];
     P.out = d_out;
     launch(P, stream, lc);
   }
 }
 
+// Pass a >= 1 reads phi(chain*, y) at its own nodes from the previous pass's
+// q output (written next to the argmin chain) instead of gathering phi.
 void CtPlan::run(const double* d_phi, double* d_out, cudaStream_t stream, LaunchCounter* lc) {
   for (int a = 0; a < g_.d; ++a) {
     CtPass P = pass_[a];
-    P.phi = d_phi;
+    P.phi = a == 0 ? d_phi : qbuf_[(a - 1) & 1];
+    P.pregathered = a > 0 ? 1 : 0;
     P.state_in = a > 0 ? state_[(a - 1) & 1] : nullptr;
     P.state_out = P.last ? nullptr : state_[a & 1];
+    P.q_out = P.last ? nullptr : qbuf_[a & 1];
     P.out = d_out;
     launch(P, stream, lc);
   }

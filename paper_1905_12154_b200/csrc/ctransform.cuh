@@ -28,11 +28,12 @@ struct CtPass {
   const uint32_t* state_in;  // argmin chain of previous passes (a > 0)
   uint32_t* state_out;       // non-last passes
   double* out;               // last pass
-  // multi-GPU slabs (0 / null on a whole grid): global row of local row 0;
-  // phi holds Q = phi(j0*, .) per node (row-slab passes); pass-0 output of Q
+  // global row of local row 0 (multi-GPU row slab), else 0
   int k0_off;
+  // phi holds phi(chain*, y) at every node y (the previous pass's q_out):
+  // candidates read their own node instead of gathering along the chain
   int pregathered;
-  double* q_out;
+  double* q_out;  // non-last passes: phi at the winner's chain, per node
   // shared-memory carve-up (bytes, per line)
   int off_fv, off_chain, off_hidx, off_H, off_flag, off_list, off_lohi, off_scal, line_bytes;
   // statistics (device counters, may be null): lines that needed exact resolution
@@ -76,6 +77,7 @@ class CtPlan {
   CtAxis ax_[3] = {};
   double4* tables_[3] = {nullptr, nullptr, nullptr};
   uint32_t* state_[2] = {nullptr, nullptr};
+  double* qbuf_[2] = {nullptr, nullptr};  // phi at the argmin chain, per node (pass outputs)
   unsigned long long* slow_ = nullptr;
   unsigned long long* stats_ = nullptr;
   CtPass pass_[3] = {};

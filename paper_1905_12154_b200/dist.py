@@ -99,17 +99,22 @@ class TorchComm:
         self.rank = dist.get_rank(group)
         self.size = dist.get_world_size(group)
 
-    def alltoallv(self, sends: List[torch.Tensor]) -> List[torch.Tensor]:
+    def alltoallv(self, sends: List[torch.Tensor],
+                  recv_counts: Optional[List[int]] = None) -> List[torch.Tensor]:
+        """sends[q] goes to rank q; returns what every rank sent here. The
+        receive sizes are exchanged first unless the caller knows them."""
         dist = self.dist
         ref = sends[0]
-        counts = torch.tensor([int(s.numel()) for s in sends], dtype=torch.int64, device=ref.device)
-        rcounts = torch.empty_like(counts)
-        dist.all_to_all_single(rcounts, counts, group=self.group)
-        rc = [int(c) for c in rcounts.tolist()]
-        out = torch.empty(sum(rc), dtype=ref.dtype, device=ref.device)
-        dist.all_to_all_single(out, torch.cat([s.reshape(-1) for s in sends]), rc,
-                               [int(c) for c in counts.tolist()], group=self.group)
-        return list(torch.split(out, rc))
+        sc = [int(x.numel()) for x in sends]
+        if recv_counts is None:
+            counts = torch.tensor(sc, dtype=torch.int64, device=ref.device)
+            rcounts = torch.empty_like(counts)
+            dist.all_to_all_single(rcounts, counts, group=self.group)
+            recv_counts = [int(c) for c in rcounts.tolist()]
+        out = torch.empty(sum(recv_counts), dtype=ref.dtype, device=ref.device)
+        dist.all_to_all_single(out, torch.cat([x.reshape(-1) for x in sends]), recv_counts, sc,
+                               group=self.group)
+        return list(torch.split(out, recv_counts))
 
     def allgather(self, values: Sequence[float]) -> np.ndarray:
         dist = self.dist
@@ -150,7 +155,8 @@ class LocalComm:
         self.sh.barrier.wait()
         return got
 
-    def alltoallv(self, sends: List[torch.Tensor]) -> List[torch.Tensor]:
+    def alltoallv(self, sends: List[torch.Tensor],
+                  recv_counts: Optional[List[int]] = None) -> List[torch.Tensor]:
         boxes = self._exchange([s.reshape(-1).clone() for s in sends])
         return [boxes[r][self.rank] for r in range(self.size)]
 
@@ -316,8 +322,8 @@ class SlabExchange:
         nr = L.nrows[r]
         x = x_rows.reshape(nr, L.M)
         sends = [x[:, L.col0[q]:L.col0[q] + L.ncols[q]].contiguous() for q in range(L.P)]
-        recv = self.comm.alltoallv(sends)
         nc = L.ncols[r]
+        recv = self.comm.alltoallv(sends, [L.nrows[q] * nc for q in range(L.P)])
         return torch.cat([recv[q].reshape(L.nrows[q], nc) for q in range(L.P)], 0).reshape(-1)
 
     def cols_to_rows(self, x_cols: torch.Tensor) -> torch.Tensor:
@@ -325,8 +331,8 @@ class SlabExchange:
         nc = L.ncols[r]
         x = x_cols.reshape(L.n0, nc)
         sends = [x[L.row0[q]:L.row0[q] + L.nrows[q], :].contiguous() for q in range(L.P)]
-        recv = self.comm.alltoallv(sends)
         nr = L.nrows[r]
+        recv = self.comm.alltoallv(sends, [nr * L.ncols[q] for q in range(L.P)])
         return torch.cat([recv[q].reshape(nr, L.ncols[q]) for q in range(L.P)], 1).reshape(-1)
 
     def halo(self, u_rows: torch.Tensor) -> torch.Tensor:
@@ -341,42 +347,53 @@ class SlabExchange:
             sends[r - 1] = u[0].contiguous()
         if r < L.P - 1:
             sends[r + 1] = u[nr - 1].contiguous()
-        recv = self.comm.alltoallv(sends)
+        recv = self.comm.alltoallv(sends, [L.M if abs(q - r) == 1 else 0 for q in range(L.P)])
         top = recv[r - 1] if r > 0 else torch.zeros(L.M, dtype=u.dtype, device=u.device)
         bot = recv[r + 1] if r < L.P - 1 else torch.zeros(L.M, dtype=u.dtype, device=u.device)
         return torch.cat([top.reshape(1, -1), u, bot.reshape(1, -1)], 0).reshape(-1)
 
-    def route_records(self, key, w, cmask, mass, num_cells_of):
+    def route_records(self, key, w, cmask, mass, num_cells_of=None):
         """Sends each deposit record to the owners of the target rows it
         reaches; returns this rank's records in global source order with keys
-        relative to its cells (global cell - (row0 - 1) * M)."""
+        relative to its cells (global cell - (row0 - 1) * M). Records travel
+        packed as (3 + d) float64 words: key bits, mass, d weights, mask."""
         L, r = self.L, self.rank
         d = L.d
         nloc = mass.numel()
+        dev = mass.device
         key64 = key.to(torch.int64) & 0xFFFFFFFF
         valid = key64 != L.N
-        i0 = torch.div(key64, L.M, rounding_mode="floor")
-        i0 = torch.where(valid, i0, torch.zeros_like(i0))
+        i0 = torch.where(valid, torch.div(key64, L.M, rounding_mode="floor"), torch.zeros_like(key64))
         own_lo = L.row_owner(i0)
         up_ok = valid & ((cmask.to(torch.int64) & 1) == 0) & (i0 + 1 < L.n0)
         own_hi = L.row_owner(torch.clamp(i0 + 1, max=L.n0 - 1))
+        second = up_ok & (own_hi != own_lo)  # then own_hi == own_lo + 1 (no empty ranks)
+        # copy slots 2s (owner of row i0) and 2s+1 (owner of row i0+1 when it
+        # differs), destination P = none; a stable sort by destination keeps
+        # every destination's records in source order
+        slot_dst = torch.stack([torch.where(valid, own_lo, torch.full_like(own_lo, L.P)),
+                                torch.where(second, own_hi, torch.full_like(own_hi, L.P))], 1)
+        slot_dst = slot_dst.reshape(-1).to(torch.int16)
+        sorted_dst, order = torch.sort(slot_dst, stable=True)
+        bounds = torch.searchsorted(sorted_dst, torch.arange(L.P + 1, device=dev, dtype=torch.int16))
+        counts = bounds[1:] - bounds[:-1]
+        total = int(bounds[L.P].item())
+        sid = torch.div(order[:total], 2, rounding_mode="floor")
+        dst = sorted_dst[:total].to(torch.int64)
+        row0s = torch.tensor(L.row0, dtype=torch.int64, device=dev)
+        rel = key64[sid] - (row0s[dst] - 1) * L.M
         wv = w.reshape(d, nloc)
-        fields = []
-        for q in range(L.P):
-            sel = (valid & (own_lo == q)) | (up_ok & (own_hi == q))
-            idx = torch.nonzero(sel, as_tuple=False).reshape(-1)  # ascending: source order kept
-            k = key64[idx] - (L.row0[q] - 1) * L.M
-            fields.append((k.to(torch.int64), mass[idx], wv[:, idx].reshape(-1),
-                           cmask[idx].to(torch.int64)))
-        ks = self.comm.alltoallv([f[0] for f in fields])
-        ms = self.comm.alltoallv([f[1] for f in fields])
-        ws = self.comm.alltoallv([f[2] for f in fields])
-        cs = self.comm.alltoallv([f[3] for f in fields])
-        keys = torch.cat(ks).to(torch.int32)
-        masses = torch.cat(ms)
-        counts = [int(m.numel()) for m in ms]
-        wcat = torch.cat([ws[q].reshape(d, counts[q]) for q in range(L.P)], 1).reshape(-1)
-        cmasks = torch.cat(cs).to(torch.uint8)
+        rec = torch.empty((sid.numel(), 3 + d), dtype=torch.float64, device=dev)
+        rec[:, 0] = rel.view(torch.float64) if rel.numel() else rec[:, 0]
+        rec[:, 1] = mass[sid]
+        rec[:, 2:2 + d] = wv[:, sid].t()
+        rec[:, 2 + d] = cmask[sid].to(torch.float64)
+        sends = list(torch.split(rec.reshape(-1), [int(c) * (3 + d) for c in counts.tolist()]))
+        got = torch.cat(self.comm.alltoallv(sends)).reshape(-1, 3 + d)
+        keys = got[:, 0].contiguous().view(torch.int64).to(torch.int32)
+        masses = got[:, 1].contiguous()
+        wcat = got[:, 2:2 + d].t().contiguous().reshape(-1)
+        cmasks = got[:, 2 + d].to(torch.uint8)
         return keys, masses, wcat, cmasks
 
     def allgather(self, values) -> np.ndarray:
