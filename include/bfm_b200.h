@@ -202,6 +202,17 @@ int bfm_slab_poisson_rows_inverse(bfm_slab* s, double* d_inout, void* stream);
 int bfm_slab_pf_map(bfm_slab* s, const double* d_u_halo, const double* d_source, uint32_t* d_key,
                     double* d_w, uint8_t* d_cmask, double* d_disp, void* stream);
 long bfm_slab_pf_num_cells(const bfm_slab* s);
+/* Routing of the map's records to the owners of the target rows they reach
+ * (row_starts[0..nranks] partitions axis 0): packed (3 + d doubles per
+ * record: key relative to the destination's cells as raw bits, mass, d
+ * weights, clamp mask; capacity 2 * nrows*M records) grouped by destination
+ * rank, each group in source order; counts[q] records for rank q. Unpack
+ * turns the received concatenation into bfm_slab_pf_gather's inputs. */
+int bfm_slab_set_partition(bfm_slab* s, int nranks, const int* row_starts);
+int bfm_slab_pf_route(bfm_slab* s, const uint32_t* d_key, const double* d_w, const uint8_t* d_cmask,
+                      const double* d_mass, double* d_packed, long* counts, void* stream);
+int bfm_slab_pf_unpack(bfm_slab* s, long nrec, const double* d_packed, uint32_t* d_keys,
+                       double* d_mass, double* d_w, uint8_t* d_cmask, void* stream);
 int bfm_slab_pf_gather(bfm_slab* s, long nrec, const uint32_t* d_keys, const double* d_mass,
                        const double* d_w, const uint8_t* d_cmask, const double* d_target,
                        double* d_out, void* stream);

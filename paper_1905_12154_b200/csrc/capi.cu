@@ -786,6 +786,32 @@ int bfm_slab_pf_map(bfm_slab* s, const double* d_u_halo, const double* d_source,
 
 long bfm_slab_pf_num_cells(const bfm_slab* s) { return s ? s->pf.num_cells() : -1; }
 
+int bfm_slab_set_partition(bfm_slab* s, int nranks, const int* row_starts) {
+  return slab_op(s, [&] {
+    if (nranks < 1 || !row_starts || row_starts[0] != 0 || row_starts[nranks] != s->g.n[0])
+      fail(BFM_ERR_INVALID_ARGUMENT, "slab: bad partition");
+    for (int q = 0; q < nranks; ++q)
+      if (row_starts[q + 1] <= row_starts[q]) fail(BFM_ERR_INVALID_ARGUMENT, "slab: empty rank");
+    s->pf.set_partition(nranks, row_starts);
+  });
+}
+
+int bfm_slab_pf_route(bfm_slab* s, const uint32_t* d_key, const double* d_w, const uint8_t* d_cmask,
+                      const double* d_mass, double* d_packed, long* counts, void* stream) {
+  return slab_op(s, [&] {
+    s->pf.route(d_key, d_w, d_cmask, d_mass, d_packed, counts, static_cast<cudaStream_t>(stream),
+                &s->lc);
+  });
+}
+
+int bfm_slab_pf_unpack(bfm_slab* s, long nrec, const double* d_packed, uint32_t* d_keys,
+                       double* d_mass, double* d_w, uint8_t* d_cmask, void* stream) {
+  return slab_op(s, [&] {
+    s->pf.unpack(d_packed, nrec, d_keys, d_mass, d_w, d_cmask, static_cast<cudaStream_t>(stream),
+                 &s->lc);
+  });
+}
+
 int bfm_slab_pf_gather(bfm_slab* s, long nrec, const uint32_t* d_keys, const double* d_mass,
                        const double* d_w, const uint8_t* d_cmask, const double* d_target,
                        double* d_out, void* stream) {

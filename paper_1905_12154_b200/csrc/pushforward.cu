@@ -413,13 +413,178 @@ unsigned grid_for(long n, int threads) {
   return static_cast<unsigned>(b);
 }
 
+// ---- multi-GPU deposit-record routing (dist.py route_records) --------------
+// Every source with mass becomes a record for the owner of its lo-corner row
+// i0 and, unless clamped on axis 0, for the owner of row i0 + 1 when that is
+// another rank. Records are packed (3 + d doubles: key relative to the
+// destination's cells as raw bits, mass, d weights, clamp mask) grouped by
+// destination and, within a destination, in source order (stable block
+// ranks; same scheme as the radix scatter).
+constexpr int kRouteThreads = 256;
+constexpr int kRouteItems = 8;
+constexpr int kRouteTile = kRouteThreads * kRouteItems;
+constexpr int kMaxRanks = 64;
+
+struct RouteArgs {
+  const uint32_t* key;
+  const uint8_t* cmask;
+  const double* w;
+  const double* mass;
+  long nloc;
+  long N;       // global sentinel
+  long M;       // nodes per row
+  int n0;
+  int d;
+  int P;
+  const int* row0;  // [P + 1] row starts (row0[P] = n0)
+  int* bcount;      // [P * nblocks] per-destination counts (dest-major)
+  double* packed;
+};
+
+__device__ __forceinline__ int route_owner(const RouteArgs& A, long row) {
+  int lo = 0, hi = A.P - 1;  // largest q with row0[q] <= row
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (A.row0[mid] <= row) lo = mid;
+    else hi = mid - 1;
+  }
+  return lo;
+}
+
+__device__ __forceinline__ void route_dests(const RouteArgs& A, long s, int& d1, int& d2) {
+  d1 = d2 = -1;
+  if (s >= A.nloc) return;
+  const long k = A.key[s];
+  if (k == A.N) return;
+  const long i0 = k / A.M;
+  d1 = route_owner(A, i0);
+  if (!(A.cmask[s] & 1u) && i0 + 1 < A.n0) {
+    const int q = route_owner(A, i0 + 1);
+    if (q != d1) d2 = q;
+  }
+}
+
+__global__ void __launch_bounds__(kRouteThreads) route_count_kernel(RouteArgs A, long nblocks) {
+  __shared__ int cnt[kMaxRanks];
+  for (int q = threadIdx.x; q < A.P; q += blockDim.x) cnt[q] = 0;
+  __syncthreads();
+  const long base = static_cast<long>(blockIdx.x) * kRouteTile;
+  for (int r = 0; r < kRouteItems; ++r) {
+    int d1, d2;
+    route_dests(A, base + static_cast<long>(r) * kRouteThreads + threadIdx.x, d1, d2);
+    if (d1 >= 0) atomicAdd(&cnt[d1], 1);
+    if (d2 >= 0) atomicAdd(&cnt[d2], 1);
+  }
+  __syncthreads();
+  for (int q = threadIdx.x; q < A.P; q += blockDim.x) A.bcount[static_cast<long>(q) * nblocks + blockIdx.x] = cnt[q];
+}
+
+// exclusive scan of m ints in place, one CTA (m = P * nblocks, small)
+__global__ void __launch_bounds__(1024) route_scan_kernel(int* a, long m, int* total) {
+  __shared__ int wsum[32];
+  __shared__ int carry;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (long b0 = 0; b0 < m; b0 += 1024) {
+    const long i = b0 + threadIdx.x;
+    const int v = i < m ? a[i] : 0;
+    int incl = v;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int u = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += u;
+    }
+    if (lane == 31) wsum[w] = incl;
+    __syncthreads();
+    if (w == 0) {
+      int t = wsum[lane];
+      int ti = t;
+      for (int o = 1; o < 32; o <<= 1) {
+        const int u = __shfl_up_sync(0xffffffffu, ti, o);
+        if (lane >= o) ti += u;
+      }
+      wsum[lane] = ti - t;
+    }
+    __syncthreads();
+    if (i < m) a[i] = carry + wsum[w] + incl - v;
+    __syncthreads();
+    if (threadIdx.x == 1023) carry += wsum[31] + incl;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *total = carry;
+}
+
+__global__ void __launch_bounds__(kRouteThreads) route_scatter_kernel(RouteArgs A, long nblocks) {
+  constexpr int kW = kRouteThreads / 32;
+  __shared__ int base[kMaxRanks];
+  __shared__ int wcnt[kW][kMaxRanks];
+  for (int q = threadIdx.x; q < A.P; q += blockDim.x)
+    base[q] = A.bcount[static_cast<long>(q) * nblocks + blockIdx.x];
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const unsigned lt = (1u << lane) - 1u;
+  const int rec = 3 + A.d;
+  const long b0 = static_cast<long>(blockIdx.x) * kRouteTile;
+  for (int r = 0; r < kRouteItems; ++r) {
+    const long s = b0 + static_cast<long>(r) * kRouteThreads + threadIdx.x;
+    int d1, d2;
+    route_dests(A, s, d1, d2);
+    int pos1 = 0, pos2 = 0;
+    for (int q = 0; q < A.P; ++q) {
+      const unsigned m = __ballot_sync(0xffffffffu, d1 == q || d2 == q);
+      if (lane == 0) wcnt[warp][q] = __popc(m);
+      if (d1 == q) pos1 = __popc(m & lt);
+      if (d2 == q) pos2 = __popc(m & lt);
+    }
+    __syncthreads();
+    if (d1 >= 0 || d2 >= 0) {
+      for (int h = 0; h < 2; ++h) {
+        const int q = h == 0 ? d1 : d2;
+        if (q < 0) continue;
+        int pre = 0;
+        for (int ww = 0; ww < warp; ++ww) pre += wcnt[ww][q];
+        const long pos = static_cast<long>(base[q]) + pre + (h == 0 ? pos1 : pos2);
+        double* out = A.packed + pos * rec;
+        const long rel = static_cast<long>(A.key[s]) - (static_cast<long>(A.row0[q]) - 1) * A.M;
+        out[0] = __longlong_as_double(rel);
+        out[1] = A.mass[s];
+        for (int a = 0; a < A.d; ++a) out[2 + a] = A.w[a * A.nloc + s];
+        out[2 + A.d] = static_cast<double>(A.cmask[s]);
+      }
+    }
+    __syncthreads();
+    for (int q = threadIdx.x; q < A.P; q += blockDim.x) {
+      int tot = 0;
+      for (int ww = 0; ww < kW; ++ww) tot += wcnt[ww][q];
+      base[q] += tot;
+    }
+    __syncthreads();
+  }
+}
+
+// packed records (received, in sender order) -> the gather's SoA inputs
+__global__ void route_unpack_kernel(const double* packed, long nrec, int d, uint32_t* keys,
+                                    double* mass, double* w, uint8_t* cmask) {
+  const int rec = 3 + d;
+  for (long i = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; i < nrec;
+       i += static_cast<long>(gridDim.x) * blockDim.x) {
+    const double* in = packed + i * rec;
+    keys[i] = static_cast<uint32_t>(__double_as_longlong(in[0]));
+    mass[i] = in[1];
+    for (int a = 0; a < d; ++a) w[a * nrec + i] = in[2 + a];
+    cmask[i] = static_cast<uint8_t>(in[2 + d]);
+  }
+}
+
 }  // namespace
 
 PushforwardPlan::~PushforwardPlan() {
   for (void* p : {static_cast<void*>(key_), static_cast<void*>(cmask_), static_cast<void*>(w_),
                   static_cast<void*>(off_), static_cast<void*>(end_), static_cast<void*>(heavy_),
-                  static_cast<void*>(nheavy_), static_cast<void*>(hbuf_)})
+                  static_cast<void*>(nheavy_), static_cast<void*>(hbuf_),
+                  static_cast<void*>(row0_), static_cast<void*>(bcount_)})
     if (p) cudaFree(p);
+  if (hcounts_) cudaFreeHost(hcounts_);
 }
 
 void PushforwardPlan::init(const GridDesc& g) { setup(g, g, 0, false); }
@@ -547,6 +712,63 @@ void PushforwardPlan::gather(long nrec, const uint32_t* d_keys, const double* d_
   pf_gather_heavy_kernel<<<2 * 148, 512, kHeavySmem, stream>>>(G, heavy_, nheavy, hbuf_, nheavy_ + 1);
   BFM_LAUNCH_CHECK("pf_gather_heavy_kernel");
   if (lc) lc->add(nrec > 0 ? 4 : 3);
+}
+
+void PushforwardPlan::set_partition(int P, const int* row_starts) {
+  if (P < 1 || P > kMaxRanks) throw std::invalid_argument("pushforward: 1..64 ranks supported");
+  nranks_ = P;
+  if (!row0_) BFM_CUDA(cudaMalloc(&row0_, (kMaxRanks + 1) * sizeof(int)));
+  BFM_CUDA(cudaMemcpy(row0_, row_starts, (P + 1) * sizeof(int), cudaMemcpyHostToDevice));
+  const long nblocks = (g_.size + kRouteTile - 1) / kRouteTile;
+  if (bcount_) cudaFree(bcount_);
+  BFM_CUDA(cudaMalloc(&bcount_, (static_cast<long>(P) * nblocks + 1) * sizeof(int)));
+  if (!hcounts_) BFM_CUDA(cudaMallocHost(&hcounts_, (kMaxRanks + 1) * sizeof(int)));
+}
+
+void PushforwardPlan::route(const uint32_t* d_key, const double* d_w, const uint8_t* d_cmask,
+                            const double* d_mass, double* d_packed, long* counts,
+                            cudaStream_t stream, LaunchCounter* lc) {
+  if (!nranks_) throw std::invalid_argument("pushforward: route needs set_partition");
+  RouteArgs A{};
+  A.key = d_key;
+  A.cmask = d_cmask;
+  A.w = d_w;
+  A.mass = d_mass;
+  A.nloc = g_.size;
+  A.N = gg_.size;
+  A.M = g_.stride[0];
+  A.n0 = gg_.n[0];
+  A.d = g_.d;
+  A.P = nranks_;
+  A.row0 = row0_;
+  A.bcount = bcount_;
+  A.packed = d_packed;
+  const long nblocks = (g_.size + kRouteTile - 1) / kRouteTile;
+  const long m = static_cast<long>(nranks_) * nblocks;
+  route_count_kernel<<<static_cast<unsigned>(nblocks), kRouteThreads, 0, stream>>>(A, nblocks);
+  // per-destination totals (before the scan turns counts into offsets)
+  int* totals = bcount_ + m;  // one spare int
+  route_scan_kernel<<<1, 1024, 0, stream>>>(bcount_, m, totals);
+  route_scatter_kernel<<<static_cast<unsigned>(nblocks), kRouteThreads, 0, stream>>>(A, nblocks);
+  BFM_LAUNCH_CHECK("pf route");
+  if (lc) lc->add(3);
+  // destination q's records are [offset(q, block 0), offset(q + 1, block 0))
+  std::vector<int> first(nranks_ + 1);
+  for (int q = 0; q < nranks_; ++q)
+    BFM_CUDA(cudaMemcpyAsync(hcounts_ + q, bcount_ + static_cast<long>(q) * nblocks, sizeof(int),
+                             cudaMemcpyDeviceToHost, stream));
+  BFM_CUDA(cudaMemcpyAsync(hcounts_ + nranks_, totals, sizeof(int), cudaMemcpyDeviceToHost, stream));
+  BFM_CUDA(cudaStreamSynchronize(stream));
+  for (int q = 0; q < nranks_; ++q) counts[q] = static_cast<long>(hcounts_[q + 1]) - hcounts_[q];
+}
+
+void PushforwardPlan::unpack(const double* d_packed, long nrec, uint32_t* d_keys, double* d_mass,
+                             double* d_w, uint8_t* d_cmask, cudaStream_t stream, LaunchCounter* lc) {
+  if (nrec <= 0) return;
+  route_unpack_kernel<<<grid_for(nrec, 256), 256, 0, stream>>>(d_packed, nrec, g_.d, d_keys, d_mass,
+                                                                d_w, d_cmask);
+  BFM_LAUNCH_CHECK("pf unpack");
+  if (lc) lc->add();
 }
 
 void PushforwardPlan::from_potential(const double* d_u, const double* d_source,

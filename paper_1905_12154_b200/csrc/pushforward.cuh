@@ -43,6 +43,19 @@ class PushforwardPlan {
               const uint8_t* d_cmask, const double* d_target, double* d_out, cudaStream_t stream,
               LaunchCounter* lc);
   long num_cells() const { return ncells_; }
+  // Multi-GPU routing of this slab's deposit records (map_records output) to
+  // the owners of the target rows they reach: row_starts[0..P] partition
+  // axis 0. packed receives, per destination in rank order and within it in
+  // source order, (3 + d) doubles per record: key relative to the
+  // destination's cells (raw bits), mass, d weights, clamp mask; counts[q]
+  // the number of records for rank q. Capacity: 2 * nodes records.
+  void set_partition(int P, const int* row_starts);
+  void route(const uint32_t* d_key, const double* d_w, const uint8_t* d_cmask,
+             const double* d_mass, double* d_packed, long* counts, cudaStream_t stream,
+             LaunchCounter* lc);
+  // received packed records -> gather inputs (keys, mass, w SoA, mask)
+  void unpack(const double* d_packed, long nrec, uint32_t* d_keys, double* d_mass, double* d_w,
+              uint8_t* d_cmask, cudaStream_t stream, LaunchCounter* lc);
 
  private:
   void setup(const GridDesc& loc, const GridDesc& global, int row0, bool slab);
@@ -53,6 +66,10 @@ class PushforwardPlan {
   long cell_shift_ = 0;
   long ncells_ = 0;
   long rec_cap_ = 0;
+  int nranks_ = 0;
+  int* row0_ = nullptr;      // [P + 1] partition (routing)
+  int* bcount_ = nullptr;    // [P * blocks + 1] routing counts / offsets
+  int* hcounts_ = nullptr;   // pinned
   uint32_t* key_ = nullptr;  // [N] lo-corner cell of each source (N = no mass)
   uint8_t* cmask_ = nullptr; // [N] axes on which the source is clamped (lo == hi)
   double* w_ = nullptr;      // [d*N] upper-node weight per axis

@@ -196,12 +196,20 @@ class CudaSlabOps:
         lib.bfm_slab_axpy.argtypes = [P, P, C.c_double, P, P]
         lib.bfm_slab_axpy.restype = C.c_int
         lib.bfm_slab_last_launches.argtypes = [P]
+        lib.bfm_slab_set_partition.argtypes = [P, C.c_int, P]
+        lib.bfm_slab_set_partition.restype = C.c_int
+        lib.bfm_slab_pf_route.argtypes = [P] * 8
+        lib.bfm_slab_pf_route.restype = C.c_int
+        lib.bfm_slab_pf_unpack.argtypes = [P, C.c_long] + [P] * 6
+        lib.bfm_slab_pf_unpack.restype = C.c_int
         r0, nr = layout.rows(rank)
         c0, nc = layout.cols(rank)
         h = C.c_void_p()
         _check(lib, lib.bfm_slab_create(layout.d, _extents(layout.shape), r0, nr, c0, nc, C.byref(h)))
         self.h = h
         self.launches = 0
+        starts = (C.c_int * (layout.P + 1))(*(layout.row0 + [layout.n0]))
+        _check(lib, lib.bfm_slab_set_partition(h, layout.P, starts))
 
     def close(self):
         if self.h:
@@ -269,6 +277,25 @@ class CudaSlabOps:
 
     def pf_num_cells(self) -> int:
         return int(self.lib.bfm_slab_pf_num_cells(self.h))
+
+    def pf_route(self, key, w, cmask, mass):
+        """Packed records per destination rank (see SlabExchange.route_records)."""
+        d = self.L.d
+        packed = self.empty(2 * mass.numel() * (3 + d))
+        counts = (C.c_long * self.L.P)()
+        self._run(self.lib.bfm_slab_pf_route(self.h, self._p(key), self._p(w), self._p(cmask),
+                                             self._p(mass), self._p(packed), counts, self._s()))
+        return packed, [int(c) for c in counts]
+
+    def pf_unpack(self, packed, nrec: int):
+        d = self.L.d
+        keys = self.empty(nrec, torch.int32)
+        mass = self.empty(nrec)
+        w = self.empty(d * nrec)
+        cmask = self.empty(nrec, torch.uint8)
+        self._run(self.lib.bfm_slab_pf_unpack(self.h, int(nrec), self._p(packed), self._p(keys),
+                                              self._p(mass), self._p(w), self._p(cmask), self._s()))
+        return keys, mass, w, cmask
 
     def pf_gather(self, keys, mass, w, cmask, target) -> torch.Tensor:
         nloc = self.L.nrows[self.rank] * self.L.M
@@ -352,12 +379,20 @@ class SlabExchange:
         bot = recv[r + 1] if r < L.P - 1 else torch.zeros(L.M, dtype=u.dtype, device=u.device)
         return torch.cat([top.reshape(1, -1), u, bot.reshape(1, -1)], 0).reshape(-1)
 
-    def route_records(self, key, w, cmask, mass, num_cells_of=None):
+    def route_records(self, key, w, cmask, mass, ops=None):
         """Sends each deposit record to the owners of the target rows it
         reaches; returns this rank's records in global source order with keys
         relative to its cells (global cell - (row0 - 1) * M). Records travel
-        packed as (3 + d) float64 words: key bits, mass, d weights, mask."""
+        packed as (3 + d) float64 words: key bits, mass, d weights, mask.
+        With CudaSlabOps the packing and unpacking are the bfm_slab_pf_route /
+        _unpack kernels; otherwise (CPU test operators) torch ops."""
         L, r = self.L, self.rank
+        if ops is not None and hasattr(ops, "pf_route"):
+            rec = 3 + L.d
+            packed, counts = ops.pf_route(key, w, cmask, mass)
+            sends = list(torch.split(packed[:sum(counts) * rec], [c * rec for c in counts]))
+            got = torch.cat(self.comm.alltoallv(sends))
+            return ops.pf_unpack(got, got.numel() // rec)
         d = L.d
         nloc = mass.numel()
         dev = mass.device
@@ -466,7 +501,7 @@ class DistSolver:
     def pushforward_residual(self, u_rows, source, target) -> torch.Tensor:
         uh = self.x.halo(u_rows)
         key, w, cmask, _ = self.ops.pf_map(uh, source)
-        keys, masses, ws, cms = self.x.route_records(key, w, cmask, source, None)
+        keys, masses, ws, cms = self.x.route_records(key, w, cmask, source, self.ops)
         return self.ops.pf_gather(keys, masses, ws, cms, target)
 
     def _dot(self, a1, b1, a2=None, b2=None) -> float:

@@ -59,8 +59,8 @@ t("halo", lambda: x.halo(s.psi))
 uh = x.halo(s.psi)
 t("pf_map", lambda: ops.pf_map(uh, s.mu))
 key, w, cm, _ = ops.pf_map(uh, s.mu)
-t("route_records", lambda: x.route_records(key, w, cm, s.mu))
-recs = x.route_records(key, w, cm, s.mu)
+t("route_records", lambda: x.route_records(key, w, cm, s.mu, ops))
+recs = x.route_records(key, w, cm, s.mu, ops)
 t("pf_gather", lambda: ops.pf_gather(*recs, s.nu))
 
 t("pushforward total", lambda: s.pushforward_residual(s.psi, s.mu, s.nu))

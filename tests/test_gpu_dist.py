@@ -93,7 +93,7 @@ def test_dist_pushforward_residual_bitwise(shape, P):
             x = D.SlabExchange(L, comm)
             src = _rows(L, r, mu)
             key, w, cm, _ = ops.pf_map(x.halo(_rows(L, r, u)), src)
-            recs = x.route_records(key, w, cm, src, None)
+            recs = x.route_records(key, w, cm, src, ops)
             return ops.pf_gather(*recs, _rows(L, r, target)).cpu().numpy()
 
         got = _assemble(L, D.spmd_local(L, fn))
