@@ -608,8 +608,8 @@ __global__ void __launch_bounds__(1024) ct_pass_kernel(CtPass p) {
         if (p.stats) {
           atomicAdd(p.stats + 0, 1ull);
           if (!lone) atomicAdd(p.stats + 1, 1ull);
-      }
-      res[k] = lone ? static_cast<uint16_t>(HH(i)) : static_cast<uint16_t>(i | 0x8000);
+        }
+        res[k] = lone ? static_cast<uint16_t>(HH(i)) : static_cast<uint16_t>(i | 0x8000);
       }
       // flagged queries are appended to the line's list (warp-aggregated)
       const unsigned fm = __ballot_sync(0xffffffffu, in && !lone);
