@@ -1,4 +1,5 @@
-// Stable LSD radix sort (8-bit digits) of (key, value) pairs.
+// Stable LSD radix sort (9-bit digits: three passes cover the 25-27-bit cell
+// keys of the pushforward) of (key, value) pairs.
 //
 // Per pass: (1) per-tile digit histograms (digit-major), (2) exclusive scan
 // of the histograms, (3) stable scatter: each tile walks its elements in
@@ -13,20 +14,22 @@ namespace {
 
 constexpr int kThreads = 256;
 constexpr int kItems = 16;
+constexpr int kBits = 9;
+constexpr int kBins = 1 << kBits;
 constexpr int kTile = kThreads * kItems;
 constexpr int kWarps = kThreads / 32;
 
 __global__ void __launch_bounds__(kThreads) rs_hist_kernel(const uint32_t* keys, long n, int shift,
                                                          long nblocks, int* hist) {
-  __shared__ int h[256];
-  h[threadIdx.x] = 0;
+  __shared__ int h[kBins];
+  for (int q = threadIdx.x; q < kBins; q += kThreads) h[q] = 0;
   __syncthreads();
   const long base = static_cast<long>(blockIdx.x) * kTile;
   const unsigned lane = threadIdx.x & 31u;
   for (int r = 0; r < kItems; ++r) {
     const long i = base + static_cast<long>(r) * kThreads + threadIdx.x;
     const bool ok = i < n;
-    const unsigned d = ok ? (keys[i] >> shift) & 255u : 256u;
+    const unsigned d = ok ? (keys[i] >> shift) & (kBins - 1u) : static_cast<unsigned>(kBins);
     const unsigned act = __ballot_sync(0xffffffffu, ok);
     if (ok) {
       const unsigned m = __match_any_sync(act, d);
@@ -34,7 +37,7 @@ __global__ void __launch_bounds__(kThreads) rs_hist_kernel(const uint32_t* keys,
     }
   }
   __syncthreads();
-  hist[static_cast<long>(threadIdx.x) * nblocks + blockIdx.x] = h[threadIdx.x];
+  for (int q = threadIdx.x; q < kBins; q += kThreads) hist[static_cast<long>(q) * nblocks + blockIdx.x] = h[q];
 }
 
 __device__ int block_exscan(int v, int* total) {
@@ -108,12 +111,14 @@ __global__ void __launch_bounds__(kThreads) rs_scatter_kernel(const uint32_t* ki
                                                             long n, int shift, long nblocks,
                                                             const int* hist, uint32_t* kout,
                                                             int* vout) {
-  __shared__ int gbase[256];
-  __shared__ int run[256];
-  __shared__ int wcnt[kWarps][256];
-  gbase[threadIdx.x] = hist[static_cast<long>(threadIdx.x) * nblocks + blockIdx.x];
-  run[threadIdx.x] = 0;
-  for (int w = 0; w < kWarps; ++w) wcnt[w][threadIdx.x] = 0;
+  __shared__ int gbase[kBins];
+  __shared__ int run[kBins];
+  __shared__ int wcnt[kWarps][kBins];
+  for (int q = threadIdx.x; q < kBins; q += kThreads) {
+    gbase[q] = hist[static_cast<long>(q) * nblocks + blockIdx.x];
+    run[q] = 0;
+    for (int w = 0; w < kWarps; ++w) wcnt[w][q] = 0;
+  }
   __syncthreads();
   const long base = static_cast<long>(blockIdx.x) * kTile;
   const unsigned lane = threadIdx.x & 31u;
@@ -124,12 +129,12 @@ __global__ void __launch_bounds__(kThreads) rs_scatter_kernel(const uint32_t* ki
     const bool ok = i < n;
     uint32_t k = 0;
     int v = 0;
-    unsigned d = 256u, m = 0u;
+    unsigned d = kBins, m = 0u;
     const unsigned act = __ballot_sync(0xffffffffu, ok);
     if (ok) {
       k = kin[i];
       v = vin ? vin[i] : static_cast<int>(i);
-      d = (k >> shift) & 255u;
+      d = (k >> shift) & (kBins - 1u);
       m = __match_any_sync(act, d);
       if ((__ffs(m) - 1) == static_cast<int>(lane)) wcnt[warp][d] = __popc(m);
     }
@@ -178,7 +183,7 @@ void RadixSorter::init(long n) {
     BFM_CUDA(cudaMalloc(&kbuf_[i], (n + 1) * sizeof(uint32_t)));
     BFM_CUDA(cudaMalloc(&vbuf_[i], (n + 1) * sizeof(int)));
   }
-  const long m = 256 * blocks_;
+  const long m = static_cast<long>(kBins) * blocks_;
   BFM_CUDA(cudaMalloc(&hist_, (m + 1) * sizeof(int)));
   BFM_CUDA(cudaMalloc(&bsum_, ((m + kScanTile - 1) / kScanTile + 1) * sizeof(int)));
 }
@@ -186,12 +191,12 @@ void RadixSorter::init(long n) {
 void RadixSorter::sort(const uint32_t* keys_in, const int* vals_in, long n, int bits, cudaStream_t s,
                        LaunchCounter* lc, const uint32_t** keys_out, const int** vals_out) {
   const long nb = (n + kTile - 1) / kTile;
-  const long m = 256 * nb;
+  const long m = static_cast<long>(kBins) * nb;
   const long sb = (m + kScanTile - 1) / kScanTile;
   const uint32_t* kin = keys_in;
   const int* vin = vals_in;
   int cur = 0;
-  for (int shift = 0; shift < bits; shift += 8) {
+  for (int shift = 0; shift < bits; shift += kBits) {
     rs_hist_kernel<<<static_cast<unsigned>(nb), kThreads, 0, s>>>(kin, n, shift, nb, hist_);
     rs_scan_reduce<<<static_cast<unsigned>(sb), 1024, 0, s>>>(hist_, m, bsum_);
     rs_scan_top<<<1, 1024, 0, s>>>(bsum_, sb);
