@@ -29,11 +29,15 @@ namespace bfmgpu {
 namespace {
 
 constexpr int kLight = 48;
-constexpr int kMedium = 2048;
+constexpr int kMedium = 512;   // warp-per-target tier: kLight < K <= kMedium
+constexpr int kLarge = 4096;   // CTA-per-target tier with a sequential fold: K <= kLarge
+constexpr int kLargeThreads = 128;
+constexpr int kLargeBlocks = 148 * 8;  // each CTA owns kLarge doubles of hbuf
 constexpr int kMedWarps = 8;
+constexpr int kMedStage = 512;  // ids staged in shared memory per warp (else ranked in global)
 constexpr int kHeavyIds = 24576;
-constexpr int kMedSmem = kMedWarps * kMedium * 4;
-constexpr int kMedBlocks = 148 * 3;  // each warp owns kMedium doubles of hbuf
+constexpr int kMedSmem = kMedWarps * kMedStage * 4;
+constexpr int kMedBlocks = 148 * 8;  // each warp owns kMedium doubles of hbuf
 constexpr int kHeavySmem = kHeavyIds * 4;
 
 struct MapArgs {
@@ -185,7 +189,7 @@ __device__ __forceinline__ double deposit_weight(const GatherArgs& A, int s, int
 // Light targets: merge the <= 2^d sorted neighbouring buckets by source id
 // and fold in place. Targets with more than kLight deposits are deferred to
 // pf_gather_heavy_kernel.
-__global__ void pf_gather_kernel(GatherArgs A, int* heavy, int* nheavy) {
+__global__ void pf_gather_kernel(GatherArgs A, int* heavy, int* large, int* nheavy) {
   const GridDesc& g = A.g;
   const int corners = 1 << g.d;
   for (long t = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; t < g.size;
@@ -216,6 +220,7 @@ __global__ void pf_gather_kernel(GatherArgs A, int* heavy, int* nheavy) {
     }
     if (total > kLight) {
       if (total <= kMedium) heavy[atomicAdd(nheavy, 1)] = static_cast<int>(t);
+      else if (total <= kLarge) large[atomicAdd(nheavy + 4, 1)] = static_cast<int>(t);
       else heavy[g.size - 1 - atomicAdd(nheavy + 1, 1)] = static_cast<int>(t);  // huge: from the top
       continue;
     }
@@ -283,7 +288,8 @@ __device__ __forceinline__ int lower_bound_ids(const int* v, int len, int key) {
 }
 
 // Medium targets (kLight < K <= kMedium): one warp each. The source ids of
-// the neighbouring buckets are staged in shared memory; every deposit's
+// the neighbouring buckets are staged in shared memory when they fit
+// (K <= kMedStage; else ranked against global memory); every deposit's
 // position in the source-ordered merge is its index in its own bucket plus
 // its rank (lower_bound) in each other bucket (a source lives in exactly one
 // bucket, so there are no ties). Lanes write the weights to those positions
@@ -292,10 +298,10 @@ __global__ void __launch_bounds__(kMedWarps * 32) pf_gather_medium_kernel(Gather
                                                                          const int* heavy,
                                                                          const int* nheavy,
                                                                          double* hbuf) {
-  extern __shared__ int med_ids[];  // [kMedWarps][kMedium]
+  extern __shared__ int med_ids[];  // [kMedWarps][kMedStage]
   const int nh = nheavy[0];
   const int lane = threadIdx.x & 31;
-  int* ids = med_ids + (threadIdx.x >> 5) * kMedium;
+  int* sids = med_ids + (threadIdx.x >> 5) * kMedStage;
   const long warp0 = (static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const long nwarps = (static_cast<long>(gridDim.x) * blockDim.x) >> 5;
   for (long q = warp0; q < nh; q += nwarps) {
@@ -308,17 +314,21 @@ __global__ void __launch_bounds__(kMedWarps * 32) pf_gather_medium_kernel(Gather
       cat[qq] = o;
       o += tb.end[qq] - tb.pos[qq];
     }
-    for (int qq = 0; qq < tb.nl; ++qq)
-      for (int i = lane; i < tb.end[qq] - tb.pos[qq]; i += 32) ids[cat[qq] + i] = A.bucket[tb.pos[qq] + i];
+    const bool staged = K <= kMedStage;
+    if (staged)
+      for (int qq = 0; qq < tb.nl; ++qq)
+        for (int i = lane; i < tb.end[qq] - tb.pos[qq]; i += 32) sids[cat[qq] + i] = A.bucket[tb.pos[qq] + i];
     double* buf = hbuf + warp0 * kMedium;  // the warp's private slice (K <= kMedium)
     __syncwarp();
     for (int qq = 0; qq < tb.nl; ++qq) {
       const int len = tb.end[qq] - tb.pos[qq];
       for (int i = lane; i < len; i += 32) {
-        const int src = ids[cat[qq] + i];
+        const int src = staged ? sids[cat[qq] + i] : A.bucket[tb.pos[qq] + i];
         int fin = i;
         for (int o = 0; o < tb.nl; ++o)
-          if (o != qq) fin += lower_bound_ids(ids + cat[o], tb.end[o] - tb.pos[o], src);
+          if (o != qq)
+            fin += staged ? lower_bound_ids(sids + cat[o], tb.end[o] - tb.pos[o], src)
+                          : lower_bound_ids(A.bucket + tb.pos[o], tb.end[o] - tb.pos[o], src);
         buf[fin] = (tb.bits[qq] & A.cmask[src]) ? 0.0 : deposit_weight(A, src, tb.bits[qq]);
       }
     }
@@ -331,11 +341,14 @@ __global__ void __launch_bounds__(kMedWarps * 32) pf_gather_medium_kernel(Gather
     int c = 0;
     for (; c + 32 <= K; c += 32) {
       const double v = buf[c + lane];
-      double x[32];
 #pragma unroll
-      for (int i = 0; i < 32; ++i) x[i] = __shfl_sync(0xffffffffu, v, i);
+      for (int i0 = 0; i0 < 32; i0 += 8) {
+        double x[8];
 #pragma unroll
-      for (int i = 0; i < 32; ++i) rho += x[i];
+        for (int i = 0; i < 8; ++i) x[i] = __shfl_sync(0xffffffffu, v, i0 + i);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) rho += x[i];
+      }
     }
     if (c < K) {
       const double v = c + lane < K ? buf[c + lane] : 0.0;
@@ -346,7 +359,69 @@ __global__ void __launch_bounds__(kMedWarps * 32) pf_gather_medium_kernel(Gather
   }
 }
 
-// Heavy targets (K > kMedium): one CTA each, same merge-rank scheme with the
+// Large targets (kMedium < K <= kLarge): one CTA of kLargeThreads each, ids
+// staged in shared memory, ranks and weights as above into the CTA's slice of
+// the global buffer, then one thread folds them in order (unrolled loads
+// ahead of the chain of adds).
+__global__ void __launch_bounds__(kLargeThreads) pf_gather_large_kernel(GatherArgs A,
+                                                                       const int* large,
+                                                                       const int* nheavy,
+                                                                       double* hbuf) {
+  __shared__ int s_pos[8], s_end[8], s_bits[8], s_cat[8], s_nl, s_K;
+  __shared__ int ids[kLarge];
+  const int nl_total = nheavy[4];
+  double* buf = hbuf + static_cast<long>(blockIdx.x) * kLarge;
+  for (int q = blockIdx.x; q < nl_total; q += gridDim.x) {
+    const long t = large[q];
+    if (threadIdx.x == 0) {
+      TargetBuckets tb;
+      target_buckets(A, t, tb);
+      for (int qq = 0, o = 0; qq < tb.nl; ++qq) {
+        s_pos[qq] = tb.pos[qq];
+        s_end[qq] = tb.end[qq];
+        s_bits[qq] = tb.bits[qq];
+        s_cat[qq] = o;
+        o += tb.end[qq] - tb.pos[qq];
+      }
+      s_nl = tb.nl;
+      s_K = tb.K;
+    }
+    __syncthreads();
+    const int nl = s_nl;
+    const int K = s_K;
+    for (int qq = 0; qq < nl; ++qq)
+      for (int i = threadIdx.x; i < s_end[qq] - s_pos[qq]; i += blockDim.x)
+        ids[s_cat[qq] + i] = A.bucket[s_pos[qq] + i];
+    __syncthreads();
+    for (int qq = 0; qq < nl; ++qq) {
+      const int len = s_end[qq] - s_pos[qq], b = s_bits[qq];
+      for (int i = threadIdx.x; i < len; i += blockDim.x) {
+        const int src = ids[s_cat[qq] + i];
+        int fin = i;
+        for (int o = 0; o < nl; ++o)
+          if (o != qq) fin += lower_bound_ids(ids + s_cat[o], s_end[o] - s_pos[o], src);
+        buf[fin] = (b & A.cmask[src]) ? 0.0 : deposit_weight(A, src, b);
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double rho = 0.0;  // zero weights: see the medium kernel
+      int i = 0;
+      for (; i + 8 <= K; i += 8) {
+        double x[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) x[u] = buf[i + u];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) rho += x[u];
+      }
+      for (; i < K; ++i) rho += buf[i];
+      A.out[t] = A.target ? A.target[t] - rho : rho;
+    }
+    __syncthreads();
+  }
+}
+
+// Heavy targets (K > kLarge): one CTA each, same merge-rank scheme with the
 // ids in shared memory when they fit (else ranked against global memory),
 // weights to the global buffer, then the CTA folds them (exact_fold.cuh).
 __global__ void __launch_bounds__(512) pf_gather_heavy_kernel(GatherArgs A, const int* heavy,
@@ -582,7 +657,8 @@ PushforwardPlan::~PushforwardPlan() {
   for (void* p : {static_cast<void*>(key_), static_cast<void*>(cmask_), static_cast<void*>(w_),
                   static_cast<void*>(off_), static_cast<void*>(end_), static_cast<void*>(heavy_),
                   static_cast<void*>(nheavy_), static_cast<void*>(hbuf_),
-                  static_cast<void*>(row0_), static_cast<void*>(bcount_)})
+                  static_cast<void*>(row0_), static_cast<void*>(bcount_),
+                  static_cast<void*>(large_)})
     if (p) cudaFree(p);
   if (hcounts_) cudaFreeHost(hcounts_);
 }
@@ -612,6 +688,7 @@ void PushforwardPlan::setup(const GridDesc& loc, const GridDesc& global, int row
   BFM_CUDA(cudaMalloc(&off_, (ncells_ + 1) * sizeof(int)));
   BFM_CUDA(cudaMalloc(&end_, (ncells_ + 1) * sizeof(int)));
   BFM_CUDA(cudaMalloc(&heavy_, (N + 1) * sizeof(int)));
+  BFM_CUDA(cudaMalloc(&large_, (N + 1) * sizeof(int)));
   BFM_CUDA(cudaMalloc(&nheavy_, 4 * sizeof(unsigned long long)));
   ensure_records(N);
   BFM_CUDA(cudaFuncSetAttribute(pf_gather_heavy_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -631,7 +708,9 @@ void PushforwardPlan::ensure_records(long nrec) {
   }
   const long deposits = (static_cast<long>(1) << g_.d) * cap;
   med_blocks_ = static_cast<int>(std::max<long>(1, std::min<long>(kMedBlocks, deposits / (kMedWarps * kMedium))));
-  const long hcap = std::max<long>(deposits, static_cast<long>(med_blocks_) * kMedWarps * kMedium);
+  large_blocks_ = static_cast<int>(std::max<long>(1, std::min<long>(kLargeBlocks, deposits / kLarge)));
+  const long hcap = std::max<long>(deposits, std::max<long>(static_cast<long>(med_blocks_) * kMedWarps * kMedium,
+                                                            static_cast<long>(large_blocks_) * kLarge));
   BFM_CUDA(cudaMalloc(&hbuf_, hcap * sizeof(double)));
   sorter_.init(cap);
   rec_cap_ = cap;
@@ -705,13 +784,15 @@ void PushforwardPlan::gather(long nrec, const uint32_t* d_keys, const double* d_
   G.target = d_target;
   G.out = d_out;
   int* nheavy = reinterpret_cast<int*>(nheavy_);
-  pf_gather_kernel<<<grid_for(N, 256), 256, 0, stream>>>(G, heavy_, nheavy);
+  pf_gather_kernel<<<grid_for(N, 256), 256, 0, stream>>>(G, heavy_, large_, nheavy);
   BFM_LAUNCH_CHECK("pf_gather_kernel");
   pf_gather_medium_kernel<<<med_blocks_, kMedWarps * 32, kMedSmem, stream>>>(G, heavy_, nheavy, hbuf_);
   BFM_LAUNCH_CHECK("pf_gather_medium_kernel");
+  pf_gather_large_kernel<<<large_blocks_, kLargeThreads, 0, stream>>>(G, large_, nheavy, hbuf_);
+  BFM_LAUNCH_CHECK("pf_gather_large_kernel");
   pf_gather_heavy_kernel<<<2 * 148, 512, kHeavySmem, stream>>>(G, heavy_, nheavy, hbuf_, nheavy_ + 1);
   BFM_LAUNCH_CHECK("pf_gather_heavy_kernel");
-  if (lc) lc->add(nrec > 0 ? 4 : 3);
+  if (lc) lc->add(nrec > 0 ? 5 : 4);
 }
 
 void PushforwardPlan::set_partition(int P, const int* row_starts) {

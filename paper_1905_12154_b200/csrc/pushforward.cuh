@@ -75,12 +75,14 @@ class PushforwardPlan {
   double* w_ = nullptr;      // [d*N] upper-node weight per axis
   int* off_ = nullptr;       // [N+1] first sorted position of each cell
   int* end_ = nullptr;       // [N+1] one past the last
-  int* heavy_ = nullptr;     // [N] targets with long deposit lists
+  int* heavy_ = nullptr;     // [N] medium targets (bottom) and huge targets (top)
   unsigned long long* nheavy_ = nullptr;  // [0] heavy count, [1] buffer fill
   double* hbuf_ = nullptr;   // [2^d * N] merged heavy deposits
   RadixSorter sorter_;
   int key_bits_ = 0;
   int med_blocks_ = 1;       // medium-gather CTAs (each warp owns a kMedium slice of hbuf_)
+  int large_blocks_ = 1;     // large-gather CTAs (each owns a kLarge slice of hbuf_)
+  int* large_ = nullptr;     // [N] targets of the CTA-per-target tier
 };
 
 }  // namespace bfmgpu

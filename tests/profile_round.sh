@@ -1,0 +1,18 @@
+# Round-end measurement bundle (run via gpurun). Plain runs first; ncu only
+# after the same command exited 0.
+set -x
+mkdir -p gpurun_out/prof
+python bench.py > gpurun_out/prof/bench_c3.json 2> gpurun_out/prof/bench_c3.err || exit 1
+python bench.py --config c4 --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/prof/bench_c4.json 2>/dev/null
+python bench.py --config c2 --steps 20 --warmup 3 --no-cpu-baseline > gpurun_out/prof/bench_c2.json 2>/dev/null
+python bench.py --config c1 --steps 50 --warmup 5 --no-cpu-baseline > gpurun_out/prof/bench_c1.json 2>/dev/null
+python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/prof/bench_ref_c3.json 2>/dev/null
+python bench.py --steps 2 --warmup 3 --no-cpu-baseline > /dev/null 2>&1 && \
+  ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/prof/launches_bench_c3.csv \
+      python bench.py --steps 2 --warmup 3 --no-cpu-baseline > /dev/null 2>&1
+python tests/ct_op_traffic.py > /dev/null 2>&1 && \
+  ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --clock-control none -k regex:ct_pass \
+      --csv --log-file gpurun_out/prof/ct_op_dram.csv python tests/ct_op_traffic.py > /dev/null 2>&1
+python tests/prof_c3.py c3 2 > /dev/null 2>&1 && \
+  ncu --set full --clock-control none --import-source on -k regex:ct_pass -s 6 -c 1 -o gpurun_out/prof/ct_full python tests/prof_c3.py c3 2 > /dev/null 2>&1
+ls -la gpurun_out/prof
