@@ -12,6 +12,7 @@
 #include <limits>
 #include <memory>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/bfm_b200.h"
@@ -144,18 +145,123 @@ double update_sigma(double sigma, double increase, double gn, const bfm_config& 
 struct DevBuf {
   double* p = nullptr;
   DevBuf() = default;
-  explicit DevBuf(long n) { BFM_CUDA(cudaMalloc(&p, n * sizeof(double))); }
+  explicit DevBuf(long n) { BFM_CUDA(dmalloc(&p, n * sizeof(double))); }
   ~DevBuf() {
-    if (p) cudaFree(p);
+    if (p) dfree(p);
   }
   DevBuf(const DevBuf&) = delete;
   DevBuf& operator=(const DevBuf&) = delete;
   void alloc(long n) {
-    if (!p) BFM_CUDA(cudaMalloc(&p, n * sizeof(double)));
+    if (!p) BFM_CUDA(dmalloc(&p, n * sizeof(double)));
   }
 };
 
 enum { kSlotPair = 0, kSlotGn = 1, kSlotShift = 2, kSlotPrimal = 3 };
+
+bool is_pinned(const void* p) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost;
+}
+
+// Host <-> device copies of a field: direct from/to pinned memory, otherwise
+// through two pinned staging chunks so the DMA overlaps the host-side copy.
+constexpr size_t kStage = size_t(8) << 20;  // bytes per staging chunk
+struct Staging {
+  double* buf[2] = {nullptr, nullptr};
+  cudaEvent_t ev[2] = {nullptr, nullptr};
+  Staging() {
+    for (int i = 0; i < 2; ++i) {
+      BFM_CUDA(cudaMallocHost(&buf[i], kStage));
+      BFM_CUDA(cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming));
+    }
+  }
+  ~Staging() {
+    for (int i = 0; i < 2; ++i) {
+      if (buf[i]) cudaFreeHost(buf[i]);
+      if (ev[i]) cudaEventDestroy(ev[i]);
+    }
+  }
+};
+Staging& staging() {
+  static thread_local Staging st;
+  return st;
+}
+
+// Host-side copy of a staging chunk split over a few threads: the first touch
+// of freshly allocated (pageable) output pages dominates a single-threaded copy.
+void par_memcpy(void* dst, const void* src, size_t len) {
+  constexpr size_t kPart = size_t(1) << 20;
+  const int parts = static_cast<int>(std::min<size_t>(8, (len + kPart - 1) / kPart));
+  if (parts <= 1) {
+    std::memcpy(dst, src, len);
+    return;
+  }
+  const size_t step = (len + parts - 1) / parts;
+  std::vector<std::thread> th;
+  for (int i = 1; i < parts; ++i) {
+    const size_t o = i * step;
+    if (o >= len) break;
+    th.emplace_back([=] {
+      std::memcpy(static_cast<char*>(dst) + o, static_cast<const char*>(src) + o, std::min(step, len - o));
+    });
+  }
+  std::memcpy(dst, src, std::min(step, len));
+  for (auto& t : th) t.join();
+}
+
+void copy_h2d(double* dst, const double* src, long n, cudaStream_t s) {
+  const size_t bytes = n * sizeof(double);
+  if (is_pinned(src) || bytes <= kStage) {
+    BFM_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s));
+    if (!is_pinned(src)) BFM_CUDA(cudaStreamSynchronize(s));
+    return;
+  }
+  Staging& st = staging();
+  size_t off = 0;
+  for (int b = 0; off < bytes; b ^= 1) {
+    const size_t len = std::min(kStage, bytes - off);
+    BFM_CUDA(cudaEventSynchronize(st.ev[b]));  // the chunk's previous DMA is done
+    par_memcpy(st.buf[b], reinterpret_cast<const char*>(src) + off, len);
+    BFM_CUDA(cudaMemcpyAsync(reinterpret_cast<char*>(dst) + off, st.buf[b], len,
+                             cudaMemcpyHostToDevice, s));
+    BFM_CUDA(cudaEventRecord(st.ev[b], s));
+    off += len;
+  }
+  BFM_CUDA(cudaStreamSynchronize(s));
+}
+
+void copy_d2h(double* dst, const double* src, long n, cudaStream_t s) {
+  const size_t bytes = n * sizeof(double);
+  if (is_pinned(dst) || bytes <= kStage) {
+    BFM_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, s));
+    BFM_CUDA(cudaStreamSynchronize(s));
+    return;
+  }
+  Staging& st = staging();
+  size_t off = 0, prev_off = 0, prev_len = 0;
+  int b = 0;
+  while (off < bytes || prev_len) {
+    size_t len = 0;
+    if (off < bytes) {
+      len = std::min(kStage, bytes - off);
+      BFM_CUDA(cudaMemcpyAsync(st.buf[b], reinterpret_cast<const char*>(src) + off, len,
+                               cudaMemcpyDeviceToHost, s));
+      BFM_CUDA(cudaEventRecord(st.ev[b], s));
+    }
+    if (prev_len) {  // previous chunk: wait for its DMA, then copy out while this one flies
+      BFM_CUDA(cudaEventSynchronize(st.ev[b ^ 1]));
+      par_memcpy(reinterpret_cast<char*>(dst) + prev_off, st.buf[b ^ 1], prev_len);
+    }
+    prev_off = off;
+    prev_len = len;
+    off += len;
+    b ^= 1;
+  }
+}
 
 }  // namespace
 
@@ -394,7 +500,7 @@ struct HostOp {
   ~HostOp() { release(); }
   double* up(const double* h, long n) {
     double* d = nullptr;
-    BFM_CUDA(cudaMalloc(&d, n * sizeof(double)));
+    BFM_CUDA(dmalloc(&d, n * sizeof(double)));
     keep.push_back(d);
     if (h) BFM_CUDA(cudaMemcpy(d, h, n * sizeof(double), cudaMemcpyHostToDevice));
     return d;
@@ -405,7 +511,7 @@ struct HostOp {
   }
   std::vector<double*> keep;
   void release() {
-    for (double* p : keep) cudaFree(p);
+    for (double* p : keep) dfree(p);
     keep.clear();
   }
 };
@@ -474,8 +580,12 @@ int bfm_solver_create(int dim, const int* extents, const double* mu, const doubl
     if (cfg) c = *cfg;
     const GridDesc g = checked_grid(dim, extents);
     check_config(c);
-    check_density("mu", mu, g);
-    check_density("nu", nu, g);
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+      cudaGetLastError();
+      check_density("mu", mu, g);  // input errors take precedence, as before a device is needed
+      check_density("nu", nu, g);
+    }
     require_device();
     std::unique_ptr<bfm_solver> s(new bfm_solver);
     s->start = std::chrono::steady_clock::now();
@@ -485,13 +595,27 @@ int bfm_solver_create(int dim, const int* extents, const double* mu, const doubl
     BFM_CUDA(cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking));
     const long N = g.size;
     for (DevBuf* b : {&s->mu, &s->nu, &s->phi, &s->psi, &s->dir, &s->dir2, &s->r}) b->alloc(N);
-    BFM_CUDA(cudaMemcpyAsync(s->mu.p, mu, N * sizeof(double), cudaMemcpyHostToDevice, s->stream));
-    BFM_CUDA(cudaMemcpyAsync(s->nu.p, nu, N * sizeof(double), cudaMemcpyHostToDevice, s->stream));
+    copy_h2d(s->mu.p, mu, N, s->stream);
+    copy_h2d(s->nu.p, nu, N, s->stream);
     BFM_CUDA(cudaMemsetAsync(s->phi.p, 0, N * sizeof(double), s->stream));
     BFM_CUDA(cudaMemsetAsync(s->psi.p, 0, N * sizeof(double), s->stream));
-    double sup = 0.0;  // solver.hpp:160-163
-    for (long i = 0; i < N; ++i) sup = std::max(sup, mu[i]);
-    for (long i = 0; i < N; ++i) sup = std::max(sup, nu[i]);
+    // solver.hpp:105-116 on the device: sup, non-finite / negative flags and
+    // the mass (double-double). Any flag, or a mass within 1e-9 of the
+    // tolerance, re-runs the reference's exact host check (first offending
+    // sample, sequential Kahan mass) so errors and messages are identical.
+    Reducer& red = s->ws.redp();
+    red.scan_density(s->mu.p, N, 4, s->stream, nullptr);
+    red.scan_density(s->nu.p, N, 7, s->stream, nullptr);
+    red.sum(s->mu.p, N, g.vol, 10, s->stream, nullptr);
+    red.sum(s->nu.p, N, g.vol, 11, s->stream, nullptr);
+    double v[12];
+    red.fetch(v, 12, s->stream);
+    auto needs_host = [](double bad, double neg, double mass) {
+      return bad != 0.0 || neg != 0.0 || !(std::abs(std::abs(mass - 1.0) - 1e-6) > 1e-9);
+    };
+    if (needs_host(v[5], v[6], v[10]) || std::abs(v[10] - 1.0) > 1e-6) check_density("mu", mu, g);
+    if (needs_host(v[8], v[9], v[11]) || std::abs(v[11] - 1.0) > 1e-6) check_density("nu", nu, g);
+    const double sup = std::max(v[4], v[7]);  // solver.hpp:160-163
     s->sigma = c.sigma_init > 0.0 ? c.sigma_init : 8.0 / sup;
     s->last_pair = 0.0;
     s->ws.ctp();
@@ -547,8 +671,7 @@ int bfm_solver_field(bfm_solver* s, int which, double* host_out) {
   return guard([&] {
     const double* src = which == BFM_FIELD_PHI ? s->phi.p : which == BFM_FIELD_PSI ? s->psi.p : nullptr;
     if (!src) fail(BFM_ERR_INVALID_ARGUMENT, "bfm_solver_field: PHI or PSI only");
-    BFM_CUDA(cudaStreamSynchronize(s->stream));
-    BFM_CUDA(cudaMemcpy(host_out, src, s->g.size * sizeof(double), cudaMemcpyDeviceToHost));
+    copy_d2h(host_out, src, s->g.size, s->stream);
   });
 }
 
@@ -561,8 +684,7 @@ int bfm_solver_report_field(bfm_solver* s, int which, double* host_out) {
     else if (which >= BFM_FIELD_MAP0 && which - BFM_FIELD_MAP0 < s->g.d)
       src = s->rep_map.p + (which - BFM_FIELD_MAP0) * s->g.size;
     else fail(BFM_ERR_INVALID_ARGUMENT, "bfm_solver_report_field: bad field");
-    BFM_CUDA(cudaStreamSynchronize(s->stream));
-    BFM_CUDA(cudaMemcpy(host_out, src, s->g.size * sizeof(double), cudaMemcpyDeviceToHost));
+    copy_d2h(host_out, src, s->g.size, s->stream);
   });
 }
 

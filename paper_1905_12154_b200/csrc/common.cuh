@@ -53,6 +53,18 @@ inline GridDesc make_grid(int d, const int* ext) {
 
 BFM_HD double coord(double h, int i) { return (static_cast<double>(i) + 0.5) * h; }
 
+// Device allocations come from the device's stream-ordered pool with an
+// unbounded release threshold: creating and destroying solvers/workspaces
+// (hundreds of MB of fields, sort and gather buffers) reuses reserved memory
+// instead of paying cudaMalloc/cudaFree page mapping each time.
+cudaError_t dev_malloc_bytes(void** p, size_t n);
+void dev_free(void* p);
+template <class T>
+inline cudaError_t dmalloc(T** p, size_t n) {
+  return dev_malloc_bytes(reinterpret_cast<void**>(p), n);
+}
+inline void dfree(const void* p) { dev_free(const_cast<void*>(p)); }
+
 // Kernel-launch counter for the "gpu_launches" evidence in bench.py.
 struct LaunchCounter {
   long count = 0;

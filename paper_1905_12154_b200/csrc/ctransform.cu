@@ -828,14 +828,14 @@ CtPlan::~CtPlan() {
     if (tables_[a]) {
       bool shared = false;
       for (int b = 0; b < a; ++b) shared |= tables_[b] == tables_[a];
-      if (!shared) cudaFree(tables_[a]);
+      if (!shared) dfree(tables_[a]);
     }
   for (auto* p : state_)
-    if (p) cudaFree(p);
+    if (p) dfree(p);
   for (auto* p : qbuf_)
-    if (p) cudaFree(p);
-  if (slow_) cudaFree(slow_);
-  if (stats_) cudaFree(stats_);
+    if (p) dfree(p);
+  if (slow_) dfree(slow_);
+  if (stats_) dfree(stats_);
 }
 
 void CtPlan::init(const GridDesc& g) { setup(g, g, 0, g.d, 0, false, false); }
@@ -907,7 +907,7 @@ void CtPlan::setup(const GridDesc& loc, const GridDesc& global, int pb, int pe, 
             host[static_cast<size_t>(k) * n + j] = make_double4(limb[0], limb[1], limb[2], 0.0);
           }
         }
-        BFM_CUDA(cudaMalloc(&tables_[a], host.size() * sizeof(double4)));
+        BFM_CUDA(dmalloc(&tables_[a], host.size() * sizeof(double4)));
         BFM_CUDA(cudaMemcpy(tables_[a], host.data(), host.size() * sizeof(double4),
                             cudaMemcpyHostToDevice));
       }
@@ -917,17 +917,17 @@ void CtPlan::setup(const GridDesc& loc, const GridDesc& global, int pb, int pe, 
   dyadic_ = true;
   for (int a = 0; a < global.d; ++a) dyadic_ = dyadic_ && is_dyadic(global.n[a]);
   if (loc.d > 1 && pe - pb > 1) {
-    BFM_CUDA(cudaMalloc(&state_[0], loc.size * sizeof(uint32_t)));
-    BFM_CUDA(cudaMalloc(&qbuf_[0], loc.size * sizeof(double)));
+    BFM_CUDA(dmalloc(&state_[0], loc.size * sizeof(uint32_t)));
+    BFM_CUDA(dmalloc(&qbuf_[0], loc.size * sizeof(double)));
     if (pe - pb > 2) {
-      BFM_CUDA(cudaMalloc(&state_[1], loc.size * sizeof(uint32_t)));
-      BFM_CUDA(cudaMalloc(&qbuf_[1], loc.size * sizeof(double)));
+      BFM_CUDA(dmalloc(&state_[1], loc.size * sizeof(uint32_t)));
+      BFM_CUDA(dmalloc(&qbuf_[1], loc.size * sizeof(double)));
     }
   }
-  BFM_CUDA(cudaMalloc(&slow_, sizeof(unsigned long long)));
+  BFM_CUDA(dmalloc(&slow_, sizeof(unsigned long long)));
   BFM_CUDA(cudaMemset(slow_, 0, sizeof(unsigned long long)));
   if (getenv("BFM_CT_STATS")) {
-    BFM_CUDA(cudaMalloc(&stats_, 32 * sizeof(unsigned long long)));
+    BFM_CUDA(dmalloc(&stats_, 32 * sizeof(unsigned long long)));
     BFM_CUDA(cudaMemset(stats_, 0, 32 * sizeof(unsigned long long)));
   }
 
@@ -1060,13 +1060,13 @@ __global__ void debug_rd_kernel(const double* t, int m, int count, double* out) 
 
 void debug_round_down(const double* h_terms, int m, int count, double* h_out) {
   double *dt = nullptr, *dout = nullptr;
-  BFM_CUDA(cudaMalloc(&dt, sizeof(double) * m * count));
-  BFM_CUDA(cudaMalloc(&dout, sizeof(double) * count));
+  BFM_CUDA(dmalloc(&dt, sizeof(double) * m * count));
+  BFM_CUDA(dmalloc(&dout, sizeof(double) * count));
   BFM_CUDA(cudaMemcpy(dt, h_terms, sizeof(double) * m * count, cudaMemcpyHostToDevice));
   debug_rd_kernel<<<(count + 127) / 128, 128>>>(dt, m, count, dout);
   BFM_LAUNCH_CHECK("debug_rd_kernel");
   BFM_CUDA(cudaMemcpy(h_out, dout, sizeof(double) * count, cudaMemcpyDeviceToHost));
-  cudaFree(dt);
-  cudaFree(dout);
+  dfree(dt);
+  dfree(dout);
 }
 }  // namespace bfmgpu

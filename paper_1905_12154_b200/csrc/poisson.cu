@@ -362,7 +362,7 @@ template <class T>
 T* upload(const std::vector<T>& v, std::vector<void*>& keep) {
   if (v.empty()) return nullptr;
   T* d = nullptr;
-  BFM_CUDA(cudaMalloc(&d, v.size() * sizeof(T)));
+  BFM_CUDA(dmalloc(&d, v.size() * sizeof(T)));
   BFM_CUDA(cudaMemcpy(d, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice));
   keep.push_back(d);
   return d;
@@ -374,12 +374,12 @@ PoissonPlan::~PoissonPlan() {
   for (int a = 0; a < 3; ++a) {
     if (tables_[a]) {
       auto* v = static_cast<std::vector<void*>*>(tables_[a]);
-      for (void* p : *v) cudaFree(p);
+      for (void* p : *v) dfree(p);
       delete v;
     }
-    if (lam_[a]) cudaFree(lam_[a]);
+    if (lam_[a]) dfree(lam_[a]);
   }
-  if (tmp_) cudaFree(tmp_);
+  if (tmp_) dfree(tmp_);
 }
 
 void PoissonPlan::init(const GridDesc& g) { setup(g, g, 0, 0, g.d); }
@@ -410,7 +410,7 @@ void PoissonPlan::setup(const GridDesc& loc, const GridDesc& global, long col0, 
     std::vector<double> lam(n);
     const double na = n;
     for (int k = 0; k < n; ++k) lam[k] = (2.0 - 2.0 * std::cos(kPi * k / na)) * na * na;
-    BFM_CUDA(cudaMalloc(&lam_[a], n * sizeof(double)));
+    BFM_CUDA(dmalloc(&lam_[a], n * sizeof(double)));
     BFM_CUDA(cudaMemcpy(lam_[a], lam.data(), n * sizeof(double), cudaMemcpyHostToDevice));
   }
   const GridDesc& g = loc;

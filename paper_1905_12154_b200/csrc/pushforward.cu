@@ -659,7 +659,7 @@ PushforwardPlan::~PushforwardPlan() {
                   static_cast<void*>(nheavy_), static_cast<void*>(hbuf_),
                   static_cast<void*>(row0_), static_cast<void*>(bcount_),
                   static_cast<void*>(large_)})
-    if (p) cudaFree(p);
+    if (p) dfree(p);
   if (hcounts_) cudaFreeHost(hcounts_);
 }
 
@@ -682,14 +682,14 @@ void PushforwardPlan::setup(const GridDesc& loc, const GridDesc& global, int row
   ncells_ = slab ? loc.size + loc.stride[0] : loc.size;
   if (global.size >= (1L << 29)) throw std::invalid_argument("pushforward: grid too large");
   const long N = loc.size;
-  BFM_CUDA(cudaMalloc(&key_, N * sizeof(uint32_t)));
-  BFM_CUDA(cudaMalloc(&cmask_, N));
-  BFM_CUDA(cudaMalloc(&w_, g_.d * N * sizeof(double)));
-  BFM_CUDA(cudaMalloc(&off_, (ncells_ + 1) * sizeof(int)));
-  BFM_CUDA(cudaMalloc(&end_, (ncells_ + 1) * sizeof(int)));
-  BFM_CUDA(cudaMalloc(&heavy_, (N + 1) * sizeof(int)));
-  BFM_CUDA(cudaMalloc(&large_, (N + 1) * sizeof(int)));
-  BFM_CUDA(cudaMalloc(&nheavy_, 4 * sizeof(unsigned long long)));
+  BFM_CUDA(dmalloc(&key_, N * sizeof(uint32_t)));
+  BFM_CUDA(dmalloc(&cmask_, N));
+  BFM_CUDA(dmalloc(&w_, g_.d * N * sizeof(double)));
+  BFM_CUDA(dmalloc(&off_, (ncells_ + 1) * sizeof(int)));
+  BFM_CUDA(dmalloc(&end_, (ncells_ + 1) * sizeof(int)));
+  BFM_CUDA(dmalloc(&heavy_, (N + 1) * sizeof(int)));
+  BFM_CUDA(dmalloc(&large_, (N + 1) * sizeof(int)));
+  BFM_CUDA(dmalloc(&nheavy_, 4 * sizeof(unsigned long long)));
   ensure_records(N);
   BFM_CUDA(cudaFuncSetAttribute(pf_gather_heavy_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 kHeavySmem));
@@ -703,7 +703,7 @@ void PushforwardPlan::ensure_records(long nrec) {
   if (nrec <= rec_cap_ && hbuf_) return;
   const long cap = std::max<long>(nrec, 1);
   if (hbuf_) {
-    cudaFree(hbuf_);
+    dfree(hbuf_);
     hbuf_ = nullptr;
   }
   const long deposits = (static_cast<long>(1) << g_.d) * cap;
@@ -711,7 +711,7 @@ void PushforwardPlan::ensure_records(long nrec) {
   large_blocks_ = static_cast<int>(std::max<long>(1, std::min<long>(kLargeBlocks, deposits / kLarge)));
   const long hcap = std::max<long>(deposits, std::max<long>(static_cast<long>(med_blocks_) * kMedWarps * kMedium,
                                                             static_cast<long>(large_blocks_) * kLarge));
-  BFM_CUDA(cudaMalloc(&hbuf_, hcap * sizeof(double)));
+  BFM_CUDA(dmalloc(&hbuf_, hcap * sizeof(double)));
   sorter_.init(cap);
   rec_cap_ = cap;
 }
@@ -798,11 +798,11 @@ void PushforwardPlan::gather(long nrec, const uint32_t* d_keys, const double* d_
 void PushforwardPlan::set_partition(int P, const int* row_starts) {
   if (P < 1 || P > kMaxRanks) throw std::invalid_argument("pushforward: 1..64 ranks supported");
   nranks_ = P;
-  if (!row0_) BFM_CUDA(cudaMalloc(&row0_, (kMaxRanks + 1) * sizeof(int)));
+  if (!row0_) BFM_CUDA(dmalloc(&row0_, (kMaxRanks + 1) * sizeof(int)));
   BFM_CUDA(cudaMemcpy(row0_, row_starts, (P + 1) * sizeof(int), cudaMemcpyHostToDevice));
   const long nblocks = (g_.size + kRouteTile - 1) / kRouteTile;
-  if (bcount_) cudaFree(bcount_);
-  BFM_CUDA(cudaMalloc(&bcount_, (static_cast<long>(P) * nblocks + 1) * sizeof(int)));
+  if (bcount_) dfree(bcount_);
+  BFM_CUDA(dmalloc(&bcount_, (static_cast<long>(P) * nblocks + 1) * sizeof(int)));
   if (!hcounts_) BFM_CUDA(cudaMallocHost(&hcounts_, (kMaxRanks + 1) * sizeof(int)));
 }
 
@@ -903,16 +903,16 @@ void debug_fold(const double* h_w, const long* h_off, int nseq, int mode, double
   const long total = h_off[nseq];
   double *dw = nullptr, *dout = nullptr;
   long* doff = nullptr;
-  BFM_CUDA(cudaMalloc(&dw, sizeof(double) * (total + 1)));
-  BFM_CUDA(cudaMalloc(&doff, sizeof(long) * (nseq + 1)));
-  BFM_CUDA(cudaMalloc(&dout, sizeof(double) * nseq));
+  BFM_CUDA(dmalloc(&dw, sizeof(double) * (total + 1)));
+  BFM_CUDA(dmalloc(&doff, sizeof(long) * (nseq + 1)));
+  BFM_CUDA(dmalloc(&dout, sizeof(double) * nseq));
   BFM_CUDA(cudaMemcpy(dw, h_w, sizeof(double) * total, cudaMemcpyHostToDevice));
   BFM_CUDA(cudaMemcpy(doff, h_off, sizeof(long) * (nseq + 1), cudaMemcpyHostToDevice));
   debug_fold_kernel<<<nseq, mode == 0 ? 512 : 32>>>(dw, doff, mode, dout);
   BFM_LAUNCH_CHECK("debug_fold_kernel");
   BFM_CUDA(cudaMemcpy(h_out, dout, sizeof(double) * nseq, cudaMemcpyDeviceToHost));
-  cudaFree(dw);
-  cudaFree(doff);
-  cudaFree(dout);
+  dfree(dw);
+  dfree(doff);
+  dfree(dout);
 }
 }  // namespace bfmgpu

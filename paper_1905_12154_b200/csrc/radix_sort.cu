@@ -159,33 +159,33 @@ __global__ void __launch_bounds__(kThreads) rs_scatter_kernel(const uint32_t* ki
 
 RadixSorter::~RadixSorter() {
   for (int i = 0; i < 2; ++i) {
-    if (kbuf_[i]) cudaFree(kbuf_[i]);
-    if (vbuf_[i]) cudaFree(vbuf_[i]);
+    if (kbuf_[i]) dfree(kbuf_[i]);
+    if (vbuf_[i]) dfree(vbuf_[i]);
   }
-  if (hist_) cudaFree(hist_);
-  if (bsum_) cudaFree(bsum_);
+  if (hist_) dfree(hist_);
+  if (bsum_) dfree(bsum_);
 }
 
 void RadixSorter::init(long n) {
   for (int i = 0; i < 2; ++i) {  // re-init (capacity growth) releases the old buffers
-    if (kbuf_[i]) cudaFree(kbuf_[i]);
-    if (vbuf_[i]) cudaFree(vbuf_[i]);
+    if (kbuf_[i]) dfree(kbuf_[i]);
+    if (vbuf_[i]) dfree(vbuf_[i]);
     kbuf_[i] = nullptr;
     vbuf_[i] = nullptr;
   }
-  if (hist_) cudaFree(hist_);
-  if (bsum_) cudaFree(bsum_);
+  if (hist_) dfree(hist_);
+  if (bsum_) dfree(bsum_);
   hist_ = nullptr;
   bsum_ = nullptr;
   cap_ = n;
   blocks_ = (n + kTile - 1) / kTile;
   for (int i = 0; i < 2; ++i) {
-    BFM_CUDA(cudaMalloc(&kbuf_[i], (n + 1) * sizeof(uint32_t)));
-    BFM_CUDA(cudaMalloc(&vbuf_[i], (n + 1) * sizeof(int)));
+    BFM_CUDA(dmalloc(&kbuf_[i], (n + 1) * sizeof(uint32_t)));
+    BFM_CUDA(dmalloc(&vbuf_[i], (n + 1) * sizeof(int)));
   }
   const long m = static_cast<long>(kBins) * blocks_;
-  BFM_CUDA(cudaMalloc(&hist_, (m + 1) * sizeof(int)));
-  BFM_CUDA(cudaMalloc(&bsum_, ((m + kScanTile - 1) / kScanTile + 1) * sizeof(int)));
+  BFM_CUDA(dmalloc(&hist_, (m + 1) * sizeof(int)));
+  BFM_CUDA(dmalloc(&bsum_, ((m + kScanTile - 1) / kScanTile + 1) * sizeof(int)));
 }
 
 void RadixSorter::sort(const uint32_t* keys_in, const int* vals_in, long n, int bits, cudaStream_t s,

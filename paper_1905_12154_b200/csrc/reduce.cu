@@ -192,15 +192,15 @@ unsigned ew_grid(long n) {
 }  // namespace
 
 Reducer::~Reducer() {
-  if (partials_) cudaFree(partials_);
-  if (results_) cudaFree(results_);
+  if (partials_) dfree(partials_);
+  if (results_) dfree(results_);
   if (pinned_) cudaFreeHost(pinned_);
 }
 
 void Reducer::init() {
   blocks_ = kRedBlocks;
-  BFM_CUDA(cudaMalloc(&partials_, 4 * blocks_ * sizeof(double)));
-  BFM_CUDA(cudaMalloc(&results_, kRedSlots * sizeof(double)));
+  BFM_CUDA(dmalloc(&partials_, 4 * blocks_ * sizeof(double)));
+  BFM_CUDA(dmalloc(&results_, kRedSlots * sizeof(double)));
   BFM_CUDA(cudaMemset(results_, 0, kRedSlots * sizeof(double)));
   BFM_CUDA(cudaMallocHost(&pinned_, kRedSlots * sizeof(double)));
 }
