@@ -204,8 +204,13 @@ __device__ __forceinline__ void slack_max(uint8_t* dlt, int e, uint8_t c) {
   }
 }
 
+// Threads per CTA (lpc * tpl) at most: dyadic lines get 768 (an 80-register
+// budget keeps their query phases nearly spill-free); the non-dyadic variant,
+// whose exact path lives in local memory anyway, runs faster at 1024.
+constexpr int ct_threads(bool dy) { return dy ? 768 : 1024; }
+
 template <bool DY>
-__global__ void __launch_bounds__(1024) ct_pass_kernel(CtPass p) {
+__global__ void __launch_bounds__(ct_threads(DY)) ct_pass_kernel(CtPass p) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int tpl = p.tpl;
   const int l = threadIdx.x / tpl;
@@ -971,7 +976,7 @@ void CtPlan::setup(const GridDesc& loc, const GridDesc& global, int pb, int pe, 
     o = align16(o + 64 + static_cast<int>(sizeof(LineGeo)));
     P.line_bytes = o;
     if (o > budget) throw std::invalid_argument("ctransform: grid line too long for shared memory");
-    int lpc = std::min<long>(budget / o, 1024 / P.tpl);
+    int lpc = std::min<long>(budget / o, ct_threads(dyadic_) / P.tpl);
     lpc = std::min(lpc, P.strided ? 16 : 8);
     if (P.tpl > 32) lpc = std::min(lpc, 15);
     lpc = static_cast<int>(std::min<long>(lpc, P.nlines));

@@ -57,11 +57,26 @@ struct MapArgs {
   double diam;          // sqrt(d)
 };
 
+// Node coordinates of a linear index (grids here have < 2^31 nodes: 32-bit
+// divisions, far cheaper than 64-bit ones on the SM).
 __device__ __forceinline__ void node_idx(const GridDesc& g, long lin, int* id) {
-  for (int a = 0; a < g.d; ++a) {
-    id[a] = static_cast<int>(lin / g.stride[a]);
-    lin -= static_cast<long>(id[a]) * g.stride[a];
+  const unsigned r = static_cast<unsigned>(lin);
+  if (g.d == 1) {
+    id[0] = static_cast<int>(r);
+    return;
   }
+  const unsigned s0 = static_cast<unsigned>(g.stride[0]);
+  const unsigned i0 = r / s0;
+  const unsigned r0 = r - i0 * s0;
+  id[0] = static_cast<int>(i0);
+  if (g.d == 2) {
+    id[1] = static_cast<int>(r0);
+    return;
+  }
+  const unsigned s1 = static_cast<unsigned>(g.stride[1]);
+  const unsigned i1 = r0 / s1;
+  id[1] = static_cast<int>(i1);
+  id[2] = static_cast<int>(r0 - i1 * s1);
 }
 
 // locate_cell (pushforward.hpp:51-63) against the node table c_i = (i+0.5)h.
@@ -189,34 +204,32 @@ __device__ __forceinline__ double deposit_weight(const GatherArgs& A, int s, int
 // Light targets: merge the <= 2^d sorted neighbouring buckets by source id
 // and fold in place. Targets with more than kLight deposits are deferred to
 // pf_gather_heavy_kernel.
-__global__ void pf_gather_kernel(GatherArgs A, int* heavy, int* large, int* nheavy) {
+template <int D>
+__global__ void __launch_bounds__(256) pf_gather_kernel(GatherArgs A, int* heavy, int* large,
+                                                        int* nheavy) {
+  constexpr int NC = 1 << D;  // corner b = bit a set: the target is the upper node on axis a
   const GridDesc& g = A.g;
-  const int corners = 1 << g.d;
   for (long t = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; t < g.size;
        t += static_cast<long>(gridDim.x) * blockDim.x) {
     int id[3] = {0, 0, 0};
     node_idx(g, t, id);
     id[0] += A.row_off;
-    int pos[8], end[8];
-    int nl = 0;
-    int bits[8];
+    // fixed-size, fully unrolled per-corner state stays in registers
+    int pos[NC], end[NC], head[NC];
     int total = 0;
-    for (int b = 0; b < corners; ++b) {
+#pragma unroll
+    for (int b = 0; b < NC; ++b) {
       long c = t + A.cell_shift;
       bool ok = true;
-      for (int a = 0; a < g.d; ++a)
+#pragma unroll
+      for (int a = 0; a < D; ++a)
         if ((b >> a) & 1) {
           if (id[a] == 0) ok = false;
           c -= g.stride[a];
         }
-      if (!ok) continue;
-      const int k = A.end[c] - A.off[c];
-      if (k <= 0) continue;
-      pos[nl] = A.off[c];
-      end[nl] = pos[nl] + k;
-      bits[nl] = b;
-      total += k;
-      ++nl;
+      pos[b] = ok ? A.off[c] : 0;
+      end[b] = ok ? A.end[c] : 0;
+      total += end[b] - pos[b];
     }
     if (total > kLight) {
       if (total <= kMedium) heavy[atomicAdd(nheavy, 1)] = static_cast<int>(t);
@@ -224,22 +237,26 @@ __global__ void pf_gather_kernel(GatherArgs A, int* heavy, int* large, int* nhea
       else heavy[g.size - 1 - atomicAdd(nheavy + 1, 1)] = static_cast<int>(t);  // huge: from the top
       continue;
     }
+#pragma unroll
+    for (int b = 0; b < NC; ++b) head[b] = pos[b] < end[b] ? A.bucket[pos[b]] : INT_MAX;
     double rho = 0.0;
-    while (true) {
-      int best = -1, bs = INT_MAX;
-      for (int q = 0; q < nl; ++q)
-        if (pos[q] < end[q]) {
-          const int s = A.bucket[pos[q]];
-          if (s < bs) {
-            bs = s;
-            best = q;
-          }
+    for (int it = 0; it < total; ++it) {
+      // next deposit in source order: the smallest bucket head
+      int best = 0, bs = head[0];
+#pragma unroll
+      for (int b = 1; b < NC; ++b)
+        if (head[b] < bs) {
+          bs = head[b];
+          best = b;
         }
-      if (best < 0) break;
-      ++pos[best];
-      const int b = bits[best];
-      if (b & A.cmask[bs]) continue;  // clamped axis: upper corner has weight 0
-      const double wt = deposit_weight(A, bs, b);
+#pragma unroll
+      for (int b = 0; b < NC; ++b)
+        if (b == best) {
+          ++pos[b];
+          head[b] = pos[b] < end[b] ? A.bucket[pos[b]] : INT_MAX;
+        }
+      if (best & A.cmask[bs]) continue;  // clamped axis: upper corner has weight 0
+      const double wt = deposit_weight(A, bs, best);
       if (wt != 0.0) rho += wt;
     }
     A.out[t] = A.target ? A.target[t] - rho : rho;
@@ -784,7 +801,9 @@ void PushforwardPlan::gather(long nrec, const uint32_t* d_keys, const double* d_
   G.target = d_target;
   G.out = d_out;
   int* nheavy = reinterpret_cast<int*>(nheavy_);
-  pf_gather_kernel<<<grid_for(N, 256), 256, 0, stream>>>(G, heavy_, large_, nheavy);
+  if (g_.d == 1) pf_gather_kernel<1><<<grid_for(N, 256), 256, 0, stream>>>(G, heavy_, large_, nheavy);
+  else if (g_.d == 2) pf_gather_kernel<2><<<grid_for(N, 256), 256, 0, stream>>>(G, heavy_, large_, nheavy);
+  else pf_gather_kernel<3><<<grid_for(N, 256), 256, 0, stream>>>(G, heavy_, large_, nheavy);
   BFM_LAUNCH_CHECK("pf_gather_kernel");
   pf_gather_medium_kernel<<<med_blocks_, kMedWarps * 32, kMedSmem, stream>>>(G, heavy_, nheavy, hbuf_);
   BFM_LAUNCH_CHECK("pf_gather_medium_kernel");
