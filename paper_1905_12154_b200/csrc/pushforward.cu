@@ -311,49 +311,67 @@ __device__ __forceinline__ int lower_bound_ids(const int* v, int len, int key) {
 // its rank (lower_bound) in each other bucket (a source lives in exactly one
 // bucket, so there are no ties). Lanes write the weights to those positions
 // in the warp's private slice of a global buffer, then fold them in order.
+template <int D>
 __global__ void __launch_bounds__(kMedWarps * 32) pf_gather_medium_kernel(GatherArgs A,
                                                                          const int* heavy,
                                                                          const int* nheavy,
                                                                          double* hbuf) {
+  constexpr int NC = 1 << D;  // per-corner state in registers (fully unrolled loops)
   extern __shared__ int med_ids[];  // [kMedWarps][kMedStage]
+  const GridDesc& g = A.g;
   const int nh = nheavy[0];
   const int lane = threadIdx.x & 31;
   int* sids = med_ids + (threadIdx.x >> 5) * kMedStage;
   const long warp0 = (static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const long nwarps = (static_cast<long>(gridDim.x) * blockDim.x) >> 5;
+  double* buf = hbuf + warp0 * kMedium;  // the warp's private slice (K <= kMedium)
   for (long q = warp0; q < nh; q += nwarps) {
     const long t = heavy[q];
-    TargetBuckets tb;
-    target_buckets(A, t, tb);
-    const int K = tb.K;
-    int cat[8];
-    for (int qq = 0, o = 0; qq < tb.nl; ++qq) {
-      cat[qq] = o;
-      o += tb.end[qq] - tb.pos[qq];
+    int id[3] = {0, 0, 0};
+    node_idx(g, t, id);
+    id[0] += A.row_off;
+    int pos[NC], len[NC], cat[NC];
+    int K = 0;
+#pragma unroll
+    for (int b = 0; b < NC; ++b) {
+      long c = t + A.cell_shift;
+      bool ok = true;
+#pragma unroll
+      for (int a = 0; a < D; ++a)
+        if ((b >> a) & 1) {
+          if (id[a] == 0) ok = false;
+          c -= g.stride[a];
+        }
+      pos[b] = ok ? A.off[c] : 0;
+      len[b] = ok ? A.end[c] - pos[b] : 0;
+      cat[b] = K;
+      K += len[b];
     }
     const bool staged = K <= kMedStage;
-    if (staged)
-      for (int qq = 0; qq < tb.nl; ++qq)
-        for (int i = lane; i < tb.end[qq] - tb.pos[qq]; i += 32) sids[cat[qq] + i] = A.bucket[tb.pos[qq] + i];
-    double* buf = hbuf + warp0 * kMedium;  // the warp's private slice (K <= kMedium)
+    if (staged) {
+#pragma unroll
+      for (int b = 0; b < NC; ++b)
+        for (int i = lane; i < len[b]; i += 32) sids[cat[b] + i] = A.bucket[pos[b] + i];
+    }
     __syncwarp();
-    for (int qq = 0; qq < tb.nl; ++qq) {
-      const int len = tb.end[qq] - tb.pos[qq];
-      for (int i = lane; i < len; i += 32) {
-        const int src = staged ? sids[cat[qq] + i] : A.bucket[tb.pos[qq] + i];
+#pragma unroll
+    for (int qq = 0; qq < NC; ++qq) {
+      for (int i = lane; i < len[qq]; i += 32) {
+        const int src = staged ? sids[cat[qq] + i] : A.bucket[pos[qq] + i];
         int fin = i;
-        for (int o = 0; o < tb.nl; ++o)
-          if (o != qq)
-            fin += staged ? lower_bound_ids(sids + cat[o], tb.end[o] - tb.pos[o], src)
-                          : lower_bound_ids(A.bucket + tb.pos[o], tb.end[o] - tb.pos[o], src);
-        buf[fin] = (tb.bits[qq] & A.cmask[src]) ? 0.0 : deposit_weight(A, src, tb.bits[qq]);
+#pragma unroll
+        for (int o = 0; o < NC; ++o)
+          if (o != qq && len[o] > 0)
+            fin += staged ? lower_bound_ids(sids + cat[o], len[o], src)
+                          : lower_bound_ids(A.bucket + pos[o], len[o], src);
+        buf[fin] = (qq & A.cmask[src]) ? 0.0 : deposit_weight(A, src, qq);
       }
     }
     __syncwarp();
     // Starting from +0.0, rho can never become -0.0, so adding a zero weight
     // leaves it unchanged: folding every weight equals the reference's skip
     // of zero weights bit for bit. K is small here: a sequential chain of
-    // adds fed by shuffles (all 32 issued ahead of the chain when unrolled).
+    // adds fed by shuffles (issued ahead of the chain in groups of 8).
     double rho = 0.0;
     int c = 0;
     for (; c + 32 <= K; c += 32) {
@@ -710,7 +728,11 @@ void PushforwardPlan::setup(const GridDesc& loc, const GridDesc& global, int row
   ensure_records(N);
   BFM_CUDA(cudaFuncSetAttribute(pf_gather_heavy_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 kHeavySmem));
-  BFM_CUDA(cudaFuncSetAttribute(pf_gather_medium_kernel,
+  BFM_CUDA(cudaFuncSetAttribute(pf_gather_medium_kernel<1>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, kMedSmem));
+  BFM_CUDA(cudaFuncSetAttribute(pf_gather_medium_kernel<2>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, kMedSmem));
+  BFM_CUDA(cudaFuncSetAttribute(pf_gather_medium_kernel<3>,
                                 cudaFuncAttributeMaxDynamicSharedMemorySize, kMedSmem));
   key_bits_ = 1;
   while ((1L << key_bits_) <= ncells_) ++key_bits_;  // cells 0..ncells-1 plus the sentinel
@@ -805,7 +827,12 @@ void PushforwardPlan::gather(long nrec, const uint32_t* d_keys, const double* d_
   else if (g_.d == 2) pf_gather_kernel<2><<<grid_for(N, 256), 256, 0, stream>>>(G, heavy_, large_, nheavy);
   else pf_gather_kernel<3><<<grid_for(N, 256), 256, 0, stream>>>(G, heavy_, large_, nheavy);
   BFM_LAUNCH_CHECK("pf_gather_kernel");
-  pf_gather_medium_kernel<<<med_blocks_, kMedWarps * 32, kMedSmem, stream>>>(G, heavy_, nheavy, hbuf_);
+  if (g_.d == 1)
+    pf_gather_medium_kernel<1><<<med_blocks_, kMedWarps * 32, kMedSmem, stream>>>(G, heavy_, nheavy, hbuf_);
+  else if (g_.d == 2)
+    pf_gather_medium_kernel<2><<<med_blocks_, kMedWarps * 32, kMedSmem, stream>>>(G, heavy_, nheavy, hbuf_);
+  else
+    pf_gather_medium_kernel<3><<<med_blocks_, kMedWarps * 32, kMedSmem, stream>>>(G, heavy_, nheavy, hbuf_);
   BFM_LAUNCH_CHECK("pf_gather_medium_kernel");
   pf_gather_large_kernel<<<large_blocks_, kLargeThreads, 0, stream>>>(G, large_, nheavy, hbuf_);
   BFM_LAUNCH_CHECK("pf_gather_large_kernel");
