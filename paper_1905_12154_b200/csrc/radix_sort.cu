@@ -26,10 +26,17 @@ __global__ void __launch_bounds__(kThreads) rs_hist_kernel(const uint32_t* keys,
   __syncthreads();
   const long base = static_cast<long>(blockIdx.x) * kTile;
   const unsigned lane = threadIdx.x & 31u;
+  uint32_t kr[kItems];  // all of the tile's loads in flight before the first use
+#pragma unroll
+  for (int r = 0; r < kItems; ++r) {
+    const long i = base + static_cast<long>(r) * kThreads + threadIdx.x;
+    kr[r] = i < n ? keys[i] : 0u;
+  }
+#pragma unroll
   for (int r = 0; r < kItems; ++r) {
     const long i = base + static_cast<long>(r) * kThreads + threadIdx.x;
     const bool ok = i < n;
-    const unsigned d = ok ? (keys[i] >> shift) & (kBins - 1u) : static_cast<unsigned>(kBins);
+    const unsigned d = ok ? (kr[r] >> shift) & (kBins - 1u) : static_cast<unsigned>(kBins);
     const unsigned act = __ballot_sync(0xffffffffu, ok);
     if (ok) {
       const unsigned m = __match_any_sync(act, d);
@@ -124,6 +131,13 @@ __global__ void __launch_bounds__(kThreads) rs_scatter_kernel(const uint32_t* ki
   const unsigned lane = threadIdx.x & 31u;
   const int warp = threadIdx.x >> 5;
   const unsigned lt = (1u << lane) - 1u;
+  uint32_t kr[kItems];  // the tile's key loads in flight before the first use
+#pragma unroll
+  for (int r = 0; r < kItems; ++r) {
+    const long i = base + static_cast<long>(r) * kThreads + threadIdx.x;
+    kr[r] = i < n ? kin[i] : 0u;
+  }
+#pragma unroll
   for (int r = 0; r < kItems; ++r) {
     const long i = base + static_cast<long>(r) * kThreads + threadIdx.x;
     const bool ok = i < n;
@@ -132,7 +146,7 @@ __global__ void __launch_bounds__(kThreads) rs_scatter_kernel(const uint32_t* ki
     unsigned d = kBins, m = 0u;
     const unsigned act = __ballot_sync(0xffffffffu, ok);
     if (ok) {
-      k = kin[i];
+      k = kr[r];
       v = vin ? vin[i] : static_cast<int>(i);
       d = (k >> shift) & (kBins - 1u);
       m = __match_any_sync(act, d);

@@ -63,4 +63,18 @@ if __name__ == "__main__":
     if len(sys.argv) > 2:
         print("\n".join(top_lines(rep, int(sys.argv[2]))))
     for name, unit, vals in raw(rep, ["dram__bytes_read.sum", "dram__bytes_write.sum"]):
-        print(name, unit, vals)
+        if name in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+            print(name, unit, vals)
+    print("pipe utilisation (% of peak, active cycles):")
+    for name, unit, vals in raw(rep, ["sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
+                                      "sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active",
+                                      "sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active",
+                                      "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed",
+                                      "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum"]):
+        print("  ", name, vals)
+    print("warp stall samples:")
+    st = [(name.replace("smsp__pcsamp_warps_issue_stalled_", ""), vals)
+          for name, unit, vals in raw(rep, ["smsp__pcsamp_warps_issue_stalled_"]) if not name.endswith("not_issued")]
+    tot = [sum(float(v[i] or 0) for _, v in st) or 1.0 for i in range(len(st[0][1]))] if st else []
+    for name, vals in sorted(st, key=lambda x: -float(x[1][0] or 0))[:10]:
+        print(f"   {name:28s}", " ".join(f"{100 * float(v or 0) / t:5.1f}%" for v, t in zip(vals, tot)))
