@@ -188,7 +188,11 @@ __device__ __forceinline__ uint8_t slack_code(double D, double sref) {
   return static_cast<uint8_t>(e);
 }
 __device__ __forceinline__ double slack_value(uint8_t c, double sref) {
-  return ldexp(sref, static_cast<int>(c) - 128);
+  // sref * 2^(c - 128): the power of two is built from its bits (c - 128 is in
+  // [-127, 127], always a normal double) — exact, like ldexp, without its
+  // range handling
+  const double p2 = __longlong_as_double(static_cast<long long>(static_cast<int>(c) - 128 + 1023) << 52);
+  return sref * p2;
 }
 __device__ __forceinline__ void slack_max(uint8_t* dlt, int e, uint8_t c) {
   unsigned* w = reinterpret_cast<unsigned*>(dlt + (e & ~3));
@@ -413,7 +417,10 @@ __global__ void __launch_bounds__(ct_threads(DY)) ct_pass_kernel(CtPass p) {
     PH(2);  // chunk hulls
     // ---- 2. tree merge by bridge walks ----------------------------------
     for (int lvl = 1; lvl < tpl; lvl <<= 1) {
-      group_sync(tpl, l);
+      // a level-lvl merge reads chunks [t, t + 2 lvl): inside one warp up to
+      // lvl = 16 (tpl is a multiple of 32)
+      if (2 * lvl <= 32) __syncwarp();
+      else group_sync(tpl, l);
       if (active && (t % (2 * lvl)) == 0 && t + lvl < tpl) {
         const int gA = t, gB = t + lvl, gE = min(t + 2 * lvl, tpl);
         int ca = gB - 1;
