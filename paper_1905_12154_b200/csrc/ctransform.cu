@@ -635,25 +635,72 @@ __global__ void __launch_bounds__(ct_threads(DY)) ct_pass_kernel(CtPass p) {
   }
   group_sync(tpl, l);
   PH(7);  // certification
-  // ---- 5c. flagged queries: full resolution from their tangent corner
-  if (active) {
-    auto Fhat = [&](int idx, double xk) { return P_f(idx) - xk * P_y(idx); };
-    // exact value V(k, j) rounded down (last pass)
-    auto rd_value = [&](int j, int k, double xk) {
-      if (DY) {
-        double G, ph;
-        dy_parts(j, G, ph);
-        const double dl = xk - coord(h, j);
-        return bfmx::round_down2(G + 0.5 * dl * dl, -ph);
-      } else {
-        double tv[12];
-        const uint32_t ch = p.a > 0 ? s.chain[j] : 0u;
-        const int m = cand_terms(p, geo, ch, j, k, tv);
-        return bfmx::round_down_sum(tv, m);
-      }
+  // ---- 5c. flagged queries: full resolution from their tangent corner. The
+  //          lists of all the CTA's lines are shared by all its threads, so a
+  //          line with many flagged queries does not hold its CTA alone.
+  // (sharing pays off with many short lines per CTA; with few long lines
+  // each line keeps its own list)
+  const bool share = lpc >= 4;
+  if (share) __syncthreads();
+  else group_sync(tpl, l);
+  {
+    auto nflagged = [&](int q) {
+      return static_cast<int>(*reinterpret_cast<const unsigned*>(&carve(p, smem, q).scal[5]));
     };
-    const int nfl = static_cast<int>(*reinterpret_cast<const unsigned*>(&s.scal[5]));
-    for (int fi = t; fi < nfl; fi += tpl) {
+    int total = 0;
+    if (share)
+      for (int q = 0; q < lpc; ++q) total += nflagged(q);
+    else
+      total = nflagged(l);
+    const int first = share ? static_cast<int>(threadIdx.x) : t;
+    const int stride = share ? static_cast<int>(blockDim.x) : tpl;
+    for (int gi = first; gi < total; gi += stride) {
+      int lq = share ? 0 : l, fi = gi;
+      while (share) {
+        const int c = nflagged(lq);
+        if (fi < c) break;
+        fi -= c;
+        ++lq;
+      }
+      // the query's line: its shared memory and constants (as computed above
+      // by that line's own threads)
+      const Smem s = carve(p, smem, lq);
+      const LineGeo geo = *s.geo;
+      const double Aabs = bitsd(s.scal[0]);
+      const double Smax = bitsd(s.scal[1]);
+      const double e_f = DY ? kU * Aabs : 8.0 * kU * Smax;
+      const double e_r = 4.0 * kU * (Aabs + 1.0);
+      const double Mc = 4.0 * (e_f + e_r);
+      const double sref = fmax(Smax, 1e-300);
+      const bool convex_line = s.scal[4] == 0ull;
+      const int hsz = convex_line ? n : static_cast<int>(s.scal[3]);
+      const double Mw = Mc + (convex_line ? 0.0 : bitsd(s.scal[2]));
+      uint16_t* res = s.hidx;
+      auto P_f = [&](int idx) { return s.fh[padj(idx)]; };
+      auto HH = [&](int i) { return convex_line ? i : static_cast<int>(s.H[i]); };
+      auto Fhat = [&](int idx, double xk) { return P_f(idx) - xk * P_y(idx); };
+      auto dy_parts = [&](int j, double& G, double& ph) {
+        uint32_t ch = 0u;
+        if (p.a > 0) ch = p.state_in[geo.base + static_cast<long>(j) * A.stride];
+        G = 0.0;
+        if (p.a >= 1) G += g_approx(p.ax[0], geo.k[0], static_cast<int>(ch & 0xFFFFu));
+        if (p.a >= 2) G += g_approx(p.ax[1], geo.k[1], static_cast<int>(ch >> 16));
+        ph = p.phi[phi_index(p, geo, ch, j)];
+      };
+      // exact value V(k, j) rounded down (last pass)
+      auto rd_value = [&](int j, int k, double xk) {
+        if (DY) {
+          double G, ph;
+          dy_parts(j, G, ph);
+          const double dl = xk - coord(h, j);
+          return bfmx::round_down2(G + 0.5 * dl * dl, -ph);
+        } else {
+          double tv[12];
+          const uint32_t ch = p.a > 0 ? s.chain[j] : 0u;
+          const int m = cand_terms(p, geo, ch, j, k, tv);
+          return bfmx::round_down_sum(tv, m);
+        }
+      };
       const int k = s.flist[fi];
       const int rv = res[k];
       const int i = rv & 0x7fff;
@@ -763,8 +810,9 @@ __global__ void __launch_bounds__(ct_threads(DY)) ct_pass_kernel(CtPass p) {
       }
     }
   }
+  if (share) __syncthreads();
+  else group_sync(tpl, l);
   PH(8);  // flagged queries
-  if (p.last) group_sync(tpl, l);  // flagged queries were resolved by any thread of the line
   if (p.last && active) {
     // lone queries: final round-downs, batched so the L2 loads overlap
     constexpr int kB = 8;
