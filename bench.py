@@ -184,6 +184,31 @@ def cpu_baseline(mu, nu, desc):
                 "sample": f"failed: {e}"}
 
 
+def live_roofline(ops, shape, hbm, hbm_kind):
+    """The dominant kernel (the c-transform, d axis-pass launches per call)
+    timed live in the timed region: CUDA events on the solver stream around
+    every c-transform call of the K steps. Algorithmic bytes 16*d per node
+    per call; traffic = ncu DRAM bytes of one call inside the
+    same C3 iteration (profiles/ctransform_dram_bytes.json)."""
+    d = len(shape)
+    N = int(np.prod(shape))
+    ms_total, calls = ops["ctransform"]
+    ms = ms_total / max(calls, 1)
+    bytes_alg = 16.0 * d * N
+    achieved = bytes_alg / (ms * 1e-3) / 1e9
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "ctransform_dram_bytes.json")
+    if os.path.exists(prof):
+        try:
+            traffic = json.load(open(prof)).get("x".join(map(str, shape)) + "_iteration")
+        except Exception:
+            traffic = None
+    return {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+            "frac": achieved / hbm, "traffic": traffic,
+            "kernel": f"c-transform ({d} ct_pass_kernel launches per call), {calls} calls in the timed region",
+            "ms_per_call": ms, "algorithmic_bytes_per_call": bytes_alg, "peak_kind": hbm_kind}
+
+
 def ctransform_roofline(lib, shape, torch, hbm, hbm_kind, reps=10):
     """Times the c-transform operator (d kernel launches, one per axis pass)
     on resident data with CUDA events on its launch stream; L2 flushed
@@ -351,9 +376,12 @@ def ours(args):
         dist.barrier()
     torch.cuda.synchronize()
     clocks.start()
+    s.set_timing(True)  # per-operator CUDA events on the solver stream (live roofline)
     ms = s.time_steps(args.steps)
     torch.cuda.synchronize()
     ck = clocks.stop()
+    ops = s.op_times()
+    s.set_timing(False)
     launches = s.launches() - l0
     t = torch.tensor([ms], dtype=torch.float64, device="cuda")
     if dist:
@@ -386,7 +414,8 @@ def ours(args):
         return
     hbm, hbm_kind = peaks()
     lib = bfm.load_library()
-    roof = ctransform_roofline(lib, desc["grid"], torch, hbm, hbm_kind)
+    roof = live_roofline(ops, desc["grid"], hbm, hbm_kind)
+    roof["c5_operator"] = ctransform_roofline(lib, desc["grid"], torch, hbm, hbm_kind)
     cpu = cpu_baseline(mu, nu, desc) if world == 1 and not args.no_cpu_baseline else None
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -398,6 +427,7 @@ def ours(args):
         "gpu_launches": int(launches),
         "clocks": ck,
         "roofline": roof,
+        "op_breakdown_ms_per_step": {k: v[0] / args.steps for k, v in ops.items()},
         "cpu_baseline": cpu,
         "e2e": e2e,
     }

@@ -234,6 +234,15 @@ long bfm_solver_launches(const bfm_solver* s);
  * solver's stream; *ms receives the device-timed duration. */
 int bfm_solver_time_steps(bfm_solver* s, int k, double* ms);
 
+/* Bench helper: per-operator device time (CUDA events on the solver stream
+ * around each operator call) accumulated while timing is on; switching it
+ * (on or off) resets the totals. ms[op] / calls[op] for op in
+ * BFM_OP_CTRANSFORM .. BFM_OP_REDUCE (reduce = pair values, gn, axpy). */
+enum { BFM_OP_CTRANSFORM = 0, BFM_OP_PUSHFORWARD = 1, BFM_OP_POISSON = 2, BFM_OP_REDUCE = 3,
+       BFM_OP_COUNT = 4 };
+int bfm_solver_set_timing(bfm_solver* s, int on);
+int bfm_solver_op_times(bfm_solver* s, double* ms, long* calls);
+
 /* Test hook: c-transform diagnostic counters (needs env BFM_CT_STATS=1). */
 int bfm_debug_ct_stats(bfm_solver* s, unsigned long long* out8);
 /* Test hook: device evaluation of the exact round-down of `count` sums of m

@@ -191,6 +191,10 @@ def load_library(path: str = LIB_PATH):
     lib.bfm_solver_launches.restype = C.c_long
     lib.bfm_solver_time_steps.argtypes = [C.c_void_p, C.c_int, C.c_void_p]
     lib.bfm_solver_time_steps.restype = C.c_int
+    lib.bfm_solver_set_timing.argtypes = [C.c_void_p, C.c_int]
+    lib.bfm_solver_set_timing.restype = C.c_int
+    lib.bfm_solver_op_times.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
+    lib.bfm_solver_op_times.restype = C.c_int
     lib.bfm_set_device.argtypes = [C.c_int]
     lib.bfm_set_device.restype = C.c_int
     _lib = lib
@@ -395,6 +399,19 @@ class Solver:
 
     def launches(self) -> int:
         return int(self._lib.bfm_solver_launches(self._h))
+
+    OPS = ("ctransform", "pushforward", "poisson", "reduce")
+
+    def set_timing(self, on: bool) -> None:
+        """Per-operator CUDA-event timing on the solver stream (resets totals)."""
+        self._check(self._lib.bfm_solver_set_timing(self._h, 1 if on else 0))
+
+    def op_times(self) -> dict:
+        """{op: (total ms, calls)} accumulated since set_timing(True)."""
+        ms = (C.c_double * 4)()
+        n = (C.c_long * 4)()
+        self._check(self._lib.bfm_solver_op_times(self._h, ms, n))
+        return {name: (ms[i], n[i]) for i, name in enumerate(self.OPS)}
 
     def time_steps(self, k: int) -> float:
         """Runs k iterations between CUDA events on the solver stream; returns ms."""

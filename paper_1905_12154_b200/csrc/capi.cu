@@ -334,7 +334,59 @@ struct bfm_solver {
   std::vector<bfm_iteration_stats> trace;
   std::chrono::steady_clock::time_point start;
 
+  // Optional per-operator device timing (bench.py's live roofline): events
+  // recorded on the solver stream around each operator, resolved lazily.
+  bool timing = false;
+  struct Pending {
+    cudaEvent_t a, b;
+    int op;
+  };
+  std::vector<Pending> pending;
+  std::vector<cudaEvent_t> free_events;
+  double op_ms[BFM_OP_COUNT] = {};
+  long op_n[BFM_OP_COUNT] = {};
+
+  cudaEvent_t take_event() {
+    if (free_events.empty()) {
+      cudaEvent_t e;
+      BFM_CUDA(cudaEventCreate(&e));
+      return e;
+    }
+    cudaEvent_t e = free_events.back();
+    free_events.pop_back();
+    return e;
+  }
+  template <class F>
+  void timed(int op, F&& f) {
+    if (!timing) {
+      f();
+      return;
+    }
+    cudaEvent_t a = take_event(), b = take_event();
+    BFM_CUDA(cudaEventRecord(a, stream));
+    f();
+    BFM_CUDA(cudaEventRecord(b, stream));
+    pending.push_back({a, b, op});
+  }
+  void resolve_times() {
+    for (const Pending& q : pending) {
+      BFM_CUDA(cudaEventSynchronize(q.b));
+      float ms = 0.0f;
+      BFM_CUDA(cudaEventElapsedTime(&ms, q.a, q.b));
+      op_ms[q.op] += ms;
+      op_n[q.op] += 1;
+      free_events.push_back(q.a);
+      free_events.push_back(q.b);
+    }
+    pending.clear();
+  }
+
   ~bfm_solver() {
+    for (const Pending& q : pending) {
+      cudaEventDestroy(q.a);
+      cudaEventDestroy(q.b);
+    }
+    for (cudaEvent_t e : free_events) cudaEventDestroy(e);
     if (stream) cudaStreamDestroy(stream);
   }
 
@@ -345,16 +397,23 @@ struct bfm_solver {
   }
 
   void pair_value_async() {  // solver.hpp:240
-    ws.redp().dot(phi.p, nu.p, psi.p, mu.p, g.size, g.vol, kSlotPair, stream, &ws.lc);
+    timed(BFM_OP_REDUCE, [&] {
+      ws.redp().dot(phi.p, nu.p, psi.p, mu.p, g.size, g.vol, kSlotPair, stream, &ws.lc);
+    });
   }
-  void ctransform(const double* in, double* out) { ws.ctp().run(in, out, stream, &ws.lc); }
+  void ctransform(const double* in, double* out) {
+    timed(BFM_OP_CTRANSFORM, [&] { ws.ctp().run(in, out, stream, &ws.lc); });
+  }
 
   // solver.hpp:245-260 (result left in d_dir, gn in kSlotGn)
   void ascent_direction_async(const double* u, const double* source, const double* target,
                               double* d_dir) {
-    ws.pfp().from_potential(u, source, target, r.p, nullptr, stream, &ws.lc);
-    ws.poisp().solve(r.p, d_dir, stream, &ws.lc);
-    ws.redp().dot(r.p, d_dir, nullptr, nullptr, g.size, g.vol, kSlotGn, stream, &ws.lc);
+    timed(BFM_OP_PUSHFORWARD,
+          [&] { ws.pfp().from_potential(u, source, target, r.p, nullptr, stream, &ws.lc); });
+    timed(BFM_OP_POISSON, [&] { ws.poisp().solve(r.p, d_dir, stream, &ws.lc); });
+    timed(BFM_OP_REDUCE, [&] {
+      ws.redp().dot(r.p, d_dir, nullptr, nullptr, g.size, g.vol, kSlotGn, stream, &ws.lc);
+    });
   }
 
   void ensure_probe() {  // solver.hpp:264-280
@@ -379,7 +438,7 @@ struct bfm_solver {
     const double v2 = probe_dual;
     st.sigma_first = sigma;
     st.grad_norm_sq_first = probe_gn;
-    axpy(phi.p, sigma, dir.p, g.size, stream, &ws.lc);
+    timed(BFM_OP_REDUCE, [&] { axpy(phi.p, sigma, dir.p, g.size, stream, &ws.lc); });
     ctransform(phi.p, psi.p);
     pair_value_async();
     const double v3 = fetch1(kSlotPair);
@@ -395,7 +454,7 @@ struct bfm_solver {
     const double gn2 = fetch1(kSlotGn);
     st.sigma_second = sigma;
     st.grad_norm_sq_second = gn2;
-    axpy(psi.p, sigma, dir2.p, g.size, stream, &ws.lc);
+    timed(BFM_OP_REDUCE, [&] { axpy(psi.p, sigma, dir2.p, g.size, stream, &ws.lc); });
     ctransform(psi.p, phi.p);
     pair_value_async();
     const double v5 = fetch1(kSlotPair);
@@ -409,7 +468,7 @@ struct bfm_solver {
     const double v1 = probe_dual;
     st.sigma_first = sigma;
     st.grad_norm_sq_first = probe_gn;
-    axpy(phi.p, sigma, dir.p, g.size, stream, &ws.lc);
+    timed(BFM_OP_REDUCE, [&] { axpy(phi.p, sigma, dir.p, g.size, stream, &ws.lc); });
     ctransform(phi.p, psi.p);
     pair_value_async();
     const double v2 = fetch1(kSlotPair);
@@ -977,6 +1036,27 @@ long bfm_solver_launches(const bfm_solver* s) { return s->ws.lc.count; }
 
 int bfm_debug_ct_stats(bfm_solver* s, unsigned long long* out8) {
   return guard([&] { s->ws.ctp().stats(out8); });
+}
+
+int bfm_solver_set_timing(bfm_solver* s, int on) {
+  return guard([&] {
+    s->resolve_times();
+    s->timing = on != 0;
+    for (int i = 0; i < BFM_OP_COUNT; ++i) {
+      s->op_ms[i] = 0.0;
+      s->op_n[i] = 0;
+    }
+  });
+}
+
+int bfm_solver_op_times(bfm_solver* s, double* ms, long* calls) {
+  return guard([&] {
+    s->resolve_times();
+    for (int i = 0; i < BFM_OP_COUNT; ++i) {
+      ms[i] = s->op_ms[i];
+      calls[i] = s->op_n[i];
+    }
+  });
 }
 
 int bfm_solver_time_steps(bfm_solver* s, int k, double* ms) {

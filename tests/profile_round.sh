@@ -20,3 +20,6 @@ python tests/prof_c3.py c4 2 > /dev/null 2>&1 && \
   ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/prof/launches_c4.csv python tests/prof_c3.py c4 2 > /dev/null 2>&1
 python tests/prof_c3.py c3 1 > /dev/null 2>&1 && \
   ncu --set full --clock-control none --import-source on -k regex:pois_fft -s 3 -c 1 -o gpurun_out/prof/pois_full python tests/prof_c3.py c3 1 > /dev/null 2>&1
+python tests/prof_c3.py c3 2 > /dev/null 2>&1 && \
+  ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --clock-control none -k regex:ct_pass -s 4 -c 2 \
+      --csv --log-file gpurun_out/prof/ct_iter_dram.csv python tests/prof_c3.py c3 2 > /dev/null 2>&1
