@@ -32,11 +32,19 @@ __device__ __forceinline__ long long fold_sat(long long v) {
   return v > kSat ? kSat : v;
 }
 
-// a then b
+// a then b. Element increments are clamped to 2^54, so up to 256 composed
+// elements stay below 2^62 without saturation (per-thread and warp scans);
+// the cross-warp combination saturates.
 __device__ __forceinline__ FoldTr fold_compose(FoldTr a, FoldTr b) {
   FoldTr r;
-  r.i0 = fold_sat(a.i0 + ((a.i0 & 1) ? b.i1 : b.i0));
-  r.i1 = fold_sat(a.i1 + (((1 + a.i1) & 1) ? b.i1 : b.i0));
+  r.i0 = a.i0 + ((a.i0 & 1) ? b.i1 : b.i0);
+  r.i1 = a.i1 + (((1 + a.i1) & 1) ? b.i1 : b.i0);
+  return r;
+}
+__device__ __forceinline__ FoldTr fold_compose_sat(FoldTr a, FoldTr b) {
+  FoldTr r = fold_compose(a, b);
+  r.i0 = fold_sat(r.i0);
+  r.i1 = fold_sat(r.i1);
   return r;
 }
 
@@ -47,7 +55,10 @@ __device__ __forceinline__ long long fold_apply(FoldTr t, long long M) {
 // Transducer of one weight w >= 0 at binade exponent e (rho in [2^e, 2^(e+1))).
 // a is returned separately (clamped to 2^54) for the crossing test.
 __device__ __forceinline__ FoldTr fold_elem(double w, int e, long long& a_out) {
-  const double x = ldexp(w, 52 - e);  // exact (power-of-two scaling)
+  // w * 2^(52 - e), exact: the power of two is built from its bits (the fold
+  // keeps e in [-960, 1020], so 52 - e is a normal exponent); products that
+  // underflow only occur for w < 2^-1000 relative, far below 1/2 an ulp
+  const double x = w * __longlong_as_double(static_cast<long long>(52 - e + 1023) << 52);
   long long a;
   int cls;  // 0: f < 1/2, 1: f == 1/2, 2: f > 1/2
   if (!(x >= 0.0 && x < 18014398509481984.0)) {  // >= 2^54, negative or NaN: a crossing
@@ -73,6 +84,7 @@ __device__ __forceinline__ FoldTr fold_elem(double w, int e, long long& a_out) {
 // NT must be a multiple of 32; `bar` synchronises the group.
 template <int NT, int ITEMS, class Sync>
 __device__ double exact_fold(const double* w, int K, FoldTr* scratch, int* iscr, Sync bar) {
+  static_assert(32 * ITEMS <= 256, "unsaturated per-warp composition range");
   constexpr int kWarps = NT / 32;
   constexpr int kChunk = NT * ITEMS;
   constexpr long long kTop = 1LL << 53;
@@ -114,6 +126,10 @@ __device__ double exact_fold(const double* w, int K, FoldTr* scratch, int* iscr,
     frexp(rho, &e);
     e -= 1;  // rho in [2^e, 2^(e+1))
     const long long M = static_cast<long long>(ldexp(rho, 52 - e));
+    // elements [i0, lim): a binade crossing is likely about when the sum has
+    // doubled, i.e. after ~i0 more elements of similar size, so the span
+    // grows with i0 (restarts then redo little work)
+    const int lim = min(K, i0 + min(kChunk, max(NT, i0)));
     // per-thread transducers of ITEMS consecutive elements
     const int base = i0 + tid * ITEMS;
     FoldTr tr[ITEMS];
@@ -122,7 +138,7 @@ __device__ double exact_fold(const double* w, int K, FoldTr* scratch, int* iscr,
 #pragma unroll
     for (int u = 0; u < ITEMS; ++u) {
       const int j = base + u;
-      if (j < K) {
+      if (j < lim) {
         tr[u] = fold_elem(w[j], e, av[u]);
       } else {
         tr[u] = FoldTr{0, 0};
@@ -146,17 +162,17 @@ __device__ double exact_fold(const double* w, int K, FoldTr* scratch, int* iscr,
     if (lane == 0) excl = FoldTr{0, 0};
     bar();
     FoldTr wpre{0, 0};
-    for (int q = 0; q < warp; ++q) wpre = fold_compose(wpre, scratch[q]);
+    for (int q = 0; q < warp; ++q) wpre = fold_compose_sat(wpre, scratch[q]);
     FoldTr total{0, 0};
-    for (int q = 0; q < kWarps; ++q) total = fold_compose(total, scratch[q]);
-    excl = fold_compose(wpre, excl);
+    for (int q = 0; q < kWarps; ++q) total = fold_compose_sat(total, scratch[q]);
+    excl = fold_compose_sat(wpre, excl);
     // M before each element, and the first element that may leave the binade
     long long Mp = M + fold_apply(excl, M);
     int cross = K;
 #pragma unroll
     for (int u = 0; u < ITEMS; ++u) {
       const int j = base + u;
-      if (j < K && cross == K && Mp + av[u] + 1 >= kTop) cross = j;
+      if (j < lim && cross == K && Mp + av[u] + 1 >= kTop) cross = j;
       if (cross == K) Mp += fold_apply(tr[u], Mp);
     }
     for (int o = 16; o > 0; o >>= 1) cross = min(cross, __shfl_xor_sync(0xffffffffu, cross, o));
@@ -167,7 +183,7 @@ __device__ double exact_fold(const double* w, int K, FoldTr* scratch, int* iscr,
     for (int q = 0; q < kWarps; ++q) jc = min(jc, iscr[q]);
     if (jc == K) {
       rho = ldexp(static_cast<double>(M + fold_apply(total, M)), e - 52);  // exact (< 2^53 u)
-      i0 = min(K, i0 + kChunk);
+      i0 = lim;
     } else {
       // M just before jc: the owner thread publishes it
       const int owner = (jc - i0) / ITEMS;
