@@ -1,7 +1,7 @@
 """Ad-hoc GPU diagnostics (not collected by pytest)."""
 import sys, os
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tests"))
 from fractions import Fraction as F
 import numpy as np
 import oracle_lib as O

@@ -10,16 +10,16 @@ python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/prof/bench_re
 python bench.py --steps 2 --warmup 3 --no-cpu-baseline > /dev/null 2>&1 && \
   ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/prof/launches_bench_c3.csv \
       python bench.py --steps 2 --warmup 3 --no-cpu-baseline > /dev/null 2>&1
-python tests/ct_op_traffic.py > /dev/null 2>&1 && \
+python tools/ct_op_traffic.py > /dev/null 2>&1 && \
   ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --clock-control none -k regex:ct_pass \
-      --csv --log-file gpurun_out/prof/ct_op_dram.csv python tests/ct_op_traffic.py > /dev/null 2>&1
-python tests/prof_c3.py c3 2 > /dev/null 2>&1 && \
-  ncu --set full --clock-control none --import-source on -k regex:ct_pass -s 6 -c 1 -o gpurun_out/prof/ct_full python tests/prof_c3.py c3 2 > /dev/null 2>&1
+      --csv --log-file gpurun_out/prof/ct_op_dram.csv python tools/ct_op_traffic.py > /dev/null 2>&1
+python tools/prof_c3.py c3 2 > /dev/null 2>&1 && \
+  ncu --set full --clock-control none --import-source on -k regex:ct_pass -s 6 -c 1 -o gpurun_out/prof/ct_full python tools/prof_c3.py c3 2 > /dev/null 2>&1
 ls -la gpurun_out/prof
-python tests/prof_c3.py c4 2 > /dev/null 2>&1 && \
-  ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/prof/launches_c4.csv python tests/prof_c3.py c4 2 > /dev/null 2>&1
-python tests/prof_c3.py c3 1 > /dev/null 2>&1 && \
-  ncu --set full --clock-control none --import-source on -k regex:pois_fft -s 3 -c 1 -o gpurun_out/prof/pois_full python tests/prof_c3.py c3 1 > /dev/null 2>&1
-python tests/prof_c3.py c3 2 > /dev/null 2>&1 && \
+python tools/prof_c3.py c4 2 > /dev/null 2>&1 && \
+  ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/prof/launches_c4.csv python tools/prof_c3.py c4 2 > /dev/null 2>&1
+python tools/prof_c3.py c3 1 > /dev/null 2>&1 && \
+  ncu --set full --clock-control none --import-source on -k regex:pois_fft -s 3 -c 1 -o gpurun_out/prof/pois_full python tools/prof_c3.py c3 1 > /dev/null 2>&1
+python tools/prof_c3.py c3 2 > /dev/null 2>&1 && \
   ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --clock-control none -k regex:ct_pass -s 4 -c 2 \
-      --csv --log-file gpurun_out/prof/ct_iter_dram.csv python tests/prof_c3.py c3 2 > /dev/null 2>&1
+      --csv --log-file gpurun_out/prof/ct_iter_dram.csv python tools/prof_c3.py c3 2 > /dev/null 2>&1
