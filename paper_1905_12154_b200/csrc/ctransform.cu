@@ -620,6 +620,10 @@ __global__ void __launch_bounds__(ct_threads(DY)) ct_pass_kernel(CtPass p) {
         if (p.stats) {
           atomicAdd(p.stats + 0, 1ull);
           if (!lone) atomicAdd(p.stats + 1, 1ull);
+          // why: a neighbouring corner within the margin, or an adjacent edge
+          if (!(Fl > F0 + Mw && Fr > F0 + Mw)) atomicAdd(p.stats + 6, 1ull);
+          if (!(Fl > F0 + Mw && Fr > F0 + Mw) && !((Fl > F0 + Mc) && (Fr > F0 + Mc)))
+            atomicAdd(p.stats + 7, 1ull);  // ... even within the corner-only margin Mc
         }
         res[k] = lone ? static_cast<uint16_t>(HH(i)) : static_cast<uint16_t>(i | 0x8000);
       }
