@@ -243,6 +243,9 @@ enum { BFM_OP_CTRANSFORM = 0, BFM_OP_PUSHFORWARD = 1, BFM_OP_POISSON = 2, BFM_OP
 int bfm_solver_set_timing(bfm_solver* s, int on);
 int bfm_solver_op_times(bfm_solver* s, double* ms, long* calls);
 
+/* Diagnostics: targets in the warp / CTA / huge gather tiers of the solver's
+ * last pushforward. */
+int bfm_debug_pf_tiers(bfm_solver* s, int* out3);
 /* Test hook: c-transform diagnostic counters (needs env BFM_CT_STATS=1). */
 int bfm_debug_ct_stats(bfm_solver* s, unsigned long long* out8);
 /* Test hook: device evaluation of the exact round-down of `count` sums of m

@@ -1034,6 +1034,10 @@ int bfm_slab_last_launches(const bfm_slab* s) { return s ? s->last_launches : 0;
 
 long bfm_solver_launches(const bfm_solver* s) { return s->ws.lc.count; }
 
+int bfm_debug_pf_tiers(bfm_solver* s, int* out3) {
+  return guard([&] { s->ws.pfp().tier_counts(out3); });
+}
+
 int bfm_debug_ct_stats(bfm_solver* s, unsigned long long* out8) {
   return guard([&] { s->ws.ctp().stats(out8); });
 }

@@ -43,6 +43,14 @@ class PushforwardPlan {
               const uint8_t* d_cmask, const double* d_target, double* d_out, cudaStream_t stream,
               LaunchCounter* lc);
   long num_cells() const { return ncells_; }
+  // diagnostics: targets in the warp / CTA / huge tiers of the last gather
+  void tier_counts(int* out3) const {
+    int v[6] = {};
+    BFM_CUDA(cudaMemcpy(v, nheavy_, sizeof(v), cudaMemcpyDeviceToHost));
+    out3[0] = v[0];
+    out3[1] = v[4];
+    out3[2] = v[1];
+  }
   // Multi-GPU routing of this slab's deposit records (map_records output) to
   // the owners of the target rows they reach: row_starts[0..P] partition
   // axis 0. packed receives, per destination in rank order and within it in
