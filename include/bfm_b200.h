@@ -173,6 +173,13 @@ int bfm_workspace_last_launches(const bfm_workspace* ws);
  * columns [col0, col0+ncols) of the n1*n2 non-axis-0 index. All pointers are
  * device pointers; `stream` is a cudaStream_t. Results equal the single-GPU
  * operators bit for bit once the exchanges in dist.py are applied. */
+/* Host-only fixtures of the paper-case harness (benchmark.hpp:27-43):
+ * indicator of a '+'-union of builtin shapes "disc:x,y,r", "ball:x,y,z,r",
+ * "square:x,y,side", "cube:x,y,z,side" (io.hpp:360-476, not normalised), and
+ * normalisation to unit mass with the Kahan mass of grid.hpp:151-164. */
+int bfm_builtin_density(int dim, const int* extents, const char* spec, double* out);
+int bfm_normalize(int dim, const int* extents, const double* raw, double* out);
+
 typedef struct bfm_slab bfm_slab;
 /* Host-only: the validation of bfm_solver_create (solver.hpp:105-142,148-167)
  * without creating a solver (every rank of the multi-GPU driver runs it). */

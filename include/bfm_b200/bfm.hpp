@@ -258,6 +258,13 @@ inline DensityField normalize(const Grid& grid, const std::vector<double>& raw) 
   return out;
 }
 
+// io.hpp:452-476: indicator of a '+'-union of builtin shapes (not normalised)
+inline DensityField builtin_density(const Grid& g, const std::string& spec) {
+  DensityField f(g);
+  detail::check(bfm_builtin_density(g.dim(), g.extents_ptr(), spec.c_str(), f.values.data()));
+  return f;
+}
+
 // poisson.hpp:40-113
 class SpectralPlan {
  public:

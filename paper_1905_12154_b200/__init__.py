@@ -195,6 +195,10 @@ def load_library(path: str = LIB_PATH):
     lib.bfm_solver_set_timing.restype = C.c_int
     lib.bfm_solver_op_times.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
     lib.bfm_solver_op_times.restype = C.c_int
+    lib.bfm_builtin_density.argtypes = [C.c_int, C.c_void_p, C.c_char_p, C.c_void_p]
+    lib.bfm_builtin_density.restype = C.c_int
+    lib.bfm_normalize.argtypes = [C.c_int, C.c_void_p, C.c_void_p, C.c_void_p]
+    lib.bfm_normalize.restype = C.c_int
     lib.bfm_set_device.argtypes = [C.c_int]
     lib.bfm_set_device.restype = C.c_int
     _lib = lib
@@ -515,20 +519,20 @@ def axis_coords(n: int) -> np.ndarray:
 
 
 def normalize(raw) -> np.ndarray:
-    """grid.hpp:151-164 (Kahan mass, then raw / mass)."""
+    """grid.hpp:151-164: raw / (Kahan sum * cell volume), the reference's own
+    summation order (host)."""
+    lib = load_library()
     raw = _f64(raw)
-    if np.any(raw < 0.0):
-        raise NegativeInput("normalize: negative density sample")
-    vol = 1.0
-    for n in raw.shape:
-        vol *= 1.0 / n
-    s = 0.0
-    c = 0.0
-    flat = raw.ravel()
-    # Kahan in numpy chunks would reorder; use math.fsum-equivalent accuracy
-    # then match the reference's definition of mass = sum * cell_volume.
-    s = math.fsum(flat.tolist()) if flat.size <= 1 << 22 else float(np.sum(flat, dtype=np.float64))
-    mass = s * vol
-    if mass <= 0.0:
-        raise AllZeroInput("normalize: density has zero total mass")
-    return raw / mass
+    out = np.empty_like(raw)
+    _check(lib, lib.bfm_normalize(raw.ndim, _extents(raw.shape), _ptr(raw), _ptr(out)))
+    return out
+
+
+def builtin_density(shape: Sequence[int], spec: str) -> np.ndarray:
+    """io.hpp:452-476: indicator of a '+'-union of builtin shapes
+    ("disc:x,y,r", "ball:x,y,z,r", "square:x,y,side", "cube:x,y,z,side") at the
+    cell centres; not normalised."""
+    lib = load_library()
+    out = np.empty(tuple(int(n) for n in shape), dtype=np.float64)
+    _check(lib, lib.bfm_builtin_density(len(shape), _extents(shape), spec.encode(), _ptr(out)))
+    return out

@@ -6,6 +6,7 @@
 // rule, dual-monotonicity checks and gauge fix. All field work runs on the
 // device through CtPlan / PushforwardPlan / PoissonPlan / Reducer; only
 // scalars cross to the host (one synchronising read per half step).
+#include <cctype>
 #include <chrono>
 #include <cmath>
 #include <cstring>
@@ -882,6 +883,122 @@ int bfm_solve_neumann_device(bfm_workspace* ws, const double* d_rhs, double* d_o
 int bfm_workspace_last_launches(const bfm_workspace* ws) { return ws->last_launches; }
 
 // ---- multi-GPU slabs -------------------------------------------------------
+// ---- fixtures of the paper-case harness (host only) --------------------------
+namespace {
+struct Shape {  // io.hpp builtin shapes: disc / ball (Euclidean), square / cube
+  bool euclid = true;
+  int dim = 2;
+  double c[3] = {0.0, 0.0, 0.0};
+  double r = 0.0;
+};
+
+double spec_number(const std::string& tok, const std::string& shape) {
+  try {
+    size_t pos = 0;
+    const double v = std::stod(tok, &pos);
+    if (pos != tok.size()) throw std::invalid_argument("");
+    return v;
+  } catch (const std::exception&) {
+    fail(BFM_ERR_INVALID_ARGUMENT, "builtin: malformed number '" + tok + "' in '" + shape + "'");
+  }
+}
+
+Shape parse_shape(const std::string& tok) {
+  const size_t colon = tok.find(':');
+  const std::string name = tok.substr(0, colon);
+  Shape s;
+  if (name == "disc") { s.euclid = true; s.dim = 2; }
+  else if (name == "ball") { s.euclid = true; s.dim = 3; }
+  else if (name == "square") { s.euclid = false; s.dim = 2; }
+  else if (name == "cube") { s.euclid = false; s.dim = 3; }
+  else fail(BFM_ERR_INVALID_ARGUMENT, "builtin: unknown shape '" + name + "'");
+  std::vector<double> prm;
+  if (colon != std::string::npos) {
+    std::string rest = tok.substr(colon + 1);
+    size_t b = 0;
+    while (true) {
+      const size_t e = rest.find(',', b);
+      prm.push_back(spec_number(rest.substr(b, e == std::string::npos ? std::string::npos : e - b), tok));
+      if (e == std::string::npos) break;
+      b = e + 1;
+    }
+  }
+  if (static_cast<int>(prm.size()) != s.dim + 1)
+    fail(BFM_ERR_INVALID_ARGUMENT, "builtin: '" + name + "' takes " + std::to_string(s.dim + 1) +
+                                       " parameters");
+  for (int a = 0; a < s.dim; ++a) s.c[a] = prm[a];
+  const double extent = prm.back();
+  if (!(extent > 0.0)) fail(BFM_ERR_INVALID_ARGUMENT, "builtin: '" + name + "' needs a positive size");
+  s.r = s.euclid ? extent : 0.5 * extent;
+  return s;
+}
+
+bool shape_contains(const Shape& s, const double* x) {
+  if (s.euclid) {
+    double d2 = 0.0;
+    for (int a = 0; a < s.dim; ++a) {
+      const double d = x[a] - s.c[a];
+      d2 += d * d;
+    }
+    return d2 <= s.r * s.r;
+  }
+  for (int a = 0; a < s.dim; ++a)
+    if (std::abs(x[a] - s.c[a]) > s.r) return false;
+  return true;
+}
+}  // namespace
+
+int bfm_builtin_density(int dim, const int* extents, const char* spec, double* out) {
+  return guard([&] {
+    const GridDesc g = checked_grid(dim, extents);
+    const std::string sp = spec ? spec : "";
+    if (sp.empty()) fail(BFM_ERR_INVALID_ARGUMENT, "builtin: empty spec");
+    // '+' separates shapes only when a shape name follows (keeps 1e+2 intact)
+    std::vector<Shape> shapes;
+    size_t start = 0;
+    for (size_t i = 0; i <= sp.size(); ++i) {
+      const bool cut = i == sp.size() ||
+                       (sp[i] == '+' && i + 1 < sp.size() && std::isalpha(static_cast<unsigned char>(sp[i + 1])));
+      if (!cut) continue;
+      const std::string tok = sp.substr(start, i - start);
+      if (tok.empty()) fail(BFM_ERR_INVALID_ARGUMENT, "builtin: empty union member");
+      shapes.push_back(parse_shape(tok));
+      if (shapes.back().dim != dim)
+        fail(BFM_ERR_INVALID_ARGUMENT, "builtin: shape dimension does not match the grid");
+      start = i + 1;
+    }
+    const int n0 = g.n[0], n1 = dim > 1 ? g.n[1] : 1, n2 = dim > 2 ? g.n[2] : 1;
+    long lin = 0;
+    for (int i0 = 0; i0 < n0; ++i0)
+      for (int i1 = 0; i1 < n1; ++i1)
+        for (int i2 = 0; i2 < n2; ++i2, ++lin) {
+          const double x[3] = {coord(g.h[0], i0), dim > 1 ? coord(g.h[1], i1) : 0.0,
+                               dim > 2 ? coord(g.h[2], i2) : 0.0};
+          double v = 0.0;
+          for (const Shape& sh : shapes)
+            if (shape_contains(sh, x)) {
+              v = 1.0;
+              break;
+            }
+          out[lin] = v;
+        }
+  });
+}
+
+int bfm_normalize(int dim, const int* extents, const double* raw, double* out) {
+  return guard([&] {
+    const GridDesc g = checked_grid(dim, extents);
+    Kahan k;  // grid.hpp:151-164
+    for (long i = 0; i < g.size; ++i) {
+      if (raw[i] < 0.0) fail(BFM_ERR_NEGATIVE_INPUT, "normalize: negative density sample");
+      k.add(raw[i]);
+    }
+    const double mass = k.sum * g.vol;
+    if (mass <= 0.0) fail(BFM_ERR_ALL_ZERO_INPUT, "normalize: density has zero total mass");
+    for (long i = 0; i < g.size; ++i) out[i] = raw[i] / mass;
+  });
+}
+
 int bfm_validate_inputs(int dim, const int* extents, const double* mu, const double* nu,
                         const bfm_config* cfg) {
   return guard([&] {

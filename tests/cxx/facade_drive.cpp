@@ -51,6 +51,24 @@ int main() {
     report(std::fabs(integrate(rep.phi)) <= 1e-12, "report potentials are gauge fixed");
   }
   {
+    // benchmark.hpp:27-43,84-124: a paper case from the builtin shapes
+    Grid g({128, 128});
+    DensityField mu = normalize(g, builtin_density(g, "square:0.5,0.5,0.25").values);
+    DensityField nu = normalize(
+        g, builtin_density(g, "square:0.1875,0.1875,0.125+square:0.8125,0.1875,0.125+"
+                              "square:0.1875,0.8125,0.125+square:0.8125,0.8125,0.125")
+               .values);
+    SolverConfig c;
+    c.tolerance = -1.0;
+    c.exact_cost = 0.0625;
+    c.exact_tolerance = 1e-4;
+    c.max_iterations = 1000;
+    SolveReport rep = solve(CostModel::quadratic(2), mu, nu, c);
+    report(rep.termination == Termination::cost_target_met && rep.iterations >= 1 &&
+               rep.iterations <= 5,
+           "four_squares reaches the exact cost 1/16 within 3+-2 iterations (benchmark.hpp:56-63)");
+  }
+  {
     Grid g({32, 32});
     DensityField mu = disc(g, 0.5, 0.5, 0.2);
     SolveReport rep = solve(CostModel::quadratic(2), mu, mu, SolverConfig{});

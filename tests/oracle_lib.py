@@ -216,3 +216,11 @@ def bits(a):
 
 def n_bit_diff(a, b):
     return int(np.count_nonzero(bits(a) != bits(b)))
+
+
+def ref_normalize(raw):
+    lib = ref_lib()
+    raw = np.ascontiguousarray(raw, dtype=np.float64)
+    out = np.empty_like(raw)
+    _chk(lib, lib.ref_normalize(raw.ndim, _ext(raw.shape), _p(raw), _p(out)), "ref_")
+    return out
