@@ -132,6 +132,12 @@ int bfm_solver_report_field(bfm_solver* s, int which, double* host_out);
 /* transforms.hpp:396-432 ctransform (quadratic cost, exactly rounded). */
 int bfm_ctransform(int dim, const int* extents, const double* phi, double* out);
 /* pushforward.hpp:70-91 map_from_conjugate: disp is d*N (SoA, axis-major). */
+/* ctransform for a CostModel::power(exponents) (cost.hpp:24-48; p_a > 1 per
+ * axis): the generic path of transforms.hpp:335-427 (all p_a == 2 is the
+ * quadratic model and takes the same shortcut as bfm_ctransform). Axis
+ * extents up to 2048 for p != 2. */
+int bfm_ctransform_cost(int dim, const int* extents, const double* exponents, const double* phi,
+                        double* out);
 int bfm_map_from_conjugate(int dim, const int* extents, const double* u, int side,
                            double* disp);
 /* pushforward.hpp:176-178 pushforward_density (disp d*N, mu N -> rho N). */

@@ -200,6 +200,52 @@ int ref_ctransform(int dim, const int* ext, const double* phi, double* out, int 
   })
 }
 
+// Power costs c = sum_a |y_a - x_a|^p_a / p_a (cost.hpp:24-31): the generic
+// path of transforms.hpp:396-427 and the pow inverse gradient of cost.hpp:59-68.
+static bfm::CostModel cost_model(int dim, const double* exponents) {
+  if (!exponents) return bfm::CostModel::quadratic(dim);
+  return bfm::CostModel::power(std::vector<double>(exponents, exponents + dim));
+}
+
+int ref_ctransform_cost(int dim, const int* ext, const double* exponents, const double* phi,
+                        double* out, int threads) {
+  GUARD({
+    const bfm::Grid g = make_grid(dim, ext);
+    bfm::Potential p(g);
+    std::memcpy(p.values.data(), phi, g.size() * sizeof(double));
+    bfm::TransformWorkspace ws(g, threads > 0 ? threads : bfm::default_thread_count());
+    const bfm::Potential r = bfm::ctransform(cost_model(dim, exponents), p, ws);
+    std::memcpy(out, r.values.data(), g.size() * sizeof(double));
+  })
+}
+
+int ref_map_from_conjugate_cost(int dim, const int* ext, const double* exponents, const double* u,
+                                int side, double* disp) {
+  GUARD({
+    const bfm::Grid g = make_grid(dim, ext);
+    bfm::Potential p(g);
+    std::memcpy(p.values.data(), u, g.size() * sizeof(double));
+    const bfm::TransportMap m = bfm::map_from_conjugate(
+        cost_model(dim, exponents), p, side == 0 ? bfm::MapSource::mu_side : bfm::MapSource::nu_side);
+    for (int a = 0; a < dim; ++a)
+      std::memcpy(disp + static_cast<size_t>(a) * g.size(), m.displacement[a].data(),
+                  g.size() * sizeof(double));
+  })
+}
+
+int ref_solver_create_cost(int dim, const int* ext, const double* exponents, const double* mu,
+                           const double* nu, const bfm_config* cfg, ref_solver** out) {
+  GUARD({
+    auto s = std::make_unique<ref_solver>();
+    s->grid = make_grid(dim, ext);
+    bfm::DensityField m(s->grid), n(s->grid);
+    std::memcpy(m.values.data(), mu, s->grid.size() * sizeof(double));
+    std::memcpy(n.values.data(), nu, s->grid.size() * sizeof(double));
+    s->solver = std::make_unique<bfm::Solver>(cost_model(dim, exponents), m, n, to_cfg(cfg));
+    *out = s.release();
+  })
+}
+
 int ref_map_from_conjugate(int dim, const int* ext, const double* u, int side, double* disp) {
   GUARD({
     const bfm::Grid g = make_grid(dim, ext);

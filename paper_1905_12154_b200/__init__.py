@@ -195,6 +195,8 @@ def load_library(path: str = LIB_PATH):
     lib.bfm_solver_set_timing.restype = C.c_int
     lib.bfm_solver_op_times.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
     lib.bfm_solver_op_times.restype = C.c_int
+    lib.bfm_ctransform_cost.argtypes = [C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
+    lib.bfm_ctransform_cost.restype = C.c_int
     lib.bfm_builtin_density.argtypes = [C.c_int, C.c_void_p, C.c_char_p, C.c_void_p]
     lib.bfm_builtin_density.restype = C.c_int
     lib.bfm_normalize.argtypes = [C.c_int, C.c_void_p, C.c_void_p, C.c_void_p]
@@ -430,12 +432,19 @@ def solve(mu, nu, config: Optional[SolverConfig] = None) -> SolveReport:
 
 
 # ---------------------------------------------------------------- operators
-def ctransform(phi) -> np.ndarray:
-    """phi^c for the quadratic cost, exactly rounded (transforms.hpp:396-432)."""
+def ctransform(phi, exponents: Optional[Sequence[float]] = None) -> np.ndarray:
+    """phi^c exactly rounded (transforms.hpp:396-432): quadratic cost, or
+    CostModel::power(exponents) (cost.hpp:24-48, p_a > 1 per axis)."""
     lib = load_library()
     phi = _f64(phi)
     out = np.empty_like(phi)
-    _check(lib, lib.bfm_ctransform(phi.ndim, _extents(phi.shape), _ptr(phi), _ptr(out)))
+    if exponents is None:
+        _check(lib, lib.bfm_ctransform(phi.ndim, _extents(phi.shape), _ptr(phi), _ptr(out)))
+    else:
+        ex = (C.c_double * 3)(*([float(e) for e in exponents] + [2.0] * (3 - len(exponents))))
+        if len(exponents) != phi.ndim:
+            raise GridMismatch("ctransform: cost dimension does not match grid")
+        _check(lib, lib.bfm_ctransform_cost(phi.ndim, _extents(phi.shape), ex, _ptr(phi), _ptr(out)))
     return out
 
 

@@ -19,6 +19,7 @@
 #include "../../include/bfm_b200.h"
 #include "common.cuh"
 #include "ctransform.cuh"
+#include "ctransform_power.cuh"
 #include "poisson.cuh"
 #include "pushforward.cuh"
 #include "reduce.cuh"
@@ -754,6 +755,30 @@ int bfm_ctransform(int dim, const int* extents, const double* phi, double* out) 
     double* a = op.up(phi, op.g.size);
     double* b = op.up(nullptr, op.g.size);
     op.ws.ctp().run(a, b, nullptr, &op.ws.lc);
+    op.down(out, b, op.g.size);
+    op.release();
+  });
+}
+
+int bfm_ctransform_cost(int dim, const int* extents, const double* exponents, const double* phi,
+                        double* out) {
+  return guard([&] {
+    HostOp op(dim, extents);
+    bool quadratic = true;
+    for (int a = 0; a < dim; ++a) {
+      if (!exponents || !(exponents[a] > 1.0))
+        fail(BFM_ERR_INVALID_ARGUMENT, "cost exponents must satisfy p > 1");
+      quadratic = quadratic && exponents[a] == 2.0;
+    }
+    double* a = op.up(phi, op.g.size);
+    double* b = op.up(nullptr, op.g.size);
+    if (quadratic) {
+      op.ws.ctp().run(a, b, nullptr, &op.ws.lc);
+    } else {
+      CtPowerPlan plan;
+      plan.init(op.g, exponents);
+      plan.run(a, b, nullptr, &op.ws.lc);
+    }
     op.down(out, b, op.g.size);
     op.release();
   });

@@ -224,3 +224,24 @@ def ref_normalize(raw):
     out = np.empty_like(raw)
     _chk(lib, lib.ref_normalize(raw.ndim, _ext(raw.shape), _p(raw), _p(out)), "ref_")
     return out
+
+
+def ref_ctransform_cost(phi, exponents, threads=0):
+    lib = ref_lib()
+    lib.ref_ctransform_cost.argtypes = [C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int]
+    phi = np.ascontiguousarray(phi, dtype=np.float64)
+    out = np.empty_like(phi)
+    ex = (C.c_double * 3)(*([float(e) for e in exponents] + [2.0] * (3 - len(exponents))))
+    _chk(lib, lib.ref_ctransform_cost(phi.ndim, _ext(phi.shape), ex, _p(phi), _p(out), threads), "ref_")
+    return out
+
+
+def ref_map_from_conjugate_cost(u, exponents, side=0):
+    lib = ref_lib()
+    lib.ref_map_from_conjugate_cost.argtypes = [C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int,
+                                                C.c_void_p]
+    u = np.ascontiguousarray(u, dtype=np.float64)
+    disp = np.empty((u.ndim,) + u.shape)
+    ex = (C.c_double * 3)(*([float(e) for e in exponents] + [2.0] * (3 - len(exponents))))
+    _chk(lib, lib.ref_map_from_conjugate_cost(u.ndim, _ext(u.shape), ex, _p(u), side, _p(disp)), "ref_")
+    return disp
