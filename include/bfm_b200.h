@@ -261,6 +261,7 @@ int bfm_solver_op_times(bfm_solver* s, double* ms, long* calls);
 int bfm_debug_pf_tiers(bfm_solver* s, int* out3);
 /* Test hook: c-transform diagnostic counters (needs env BFM_CT_STATS=1). */
 int bfm_debug_ct_stats(bfm_solver* s, unsigned long long* out8);
+int bfm_debug_ws_ct_stats(bfm_workspace* ws, unsigned long long* out32);
 /* Test hook: device evaluation of the exact round-down of `count` sums of m
  * doubles each (terms row-major). Used by the parity tests only. */
 int bfm_debug_round_down(const double* terms, int m, int count, double* out);

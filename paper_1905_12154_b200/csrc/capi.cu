@@ -1184,6 +1184,10 @@ int bfm_debug_ct_stats(bfm_solver* s, unsigned long long* out8) {
   return guard([&] { s->ws.ctp().stats(out8); });
 }
 
+int bfm_debug_ws_ct_stats(bfm_workspace* ws, unsigned long long* out32) {
+  return guard([&] { ws->ctp().stats(out32); });
+}
+
 int bfm_solver_set_timing(bfm_solver* s, int on) {
   return guard([&] {
     s->resolve_times();

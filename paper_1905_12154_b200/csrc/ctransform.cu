@@ -881,6 +881,656 @@ __global__ void __launch_bounds__(ct_threads(DY)) ct_pass_kernel(CtPass p) {
   }
 }
 
+// ============================================================================
+// Dyadic grids (every n_a a power of two): exact-hull kernel.
+//
+// On a dyadic grid every candidate of pass a is
+//   V(k, j) = s_j - x_k y_j - q_j (+ hs(x_k)),   s_j = G_j + hs(y_j),
+// where G_j = sum_{b<a} g_b(k_b, j_b*) (from the argmin chain) and s_j are
+// exact doubles (multiples of 2^-(2L+3), far below 2^53 units) and q_j = phi
+// at the chain. Each line keeps f~_j = fl(s_j - q_j), q_j and the chain in
+// shared memory, so every decision is made on-chip:
+//  * f~ drives the fp64 filters; the exact f_j = s_j - q_j (s_j recomputed
+//    from the chain) is used only where a filter cannot decide.
+//  * The lower hull is the EXACT hull of (y_j, f_j) with strict corners only:
+//    orientation tests use a rigorous fp64 filter and fall back to an exact
+//    sign (sum_i w_i s_i is exact in fp64; the w_i q_i are summed in 127-bit
+//    integers when their exponents are close, else by error-free cascades).
+//    C-concave potentials (phi = psi^c, every other c-transform of an
+//    iteration) have exactly collinear runs on ~40% of their nodes; the exact
+//    hull drops those runs' interior points, which can never be strictly
+//    better than the run's end corners.
+//  * Hulls are built per thread chunk (monotone chain) and merged in a
+//    log2(threads) tree; each merged group's hull is contiguous, so a bridge
+//    is found by galloping searches on the two monotone predicates of the
+//    classic bridge walk, and B's surviving corners are moved next to A's.
+//  * Over strict corners F(i) = f_{H_i} - x y_{H_i} is exactly unimodal, so a
+//    query is decided by its tangent corner when both neighbours are beyond
+//    the fp64 margin; otherwise the corners within the margin (usually two,
+//    exactly tied on c-concave input) are compared exactly as
+//    two_sum(s_j - x_k y_j, -q_j) — exact because s_j - x_k y_j is.
+//  * The last pass writes RD((s_w - hs(y_w)) + 0.5 (x_k - y_w)^2 - q_w), the
+//    reference's single round-down (exact.hpp:167-179).
+// Non-dyadic grids keep ct_pass_kernel<false> (3-limb g tables).
+// ============================================================================
+constexpr int kDyThreads = 768;
+constexpr int kDyStage = 6;  // corners staged per thread and round of a merge move
+
+struct DySmem {
+  double* f;       // f~_j (padded index)
+  double* q;       // exact q_j (padded index)
+  uint32_t* ch;    // argmin chain of element j (passes a >= 1)
+  uint16_t* H;     // hull: the hull of the chunk group led by chunk g is
+                   //   stored contiguously from g * C
+  uint16_t* res;   // per-query tangent corner, then winner
+  int* gsz;        // hull size of the group led by chunk t
+  int* bA;         // bridge of the merge led by chunk t: keep A[0..bA], B[bB..)
+  int* bB;
+  unsigned long long* scal;  // 0 A (max |f~|), 3 hull size, 4 #uncertified interior points
+  LineGeo* geo;
+};
+
+__device__ __forceinline__ DySmem dy_carve(const CtPass& p, unsigned char* base, int l) {
+  DySmem s;
+  unsigned char* b = base + static_cast<long>(l) * p.line_bytes;
+  s.f = reinterpret_cast<double*>(b + p.off_fv);
+  s.q = reinterpret_cast<double*>(b + p.off_chain);
+  s.ch = reinterpret_cast<uint32_t*>(b + p.off_flag);
+  s.H = reinterpret_cast<uint16_t*>(b + p.off_hidx);
+  s.res = reinterpret_cast<uint16_t*>(b + p.off_H);
+  s.gsz = reinterpret_cast<int*>(b + p.off_lohi);
+  s.bA = s.gsz + p.tpl;
+  s.bB = s.bA + p.tpl;
+  s.scal = reinterpret_cast<unsigned long long*>(b + p.off_scal);
+  s.geo = reinterpret_cast<LineGeo*>(b + p.off_scal + 64);
+  return s;
+}
+
+// Exact s_j = G_j + hs(y_j) of element j (G from the chain; exact on dyadic grids).
+__device__ __forceinline__ double dy_s(const CtPass& p, const LineGeo& g, const uint32_t* ch, int j) {
+  const double y = coord(p.ax[p.a].h, j);
+  double G = 0.0;
+  if (p.a >= 1) {
+    const uint32_t c = ch[j];
+    G = g_approx(p.ax[0], g.k[0], static_cast<int>(c & 0xFFFFu));
+    if (p.a >= 2) G += g_approx(p.ax[1], g.k[1], static_cast<int>(c >> 16));
+  }
+  return G + 0.5 * y * y;
+}
+
+// Integer path for the sign of sum_i coef_i v_i: the four doubles as m 2^e
+// with 53-bit m; when their exponents lie within 56 of each other the signed
+// sum of coef_i m_i 2^(e_i - emin) fits in 127 bits (|coef m| < 2^69).
+__device__ __forceinline__ bool dy_sign_int(const double* v, const int* coef, int& sgn) {
+  int e[4];
+  int emin = 4096, emax = -4096;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const long long b = __double_as_longlong(v[i]);
+    const int ex = static_cast<int>((b >> 52) & 0x7ff);
+    e[i] = ex ? ex : 1;
+    if ((b & 0x7FFFFFFFFFFFFFFFll) != 0) {
+      emin = min(emin, e[i]);
+      emax = max(emax, e[i]);
+    }
+  }
+  if (emax < emin) {
+    sgn = 0;
+    return true;
+  }
+  if (emax - emin > 56) return false;
+  __int128 acc = 0;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const long long b = __double_as_longlong(v[i]);
+    long long mm = b & 0xFFFFFFFFFFFFFll;
+    if (((b >> 52) & 0x7ff) != 0) mm |= 1ll << 52;
+    if (mm == 0) continue;
+    __int128 t = static_cast<__int128>(mm) * coef[i];
+    t <<= (e[i] - emin);
+    acc += b < 0 ? -t : t;
+  }
+  sgn = acc > 0 ? 1 : (acc < 0 ? -1 : 0);
+  return true;
+}
+
+__device__ __noinline__ int dy_sign_slow(const double* x) {
+  bfmx::Exp<8> e;
+  e.clear();
+  for (int i = 0; i < 7; ++i) e.grow(x[i]);
+  return e.sign();
+}
+
+// Exact sign of (c-a) f_b - (c-b) f_a - (b-a) f_c with f = s - q (a < b < c):
+// negative iff b is a strict lower-hull corner of (a, b, c).
+// Exact sign of 2 f_b - f_a - f_c for consecutive a = b-1, c = b+1 (the
+// local-corner test): (2 s_b - s_a - s_c) is exact in fp64 and 2 q_b is
+// exact, so the value is an exact sum of four doubles, distilled by
+// error-free cascades (usually one pass decides).
+__device__ __forceinline__ int dy_orient_local(const CtPass& p, const LineGeo& g, const uint32_t* ch,
+                                               const double* Q, int b) {
+  const double sa = dy_s(p, g, ch, b - 1), sb = dy_s(p, g, ch, b), sc = dy_s(p, g, ch, b + 1);
+  double x0 = (2.0 * sb - sa) - sc;
+  double x1 = -2.0 * Q[padj(b)];
+  double x2 = Q[padj(b - 1)];
+  double x3 = Q[padj(b + 1)];
+  for (int pass = 0; pass < 16; ++pass) {
+    double sm, er;
+    bfmx::two_sum(x1, x0, sm, er);
+    x1 = sm;
+    x0 = er;
+    bfmx::two_sum(x2, x1, sm, er);
+    x2 = sm;
+    x1 = er;
+    bfmx::two_sum(x3, x2, sm, er);
+    x3 = sm;
+    x2 = er;
+    const double rest = (fabs(x0) + fabs(x1)) + fabs(x2);
+    if (rest == 0.0) return x3 > 0.0 ? 1 : (x3 < 0.0 ? -1 : 0);
+    if (fabs(x3) > 1.01 * rest) return x3 > 0.0 ? 1 : -1;
+  }
+  bfmx::Exp<8> e;
+  e.clear();
+  e.grow(x0);
+  e.grow(x1);
+  e.grow(x2);
+  e.grow(x3);
+  return e.sign();
+}
+
+__device__ __noinline__ int dy_orient_exact(const CtPass& p, const LineGeo& g, const uint32_t* ch,
+                                            const double* Q, int a, int b, int c) {
+  const double sa = dy_s(p, g, ch, a), sb = dy_s(p, g, ch, b), sc = dy_s(p, g, ch, c);
+  const double qa = Q[padj(a)], qb = Q[padj(b)], qc = Q[padj(c)];
+  const double w1 = static_cast<double>(c - a), w2 = static_cast<double>(c - b),
+               w3 = static_cast<double>(b - a);
+  // exact: integers below 2^16 times multiples of 2^-(2L+3) bounded by 1.5
+  const double S = (w1 * sb - w2 * sa) - w3 * sc;
+  {
+    const double v[4] = {S, qb, qa, qc};
+    const int coef[4] = {1, -(c - a), c - b, b - a};
+    int sg;
+    if (dy_sign_int(v, coef, sg)) return sg;
+  }
+  // error-free cascades (VecSum) until the leading term dominates
+  double x[7];
+  double pr, r;
+  x[0] = S;
+  bfmx::two_prod(w1, qb, pr, r);
+  x[1] = -r;
+  x[4] = -pr;
+  bfmx::two_prod(w2, qa, pr, r);
+  x[2] = r;
+  x[5] = pr;
+  bfmx::two_prod(w3, qc, pr, r);
+  x[3] = r;
+  x[6] = pr;
+  for (int pass = 0; pass < 12; ++pass) {
+#pragma unroll
+    for (int i = 1; i < 7; ++i) {
+      double sm, er;
+      bfmx::two_sum(x[i], x[i - 1], sm, er);
+      x[i] = sm;
+      x[i - 1] = er;
+    }
+    double rest = 0.0;
+#pragma unroll
+    for (int i = 0; i < 6; ++i) rest += fabs(x[i]);
+    if (rest == 0.0) return x[6] > 0.0 ? 1 : (x[6] < 0.0 ? -1 : 0);
+    if (fabs(x[6]) > 1.01 * rest) return x[6] > 0.0 ? 1 : -1;
+  }
+  return dy_sign_slow(x);
+}
+
+__global__ void __launch_bounds__(kDyThreads) ct_dy_kernel(CtPass p) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int tpl = p.tpl;
+  const int l = threadIdx.x / tpl;
+  const int t = threadIdx.x - l * tpl;
+  const int lpc = p.lpc;
+  const CtAxis& A = p.ax[p.a];
+  const int n = A.n;
+  const double h = A.h;
+  const int C = p.C;
+  DySmem s = dy_carve(p, smem, l);
+
+  if (t == 0) {
+    const long L = static_cast<long>(blockIdx.x) * lpc + l;
+    LineGeo g;
+    g.valid = L < p.nlines;
+    g.base = 0;
+    g.phi_other = 0;
+    g.k[0] = g.k[1] = g.k[2] = 0;
+    if (g.valid) {
+      const long inner = L % A.stride, outer = L / A.stride;
+      g.base = outer * static_cast<long>(n) * A.stride + inner;
+      long rem = g.base;
+      for (int b = 0; b < p.d; ++b) {
+        const int c = static_cast<int>(rem / p.ax[b].stride);
+        rem -= static_cast<long>(c) * p.ax[b].stride;
+        g.k[b] = c;
+        if (b > p.a) g.phi_other += static_cast<long>(c) * p.ax[b].stride;
+      }
+    }
+    g.k[0] += p.k0_off;
+    *s.geo = g;
+    for (int q = 0; q < 8; ++q) s.scal[q] = 0ull;
+  }
+  __syncthreads();
+
+  // diagnostics (p.stats): per-thread counters flushed once at the end, and
+  // per-phase clocks of each line's thread 0
+  long long tph = clock64();
+  unsigned c_flag = 0, c_walk = 0, c_xchunk = 0, c_xmerge = 0, c_merge = 0;
+  int in_merge = 0;
+  auto PH = [&](int i) {
+    if (p.stats && t == 0) {
+      const long long now = clock64();
+      atomicAdd(p.stats + 8 + i, static_cast<unsigned long long>(now - tph));
+      tph = now;
+    }
+  };
+
+  // ---- load: q_j (cp.async), chain_j; then f~_j = fl(s_j - q_j) ----------
+  {
+    const int ml = p.strided ? static_cast<int>(threadIdx.x % lpc) : l;
+    const DySmem sm = dy_carve(p, smem, ml);
+    const LineGeo g = *sm.geo;
+    const int step = p.strided ? blockDim.x / lpc : tpl;
+    const int first = p.strided ? static_cast<int>(threadIdx.x / lpc) : t;
+    if (g.valid) {
+      if (p.a == 0) {
+        for (int j = first; j < n; j += step)
+          cp_async8(&sm.q[padj(j)], &p.phi[g.phi_other + static_cast<long>(j) * A.stride]);
+      } else {
+        constexpr int kBatch = 8;
+        for (int j0 = first; j0 < n; j0 += kBatch * step) {
+          uint32_t chv[kBatch];
+#pragma unroll
+          for (int u = 0; u < kBatch; ++u) {
+            const int j = j0 + u * step;
+            chv[u] = j < n ? p.state_in[g.base + static_cast<long>(j) * A.stride] : 0u;
+          }
+#pragma unroll
+          for (int u = 0; u < kBatch; ++u) {
+            const int j = j0 + u * step;
+            if (j >= n) continue;
+            cp_async8(&sm.q[padj(j)], &p.phi[phi_index(p, g, chv[u], j)]);
+            sm.ch[j] = chv[u];
+          }
+        }
+      }
+    }
+    cp_async_wait_all();
+  }
+  __syncthreads();
+
+  const LineGeo geo = *s.geo;
+  const bool active = geo.valid;
+  const double* F = s.f;
+  const double* Q = s.q;
+  const uint32_t* CH = s.ch;
+  auto P_f = [&](int j) { return F[padj(j)]; };
+  auto P_y = [&](int j) { return coord(h, j); };
+  // ---- f~ and the line maximum of |f~| (rounding bounds) -------------------
+  {
+    double amax = 0.0;
+    if (active)
+      for (int j = t; j < n; j += tpl) {
+        const double f = dy_s(p, geo, CH, j) - Q[padj(j)];
+        s.f[padj(j)] = f;
+        amax = fmax(amax, fabs(f));
+      }
+    for (int o = 16; o > 0; o >>= 1) amax = fmax(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+    if ((threadIdx.x & 31) == 0) atomicMax(&s.scal[0], dbits(amax));
+  }
+  group_sync(tpl, l);
+  PH(0);
+  const double Aabs = bitsd(s.scal[0]);
+  // (the 1e-290 floors cover gradual underflow of tiny values)
+  const double e_f = kU * Aabs + 1e-290;             // |f_j - f~_j|
+  const double ef2 = 2.0000001 * e_f;                // filter slack per unit index span
+  const double e_F = e_f + 4.0 * kU * (Aabs + 1.0);  // |F^_j - (f_j - x y_j)|
+  const double Mc = 4.0 * e_F;                       // > 2 e_F: margin on F^ differences
+  // Orientation filter on index differences (the common factor h dropped):
+  // D = (f_b - f_a)(c - b) - (f_c - f_b)(b - a) with f~; certified when
+  // |D| exceeds the rounding of the products plus 2 e_f (c - a).
+  auto filt = [&](int a, double fa, int b, double fb, int c, double fc, int& und) {
+    const double t1 = (fb - fa) * static_cast<double>(c - b);
+    const double t2 = (fc - fb) * static_cast<double>(b - a);
+    const double bound = 8.0 * kU * (fabs(t1) + fabs(t2)) + ef2 * static_cast<double>(c - a) + 1e-290;
+    const double D = t1 - t2;
+    und = !(D < -bound) && !(D > bound);
+    return D < -bound;
+  };
+  auto convex_x = [&](int a, double fa, int b, double fb, int c, double fc) {
+    int und;
+    const bool cv = filt(a, fa, b, fb, c, fc, und);
+    if (p.stats) c_merge += in_merge;
+    if (!und) return cv;
+    if (p.stats) {
+      if (in_merge) ++c_xmerge;
+      else ++c_xchunk;
+    }
+    return dy_orient_exact(p, geo, CH, Q, a, b, c) < 0;
+  };
+  const int j0 = t * C;
+  const int j1 = min(n, j0 + C);
+  // ---- 0. local corners: a point that is not a strict corner of (j-1, j, j+1)
+  //         lies on or above that chord and can never be a strict hull
+  //         corner, so it is dropped here (exactly: the filter, then the exact
+  //         sign). This removes the interiors of exactly collinear runs before
+  //         any merge. A line without drops is convex: its hull is the line.
+  uint8_t* keep = reinterpret_cast<uint8_t*>(s.res);  // res is free until phase 4
+  {
+    int bad = 0;
+    if (active && j0 < j1) {
+      double fa = j0 > 0 ? P_f(j0 - 1) : 0.0, fb = P_f(j0);
+      for (int j = j0; j < j1; ++j) {
+        const double fc = j + 1 < n ? P_f(j + 1) : 0.0;
+        int k = 1;
+        if (j > 0 && j + 1 < n) {
+          int und;
+          k = filt(j - 1, fa, j, fb, j + 1, fc, und);
+          if (und) {
+            if (p.stats) ++c_xchunk;
+            k = dy_orient_local(p, geo, CH, Q, j) < 0;
+          }
+        }
+        keep[j] = static_cast<uint8_t>(k);
+        bad += !k;
+        fa = fb;
+        fb = fc;
+      }
+    }
+    if (bad) atomicAdd(reinterpret_cast<unsigned int*>(&s.scal[4]), static_cast<unsigned>(bad));
+  }
+  group_sync(tpl, l);
+  PH(1);
+  const bool convex_line = s.scal[4] == 0ull;
+
+  if (!convex_line) {
+    // ---- 1. chunk hulls (monotone chain, exact strict corners) at H[t*C..)
+    uint16_t* st = s.H + t * C;
+    if (active) {
+      int sz = 0;
+      double fa = 0, fb = 0;
+      int ia = 0, ib = 0;
+      for (int j = j0; j < j1; ++j) {
+        if (!keep[j]) continue;
+        const double fj = P_f(j);
+        while (sz >= 2) {
+          if (convex_x(ia, fa, ib, fb, j, fj)) break;
+          --sz;
+          ib = ia;
+          fb = fa;
+          if (sz >= 2) {
+            ia = st[sz - 2];
+            fa = P_f(ia);
+          }
+        }
+        st[sz++] = static_cast<uint16_t>(j);
+        ia = ib;
+        fa = fb;
+        ib = j;
+        fb = fj;
+      }
+      s.gsz[t] = sz;
+    }
+    PH(2);
+    in_merge = 1;
+    // ---- 2. tree merge: bridge by galloping searches, then B's surviving
+    //         corners are moved next to A's (register-staged, in place)
+    auto cvx3 = [&](int i0, int i1, int i2) { return convex_x(i0, P_f(i0), i1, P_f(i1), i2, P_f(i2)); };
+    uint16_t* Hh = s.H;
+    for (int lvl = 1, li = 0; lvl < tpl; lvl <<= 1, ++li) {
+      if (2 * lvl <= 32) __syncwarp();
+      else group_sync(tpl, l);
+      if (p.stats && t == 0) {  // per-level clocks of thread 0 (diagnostics)
+        const long long now = clock64();
+        if (li > 0) atomicAdd(p.stats + 18 + li - 1, static_cast<unsigned long long>(now - tph));
+        tph = now;
+      }
+      if (active && (t % (2 * lvl)) == 0) {
+        const int gB = t + lvl;
+        const int szA = s.gsz[t];
+        const int szB = gB < tpl ? s.gsz[gB] : 0;
+        const uint16_t* HA = Hh + t * C;
+        const uint16_t* HB = Hh + gB * C;
+        int ia = szA - 1, ib = 0;
+        if (szA > 0 && szB > 0) {
+          while (true) {
+            bool moved = false;
+            // retreat: P(a) = (a == 0 || cvx(A[a-1], A[a], B[ib])) holds up to
+            // the tangent from B[ib] and fails after it
+            const int qb = HB[ib];
+            if (ia > 0 && !cvx3(HA[ia - 1], HA[ia], qb)) {
+              int bad = ia, good = 0, step = 1;
+              while (true) {
+                const int c = bad - step;
+                if (c <= 0) break;
+                if (cvx3(HA[c - 1], HA[c], qb)) {
+                  good = c;
+                  break;
+                }
+                bad = c;
+                step <<= 1;
+              }
+              while (bad - good > 1) {
+                const int mid = (bad + good) >> 1;
+                if (cvx3(HA[mid - 1], HA[mid], qb)) good = mid;
+                else bad = mid;
+              }
+              ia = good;
+              moved = true;
+            }
+            // advance: Q(b) = (b == last || cvx(A[ia], B[b], B[b+1])) fails
+            // before the tangent from A[ia] and holds from it on
+            const int pa = HA[ia];
+            if (ib < szB - 1 && !cvx3(pa, HB[ib], HB[ib + 1])) {
+              int bad = ib, good = szB - 1, step = 1;
+              while (true) {
+                const int c = bad + step;
+                if (c >= szB - 1) break;
+                if (cvx3(pa, HB[c], HB[c + 1])) {
+                  good = c;
+                  break;
+                }
+                bad = c;
+                step <<= 1;
+              }
+              while (good - bad > 1) {
+                const int mid = (bad + good) >> 1;
+                if (cvx3(pa, HB[mid], HB[mid + 1])) good = mid;
+                else bad = mid;
+              }
+              ib = good;
+              moved = true;
+            }
+            if (!moved) break;
+          }
+        }
+        s.bA[t] = ia;
+        s.bB[t] = ib;
+        s.gsz[t] = (ia + 1) + (szB - ib);
+      }
+      if (2 * lvl <= 32) __syncwarp();
+      else group_sync(tpl, l);
+      // move B[ib..szB) to A's end (a left move): each round reads its corners
+      // before any is written; at most lvl*C corners over 2*lvl threads, so
+      // ceil(C / (2 kDyStage)) rounds (uniform over the line) suffice
+      const int g = t & ~(2 * lvl - 1);
+      const int gthreads = min(2 * lvl, tpl - g);
+      int nmv = 0, dst0 = 0;
+      const uint16_t* src = Hh;
+      if (active && g + lvl < tpl) {
+        const int ia = s.bA[g], ib = s.bB[g];
+        nmv = s.gsz[g] - (ia + 1);
+        src = Hh + (g + lvl) * C + ib;
+        dst0 = g * C + ia + 1;
+      }
+      const int rounds = (C + 2 * kDyStage - 1) / (2 * kDyStage);
+      for (int rd = 0; rd < rounds; ++rd) {
+        const int base = rd * kDyStage * gthreads + (t - g);
+        uint16_t v[kDyStage];
+#pragma unroll
+        for (int r = 0; r < kDyStage; ++r) {
+          const int i = base + r * gthreads;
+          if (i < nmv) v[r] = src[i];
+        }
+        if (2 * lvl <= 32) __syncwarp();
+        else group_sync(tpl, l);
+#pragma unroll
+        for (int r = 0; r < kDyStage; ++r) {
+          const int i = base + r * gthreads;
+          if (i < nmv) Hh[dst0 + i] = v[r];
+        }
+      }
+    }
+    group_sync(tpl, l);
+    if (p.stats && t == 0) atomicAdd(p.stats + 27, static_cast<unsigned long long>(clock64() - tph));
+    if (t == 0) s.scal[3] = static_cast<unsigned long long>(s.gsz[0]);
+    PH(3);
+  }
+  group_sync(tpl, l);
+  const int hsz = convex_line ? n : static_cast<int>(s.scal[3]);
+  BFM_DASSERT(!active || (hsz >= 1 && hsz <= n));
+  const uint16_t* Hf = s.H;
+  uint16_t* res = s.res;
+  auto HH = [&](int i) { return convex_line ? i : static_cast<int>(Hf[i]); };
+
+  // ---- 4. tangent corner of every query: balanced merge path of the query
+  //         slopes x_k against the hull-edge slopes (ties: query first)
+  if (active) {
+    auto slope_ge = [&](int i, double xh) {  // xh = x_k h
+      const int a = HH(i), b = HH(i + 1);
+      return (P_f(b) - P_f(a)) >= xh * static_cast<double>(b - a);
+    };
+    const int E = hsz - 1;
+    const int total = n + E;
+    const int per = (total + tpl - 1) / tpl;
+    const int d0 = min(total, t * per), d1 = min(total, d0 + per);
+    if (d0 < d1) {
+      int lo = max(0, d0 - E), hi = min(d0, n);
+      while (lo < hi) {
+        const int qm = (lo + hi) >> 1;
+        if (slope_ge(d0 - qm - 1, coord(h, qm) * h)) lo = qm + 1;
+        else hi = qm;
+      }
+      int k = lo, i = d0 - lo;
+      double xh = coord(h, k) * h;
+      for (int d = d0; d < d1; ++d) {
+        if (k < n && (i >= E || slope_ge(i, xh))) {
+          res[k] = static_cast<uint16_t>(i);
+          ++k;
+          xh = coord(h, k) * h;
+        } else {
+          ++i;
+        }
+      }
+    }
+  }
+  group_sync(tpl, l);
+  PH(4);
+
+  // ---- 5. certification and exact resolution, per query --------------------
+  if (active) {
+    for (int k = t; k < n; k += tpl) {
+      const int i = res[k];
+      const double xk = coord(h, k);
+      auto Fh = [&](int c) {
+        const int j = HH(c);
+        return P_f(j) - xk * P_y(j);
+      };
+      const double F0 = Fh(i);
+      bool lone = true;
+      if (i > 0) lone = Fh(i - 1) > F0 + Mc;
+      if (lone && i < hsz - 1) lone = Fh(i + 1) > F0 + Mc;
+      int win = HH(i);
+      if (!lone) {
+        if (p.stats) ++c_flag;
+        // descend to the local minimum of F^, then take every corner within
+        // the margin: the exact minimum over (unimodal) corners lies inside
+        int L = i;
+        double Fmin = F0;
+        while (L > 0) {
+          const double Fl = Fh(L - 1);
+          if (Fl < Fmin) { --L; Fmin = Fl; } else break;
+        }
+        int R = L;
+        if (L == i) {
+          while (R < hsz - 1) {
+            const double Fr = Fh(R + 1);
+            if (Fr < Fmin) { ++R; Fmin = Fr; } else break;
+          }
+          L = R;
+        }
+        while (L > 0) {
+          const double Fl = Fh(L - 1);
+          if (Fl <= Fmin + Mc) { --L; Fmin = fmin(Fmin, Fl); } else break;
+        }
+        while (R < hsz - 1) {
+          const double Fr = Fh(R + 1);
+          if (Fr <= Fmin + Mc) { ++R; Fmin = fmin(Fmin, Fr); } else break;
+        }
+        if (p.stats) c_walk += R - L + 1;
+        // exact: V_j - hs(x_k) = two_sum(s_j - x_k y_j, -q_j), lexicographic
+        double bh = 0.0, bl = 0.0;
+        for (int c = L; c <= R; ++c) {
+          const int j = HH(c);
+          double vh, vl;
+          bfmx::two_sum(dy_s(p, geo, CH, j) - xk * P_y(j), -Q[padj(j)], vh, vl);
+          if (c == L || vh < bh || (vh == bh && vl < bl)) {
+            win = j;
+            bh = vh;
+            bl = vl;
+          }
+        }
+      }
+      if (p.last) {
+        const double yw = P_y(win);
+        const double dl = xk - yw;
+        const double G = dy_s(p, geo, CH, win) - 0.5 * yw * yw;  // exact
+        p.out[geo.base + static_cast<long>(k) * A.stride] =
+            bfmx::round_down2(G + 0.5 * dl * dl, -Q[padj(win)]);
+      } else {
+        res[k] = static_cast<uint16_t>(win);
+      }
+    }
+  }
+  PH(5);
+  if (p.stats) {
+    unsigned vv[5] = {c_flag, c_walk, c_xchunk, c_xmerge, c_merge};
+#pragma unroll
+    for (int i = 0; i < 5; ++i) {
+      unsigned x = vv[i];
+      for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+      if ((threadIdx.x & 31) == 0 && x) atomicAdd(p.stats + 1 + i, static_cast<unsigned long long>(x));
+    }
+    if (t == 0 && active) atomicAdd(p.stats + 0, static_cast<unsigned long long>(n));
+  }
+  if (p.last) return;
+  __syncthreads();
+
+  // ---- 6. intermediate passes: argmin chain and q at the winner ------------
+  {
+    const int ml = p.strided ? static_cast<int>(threadIdx.x % lpc) : l;
+    const int step = p.strided ? blockDim.x / lpc : tpl;
+    const int first = p.strided ? static_cast<int>(threadIdx.x / lpc) : t;
+    const DySmem sm = dy_carve(p, smem, ml);
+    const LineGeo g = *sm.geo;
+    if (g.valid)
+      for (int k = first; k < n; k += step) {
+        const long node = g.base + static_cast<long>(k) * A.stride;
+        const int win = sm.res[k];
+        const uint32_t packed = p.a == 0 ? static_cast<uint32_t>(win)
+                                         : (sm.ch[win] | (static_cast<uint32_t>(win) << 16));
+        p.state_out[node] = packed;
+        if (p.q_out) p.q_out[node] = sm.q[padj(win)];
+      }
+  }
+}
+
 int align16(int v) { return (v + 15) & ~15; }
 
 bool is_dyadic(int n) { return n > 0 && (n & (n - 1)) == 0 && n <= (1 << 25); }
@@ -1012,10 +1662,41 @@ void CtPlan::setup(const GridDesc& loc, const GridDesc& global, int pb, int pe, 
     for (int b = 0; b < loc.d; ++b) P.ax[b] = ax_[b];
     const int n = loc.n[a];
     P.nlines = loc.size / n;
-    P.tpl = n <= 512 ? 32 : (n <= 1024 ? 64 : (n <= 2048 ? 128 : 256));
-    P.C = (n + P.tpl - 1) / P.tpl;
     P.strided = a != loc.d - 1;
     const bool dy = dyadic_;
+    if (dy) {
+      // exact-hull kernel: (s, q) per point in shared memory; about 11 points
+      // per thread, up to kDyThreads threads per line
+      P.tpl = std::min(kDyThreads, std::max(32, ((n + 10) / 11 + 31) / 32 * 32));
+      P.C = (n + P.tpl - 1) / P.tpl;
+      int o = 0;
+      P.off_fv = o;
+      o = align16(o + 8 * (n + n / 32 + 1));
+      P.off_chain = o;
+      o = align16(o + 8 * (n + n / 32 + 1));
+      P.off_flag = o;  // chain (uint32, passes a >= 1)
+      if (a > 0) o = align16(o + 4 * n);
+      P.off_hidx = o;  // hull
+      o = align16(o + 2 * P.tpl * P.C);
+      P.off_H = o;  // per-query tangent / winner
+      o = align16(o + 2 * n);
+      P.off_list = o;  // unused
+      P.off_lohi = o;  // gsz, bA, bB
+      o = align16(o + 12 * P.tpl);
+      P.off_scal = o;
+      o = align16(o + 64 + static_cast<int>(sizeof(LineGeo)));
+      P.line_bytes = o;
+      if (o > budget) throw std::invalid_argument("ctransform: grid line too long for shared memory");
+      int lpc = std::min<long>(budget / o, kDyThreads / P.tpl);
+      lpc = std::min(lpc, P.strided ? 16 : 8);
+      lpc = static_cast<int>(std::min<long>(lpc, P.nlines));
+      P.lpc = std::max(lpc, 1);
+      P.slow_queries = slow_;
+      P.stats = stats_;
+      continue;
+    }
+    P.tpl = n <= 512 ? 32 : (n <= 1024 ? 64 : (n <= 2048 ? 128 : 256));
+    P.C = (n + P.tpl - 1) / P.tpl;
     int o = 0;
     P.off_fv = o;
     o = align16(o + 8 * (n + n / 32 + 1));
@@ -1043,8 +1724,7 @@ void CtPlan::setup(const GridDesc& loc, const GridDesc& global, int pb, int pe, 
     P.slow_queries = slow_;
     P.stats = stats_;
   }
-  BFM_CUDA(cudaFuncSetAttribute(ct_pass_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                budget));
+  BFM_CUDA(cudaFuncSetAttribute(ct_dy_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, budget));
   BFM_CUDA(cudaFuncSetAttribute(ct_pass_kernel<false>,
                                 cudaFuncAttributeMaxDynamicSharedMemorySize, budget));
   ready_ = true;
@@ -1053,8 +1733,7 @@ void CtPlan::setup(const GridDesc& loc, const GridDesc& global, int pb, int pe, 
 void CtPlan::launch(const CtPass& P, cudaStream_t stream, LaunchCounter* lc) {
   const long blocks = (P.nlines + P.lpc - 1) / P.lpc;
   if (dyadic_)
-    ct_pass_kernel<true><<<static_cast<unsigned>(blocks), P.lpc * P.tpl, P.lpc * P.line_bytes,
-                           stream>>>(P);
+    ct_dy_kernel<<<static_cast<unsigned>(blocks), P.lpc * P.tpl, P.lpc * P.line_bytes, stream>>>(P);
   else
     ct_pass_kernel<false><<<static_cast<unsigned>(blocks), P.lpc * P.tpl, P.lpc * P.line_bytes,
                             stream>>>(P);
