@@ -1667,7 +1667,9 @@ void CtPlan::setup(const GridDesc& loc, const GridDesc& global, int pb, int pe, 
     if (dy) {
       // exact-hull kernel: (s, q) per point in shared memory; about 11 points
       // per thread, up to kDyThreads threads per line
-      P.tpl = std::min(kDyThreads, std::max(32, ((n + 10) / 11 + 31) / 32 * 32));
+      int cpt = 11;
+      if (const char* e = getenv("BFM_CT_C")) cpt = std::max(2, atoi(e));  // tuning experiments
+      P.tpl = std::min(kDyThreads, std::max(32, ((n + cpt - 1) / cpt + 31) / 32 * 32));
       P.C = (n + P.tpl - 1) / P.tpl;
       int o = 0;
       P.off_fv = o;
@@ -1687,7 +1689,8 @@ void CtPlan::setup(const GridDesc& loc, const GridDesc& global, int pb, int pe, 
       o = align16(o + 64 + static_cast<int>(sizeof(LineGeo)));
       P.line_bytes = o;
       if (o > budget) throw std::invalid_argument("ctransform: grid line too long for shared memory");
-      int lpc = std::min<long>(budget / o, kDyThreads / P.tpl);
+      // two CTAs per SM: a CTA's loads overlap the other's hull work
+      int lpc = std::min<long>(budget / (2 * o), kDyThreads / (2 * P.tpl));
       lpc = std::min(lpc, P.strided ? 16 : 8);
       lpc = static_cast<int>(std::min<long>(lpc, P.nlines));
       P.lpc = std::max(lpc, 1);
