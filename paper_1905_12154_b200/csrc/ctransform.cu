@@ -914,6 +914,12 @@ __global__ void __launch_bounds__(ct_threads(DY)) ct_pass_kernel(CtPass p) {
 // Non-dyadic grids keep ct_pass_kernel<false> (3-limb g tables).
 // ============================================================================
 constexpr int kDyThreads = 768;
+
+// Lines are stored unpadded: setup picks an odd number of points per thread,
+// so the per-thread chunk walks (stride C doubles) are bank-conflict free.
+__device__ __forceinline__ int dyi(int j) { return j; }
+// Exact node coordinate on a dyadic grid: (2j + 1) * (h / 2) == (j + 0.5) * h.
+__device__ __forceinline__ double dy_coord(double hh, int j) { return static_cast<double>(2 * j + 1) * hh; }
 constexpr int kDyStage = 6;  // corners staged per thread and round of a merge move
 
 struct DySmem {
@@ -948,7 +954,7 @@ __device__ __forceinline__ DySmem dy_carve(const CtPass& p, unsigned char* base,
 
 // Exact s_j = G_j + hs(y_j) of element j (G from the chain; exact on dyadic grids).
 __device__ __forceinline__ double dy_s(const CtPass& p, const LineGeo& g, const uint32_t* ch, int j) {
-  const double y = coord(p.ax[p.a].h, j);
+  const double y = dy_coord(0.5 * p.ax[p.a].h, j);
   double G = 0.0;
   if (p.a >= 1) {
     const uint32_t c = ch[j];
@@ -1011,9 +1017,9 @@ __device__ __forceinline__ int dy_orient_local(const CtPass& p, const LineGeo& g
                                                const double* Q, int b) {
   const double sa = dy_s(p, g, ch, b - 1), sb = dy_s(p, g, ch, b), sc = dy_s(p, g, ch, b + 1);
   double x0 = (2.0 * sb - sa) - sc;
-  double x1 = -2.0 * Q[padj(b)];
-  double x2 = Q[padj(b - 1)];
-  double x3 = Q[padj(b + 1)];
+  double x1 = -2.0 * Q[dyi(b)];
+  double x2 = Q[dyi(b - 1)];
+  double x3 = Q[dyi(b + 1)];
   for (int pass = 0; pass < 16; ++pass) {
     double sm, er;
     bfmx::two_sum(x1, x0, sm, er);
@@ -1041,7 +1047,7 @@ __device__ __forceinline__ int dy_orient_local(const CtPass& p, const LineGeo& g
 __device__ __noinline__ int dy_orient_exact(const CtPass& p, const LineGeo& g, const uint32_t* ch,
                                             const double* Q, int a, int b, int c) {
   const double sa = dy_s(p, g, ch, a), sb = dy_s(p, g, ch, b), sc = dy_s(p, g, ch, c);
-  const double qa = Q[padj(a)], qb = Q[padj(b)], qc = Q[padj(c)];
+  const double qa = Q[dyi(a)], qb = Q[dyi(b)], qc = Q[dyi(c)];
   const double w1 = static_cast<double>(c - a), w2 = static_cast<double>(c - b),
                w3 = static_cast<double>(b - a);
   // exact: integers below 2^16 times multiples of 2^-(2L+3) bounded by 1.5
@@ -1141,7 +1147,7 @@ __global__ void __launch_bounds__(kDyThreads) ct_dy_kernel(CtPass p) {
     if (g.valid) {
       if (p.a == 0) {
         for (int j = first; j < n; j += step)
-          cp_async8(&sm.q[padj(j)], &p.phi[g.phi_other + static_cast<long>(j) * A.stride]);
+          cp_async8(&sm.q[dyi(j)], &p.phi[g.phi_other + static_cast<long>(j) * A.stride]);
       } else {
         constexpr int kBatch = 8;
         for (int j0 = first; j0 < n; j0 += kBatch * step) {
@@ -1155,7 +1161,7 @@ __global__ void __launch_bounds__(kDyThreads) ct_dy_kernel(CtPass p) {
           for (int u = 0; u < kBatch; ++u) {
             const int j = j0 + u * step;
             if (j >= n) continue;
-            cp_async8(&sm.q[padj(j)], &p.phi[phi_index(p, g, chv[u], j)]);
+            cp_async8(&sm.q[dyi(j)], &p.phi[phi_index(p, g, chv[u], j)]);
             sm.ch[j] = chv[u];
           }
         }
@@ -1170,15 +1176,16 @@ __global__ void __launch_bounds__(kDyThreads) ct_dy_kernel(CtPass p) {
   const double* F = s.f;
   const double* Q = s.q;
   const uint32_t* CH = s.ch;
-  auto P_f = [&](int j) { return F[padj(j)]; };
-  auto P_y = [&](int j) { return coord(h, j); };
+  auto P_f = [&](int j) { return F[dyi(j)]; };
+  const double hh = 0.5 * h;
+  auto P_y = [&](int j) { return dy_coord(hh, j); };
   // ---- f~ and the line maximum of |f~| (rounding bounds) -------------------
   {
     double amax = 0.0;
     if (active)
       for (int j = t; j < n; j += tpl) {
-        const double f = dy_s(p, geo, CH, j) - Q[padj(j)];
-        s.f[padj(j)] = f;
+        const double f = dy_s(p, geo, CH, j) - Q[dyi(j)];
+        s.f[dyi(j)] = f;
         amax = fmax(amax, fabs(f));
       }
     for (int o = 16; o > 0; o >>= 1) amax = fmax(amax, __shfl_xor_sync(0xffffffffu, amax, o));
@@ -1414,16 +1421,16 @@ __global__ void __launch_bounds__(kDyThreads) ct_dy_kernel(CtPass p) {
       int lo = max(0, d0 - E), hi = min(d0, n);
       while (lo < hi) {
         const int qm = (lo + hi) >> 1;
-        if (slope_ge(d0 - qm - 1, coord(h, qm) * h)) lo = qm + 1;
+        if (slope_ge(d0 - qm - 1, P_y(qm) * h)) lo = qm + 1;
         else hi = qm;
       }
       int k = lo, i = d0 - lo;
-      double xh = coord(h, k) * h;
+      double xh = P_y(k) * h;
       for (int d = d0; d < d1; ++d) {
         if (k < n && (i >= E || slope_ge(i, xh))) {
           res[k] = static_cast<uint16_t>(i);
           ++k;
-          xh = coord(h, k) * h;
+          xh = P_y(k) * h;
         } else {
           ++i;
         }
@@ -1437,7 +1444,7 @@ __global__ void __launch_bounds__(kDyThreads) ct_dy_kernel(CtPass p) {
   if (active) {
     for (int k = t; k < n; k += tpl) {
       const int i = res[k];
-      const double xk = coord(h, k);
+      const double xk = P_y(k);
       auto Fh = [&](int c) {
         const int j = HH(c);
         return P_f(j) - xk * P_y(j);
@@ -1479,7 +1486,7 @@ __global__ void __launch_bounds__(kDyThreads) ct_dy_kernel(CtPass p) {
         for (int c = L; c <= R; ++c) {
           const int j = HH(c);
           double vh, vl;
-          bfmx::two_sum(dy_s(p, geo, CH, j) - xk * P_y(j), -Q[padj(j)], vh, vl);
+          bfmx::two_sum(dy_s(p, geo, CH, j) - xk * P_y(j), -Q[dyi(j)], vh, vl);
           if (c == L || vh < bh || (vh == bh && vl < bl)) {
             win = j;
             bh = vh;
@@ -1492,7 +1499,7 @@ __global__ void __launch_bounds__(kDyThreads) ct_dy_kernel(CtPass p) {
         const double dl = xk - yw;
         const double G = dy_s(p, geo, CH, win) - 0.5 * yw * yw;  // exact
         p.out[geo.base + static_cast<long>(k) * A.stride] =
-            bfmx::round_down2(G + 0.5 * dl * dl, -Q[padj(win)]);
+            bfmx::round_down2(G + 0.5 * dl * dl, -Q[dyi(win)]);
       } else {
         res[k] = static_cast<uint16_t>(win);
       }
@@ -1526,7 +1533,7 @@ __global__ void __launch_bounds__(kDyThreads) ct_dy_kernel(CtPass p) {
         const uint32_t packed = p.a == 0 ? static_cast<uint32_t>(win)
                                          : (sm.ch[win] | (static_cast<uint32_t>(win) << 16));
         p.state_out[node] = packed;
-        if (p.q_out) p.q_out[node] = sm.q[padj(win)];
+        if (p.q_out) p.q_out[node] = sm.q[dyi(win)];
       }
   }
 }
@@ -1667,15 +1674,26 @@ void CtPlan::setup(const GridDesc& loc, const GridDesc& global, int pb, int pe, 
     if (dy) {
       // exact-hull kernel: (s, q) per point in shared memory; about 11 points
       // per thread, up to kDyThreads threads per line
+      // about cpt points per thread, and an ODD count C (the unpadded
+      // per-thread chunk walks are then bank-conflict free)
       int cpt = 11;
       if (const char* e = getenv("BFM_CT_C")) cpt = std::max(2, atoi(e));  // tuning experiments
-      P.tpl = std::min(kDyThreads, std::max(32, ((n + cpt - 1) / cpt + 31) / 32 * 32));
+      int best_tpl = 32, best_err = 1 << 30;
+      for (int tp = 32; tp <= kDyThreads; tp += 32) {
+        const int c = (n + tp - 1) / tp;
+        const int err = std::abs(c - cpt) + ((c & 1) ? 0 : 3) + (tp > n ? 2000 : 0);
+        if (err < best_err) {
+          best_err = err;
+          best_tpl = tp;
+        }
+      }
+      P.tpl = best_tpl;
       P.C = (n + P.tpl - 1) / P.tpl;
       int o = 0;
       P.off_fv = o;
-      o = align16(o + 8 * (n + n / 32 + 1));
+      o = align16(o + 8 * n);
       P.off_chain = o;
-      o = align16(o + 8 * (n + n / 32 + 1));
+      o = align16(o + 8 * n);
       P.off_flag = o;  // chain (uint32, passes a >= 1)
       if (a > 0) o = align16(o + 4 * n);
       P.off_hidx = o;  // hull
