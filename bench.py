@@ -122,6 +122,32 @@ def reference_arm(args):
     if O.ref_lib() is None:
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libbfmref.so not built"}))
         return
+    if args.config == "c5":
+        # the reference's c-transform operator (transforms.hpp:396-432) on all
+        # host threads, bounded sample: the 1024^2 C5 potential
+        from paper_1905_12154_b200 import synthetic
+
+        shape = (1024, 1024)
+        phi = synthetic.c5_potential(shape)[0]
+        O.ref_ctransform(phi)
+        t0 = time.perf_counter()
+        done = 0
+        while done < max(1, args.steps) and time.perf_counter() - t0 < 120.0:
+            O.ref_ctransform(phi)
+            done += 1
+        dt = (time.perf_counter() - t0) / done
+        v = 16.0 * 2 * phi.size / dt / 1e9
+        cores = os.cpu_count()
+        print(json.dumps({
+            "impl": "reference", "metric": "C5 isolated operator sweep: c-transform HBM GB/s (float64)",
+            "value": v, "unit": "GB/s", "n_gpus": world, "steps": done, "warmup": 1,
+            "ms_per_step": 1e3 * dt, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic (seeded C5 potential)",
+            "config": {"workload": "C5: c-transform operator, 1024^2 sample (BASELINE configs[4])"},
+            "cpu_baseline": {"value": v, "unit": "GB/s", "cores": cores, "kind": "reference",
+                             "sample": f"{done} reference c-transforms of the 1024^2 C5 potential"},
+            "e2e": {"value": v, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}))
+        return
     mu, nu, desc = workload(args.config)
     N = mu.size
     s = O.RefSolver(mu, nu, SolverConfig(tolerance=-1.0, max_iterations=10 ** 6))
@@ -255,6 +281,96 @@ def ctransform_roofline(lib, shape, torch, hbm, hbm_kind, reps=10):
             "frac": achieved / hbm, "traffic": traffic,
             "kernel": f"c-transform operator ({launches} axis-pass launches) on {'x'.join(map(str, shape))}",
             "ms_per_launch_group": ms, "algorithmic_bytes": bytes_alg, "peak_kind": hbm_kind}
+
+
+def c5_sweep(args):
+    """BASELINE configs[4]: each operator timed separately
+    on resident float64 data — ctransform(phi), solve_neumann(P - mean), and
+    the fused map + pushforward + residual of the uniform mu through u — on
+    2D 512^2..8192^2 and 3D 128^3..512^3, L2 flushed before every launch
+    group, CUDA events on the launch stream. Algorithmic bytes per node:
+    c-transform 16 d, Poisson 16 (2d - 1), pushforward + residual 32.
+    Prints ONE JSON line; `sweep` lists every (operator, grid)."""
+    import ctypes as C
+
+    import torch
+
+    import paper_1905_12154_b200 as bfm
+    from paper_1905_12154_b200 import synthetic
+
+    lib = bfm.load_library()
+    hbm, hbm_kind = peaks()
+    grids = [(n, n) for n in (512, 1024, 2048, 4096, 8192)] + [(n, n, n) for n in (128, 256, 384, 512)]
+    if args.sweep_max:
+        grids = [g for g in grids if int(np.prod(g)) <= args.sweep_max]
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+    stream = torch.cuda.current_stream()
+    sp = C.c_void_p(stream.cuda_stream)
+    reps = max(1, args.steps)
+    rows = []
+    launches = 0
+    for shape in grids:
+        d = len(shape)
+        N = int(np.prod(shape))
+        phi_np, P_np = synthetic.c5_potential(shape)
+        u_np = synthetic.c5_pushforward_potential(shape)
+        phi = torch.from_numpy(phi_np).cuda()
+        rhs = torch.from_numpy(P_np - P_np.mean()).cuda()
+        u = torch.from_numpy(u_np).cuda()
+        mu = torch.ones(shape, dtype=torch.float64, device="cuda")
+        tgt = torch.zeros_like(mu)
+        out = torch.empty_like(phi)
+        del phi_np, P_np, u_np
+        ws = C.c_void_p()
+        assert lib.bfm_workspace_create(d, (C.c_int * d)(*shape), C.byref(ws)) == 0
+        ops = {
+            "ctransform": (lambda: lib.bfm_ctransform_device(ws, C.c_void_p(phi.data_ptr()),
+                                                             C.c_void_p(out.data_ptr()), sp), 16.0 * d),
+            "solve_neumann": (lambda: lib.bfm_solve_neumann_device(ws, C.c_void_p(rhs.data_ptr()),
+                                                                   C.c_void_p(out.data_ptr()), sp),
+                              16.0 * (2 * d - 1)),
+            "pushforward_residual": (lambda: lib.bfm_pushforward_residual_device(
+                ws, C.c_void_p(u.data_ptr()), C.c_void_p(mu.data_ptr()), C.c_void_p(tgt.data_ptr()),
+                C.c_void_p(out.data_ptr()), sp), 32.0),
+        }
+        for name, (fn, bpn) in ops.items():
+            for _ in range(max(1, args.warmup)):
+                assert fn() == 0
+            nl = lib.bfm_workspace_last_launches(ws)
+            tot = 0.0
+            for _ in range(reps):
+                flush.fill_(1.0)
+                e0 = torch.cuda.Event(enable_timing=True)
+                e1 = torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                assert fn() == 0
+                e1.record(stream)
+                torch.cuda.synchronize()
+                tot += e0.elapsed_time(e1)
+                launches += nl
+            ms = tot / reps
+            gbs = bpn * N / (ms * 1e-3) / 1e9
+            rows.append({"op": name, "grid": list(shape), "ms": ms, "launches_per_call": nl,
+                         "algorithmic_bytes_per_node": bpn, "achieved_gbs": gbs, "frac": gbs / hbm})
+            print(f"# {name:22s} {'x'.join(map(str, shape)):>14s} {ms:9.3f} ms {gbs:8.1f} GB/s "
+                  f"{100 * gbs / hbm:5.2f}%", file=sys.stderr, flush=True)
+        lib.bfm_workspace_destroy(ws)
+        del phi, rhs, u, mu, tgt, out
+        torch.cuda.empty_cache()
+    ct = [r for r in rows if r["op"] == "ctransform"]
+    head = max(ct, key=lambda r: int(np.prod(r["grid"]))) if ct else rows[0]
+    line = {"metric": "C5 isolated operator sweep: c-transform HBM GB/s (float64)",
+            "value": head["achieved_gbs"], "unit": "GB/s", "n_gpus": 1, "steps": reps,
+            "warmup": args.warmup, "ms_per_step": head["ms"], "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded C5 potentials, SURVEY §8(d))",
+            "config": {"workload": "C5: isolated operator sweep (BASELINE configs[4])",
+                       "l2": "flushed (256 MiB write) before every launch group"},
+            "gpu_launches": launches,
+            "roofline": {"bound": "hbm", "achieved": head["achieved_gbs"], "peak": hbm, "unit": "GB/s",
+                         "frac": head["achieved_gbs"] / hbm, "traffic": None, "peak_kind": hbm_kind,
+                         "kernel": f"c-transform operator on {'x'.join(map(str, head['grid']))}"},
+            "sweep": rows}
+    print(json.dumps(line), flush=True)
 
 
 def ours_dist(args):
@@ -442,7 +558,9 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="c3", choices=["c1", "c2", "c3", "c4"])
+    ap.add_argument("--config", default="c3", choices=["c1", "c2", "c3", "c4", "c5"])
+    ap.add_argument("--sweep-max", type=int, default=0,
+                    help="c5: skip grids with more nodes than this (0: all)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--slabs", action="store_true",
                     help="use the slab-decomposition driver even at N = 1 (checks the NCCL path)")
@@ -451,6 +569,9 @@ def main():
     args = ap.parse_args()
     if args.impl == "reference":
         reference_arm(args)
+    elif args.config == "c5":
+        if dist_env()[0] == 0:
+            c5_sweep(args)
     else:
         ours(args)
 
