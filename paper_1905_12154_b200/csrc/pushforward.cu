@@ -167,7 +167,9 @@ __global__ void pf_map_kernel(MapArgs A) {
 }
 
 // Bucket boundaries of the sorted (cell, source) pairs: off[c] = first, end[c] = one past last.
-__global__ void pf_bounds_kernel(const uint32_t* keys, long n, uint32_t sentinel, int* off, int* end) {
+__global__ void pf_bounds_kernel(const uint32_t* keys, long n_max, const int* d_n, uint32_t sentinel, int* off,
+                                 int* end) {
+  const long n = d_n ? *d_n : n_max;
   for (long i = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<long>(gridDim.x) * blockDim.x) {
     const uint32_t k = keys[i];
@@ -190,6 +192,11 @@ struct GatherArgs {
   const double* src;  // record mass
   const double* target;  // may be null: output rho
   double* out;
+  // records in sorted (bucket) order, packed by pf_pack_kernel: (mass,
+  // upper weights per axis) and the clamp mask of the record at each sorted
+  // position — one contiguous read per deposit instead of 2 + d scattered ones
+  const double4* rec;
+  const uint8_t* rmask;
 };
 
 __device__ __forceinline__ double deposit_weight(const GatherArgs& A, int s, int b) {
@@ -199,6 +206,37 @@ __device__ __forceinline__ double deposit_weight(const GatherArgs& A, int s, int
     wt *= ((b >> a) & 1) ? wh : 1.0 - wh;
   }
   return wt;
+}
+
+// Weight of the deposit at sorted position pos into the corner-b target
+// (0 on a clamped axis's upper corner): the same IEEE sequence as
+// deposit_weight, ((m w_0) w_1) w_2, from the packed record.
+__device__ __forceinline__ double pos_weight(const GatherArgs& A, int pos, int b) {
+  if (b & A.rmask[pos]) return 0.0;
+  const double4 r = A.rec[pos];
+  double wt = r.x;
+  const double wa[3] = {r.y, r.z, r.w};
+#pragma unroll
+  for (int a = 0; a < 3; ++a)
+    if (a < A.g.d) wt *= ((b >> a) & 1) ? wa[a] : 1.0 - wa[a];
+  return wt;
+}
+
+// records -> sorted order (one pass after the sort)
+__global__ void pf_pack_kernel(const int* bucket, long nrec, const int* d_n, const double* src, const double* w,
+                               const uint8_t* cmask, int d, double4* rec, uint8_t* rmask) {
+  const long n = d_n ? *d_n : nrec;
+  for (long i = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<long>(gridDim.x) * blockDim.x) {
+    const int s = bucket[i];
+    double4 r;
+    r.x = src[s];
+    r.y = d > 0 ? w[s] : 0.0;
+    r.z = d > 1 ? w[nrec + s] : 0.0;
+    r.w = d > 2 ? w[2 * nrec + s] : 0.0;
+    rec[i] = r;
+    rmask[i] = cmask[s];
+  }
 }
 
 // Light targets: merge the <= 2^d sorted neighbouring buckets by source id
@@ -249,14 +287,15 @@ __global__ void __launch_bounds__(256) pf_gather_kernel(GatherArgs A, int* heavy
           bs = head[b];
           best = b;
         }
+      int bp = 0;
 #pragma unroll
       for (int b = 0; b < NC; ++b)
         if (b == best) {
+          bp = pos[b];
           ++pos[b];
           head[b] = pos[b] < end[b] ? A.bucket[pos[b]] : INT_MAX;
         }
-      if (best & A.cmask[bs]) continue;  // clamped axis: upper corner has weight 0
-      const double wt = deposit_weight(A, bs, best);
+      const double wt = pos_weight(A, bp, best);  // 0 on a clamped axis's upper corner
       if (wt != 0.0) rho += wt;
     }
     A.out[t] = A.target ? A.target[t] - rho : rho;
@@ -354,17 +393,37 @@ __global__ void __launch_bounds__(kMedWarps * 32) pf_gather_medium_kernel(Gather
         for (int i = lane; i < len[b]; i += 32) sids[cat[b] + i] = A.bucket[pos[b] + i];
     }
     __syncwarp();
-#pragma unroll
+    // every deposit's merged position: its index in its own bucket plus its
+    // rank in each other bucket. The loops are deliberately not unrolled
+    // (2^d x 2^d inlined searches overflow the instruction cache for d = 3);
+    // the per-corner extents are read from registers by a select.
+#pragma unroll 1
     for (int qq = 0; qq < NC; ++qq) {
-      for (int i = lane; i < len[qq]; i += 32) {
-        const int src = staged ? sids[cat[qq] + i] : A.bucket[pos[qq] + i];
-        int fin = i;
+      int lq = 0, cq = 0, pq = 0;
 #pragma unroll
-        for (int o = 0; o < NC; ++o)
-          if (o != qq && len[o] > 0)
-            fin += staged ? lower_bound_ids(sids + cat[o], len[o], src)
-                          : lower_bound_ids(A.bucket + pos[o], len[o], src);
-        buf[fin] = (qq & A.cmask[src]) ? 0.0 : deposit_weight(A, src, qq);
+      for (int b = 0; b < NC; ++b)
+        if (b == qq) {
+          lq = len[b];
+          cq = cat[b];
+          pq = pos[b];
+        }
+      for (int i = lane; i < lq; i += 32) {
+        const int src = staged ? sids[cq + i] : A.bucket[pq + i];
+        int fin = i;
+#pragma unroll 1
+        for (int o = 0; o < NC; ++o) {
+          int lo_ = 0, co = 0, po = 0;
+#pragma unroll
+          for (int b = 0; b < NC; ++b)
+            if (b == o) {
+              lo_ = len[b];
+              co = cat[b];
+              po = pos[b];
+            }
+          if (o != qq && lo_ > 0)
+            fin += staged ? lower_bound_ids(sids + co, lo_, src) : lower_bound_ids(A.bucket + po, lo_, src);
+        }
+        buf[fin] = pos_weight(A, pq + i, qq);
       }
     }
     __syncwarp();
@@ -435,7 +494,7 @@ __global__ void __launch_bounds__(kLargeThreads) pf_gather_large_kernel(GatherAr
         int fin = i;
         for (int o = 0; o < nl; ++o)
           if (o != qq) fin += lower_bound_ids(ids + s_cat[o], s_end[o] - s_pos[o], src);
-        buf[fin] = (b & A.cmask[src]) ? 0.0 : deposit_weight(A, src, b);
+        buf[fin] = pos_weight(A, s_pos[qq] + i, b);
       }
     }
     __syncthreads();
@@ -505,7 +564,7 @@ __global__ void __launch_bounds__(512) pf_gather_heavy_kernel(GatherArgs A, cons
           fin += staged ? lower_bound_ids(ids + s_cat[o], s_end[o] - s_pos[o], src)
                         : lower_bound_ids(A.bucket + s_pos[o], s_end[o] - s_pos[o], src);
         }
-        buf[fin] = (b & A.cmask[src]) ? 0.0 : deposit_weight(A, src, b);
+        buf[fin] = pos_weight(A, p0 + i, b);
       }
     }
     __syncthreads();
@@ -693,7 +752,7 @@ PushforwardPlan::~PushforwardPlan() {
                   static_cast<void*>(off_), static_cast<void*>(end_), static_cast<void*>(heavy_),
                   static_cast<void*>(nheavy_), static_cast<void*>(hbuf_),
                   static_cast<void*>(row0_), static_cast<void*>(bcount_),
-                  static_cast<void*>(large_)})
+                  static_cast<void*>(large_), static_cast<void*>(rec_), static_cast<void*>(rmask_)})
     if (p) dfree(p);
   if (hcounts_) cudaFreeHost(hcounts_);
 }
@@ -751,6 +810,10 @@ void PushforwardPlan::ensure_records(long nrec) {
   const long hcap = std::max<long>(deposits, std::max<long>(static_cast<long>(med_blocks_) * kMedWarps * kMedium,
                                                             static_cast<long>(large_blocks_) * kLarge));
   BFM_CUDA(dmalloc(&hbuf_, hcap * sizeof(double)));
+  if (rec_) dfree(rec_);
+  if (rmask_) dfree(rmask_);
+  BFM_CUDA(dmalloc(&rec_, cap * sizeof(double4)));
+  BFM_CUDA(dmalloc(&rmask_, cap * sizeof(uint8_t)));
   sorter_.init(cap);
   rec_cap_ = cap;
 }
@@ -805,9 +868,17 @@ void PushforwardPlan::gather(long nrec, const uint32_t* d_keys, const double* d_
   const int* svals = nullptr;
   if (nrec > 0) {
     const uint32_t* skeys = nullptr;
-    sorter_.sort(d_keys, nullptr, nrec, key_bits_, stream, lc, &skeys, &svals);
-    pf_bounds_kernel<<<grid_for(nrec, 256), 256, 0, stream>>>(
-        skeys, nrec, static_cast<uint32_t>(ncells_), off_, end_);
+    // massless sources (sentinel keys) deposit nothing: a stable compaction
+    // drops them before the sort (their count stays on the device)
+    const uint32_t sentinel = static_cast<uint32_t>(ncells_);
+    const uint32_t* ckeys = nullptr;
+    const int* cvals = nullptr;
+    const int* d_n = sorter_.compact(d_keys, nrec, sentinel, stream, lc, &ckeys, &cvals);
+    sorter_.sort(ckeys, cvals, nrec, key_bits_, stream, lc, &skeys, &svals, d_n);
+    pf_bounds_kernel<<<grid_for(nrec, 256), 256, 0, stream>>>(skeys, nrec, d_n, sentinel, off_, end_);
+    pf_pack_kernel<<<grid_for(nrec, 256), 256, 0, stream>>>(svals, nrec, d_n, d_mass, d_w, d_cmask, g_.d, rec_,
+                                                             rmask_);
+    BFM_LAUNCH_CHECK("pf_pack_kernel");
   }
   GatherArgs G{};
   G.g = g_;
@@ -822,6 +893,8 @@ void PushforwardPlan::gather(long nrec, const uint32_t* d_keys, const double* d_
   G.src = d_mass;
   G.target = d_target;
   G.out = d_out;
+  G.rec = rec_;
+  G.rmask = rmask_;
   int* nheavy = reinterpret_cast<int*>(nheavy_);
   if (g_.d == 1) pf_gather_kernel<1><<<grid_for(N, 256), 256, 0, stream>>>(G, heavy_, large_, nheavy);
   else if (g_.d == 2) pf_gather_kernel<2><<<grid_for(N, 256), 256, 0, stream>>>(G, heavy_, large_, nheavy);
@@ -838,7 +911,7 @@ void PushforwardPlan::gather(long nrec, const uint32_t* d_keys, const double* d_
   BFM_LAUNCH_CHECK("pf_gather_large_kernel");
   pf_gather_heavy_kernel<<<2 * 148, 512, kHeavySmem, stream>>>(G, heavy_, nheavy, hbuf_, nheavy_ + 1);
   BFM_LAUNCH_CHECK("pf_gather_heavy_kernel");
-  if (lc) lc->add(nrec > 0 ? 5 : 4);
+  if (lc) lc->add(nrec > 0 ? 6 : 4);
 }
 
 void PushforwardPlan::set_partition(int P, const int* row_starts) {

@@ -19,8 +19,9 @@ constexpr int kBins = 1 << kBits;
 constexpr int kTile = kThreads * kItems;
 constexpr int kWarps = kThreads / 32;
 
-__global__ void __launch_bounds__(kThreads) rs_hist_kernel(const uint32_t* keys, long n, int shift,
-                                                         long nblocks, int* hist) {
+__global__ void __launch_bounds__(kThreads) rs_hist_kernel(const uint32_t* keys, long n_max, const int* d_n,
+                                                         int shift, long nblocks, int* hist) {
+  const long n = d_n ? *d_n : n_max;
   __shared__ int h[kBins];
   for (int q = threadIdx.x; q < kBins; q += kThreads) h[q] = 0;
   __syncthreads();
@@ -115,9 +116,10 @@ __global__ void __launch_bounds__(1024) rs_scan_apply(int* a, long m, const int*
 }
 
 __global__ void __launch_bounds__(kThreads) rs_scatter_kernel(const uint32_t* kin, const int* vin,
-                                                            long n, int shift, long nblocks,
-                                                            const int* hist, uint32_t* kout,
+                                                            long n_max, const int* d_n, int shift,
+                                                            long nblocks, const int* hist, uint32_t* kout,
                                                             int* vout) {
+  const long n = d_n ? *d_n : n_max;
   __shared__ int gbase[kBins];
   __shared__ int run[kBins];
   __shared__ int wcnt[kWarps][kBins];
@@ -169,6 +171,47 @@ __global__ void __launch_bounds__(kThreads) rs_scatter_kernel(const uint32_t* ki
   }
 }
 
+// Stable compaction of the (key, index) pairs whose key differs from the
+// sentinel: per-tile counts, an exclusive scan (the total lands in entry nb),
+// then each tile writes its kept pairs in input order.
+__global__ void __launch_bounds__(kThreads) rs_count_kernel(const uint32_t* keys, long n, uint32_t sentinel,
+                                                          int* cnt) {
+  const long base = static_cast<long>(blockIdx.x) * kTile;
+  int c = 0;
+#pragma unroll
+  for (int r = 0; r < kItems; ++r) {
+    const long i = base + static_cast<long>(r) * kThreads + threadIdx.x;
+    c += (i < n && keys[i] != sentinel) ? 1 : 0;
+  }
+  __shared__ int tot;
+  block_exscan(c, &tot);
+  if (threadIdx.x == 0) cnt[blockIdx.x] = tot;
+}
+
+__global__ void __launch_bounds__(kThreads) rs_compact_kernel(const uint32_t* keys, long n, uint32_t sentinel,
+                                                            const int* off, uint32_t* kout, int* vout) {
+  const long base = static_cast<long>(blockIdx.x) * kTile;
+  __shared__ int tot;
+  int run = off[blockIdx.x];
+  uint32_t kr[kItems];
+#pragma unroll
+  for (int r = 0; r < kItems; ++r) {
+    const long i = base + static_cast<long>(r) * kThreads + threadIdx.x;
+    kr[r] = i < n ? keys[i] : sentinel;
+  }
+#pragma unroll
+  for (int r = 0; r < kItems; ++r) {
+    const long i = base + static_cast<long>(r) * kThreads + threadIdx.x;
+    const bool keep = kr[r] != sentinel;
+    const int pre = block_exscan(keep ? 1 : 0, &tot);
+    if (keep) {
+      kout[run + pre] = kr[r];
+      vout[run + pre] = static_cast<int>(i);
+    }
+    run += tot;
+  }
+}
+
 }  // namespace
 
 RadixSorter::~RadixSorter() {
@@ -178,6 +221,7 @@ RadixSorter::~RadixSorter() {
   }
   if (hist_) dfree(hist_);
   if (bsum_) dfree(bsum_);
+  if (cnt_) dfree(cnt_);
 }
 
 void RadixSorter::init(long n) {
@@ -189,8 +233,10 @@ void RadixSorter::init(long n) {
   }
   if (hist_) dfree(hist_);
   if (bsum_) dfree(bsum_);
+  if (cnt_) dfree(cnt_);
   hist_ = nullptr;
   bsum_ = nullptr;
+  cnt_ = nullptr;
   cap_ = n;
   blocks_ = (n + kTile - 1) / kTile;
   for (int i = 0; i < 2; ++i) {
@@ -200,10 +246,11 @@ void RadixSorter::init(long n) {
   const long m = static_cast<long>(kBins) * blocks_;
   BFM_CUDA(dmalloc(&hist_, (m + 1) * sizeof(int)));
   BFM_CUDA(dmalloc(&bsum_, ((m + kScanTile - 1) / kScanTile + 1) * sizeof(int)));
+  BFM_CUDA(dmalloc(&cnt_, (blocks_ + 2) * sizeof(int)));
 }
 
 void RadixSorter::sort(const uint32_t* keys_in, const int* vals_in, long n, int bits, cudaStream_t s,
-                       LaunchCounter* lc, const uint32_t** keys_out, const int** vals_out) {
+                       LaunchCounter* lc, const uint32_t** keys_out, const int** vals_out, const int* d_n) {
   const long nb = (n + kTile - 1) / kTile;
   const long m = static_cast<long>(kBins) * nb;
   const long sb = (m + kScanTile - 1) / kScanTile;
@@ -211,11 +258,11 @@ void RadixSorter::sort(const uint32_t* keys_in, const int* vals_in, long n, int 
   const int* vin = vals_in;
   int cur = 0;
   for (int shift = 0; shift < bits; shift += kBits) {
-    rs_hist_kernel<<<static_cast<unsigned>(nb), kThreads, 0, s>>>(kin, n, shift, nb, hist_);
+    rs_hist_kernel<<<static_cast<unsigned>(nb), kThreads, 0, s>>>(kin, n, d_n, shift, nb, hist_);
     rs_scan_reduce<<<static_cast<unsigned>(sb), 1024, 0, s>>>(hist_, m, bsum_);
     rs_scan_top<<<1, 1024, 0, s>>>(bsum_, sb);
     rs_scan_apply<<<static_cast<unsigned>(sb), 1024, 0, s>>>(hist_, m, bsum_);
-    rs_scatter_kernel<<<static_cast<unsigned>(nb), kThreads, 0, s>>>(kin, vin, n, shift, nb, hist_,
+    rs_scatter_kernel<<<static_cast<unsigned>(nb), kThreads, 0, s>>>(kin, vin, n, d_n, shift, nb, hist_,
                                                                      kbuf_[cur], vbuf_[cur]);
     BFM_LAUNCH_CHECK("radix sort pass");
     if (lc) lc->add(5);
@@ -225,6 +272,30 @@ void RadixSorter::sort(const uint32_t* keys_in, const int* vals_in, long n, int 
   }
   *keys_out = kin;
   *vals_out = vin;
+}
+
+}  // namespace bfmgpu
+
+namespace bfmgpu {
+
+const int* RadixSorter::compact(const uint32_t* keys_in, long n, uint32_t sentinel, cudaStream_t s,
+                                LaunchCounter* lc, const uint32_t** keys_out, const int** vals_out) {
+  const long nb = (n + kTile - 1) / kTile;
+  const long m = nb + 1;  // entry nb receives the total
+  const long sb = (m + kScanTile - 1) / kScanTile;
+  BFM_CUDA(cudaMemsetAsync(cnt_ + nb, 0, sizeof(int), s));
+  rs_count_kernel<<<static_cast<unsigned>(nb), kThreads, 0, s>>>(keys_in, n, sentinel, cnt_);
+  rs_scan_reduce<<<static_cast<unsigned>(sb), 1024, 0, s>>>(cnt_, m, bsum_);
+  rs_scan_top<<<1, 1024, 0, s>>>(bsum_, sb);
+  rs_scan_apply<<<static_cast<unsigned>(sb), 1024, 0, s>>>(cnt_, m, bsum_);
+  // kbuf_/vbuf_[1]: the first sort pass reads them and writes buffer 0
+  rs_compact_kernel<<<static_cast<unsigned>(nb), kThreads, 0, s>>>(keys_in, n, sentinel, cnt_, kbuf_[1],
+                                                                   vbuf_[1]);
+  BFM_LAUNCH_CHECK("radix compact");
+  if (lc) lc->add(5);
+  *keys_out = kbuf_[1];
+  *vals_out = vbuf_[1];
+  return cnt_ + nb;
 }
 
 }  // namespace bfmgpu

@@ -20,8 +20,13 @@ class RadixSorter {
   void init(long n);
   // Sorts keys[0,n) (values = element index when vals_in == nullptr) by the
   // low `bits` key bits, stably. Result pointers valid until the next call.
+  // d_n (optional): device-side element count <= n (n sizes the grids).
   void sort(const uint32_t* keys_in, const int* vals_in, long n, int bits, cudaStream_t s,
-            LaunchCounter* lc, const uint32_t** keys_out, const int** vals_out);
+            LaunchCounter* lc, const uint32_t** keys_out, const int** vals_out, const int* d_n = nullptr);
+  // Stable compaction of the pairs (keys_in[i], i) with keys_in[i] != sentinel
+  // into the sorter's buffers; returns the device pointer of the kept count.
+  const int* compact(const uint32_t* keys_in, long n, uint32_t sentinel, cudaStream_t s, LaunchCounter* lc,
+                     const uint32_t** keys_out, const int** vals_out);
 
  private:
   long cap_ = 0;
@@ -30,6 +35,7 @@ class RadixSorter {
   int* vbuf_[2] = {nullptr, nullptr};
   int* hist_ = nullptr;   // [256 * blocks]
   int* bsum_ = nullptr;   // scan scratch
+  int* cnt_ = nullptr;    // [blocks + 2] compaction tile counts -> offsets, total at [blocks]
 };
 
 }  // namespace bfmgpu

@@ -1,5 +1,5 @@
 # pushforward iteration loop (run via gpurun): GPU parity tests, short bench, launch list
-timeout 600 python -m pytest tests -m gpu -x -q > gpurun_out/t.log 2>&1; tail -3 gpurun_out/t.log
+[ -n "$SKIP_TESTS" ] || { timeout 600 python -m pytest tests -m gpu -x -q > gpurun_out/t.log 2>&1; tail -3 gpurun_out/t.log; }
 timeout 200 python bench.py --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/b.log 2>&1
 python - <<'PY'
 import json; d = json.loads(open("gpurun_out/b.log").read().strip().splitlines()[-1])
