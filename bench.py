@@ -231,7 +231,7 @@ def live_roofline(ops, shape, hbm, hbm_kind):
             traffic = None
     return {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
             "frac": achieved / hbm, "traffic": traffic,
-            "kernel": f"c-transform ({d} ct_pass_kernel launches per call), {calls} calls in the timed region",
+            "kernel": f"c-transform ({d} axis-pass launches per call: ct_dy_kernel on dyadic grids, ct_pass_kernel otherwise), {calls} calls in the timed region",
             "ms_per_call": ms, "algorithmic_bytes_per_call": bytes_alg, "peak_kind": hbm_kind}
 
 
