@@ -498,18 +498,32 @@ __global__ void __launch_bounds__(kLargeThreads) pf_gather_large_kernel(GatherAr
       }
     }
     __syncthreads();
-    if (threadIdx.x == 0) {
-      double rho = 0.0;  // zero weights: see the medium kernel
-      int i = 0;
-      for (; i + 8 <= K; i += 8) {
-        double x[8];
+    // warp 0 folds the weights in order (zero weights: see the medium
+    // kernel): its lanes load 32 consecutive weights per round (coalesced,
+    // one round ahead of the chain) and every lane runs the same chain of
+    // adds fed by shuffles — the reference's sequential sum, bit for bit
+    if (threadIdx.x < 32) {
+      const int lane = threadIdx.x;
+      double rho = 0.0;
+      double nxt = lane < K ? buf[lane] : 0.0;
+      for (int c = 0; c < K; c += 32) {
+        const double v = nxt;
+        nxt = c + 32 + lane < K ? buf[c + 32 + lane] : 0.0;
+        const int cnt = min(32, K - c);
+        if (cnt == 32) {
 #pragma unroll
-        for (int u = 0; u < 8; ++u) x[u] = buf[i + u];
+          for (int i0 = 0; i0 < 32; i0 += 8) {
+            double x[8];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) rho += x[u];
+            for (int i = 0; i < 8; ++i) x[i] = __shfl_sync(0xffffffffu, v, i0 + i);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) rho += x[i];
+          }
+        } else {
+          for (int i = 0; i < cnt; ++i) rho += __shfl_sync(0xffffffffu, v, i);
+        }
       }
-      for (; i < K; ++i) rho += buf[i];
-      A.out[t] = A.target ? A.target[t] - rho : rho;
+      if (lane == 0) A.out[t] = A.target ? A.target[t] - rho : rho;
     }
     __syncthreads();
   }
