@@ -6,27 +6,23 @@
 // toward -inf (-0 -> +0). The minimum is unique, so any exact algorithm gives
 // the reference's bits (checked against oracle/_ref in tests/).
 //
-// Design (one kernel per axis pass, reference axis order 0..d-1):
-//  * Inter-pass state is the argmin INDEX chain (uint32: j0 | j1<<16), not an
-//    expansion: the exact candidate value is recomputed from the chain, one
-//    phi gather and the per-axis g_a(k,j) = hs(x_k)+hs(y_j)-x_k*y_j terms
-//    (an exact double 0.5*(x-y)^2 on dyadic grids, an exact double-double
-//    table otherwise). Traffic per pass: read phi or (chain + gathered phi),
-//    write chain or psi — the 16*d B/node algorithmic figure of SURVEY §8(d).
-//  * Per grid line (staged in shared memory, TPL threads per line): the
-//    minimisation min_j f_j - x_k*y_j is a discrete Legendre transform. Each
-//    thread builds the lower hull of its chunk (monotone chain, fp64
-//    orientation that pops anything not CERTIFIED strictly convex), a
-//    log2(TPL)-level tree merges neighbouring hulls by bridge walks, the hull
-//    is compacted, and every non-corner point is checked against its hull
-//    edge: a point above the edge by more than the rounding bound can never
-//    be a minimiser; closer points are flagged "suspect" with their slack.
-//  * Each query walks to its tangent corner, expands to every corner within
-//    a rigorous margin of the approximate minimum, and adds the suspects of
-//    the adjacent edges. One candidate (the normal case) is the exact
-//    argmin with no exact arithmetic at all; otherwise candidates are
-//    compared with exact expansion arithmetic (exact.cuh).
-//  * The last pass rounds the winner's exact value down once.
+// One kernel launch per axis pass, reference axis order 0..d-1. Inter-pass
+// state is the argmin INDEX chain (uint32: j0 | j1<<16) plus phi at the chain
+// (q): the exact candidate value is recomputed from the chain and the per-axis
+// terms g_a(k,j) = hs(x_k)+hs(y_j)-x_k*y_j. Two kernels:
+//  * ct_dy_kernel (every extent a power of two; see the section header
+//    below): an EXACT lower hull with strict corners, every exact decision
+//    made on shared-memory-resident exact data.
+//  * ct_pass_kernel (other extents, e.g. C4's 384^3): g from exact 3-limb host
+//    tables; per grid line (staged in shared memory, tpl threads per line) the
+//    lower hull is built with fp64 orientation tests that only keep CERTIFIED
+//    strict corners (monotone chains + a log2(tpl)-level bridge-merge tree),
+//    every non-corner point within the rounding bound of its hull edge is
+//    flagged "suspect" (log-coded per-edge slack), each query walks to its
+//    tangent corner, and queries whose neighbourhood is not certified are
+//    resolved exactly among the corners and suspects within a rigorous
+//    margin (exact.cuh expansions). The last pass rounds the winner's exact
+//    value down once.
 #include <cassert>
 #include <cmath>
 #include <cstdlib>
@@ -140,9 +136,8 @@ __device__ __forceinline__ bool convex3(double ya, double fa, double yb, double 
 }
 
 struct Smem {
-  double* fh;          // f~_j (DY: exact high part of f_j)
-  double* fl;          // DY: exact low part (f_j = fh + fl)
-  uint32_t* chain;     // !DY: argmin chain of element j
+  double* fh;          // f~_j
+  uint32_t* chain;     // argmin chain of element j
   uint16_t* hidx;      // chunk hull stacks, later per-query winners
   uint16_t* H;         // compacted hull corners
   uint8_t* dlt;        // per-edge slack code (0: no suspects)
@@ -158,7 +153,6 @@ __device__ __forceinline__ Smem carve(const CtPass& p, unsigned char* base, int 
   Smem s;
   unsigned char* b = base + static_cast<long>(l) * p.line_bytes;
   s.fh = reinterpret_cast<double*>(b + p.off_fv);
-  s.fl = reinterpret_cast<double*>(b + p.off_chain);
   s.chain = reinterpret_cast<uint32_t*>(b + p.off_chain);
   s.hidx = reinterpret_cast<uint16_t*>(b + p.off_hidx);
   s.H = reinterpret_cast<uint16_t*>(b + p.off_H);
@@ -208,13 +202,11 @@ __device__ __forceinline__ void slack_max(uint8_t* dlt, int e, uint8_t c) {
   }
 }
 
-// Threads per CTA (lpc * tpl) at most: dyadic lines get 768 (an 80-register
-// budget keeps their query phases nearly spill-free); the non-dyadic variant,
-// whose exact path lives in local memory anyway, runs faster at 1024.
-constexpr int ct_threads(bool dy) { return dy ? 768 : 1024; }
+// Threads per CTA (lpc * tpl) at most for the non-dyadic kernel (its exact
+// path lives in local memory anyway; 1024 measured fastest).
+constexpr int kNdThreads = 1024;
 
-template <bool DY>
-__global__ void __launch_bounds__(ct_threads(DY)) ct_pass_kernel(CtPass p) {
+__global__ void __launch_bounds__(kNdThreads) ct_pass_kernel(CtPass p) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int tpl = p.tpl;
   const int l = threadIdx.x / tpl;
@@ -259,9 +251,7 @@ __global__ void __launch_bounds__(ct_threads(DY)) ct_pass_kernel(CtPass p) {
       tph = now;
     }
   };
-  // ---- load: every element copied asynchronously (cp.async) -------------
-  // DY: fh <- phi_j (exact), fl <- G_j = sum_{b<a} g_b(k_b, j_b*) (exact);
-  // !DY: fh <- f~_j, chain <- chain_j.
+  // ---- load: phi at the chain (cp.async) into fh, the chain into chain ---
   {
     const int ml = p.strided ? static_cast<int>(threadIdx.x % lpc) : l;
     const Smem sm = carve(p, smem, ml);
@@ -270,10 +260,7 @@ __global__ void __launch_bounds__(ct_threads(DY)) ct_pass_kernel(CtPass p) {
     const int first = p.strided ? static_cast<int>(threadIdx.x / lpc) : t;
     for (int j = first; j < n + 4; j += step) sm.dlt[j] = 0;
     if (g.valid) {
-      if (p.a == 0 && DY) {
-        for (int j = first; j < n; j += step)
-          cp_async8(&sm.fh[padj(j)], &p.phi[g.phi_other + static_cast<long>(j) * A.stride]);
-      } else {
+      {
         constexpr int kBatch = 8;
         for (int j0 = first; j0 < n; j0 += kBatch * step) {
           uint32_t ch[kBatch];
@@ -286,12 +273,8 @@ __global__ void __launch_bounds__(ct_threads(DY)) ct_pass_kernel(CtPass p) {
           for (int u = 0; u < kBatch; ++u) {
             const int j = j0 + u * step;
             if (j >= n) continue;
-            double G = 0.0;
-            if (p.a >= 1) G += g_approx(p.ax[0], g.k[0], static_cast<int>(ch[u] & 0xFFFFu));
-            if (p.a >= 2) G += g_approx(p.ax[1], g.k[1], static_cast<int>(ch[u] >> 16));
-            const double* src = &p.phi[phi_index(p, g, ch[u], j)];
-            cp_async8(&sm.fh[padj(j)], src);
-            if (!DY && p.a > 0) sm.chain[j] = ch[u];
+            cp_async8(&sm.fh[padj(j)], &p.phi[phi_index(p, g, ch[u], j)]);
+            if (p.a > 0) sm.chain[j] = ch[u];
           }
         }
       }
@@ -307,29 +290,15 @@ __global__ void __launch_bounds__(ct_threads(DY)) ct_pass_kernel(CtPass p) {
       for (int j = t; j < n; j += tpl) {
         const double y = coord(h, j);
         const double hy = 0.5 * y * y;
-        double f, S;
-        if (DY) {
-          // f~_j = fl((G_j + hs(y_j)) - phi_j) in place of phi_j (G exact)
-          const double ph = s.fh[padj(j)];
-          double G = 0.0;
-          if (p.a > 0) {
-            const uint32_t ch = p.state_in[g.base + static_cast<long>(j) * A.stride];
-            G = g_approx(p.ax[0], g.k[0], static_cast<int>(ch & 0xFFFFu));
-            if (p.a >= 2) G += g_approx(p.ax[1], g.k[1], static_cast<int>(ch >> 16));
-          }
-          f = (G + hy) - ph;
-          s.fh[padj(j)] = f;
-          S = fabs(ph) + G + hy;
-        } else {
-          const double ph = s.fh[padj(j)];
-          const uint32_t ch = p.a > 0 ? s.chain[j] : 0u;
-          double G = 0.0;
-          if (p.a >= 1) G += g_approx(p.ax[0], g.k[0], static_cast<int>(ch & 0xFFFFu));
-          if (p.a >= 2) G += g_approx(p.ax[1], g.k[1], static_cast<int>(ch >> 16));
-          f = (-ph + G) + hy;
-          s.fh[padj(j)] = f;
-          S = fabs(ph) + G + hy;
-        }
+        // f~_j = fl(fl(-phi_j + G~_j) + hs(y_j)) in place of phi_j
+        const double ph = s.fh[padj(j)];
+        const uint32_t ch = p.a > 0 ? s.chain[j] : 0u;
+        double G = 0.0;
+        if (p.a >= 1) G += g_approx(p.ax[0], g.k[0], static_cast<int>(ch & 0xFFFFu));
+        if (p.a >= 2) G += g_approx(p.ax[1], g.k[1], static_cast<int>(ch >> 16));
+        const double f = (-ph + G) + hy;
+        s.fh[padj(j)] = f;
+        const double S = fabs(ph) + G + hy;
         amax = fmax(amax, fabs(f));
         smax = fmax(smax, S);
       }
@@ -349,8 +318,8 @@ __global__ void __launch_bounds__(ct_threads(DY)) ct_pass_kernel(CtPass p) {
   const bool active = geo.valid;
   const double Aabs = bitsd(s.scal[0]);
   const double Smax = bitsd(s.scal[1]);
-  const double e_f = DY ? kU * Aabs : 8.0 * kU * Smax;  // |f_j - f~_j|
-  const double e_r = 4.0 * kU * (Aabs + 1.0);           // |F^ - (f~ - x y)|
+  const double e_f = 8.0 * kU * Smax;          // |f_j - f~_j|
+  const double e_r = 4.0 * kU * (Aabs + 1.0);  // |F^ - (f~ - x y)|
   const double e_F = e_f + e_r;
   const double e_d = 32.0 * kU * Aabs;                  // chord slack error
   const double tau = 2.0 * e_f + e_d;
@@ -360,17 +329,7 @@ __global__ void __launch_bounds__(ct_threads(DY)) ct_pass_kernel(CtPass p) {
   const int j1 = min(n, j0 + C);
   uint16_t* st = s.hidx + t * (C + 2);
   auto P_y = [&](int idx) { return coord(h, idx); };
-  // f~_j: DY recomputes fl((G_j + hs(y_j)) - phi_j) from the stored exact parts
   auto P_f = [&](int idx) { return s.fh[padj(idx)]; };
-  // DY exact parts of candidate j, re-read from L2: G_j (exact) and phi_j.
-  auto dy_parts = [&](int j, double& G, double& ph) {
-    uint32_t ch = 0u;
-    if (p.a > 0) ch = p.state_in[geo.base + static_cast<long>(j) * A.stride];
-    G = 0.0;
-    if (p.a >= 1) G += g_approx(p.ax[0], geo.k[0], static_cast<int>(ch & 0xFFFFu));
-    if (p.a >= 2) G += g_approx(p.ax[1], geo.k[1], static_cast<int>(ch >> 16));
-    ph = p.phi[phi_index(p, geo, ch, j)];
-  };
 
   PH(0);  // load + maxima
   // ---- 0. convex fast path: every interior point a certified strict corner?
@@ -544,18 +503,11 @@ __global__ void __launch_bounds__(ct_threads(DY)) ct_pass_kernel(CtPass p) {
       return (P_f(b) - P_f(a)) >= xk * (P_y(b) - P_y(a));
     };
     // exact value V(k, j) rounded down (last pass)
-    auto rd_value = [&](int j, int k, double xk) {
-      if (DY) {
-        double G, ph;
-        dy_parts(j, G, ph);
-        const double dl = xk - coord(h, j);
-        return bfmx::round_down2(G + 0.5 * dl * dl, -ph);
-      } else {
-        double tv[12];
-        const uint32_t ch = p.a > 0 ? s.chain[j] : 0u;
-        const int m = cand_terms(p, geo, ch, j, k, tv);
-        return bfmx::round_down_sum(tv, m);
-      }
+    auto rd_value = [&](int j, int k) {
+      double tv[12];
+      const uint32_t ch = p.a > 0 ? s.chain[j] : 0u;
+      const int m = cand_terms(p, geo, ch, j, k, tv);
+      return bfmx::round_down_sum(tv, m);
     };
     // ---- 5a. tangent corner of every query: balanced merge path of the
     //          query slopes x_k against the hull-edge slopes (ties: query first)
@@ -672,7 +624,7 @@ __global__ void __launch_bounds__(ct_threads(DY)) ct_pass_kernel(CtPass p) {
       const LineGeo geo = *s.geo;
       const double Aabs = bitsd(s.scal[0]);
       const double Smax = bitsd(s.scal[1]);
-      const double e_f = DY ? kU * Aabs : 8.0 * kU * Smax;
+      const double e_f = 8.0 * kU * Smax;
       const double e_r = 4.0 * kU * (Aabs + 1.0);
       const double Mc = 4.0 * (e_f + e_r);
       const double sref = fmax(Smax, 1e-300);
@@ -683,27 +635,12 @@ __global__ void __launch_bounds__(ct_threads(DY)) ct_pass_kernel(CtPass p) {
       auto P_f = [&](int idx) { return s.fh[padj(idx)]; };
       auto HH = [&](int i) { return convex_line ? i : static_cast<int>(s.H[i]); };
       auto Fhat = [&](int idx, double xk) { return P_f(idx) - xk * P_y(idx); };
-      auto dy_parts = [&](int j, double& G, double& ph) {
-        uint32_t ch = 0u;
-        if (p.a > 0) ch = p.state_in[geo.base + static_cast<long>(j) * A.stride];
-        G = 0.0;
-        if (p.a >= 1) G += g_approx(p.ax[0], geo.k[0], static_cast<int>(ch & 0xFFFFu));
-        if (p.a >= 2) G += g_approx(p.ax[1], geo.k[1], static_cast<int>(ch >> 16));
-        ph = p.phi[phi_index(p, geo, ch, j)];
-      };
       // exact value V(k, j) rounded down (last pass)
-      auto rd_value = [&](int j, int k, double xk) {
-        if (DY) {
-          double G, ph;
-          dy_parts(j, G, ph);
-          const double dl = xk - coord(h, j);
-          return bfmx::round_down2(G + 0.5 * dl * dl, -ph);
-        } else {
-          double tv[12];
-          const uint32_t ch = p.a > 0 ? s.chain[j] : 0u;
-          const int m = cand_terms(p, geo, ch, j, k, tv);
-          return bfmx::round_down_sum(tv, m);
-        }
+      auto rd_value = [&](int j, int k) {
+        double tv[12];
+        const uint32_t ch = p.a > 0 ? s.chain[j] : 0u;
+        const int m = cand_terms(p, geo, ch, j, k, tv);
+        return bfmx::round_down_sum(tv, m);
       };
       const int k = s.flist[fi];
       const int rv = res[k];
@@ -764,26 +701,10 @@ __global__ void __launch_bounds__(ct_threads(DY)) ct_pass_kernel(CtPass p) {
           // RD is monotone: RD(min_j V_j) = min_j RD(V_j); no exact argmin needed.
           double best = INFINITY;
           visit([&](int j) {
-            if (Fhat(j, xk) <= Fbest + Mc) best = fmin(best, rd_value(j, k, xk));
+            if (Fhat(j, xk) <= Fbest + Mc) best = fmin(best, rd_value(j, k));
           });
           outv = best;
           have_out = true;
-        } else if (DY) {
-          // exact: V_j = two_sum(Gsum_j, -phi_j) normalised; compare lexicographically
-          int bestj = -1;
-          double bh = 0.0, bl = 0.0;
-          visit([&](int j) {
-            if (Fhat(j, xk) > Fbest + Mc) return;
-            double vh, vl, G, ph;
-            dy_parts(j, G, ph);
-            const double dl = xk - coord(h, j);
-            bfmx::two_sum(G + 0.5 * dl * dl, -ph, vh, vl);
-            if (bestj >= 0 && (vh > bh || (vh == bh && vl >= bl))) return;
-            bestj = j;
-            bh = vh;
-            bl = vl;
-          });
-          win = bestj;
         } else {
           int bestj = -1;
           double bt[12];
@@ -806,7 +727,7 @@ __global__ void __launch_bounds__(ct_threads(DY)) ct_pass_kernel(CtPass p) {
       }
       BFM_DASSERT(win >= 0 && win < n);
       if (p.last) {
-        if (!have_out) outv = rd_value(win, k, xk);
+        if (!have_out) outv = rd_value(win, k);
         p.out[geo.base + static_cast<long>(k) * A.stride] = outv;
         res[k] = 0xffffu;  // done
       } else {
@@ -818,35 +739,23 @@ __global__ void __launch_bounds__(ct_threads(DY)) ct_pass_kernel(CtPass p) {
   else group_sync(tpl, l);
   PH(8);  // flagged queries
   if (p.last && active) {
-    // lone queries: final round-downs, batched so the L2 loads overlap
+    // lone queries: final round-downs
     constexpr int kB = 8;
     for (int kk = t; kk < n; kk += kB * tpl) {
-      double G[kB], ph[kB];
       int wv[kB];
 #pragma unroll
       for (int u = 0; u < kB; ++u) {
         const int k = kk + u * tpl;
         wv[u] = (k < n) ? static_cast<int>(res[k]) : 0xffff;
-        G[u] = 0.0;
-        ph[u] = 0.0;
-        if (DY && wv[u] != 0xffff) dy_parts(wv[u], G[u], ph[u]);
       }
 #pragma unroll
       for (int u = 0; u < kB; ++u) {
         const int k = kk + u * tpl;
         if (wv[u] == 0xffff) continue;
-        const double xk = coord(h, k);
-        double v;
-        if (DY) {
-          const double dl = xk - coord(h, wv[u]);
-          v = bfmx::round_down2(G[u] + 0.5 * dl * dl, -ph[u]);
-        } else {
-          double tv[12];
-          const uint32_t ch = p.a > 0 ? s.chain[wv[u]] : 0u;
-          const int m = cand_terms(p, geo, ch, wv[u], k, tv);
-          v = bfmx::round_down_sum(tv, m);
-        }
-        p.out[geo.base + static_cast<long>(k) * A.stride] = v;
+        double tv[12];
+        const uint32_t ch = p.a > 0 ? s.chain[wv[u]] : 0u;
+        const int m = cand_terms(p, geo, ch, wv[u], k, tv);
+        p.out[geo.base + static_cast<long>(k) * A.stride] = bfmx::round_down_sum(tv, m);
       }
     }
   }
@@ -871,7 +780,7 @@ __global__ void __launch_bounds__(ct_threads(DY)) ct_pass_kernel(CtPass p) {
         if (p.a == 0) {
           packed = static_cast<uint32_t>(win);
         } else {
-          ch = DY ? p.state_in[g.base + static_cast<long>(win) * A.stride] : sm.chain[win];
+          ch = sm.chain[win];
           packed = ch | (static_cast<uint32_t>(win) << 16);
         }
         p.state_out[node] = packed;
@@ -1721,8 +1630,8 @@ void CtPlan::setup(const GridDesc& loc, const GridDesc& global, int pb, int pe, 
     int o = 0;
     P.off_fv = o;
     o = align16(o + 8 * (n + n / 32 + 1));
-    P.off_chain = o;  // DY: fl (double, padded); else chain (uint32)
-    if (!dy && a > 0) o = align16(o + 4 * n);
+    P.off_chain = o;  // chain (uint32, passes a > 0)
+    if (a > 0) o = align16(o + 4 * n);
     P.off_hidx = o;
     o = align16(o + 2 * std::max(P.tpl * (P.C + 2), n));
     P.off_H = o;
@@ -1737,7 +1646,7 @@ void CtPlan::setup(const GridDesc& loc, const GridDesc& global, int pb, int pe, 
     o = align16(o + 64 + static_cast<int>(sizeof(LineGeo)));
     P.line_bytes = o;
     if (o > budget) throw std::invalid_argument("ctransform: grid line too long for shared memory");
-    int lpc = std::min<long>(budget / o, ct_threads(dyadic_) / P.tpl);
+    int lpc = std::min<long>(budget / o, kNdThreads / P.tpl);
     lpc = std::min(lpc, P.strided ? 16 : 8);
     if (P.tpl > 32) lpc = std::min(lpc, 15);
     lpc = static_cast<int>(std::min<long>(lpc, P.nlines));
@@ -1746,8 +1655,7 @@ void CtPlan::setup(const GridDesc& loc, const GridDesc& global, int pb, int pe, 
     P.stats = stats_;
   }
   BFM_CUDA(cudaFuncSetAttribute(ct_dy_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, budget));
-  BFM_CUDA(cudaFuncSetAttribute(ct_pass_kernel<false>,
-                                cudaFuncAttributeMaxDynamicSharedMemorySize, budget));
+  BFM_CUDA(cudaFuncSetAttribute(ct_pass_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, budget));
   ready_ = true;
 }
 
@@ -1756,8 +1664,7 @@ void CtPlan::launch(const CtPass& P, cudaStream_t stream, LaunchCounter* lc) {
   if (dyadic_)
     ct_dy_kernel<<<static_cast<unsigned>(blocks), P.lpc * P.tpl, P.lpc * P.line_bytes, stream>>>(P);
   else
-    ct_pass_kernel<false><<<static_cast<unsigned>(blocks), P.lpc * P.tpl, P.lpc * P.line_bytes,
-                            stream>>>(P);
+    ct_pass_kernel<<<static_cast<unsigned>(blocks), P.lpc * P.tpl, P.lpc * P.line_bytes, stream>>>(P);
   BFM_LAUNCH_CHECK("ct_pass_kernel");
   if (lc) lc->add();
 }
