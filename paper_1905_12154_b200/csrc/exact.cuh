@@ -90,8 +90,14 @@ struct Exp {
   }
 };
 
-// Sign of (sum a[0..na) - sum b[0..nb)), exact. na + nb <= 24.
-BFM_HD int sign_diff(const double* a, int na, const double* b, int nb) {
+// Sign of (sum a[0..na) - sum b[0..nb)), exact. na + nb <= 24. (Out of line
+// on the device: reached only when two candidates need an exact compare.)
+#if defined(__CUDACC__)
+static __host__ __device__ __noinline__
+#else
+inline
+#endif
+int sign_diff(const double* a, int na, const double* b, int nb) {
   Exp<24> e;
   e.clear();
   for (int i = 0; i < na; ++i) e.grow(a[i]);
@@ -99,8 +105,14 @@ BFM_HD int sign_diff(const double* a, int na, const double* b, int nb) {
   return e.sign();
 }
 
-// Slow exact round-down of a sum of m <= 16 doubles.
-BFM_HD double round_down_slow(const double* t, int m) {
+// Slow exact round-down of a sum of m <= 16 doubles (rare: kept out of line
+// on the device so the kernels' hot code stays small).
+#if defined(__CUDACC__)
+static __host__ __device__ __noinline__
+#else
+inline
+#endif
+double round_down_slow(const double* t, int m) {
   Exp<16> e;
   e.clear();
   for (int i = 0; i < m; ++i) e.grow(t[i]);
