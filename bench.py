@@ -8,7 +8,8 @@ run() loop body: probe + step(), solver.hpp:211-226, i.e. 4 c-transforms, 2
 ascent directions, 4 pair values, 2 axpys). Inputs are seeded synthetic
 densities of the BASELINE shapes (paper_1905_12154_b200/synthetic.py).
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c3|c4]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c1|c2|c3|c4|c5]
+  (K defaults to the config's own iteration count: C3 50, C4 30, C1 100)
   python bench.py --impl reference ...   (the reference's own CPU solver,
         oracle/_ref = unmodified headers + FFTW shim, on the host cores)
 
@@ -555,7 +556,9 @@ def ours(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=None,
+                    help="timed steps (default: the config's own iteration count, BASELINE configs: "
+                         "C1 100, C3 50, C4 30; C2 50; the C5 sweep 3; the reference arm 5)")
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c3", choices=["c1", "c2", "c3", "c4", "c5"])
@@ -567,6 +570,8 @@ def main():
     ap.add_argument("--replicas", action="store_true",
                     help="N > 1: independent single-GPU replicas instead of the slab decomposition")
     args = ap.parse_args()
+    if args.steps is None:
+        args.steps = 5 if args.impl == "reference" else {"c1": 100, "c2": 50, "c3": 50, "c4": 30, "c5": 3}[args.config]
     if args.impl == "reference":
         reference_arm(args)
     elif args.config == "c5":

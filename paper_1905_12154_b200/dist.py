@@ -116,6 +116,14 @@ class TorchComm:
                                group=self.group)
         return list(torch.split(out, recv_counts))
 
+    def alltoall_flat(self, send: torch.Tensor, send_counts: List[int],
+                      recv_counts: List[int]) -> torch.Tensor:
+        """send is already packed by destination (send_counts elements per
+        rank, in rank order); returns the packed receive buffer."""
+        out = torch.empty(sum(recv_counts), dtype=send.dtype, device=send.device)
+        self.dist.all_to_all_single(out, send, recv_counts, send_counts, group=self.group)
+        return out
+
     def allgather(self, values: Sequence[float]) -> np.ndarray:
         dist = self.dist
         dev = "cuda" if dist.get_backend(self.group) == "nccl" else "cpu"
@@ -159,6 +167,11 @@ class LocalComm:
                   recv_counts: Optional[List[int]] = None) -> List[torch.Tensor]:
         boxes = self._exchange([s.reshape(-1).clone() for s in sends])
         return [boxes[r][self.rank] for r in range(self.size)]
+
+    def alltoall_flat(self, send: torch.Tensor, send_counts: List[int],
+                      recv_counts: List[int]) -> torch.Tensor:
+        got = self.alltoallv(list(torch.split(send.reshape(-1), send_counts)), recv_counts)
+        return torch.cat(got)
 
     def allgather(self, values: Sequence[float]) -> np.ndarray:
         boxes = self._exchange(np.asarray(list(values), dtype=np.float64))
@@ -345,22 +358,34 @@ class SlabExchange:
         self.rank = comm.rank
 
     def rows_to_cols(self, x_rows: torch.Tensor) -> torch.Tensor:
+        """Row slab (nrows_r x M) -> column slab (n0 x ncols_r). Packing by
+        destination is one strided copy when the column blocks are equal;
+        the received blocks (source-rank order = row order) ARE the column
+        slab, so nothing is copied after the exchange."""
         L, r = self.L, self.rank
         nr = L.nrows[r]
-        x = x_rows.reshape(nr, L.M)
-        sends = [x[:, L.col0[q]:L.col0[q] + L.ncols[q]].contiguous() for q in range(L.P)]
         nc = L.ncols[r]
-        recv = self.comm.alltoallv(sends, [L.nrows[q] * nc for q in range(L.P)])
-        return torch.cat([recv[q].reshape(L.nrows[q], nc) for q in range(L.P)], 0).reshape(-1)
+        x = x_rows.reshape(nr, L.M)
+        if len(set(L.ncols)) == 1:
+            send = x.reshape(nr, L.P, nc).transpose(0, 1).contiguous().reshape(-1)
+        else:
+            send = torch.cat([x[:, L.col0[q]:L.col0[q] + L.ncols[q]].reshape(-1) for q in range(L.P)])
+        return self.comm.alltoall_flat(send, [nr * L.ncols[q] for q in range(L.P)],
+                                       [L.nrows[q] * nc for q in range(L.P)])
 
     def cols_to_rows(self, x_cols: torch.Tensor) -> torch.Tensor:
+        """Column slab (n0 x ncols_r) -> row slab (nrows_r x M). The row
+        blocks of the column slab are already packed by destination; one
+        strided copy interleaves the received column blocks."""
         L, r = self.L, self.rank
         nc = L.ncols[r]
-        x = x_cols.reshape(L.n0, nc)
-        sends = [x[L.row0[q]:L.row0[q] + L.nrows[q], :].contiguous() for q in range(L.P)]
         nr = L.nrows[r]
-        recv = self.comm.alltoallv(sends, [nr * L.ncols[q] for q in range(L.P)])
-        return torch.cat([recv[q].reshape(nr, L.ncols[q]) for q in range(L.P)], 1).reshape(-1)
+        out = self.comm.alltoall_flat(x_cols.reshape(-1), [L.nrows[q] * nc for q in range(L.P)],
+                                      [nr * L.ncols[q] for q in range(L.P)])
+        if len(set(L.ncols)) == 1:
+            return out.reshape(L.P, nr, nc).transpose(0, 1).contiguous().reshape(-1)
+        parts = torch.split(out, [nr * L.ncols[q] for q in range(L.P)])
+        return torch.cat([parts[q].reshape(nr, L.ncols[q]) for q in range(L.P)], 1).reshape(-1)
 
     def halo(self, u_rows: torch.Tensor) -> torch.Tensor:
         """u with the neighbours' boundary rows above and below (zeros at the

@@ -3,9 +3,9 @@
 set -x
 mkdir -p gpurun_out/prof
 python bench.py > gpurun_out/prof/bench_c3.json 2> gpurun_out/prof/bench_c3.err || exit 1
-python bench.py --config c4 --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/prof/bench_c4.json 2>/dev/null
-python bench.py --config c2 --steps 20 --warmup 3 --no-cpu-baseline > gpurun_out/prof/bench_c2.json 2>/dev/null
-python bench.py --config c1 --steps 50 --warmup 5 --no-cpu-baseline > gpurun_out/prof/bench_c1.json 2>/dev/null
+python bench.py --config c4 --warmup 3 --no-cpu-baseline > gpurun_out/prof/bench_c4.json 2>/dev/null
+python bench.py --config c2 --warmup 3 --no-cpu-baseline > gpurun_out/prof/bench_c2.json 2>/dev/null
+python bench.py --config c1 --warmup 5 --no-cpu-baseline > gpurun_out/prof/bench_c1.json 2>/dev/null
 python bench.py --config c5 --steps 3 --warmup 1 > gpurun_out/prof/bench_c5.json 2> gpurun_out/prof/bench_c5.txt
 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/prof/bench_ref_c3.json 2>/dev/null
 # launch list of the bench command itself (C3)
