@@ -29,6 +29,7 @@ namespace bfmgpu {
 namespace {
 
 constexpr int kLight = 48;
+constexpr int kSeqFold = 16384;  // heavy tier: warp-sequential fold up to this many deposits
 constexpr int kMedium = 512;   // warp-per-target tier: kLight < K <= kMedium
 constexpr int kLarge = 4096;   // CTA-per-target tier with a sequential fold: K <= kLarge
 constexpr int kLargeThreads = 128;
@@ -453,6 +454,35 @@ __global__ void __launch_bounds__(kMedWarps * 32) pf_gather_medium_kernel(Gather
   }
 }
 
+// Sequential fold of w[0..K) from +0.0 by one warp, bit for bit the
+// reference's loop (zero weights leave rho unchanged: see the medium tier):
+// the lanes load 32 consecutive weights per round (coalesced, one round
+// ahead of the chain) and every lane runs the same chain of adds fed by
+// shuffles. Call from all 32 lanes of the warp.
+__device__ __forceinline__ double warp_seq_fold(const double* w, int K) {
+  const int lane = threadIdx.x & 31;
+  double rho = 0.0;
+  double nxt = lane < K ? w[lane] : 0.0;
+  for (int c = 0; c < K; c += 32) {
+    const double v = nxt;
+    nxt = c + 32 + lane < K ? w[c + 32 + lane] : 0.0;
+    const int cnt = min(32, K - c);
+    if (cnt == 32) {
+#pragma unroll
+      for (int i0 = 0; i0 < 32; i0 += 8) {
+        double x[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) x[i] = __shfl_sync(0xffffffffu, v, i0 + i);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) rho += x[i];
+      }
+    } else {
+      for (int i = 0; i < cnt; ++i) rho += __shfl_sync(0xffffffffu, v, i);
+    }
+  }
+  return rho;
+}
+
 // Large targets (kMedium < K <= kLarge): one CTA of kLargeThreads each, ids
 // staged in shared memory, ranks and weights as above into the CTA's slice of
 // the global buffer, then one thread folds them in order (unrolled loads
@@ -498,31 +528,10 @@ __global__ void __launch_bounds__(kLargeThreads) pf_gather_large_kernel(GatherAr
       }
     }
     __syncthreads();
-    // warp 0 folds the weights in order (zero weights: see the medium
-    // kernel): its lanes load 32 consecutive weights per round (coalesced,
-    // one round ahead of the chain) and every lane runs the same chain of
-    // adds fed by shuffles — the reference's sequential sum, bit for bit
+    // warp 0 folds the weights in order (warp_seq_fold)
     if (threadIdx.x < 32) {
       const int lane = threadIdx.x;
-      double rho = 0.0;
-      double nxt = lane < K ? buf[lane] : 0.0;
-      for (int c = 0; c < K; c += 32) {
-        const double v = nxt;
-        nxt = c + 32 + lane < K ? buf[c + 32 + lane] : 0.0;
-        const int cnt = min(32, K - c);
-        if (cnt == 32) {
-#pragma unroll
-          for (int i0 = 0; i0 < 32; i0 += 8) {
-            double x[8];
-#pragma unroll
-            for (int i = 0; i < 8; ++i) x[i] = __shfl_sync(0xffffffffu, v, i0 + i);
-#pragma unroll
-            for (int i = 0; i < 8; ++i) rho += x[i];
-          }
-        } else {
-          for (int i = 0; i < cnt; ++i) rho += __shfl_sync(0xffffffffu, v, i);
-        }
-      }
+      const double rho = warp_seq_fold(buf, K);
       if (lane == 0) A.out[t] = A.target ? A.target[t] - rho : rho;
     }
     __syncthreads();
@@ -582,8 +591,17 @@ __global__ void __launch_bounds__(512) pf_gather_heavy_kernel(GatherArgs A, cons
       }
     }
     __syncthreads();
-    const double rho = exact_fold<512, 8>(buf, K, fold_scr, fold_iscr, [] { __syncthreads(); });
-    if (threadIdx.x == 0) A.out[t] = A.target ? A.target[t] - rho : rho;
+    // up to kSeqFold deposits a warp's sequential chain is cheaper than the
+    // parallel fold's transducer scans and binade restarts
+    if (K <= kSeqFold) {
+      if (threadIdx.x < 32) {
+        const double rho = warp_seq_fold(buf, K);
+        if (threadIdx.x == 0) A.out[t] = A.target ? A.target[t] - rho : rho;
+      }
+    } else {
+      const double rho = exact_fold<512, 8>(buf, K, fold_scr, fold_iscr, [] { __syncthreads(); });
+      if (threadIdx.x == 0) A.out[t] = A.target ? A.target[t] - rho : rho;
+    }
     __syncthreads();
   }
 }
