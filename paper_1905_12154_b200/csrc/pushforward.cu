@@ -358,6 +358,7 @@ __global__ void __launch_bounds__(kMedWarps * 32) pf_gather_medium_kernel(Gather
                                                                          double* hbuf) {
   constexpr int NC = 1 << D;  // per-corner state in registers (fully unrolled loops)
   extern __shared__ int med_ids[];  // [kMedWarps][kMedStage]
+  __shared__ int med_tab[kMedWarps * 24];  // per warp: the non-empty buckets' (len, cat, pos)
   const GridDesc& g = A.g;
   const int nh = nheavy[0];
   const int lane = threadIdx.x & 31;
@@ -397,32 +398,39 @@ __global__ void __launch_bounds__(kMedWarps * 32) pf_gather_medium_kernel(Gather
     // every deposit's merged position: its index in its own bucket plus its
     // rank in each other bucket. The loops are deliberately not unrolled
     // (2^d x 2^d inlined searches overflow the instruction cache for d = 3);
-    // the per-corner extents are read from registers by a select.
+    // the non-empty buckets' extents are read from a per-warp shared table.
+    int* tb = med_tab + (threadIdx.x >> 5) * 24;  // [nl][3]: len, cat, pos
+    int nl = 0;
+    int bits_of[NC];
+#pragma unroll
+    for (int b = 0; b < NC; ++b) {
+      bits_of[b] = 0;
+      if (len[b] > 0) {
+        if (lane == 0) {
+          tb[3 * nl] = len[b];
+          tb[3 * nl + 1] = cat[b];
+          tb[3 * nl + 2] = pos[b];
+        }
+        bits_of[nl] = b;
+        ++nl;
+      }
+    }
+    __syncwarp();
 #pragma unroll 1
-    for (int qq = 0; qq < NC; ++qq) {
-      int lq = 0, cq = 0, pq = 0;
+    for (int qi = 0; qi < nl; ++qi) {
+      const int lq = tb[3 * qi], cq = tb[3 * qi + 1], pq = tb[3 * qi + 2];
+      int qq = 0;
 #pragma unroll
       for (int b = 0; b < NC; ++b)
-        if (b == qq) {
-          lq = len[b];
-          cq = cat[b];
-          pq = pos[b];
-        }
+        if (b == qi) qq = bits_of[b];
       for (int i = lane; i < lq; i += 32) {
         const int src = staged ? sids[cq + i] : A.bucket[pq + i];
         int fin = i;
 #pragma unroll 1
-        for (int o = 0; o < NC; ++o) {
-          int lo_ = 0, co = 0, po = 0;
-#pragma unroll
-          for (int b = 0; b < NC; ++b)
-            if (b == o) {
-              lo_ = len[b];
-              co = cat[b];
-              po = pos[b];
-            }
-          if (o != qq && lo_ > 0)
-            fin += staged ? lower_bound_ids(sids + co, lo_, src) : lower_bound_ids(A.bucket + po, lo_, src);
+        for (int oi = 0; oi < nl; ++oi) {
+          if (oi == qi) continue;
+          const int lo_ = tb[3 * oi], co = tb[3 * oi + 1], po = tb[3 * oi + 2];
+          fin += staged ? lower_bound_ids(sids + co, lo_, src) : lower_bound_ids(A.bucket + po, lo_, src);
         }
         buf[fin] = pos_weight(A, pq + i, qq);
       }
