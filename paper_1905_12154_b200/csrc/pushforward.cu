@@ -35,9 +35,8 @@ constexpr int kLarge = 4096;   // CTA-per-target tier with a sequential fold: K 
 constexpr int kLargeThreads = 128;
 constexpr int kLargeBlocks = 148 * 8;  // each CTA owns kLarge doubles of hbuf
 constexpr int kMedWarps = 8;
-constexpr int kMedStage = 512;  // ids staged in shared memory per warp (else ranked in global)
 constexpr int kHeavyIds = 24576;
-constexpr int kMedSmem = kMedWarps * kMedStage * 4;
+constexpr int kMedSmem = kMedWarps * 2 * kMedium * (4 + 2);  // ids + payloads, ping-pong
 constexpr int kMedBlocks = 148 * 8;  // each warp owns kMedium doubles of hbuf
 constexpr int kHeavySmem = kHeavyIds * 4;
 
@@ -344,124 +343,6 @@ __device__ __forceinline__ int lower_bound_ids(const int* v, int len, int key) {
   return lo;
 }
 
-// Medium targets (kLight < K <= kMedium): one warp each. The source ids of
-// the neighbouring buckets are staged in shared memory when they fit
-// (K <= kMedStage; else ranked against global memory); every deposit's
-// position in the source-ordered merge is its index in its own bucket plus
-// its rank (lower_bound) in each other bucket (a source lives in exactly one
-// bucket, so there are no ties). Lanes write the weights to those positions
-// in the warp's private slice of a global buffer, then fold them in order.
-template <int D>
-__global__ void __launch_bounds__(kMedWarps * 32) pf_gather_medium_kernel(GatherArgs A,
-                                                                         const int* heavy,
-                                                                         const int* nheavy,
-                                                                         double* hbuf) {
-  constexpr int NC = 1 << D;  // per-corner state in registers (fully unrolled loops)
-  extern __shared__ int med_ids[];  // [kMedWarps][kMedStage]
-  __shared__ int med_tab[kMedWarps * 24];  // per warp: the non-empty buckets' (len, cat, pos)
-  const GridDesc& g = A.g;
-  const int nh = nheavy[0];
-  const int lane = threadIdx.x & 31;
-  int* sids = med_ids + (threadIdx.x >> 5) * kMedStage;
-  const long warp0 = (static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-  const long nwarps = (static_cast<long>(gridDim.x) * blockDim.x) >> 5;
-  double* buf = hbuf + warp0 * kMedium;  // the warp's private slice (K <= kMedium)
-  for (long q = warp0; q < nh; q += nwarps) {
-    const long t = heavy[q];
-    int id[3] = {0, 0, 0};
-    node_idx(g, t, id);
-    id[0] += A.row_off;
-    int pos[NC], len[NC], cat[NC];
-    int K = 0;
-#pragma unroll
-    for (int b = 0; b < NC; ++b) {
-      long c = t + A.cell_shift;
-      bool ok = true;
-#pragma unroll
-      for (int a = 0; a < D; ++a)
-        if ((b >> a) & 1) {
-          if (id[a] == 0) ok = false;
-          c -= g.stride[a];
-        }
-      pos[b] = ok ? A.off[c] : 0;
-      len[b] = ok ? A.end[c] - pos[b] : 0;
-      cat[b] = K;
-      K += len[b];
-    }
-    const bool staged = K <= kMedStage;
-    if (staged) {
-#pragma unroll
-      for (int b = 0; b < NC; ++b)
-        for (int i = lane; i < len[b]; i += 32) sids[cat[b] + i] = A.bucket[pos[b] + i];
-    }
-    __syncwarp();
-    // every deposit's merged position: its index in its own bucket plus its
-    // rank in each other bucket. The loops are deliberately not unrolled
-    // (2^d x 2^d inlined searches overflow the instruction cache for d = 3);
-    // the non-empty buckets' extents are read from a per-warp shared table.
-    int* tb = med_tab + (threadIdx.x >> 5) * 24;  // [nl][3]: len, cat, pos
-    int nl = 0;
-    int bits_of[NC];
-#pragma unroll
-    for (int b = 0; b < NC; ++b) {
-      bits_of[b] = 0;
-      if (len[b] > 0) {
-        if (lane == 0) {
-          tb[3 * nl] = len[b];
-          tb[3 * nl + 1] = cat[b];
-          tb[3 * nl + 2] = pos[b];
-        }
-        bits_of[nl] = b;
-        ++nl;
-      }
-    }
-    __syncwarp();
-#pragma unroll 1
-    for (int qi = 0; qi < nl; ++qi) {
-      const int lq = tb[3 * qi], cq = tb[3 * qi + 1], pq = tb[3 * qi + 2];
-      int qq = 0;
-#pragma unroll
-      for (int b = 0; b < NC; ++b)
-        if (b == qi) qq = bits_of[b];
-      for (int i = lane; i < lq; i += 32) {
-        const int src = staged ? sids[cq + i] : A.bucket[pq + i];
-        int fin = i;
-#pragma unroll 1
-        for (int oi = 0; oi < nl; ++oi) {
-          if (oi == qi) continue;
-          const int lo_ = tb[3 * oi], co = tb[3 * oi + 1], po = tb[3 * oi + 2];
-          fin += staged ? lower_bound_ids(sids + co, lo_, src) : lower_bound_ids(A.bucket + po, lo_, src);
-        }
-        buf[fin] = pos_weight(A, pq + i, qq);
-      }
-    }
-    __syncwarp();
-    // Starting from +0.0, rho can never become -0.0, so adding a zero weight
-    // leaves it unchanged: folding every weight equals the reference's skip
-    // of zero weights bit for bit. K is small here: a sequential chain of
-    // adds fed by shuffles (issued ahead of the chain in groups of 8).
-    double rho = 0.0;
-    int c = 0;
-    for (; c + 32 <= K; c += 32) {
-      const double v = buf[c + lane];
-#pragma unroll
-      for (int i0 = 0; i0 < 32; i0 += 8) {
-        double x[8];
-#pragma unroll
-        for (int i = 0; i < 8; ++i) x[i] = __shfl_sync(0xffffffffu, v, i0 + i);
-#pragma unroll
-        for (int i = 0; i < 8; ++i) rho += x[i];
-      }
-    }
-    if (c < K) {
-      const double v = c + lane < K ? buf[c + lane] : 0.0;
-      for (int i = 0; i < K - c; ++i) rho += __shfl_sync(0xffffffffu, v, i);
-    }
-    if (lane == 0) A.out[t] = A.target ? A.target[t] - rho : rho;
-    __syncwarp();
-  }
-}
-
 // Sequential fold of w[0..K) from +0.0 by one warp, bit for bit the
 // reference's loop (zero weights leave rho unchanged: see the medium tier):
 // the lanes load 32 consecutive weights per round (coalesced, one round
@@ -489,6 +370,155 @@ __device__ __forceinline__ double warp_seq_fold(const double* w, int K) {
     }
   }
   return rho;
+}
+
+// Warp-wide merge of the sorted runs A = x[a0, a0 + la) and B = x[a0 + la,
+// a0 + la + lb) (source ids, unique) with their 16-bit payloads into
+// y/py[a0, ...): merge path, every lane emits a contiguous output range.
+__device__ __forceinline__ void warp_merge2(const int* x, const uint16_t* px, int* y, uint16_t* py, int a0,
+                                           int la, int lb) {
+  const int lane = threadIdx.x & 31;
+  const int tot = la + lb;
+  const int per = (tot + 31) >> 5;
+  const int d0 = min(tot, lane * per), d1 = min(tot, d0 + per);
+  if (d0 >= d1) return;
+  const int* A = x + a0;
+  const int* B = A + la;
+  // split: i elements from A and d0 - i from B precede output d0
+  int lo = max(0, d0 - lb), hi = min(d0, la);
+  while (lo < hi) {
+    const int i = (lo + hi) >> 1;
+    if (A[i] < B[d0 - i - 1]) lo = i + 1;
+    else hi = i;
+  }
+  int i = lo, j = d0 - lo;
+  for (int d = d0; d < d1; ++d) {
+    const bool takeA = j >= lb || (i < la && A[i] < B[j]);
+    if (takeA) {
+      y[a0 + d] = A[i];
+      py[a0 + d] = px[a0 + i];
+      ++i;
+    } else {
+      y[a0 + d] = B[j];
+      py[a0 + d] = px[a0 + la + j];
+      ++j;
+    }
+  }
+}
+
+// Medium targets (kLight < K <= kMedium): one warp each. The <= 2^d sorted
+// buckets (source ids) are staged in shared memory with a 16-bit payload
+// (corner bit, index in the bucket) and merged by a log2(buckets)-level tree
+// of merge-path merges; the merged order is the source order, the order in
+// which the reference adds the deposits. Weights are then written in that
+// order to the warp's slice of a global buffer and folded sequentially.
+template <int D>
+__global__ void __launch_bounds__(kMedWarps * 32) pf_gather_medium_kernel(GatherArgs A,
+                                                                         const int* heavy,
+                                                                         const int* nheavy,
+                                                                         double* hbuf) {
+  constexpr int NC = 1 << D;
+  extern __shared__ __align__(16) unsigned char med_smem[];
+  __shared__ int med_tab[kMedWarps][2 * 8 + 8];  // run starts, run lengths, bucket start per corner
+  const GridDesc& g = A.g;
+  const int nh = nheavy[0];
+  const int lane = threadIdx.x & 31;
+  const int wib = threadIdx.x >> 5;
+  int* idsA = reinterpret_cast<int*>(med_smem) + wib * (2 * kMedium);
+  int* idsB = idsA + kMedium;
+  uint16_t* payA = reinterpret_cast<uint16_t*>(reinterpret_cast<int*>(med_smem) + kMedWarps * 2 * kMedium) +
+                   wib * (2 * kMedium);
+  uint16_t* payB = payA + kMedium;
+  int* tab = med_tab[wib];
+  const long warp0 = (static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const long nwarps = (static_cast<long>(gridDim.x) * blockDim.x) >> 5;
+  double* buf = hbuf + warp0 * kMedium;  // the warp's private slice (K <= kMedium)
+  for (long q = warp0; q < nh; q += nwarps) {
+    const long t = heavy[q];
+    int id[3] = {0, 0, 0};
+    node_idx(g, t, id);
+    id[0] += A.row_off;
+    int pos[NC], len[NC];
+    int K = 0, nl = 0;
+#pragma unroll
+    for (int b = 0; b < NC; ++b) {
+      long c = t + A.cell_shift;
+      bool ok = true;
+#pragma unroll
+      for (int a = 0; a < D; ++a)
+        if ((b >> a) & 1) {
+          if (id[a] == 0) ok = false;
+          c -= g.stride[a];
+        }
+      pos[b] = ok ? A.off[c] : 0;
+      len[b] = ok ? A.end[c] - pos[b] : 0;
+      if (lane == 0) {
+        tab[16 + b] = pos[b];
+        if (len[b] > 0) {
+          tab[nl] = K;
+          tab[8 + nl] = len[b];
+        }
+      }
+      if (len[b] > 0) ++nl;
+      K += len[b];
+    }
+    // stage the runs: ids and (corner << 9 | index) payloads (len <= 512)
+#pragma unroll
+    for (int b = 0, o = 0; b < NC; ++b) {
+      for (int i = lane; i < len[b]; i += 32) {
+        idsA[o + i] = A.bucket[pos[b] + i];
+        payA[o + i] = static_cast<uint16_t>((b << 9) | i);
+      }
+      o += len[b];
+    }
+    __syncwarp();
+    // merge tree: runs r and r+1 are adjacent; each level halves the runs
+    int* xs = idsA;
+    int* ys = idsB;
+    uint16_t* px = payA;
+    uint16_t* py = payB;
+    int runs = nl;
+    while (runs > 1) {
+      for (int r = 0; r + 1 < runs; r += 2)
+        warp_merge2(xs, px, ys, py, tab[r], tab[8 + r], tab[8 + r + 1]);
+      if (runs & 1) {  // the odd run is copied across
+        const int a0 = tab[runs - 1], l0 = tab[8 + runs - 1];
+        for (int i = lane; i < l0; i += 32) {
+          ys[a0 + i] = xs[a0 + i];
+          py[a0 + i] = px[a0 + i];
+        }
+      }
+      __syncwarp();
+      const int nr = (runs + 1) >> 1;
+      if (lane == 0)
+        for (int r = 0; r < nr; ++r) {
+          const int l0 = tab[8 + 2 * r] + (2 * r + 1 < runs ? tab[8 + 2 * r + 1] : 0);
+          tab[r] = tab[2 * r];
+          tab[8 + r] = l0;
+        }
+      __syncwarp();
+      runs = nr;
+      int* ti = xs;
+      xs = ys;
+      ys = ti;
+      uint16_t* tp = px;
+      px = py;
+      py = tp;
+    }
+    // weights in source order
+    for (int r = lane; r < K; r += 32) {
+      const int pl = px[r];
+      const int b = pl >> 9;
+      buf[r] = pos_weight(A, tab[16 + b] + (pl & 511), b);
+    }
+    __syncwarp();
+    // Starting from +0.0, rho can never become -0.0, so adding a zero weight
+    // leaves it unchanged: folding every weight equals the reference's skip
+    // of zero weights bit for bit.
+    const double rho = warp_seq_fold(buf, K);
+    if (lane == 0) A.out[t] = A.target ? A.target[t] - rho : rho;
+    __syncwarp();
+  }
 }
 
 // Large targets (kMedium < K <= kLarge): one CTA of kLargeThreads each, ids
