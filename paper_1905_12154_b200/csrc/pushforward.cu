@@ -34,6 +34,7 @@ constexpr int kMedium = 512;   // warp-per-target tier: kLight < K <= kMedium
 constexpr int kLarge = 4096;   // CTA-per-target tier with a sequential fold: K <= kLarge
 constexpr int kLargeThreads = 128;
 constexpr int kLargeBlocks = 148 * 8;  // each CTA owns kLarge doubles of hbuf
+constexpr int kLargeSmem = kLarge * 2 * (4 + 2);  // ids + payloads, ping-pong
 constexpr int kMedWarps = 8;
 constexpr int kHeavyIds = 24576;
 constexpr int kMedSmem = kMedWarps * 2 * kMedium * (4 + 2);  // ids + payloads, ping-pong
@@ -372,15 +373,15 @@ __device__ __forceinline__ double warp_seq_fold(const double* w, int K) {
   return rho;
 }
 
-// Warp-wide merge of the sorted runs A = x[a0, a0 + la) and B = x[a0 + la,
-// a0 + la + lb) (source ids, unique) with their 16-bit payloads into
-// y/py[a0, ...): merge path, every lane emits a contiguous output range.
-__device__ __forceinline__ void warp_merge2(const int* x, const uint16_t* px, int* y, uint16_t* py, int a0,
-                                           int la, int lb) {
-  const int lane = threadIdx.x & 31;
+// Group-wide merge (threads gt of ng) of the sorted runs A = x[a0, a0 + la)
+// and B = x[a0 + la, a0 + la + lb) (source ids, unique) with their 16-bit
+// payloads into y/py[a0, ...): merge path, each thread emits a contiguous
+// output range after one binary search for its split.
+__device__ __forceinline__ void group_merge2(const int* x, const uint16_t* px, int* y, uint16_t* py, int a0,
+                                            int la, int lb, int gt, int ng) {
   const int tot = la + lb;
-  const int per = (tot + 31) >> 5;
-  const int d0 = min(tot, lane * per), d1 = min(tot, d0 + per);
+  const int per = (tot + ng - 1) / ng;
+  const int d0 = min(tot, gt * per), d1 = min(tot, d0 + per);
   if (d0 >= d1) return;
   const int* A = x + a0;
   const int* B = A + la;
@@ -403,6 +404,40 @@ __device__ __forceinline__ void warp_merge2(const int* x, const uint16_t* px, in
       py[a0 + d] = px[a0 + la + j];
       ++j;
     }
+  }
+}
+
+// Merge tree over the runs listed in tab (tab[r]: start, tab[8 + r]: length;
+// adjacent in x/px) by the group (threads gt of ng, `bar` synchronises it).
+// Returns in x/px the buffer holding the merged sequence.
+template <class Sync>
+__device__ __forceinline__ void group_merge_runs(int*& x, uint16_t*& px, int*& y, uint16_t*& py, int* tab,
+                                                int runs, int gt, int ng, Sync bar) {
+  while (runs > 1) {
+    for (int r = 0; r + 1 < runs; r += 2) group_merge2(x, px, y, py, tab[r], tab[8 + r], tab[8 + r + 1], gt, ng);
+    if (runs & 1) {  // the odd run is copied across
+      const int a0 = tab[runs - 1], l0 = tab[8 + runs - 1];
+      for (int i = gt; i < l0; i += ng) {
+        y[a0 + i] = x[a0 + i];
+        py[a0 + i] = px[a0 + i];
+      }
+    }
+    bar();
+    const int nr = (runs + 1) >> 1;
+    if (gt == 0)
+      for (int r = 0; r < nr; ++r) {
+        const int l0 = tab[8 + 2 * r] + (2 * r + 1 < runs ? tab[8 + 2 * r + 1] : 0);
+        tab[r] = tab[2 * r];
+        tab[8 + r] = l0;
+      }
+    bar();
+    runs = nr;
+    int* ti = x;
+    x = y;
+    y = ti;
+    uint16_t* tp = px;
+    px = py;
+    py = tp;
   }
 }
 
@@ -477,34 +512,7 @@ __global__ void __launch_bounds__(kMedWarps * 32) pf_gather_medium_kernel(Gather
     int* ys = idsB;
     uint16_t* px = payA;
     uint16_t* py = payB;
-    int runs = nl;
-    while (runs > 1) {
-      for (int r = 0; r + 1 < runs; r += 2)
-        warp_merge2(xs, px, ys, py, tab[r], tab[8 + r], tab[8 + r + 1]);
-      if (runs & 1) {  // the odd run is copied across
-        const int a0 = tab[runs - 1], l0 = tab[8 + runs - 1];
-        for (int i = lane; i < l0; i += 32) {
-          ys[a0 + i] = xs[a0 + i];
-          py[a0 + i] = px[a0 + i];
-        }
-      }
-      __syncwarp();
-      const int nr = (runs + 1) >> 1;
-      if (lane == 0)
-        for (int r = 0; r < nr; ++r) {
-          const int l0 = tab[8 + 2 * r] + (2 * r + 1 < runs ? tab[8 + 2 * r + 1] : 0);
-          tab[r] = tab[2 * r];
-          tab[8 + r] = l0;
-        }
-      __syncwarp();
-      runs = nr;
-      int* ti = xs;
-      xs = ys;
-      ys = ti;
-      uint16_t* tp = px;
-      px = py;
-      py = tp;
-    }
+    group_merge_runs(xs, px, ys, py, tab, nl, lane, 32, [] { __syncwarp(); });
     // weights in source order
     for (int r = lane; r < K; r += 32) {
       const int pl = px[r];
@@ -529,8 +537,16 @@ __global__ void __launch_bounds__(kLargeThreads) pf_gather_large_kernel(GatherAr
                                                                        const int* large,
                                                                        const int* nheavy,
                                                                        double* hbuf) {
-  __shared__ int s_pos[8], s_end[8], s_bits[8], s_cat[8], s_nl, s_K;
-  __shared__ int ids[kLarge];
+  // the target's buckets (source ids) are merged by a merge-path tree in
+  // shared memory, as in the warp tier, with 16-bit (run << 12 | index)
+  // payloads; the weights then go to the CTA's buffer slice in source order
+  extern __shared__ __align__(16) unsigned char large_smem[];
+  __shared__ int tab[24];  // run starts, run lengths (merge tree)
+  __shared__ int s_pos[8], s_bits[8], s_nl, s_K;
+  int* idsA = reinterpret_cast<int*>(large_smem);
+  int* idsB = idsA + kLarge;
+  uint16_t* payA = reinterpret_cast<uint16_t*>(idsB + kLarge);
+  uint16_t* payB = payA + kLarge;
   const int nl_total = nheavy[4];
   double* buf = hbuf + static_cast<long>(blockIdx.x) * kLarge;
   for (int q = blockIdx.x; q < nl_total; q += gridDim.x) {
@@ -539,10 +555,10 @@ __global__ void __launch_bounds__(kLargeThreads) pf_gather_large_kernel(GatherAr
       TargetBuckets tb;
       target_buckets(A, t, tb);
       for (int qq = 0, o = 0; qq < tb.nl; ++qq) {
+        tab[qq] = o;
+        tab[8 + qq] = tb.end[qq] - tb.pos[qq];
         s_pos[qq] = tb.pos[qq];
-        s_end[qq] = tb.end[qq];
         s_bits[qq] = tb.bits[qq];
-        s_cat[qq] = o;
         o += tb.end[qq] - tb.pos[qq];
       }
       s_nl = tb.nl;
@@ -551,26 +567,29 @@ __global__ void __launch_bounds__(kLargeThreads) pf_gather_large_kernel(GatherAr
     __syncthreads();
     const int nl = s_nl;
     const int K = s_K;
-    for (int qq = 0; qq < nl; ++qq)
-      for (int i = threadIdx.x; i < s_end[qq] - s_pos[qq]; i += blockDim.x)
-        ids[s_cat[qq] + i] = A.bucket[s_pos[qq] + i];
-    __syncthreads();
     for (int qq = 0; qq < nl; ++qq) {
-      const int len = s_end[qq] - s_pos[qq], b = s_bits[qq];
+      const int o = tab[qq], len = tab[8 + qq], p0 = s_pos[qq];
       for (int i = threadIdx.x; i < len; i += blockDim.x) {
-        const int src = ids[s_cat[qq] + i];
-        int fin = i;
-        for (int o = 0; o < nl; ++o)
-          if (o != qq) fin += lower_bound_ids(ids + s_cat[o], s_end[o] - s_pos[o], src);
-        buf[fin] = pos_weight(A, s_pos[qq] + i, b);
+        idsA[o + i] = A.bucket[p0 + i];
+        payA[o + i] = static_cast<uint16_t>((qq << 12) | i);
       }
+    }
+    __syncthreads();
+    int* xs = idsA;
+    int* ys = idsB;
+    uint16_t* px = payA;
+    uint16_t* py = payB;
+    group_merge_runs(xs, px, ys, py, tab, nl, threadIdx.x, blockDim.x, [] { __syncthreads(); });
+    for (int r = threadIdx.x; r < K; r += blockDim.x) {
+      const int pl = px[r];
+      const int qq = pl >> 12;
+      buf[r] = pos_weight(A, s_pos[qq] + (pl & 4095), s_bits[qq]);
     }
     __syncthreads();
     // warp 0 folds the weights in order (warp_seq_fold)
     if (threadIdx.x < 32) {
-      const int lane = threadIdx.x;
       const double rho = warp_seq_fold(buf, K);
-      if (lane == 0) A.out[t] = A.target ? A.target[t] - rho : rho;
+      if (threadIdx.x == 0) A.out[t] = A.target ? A.target[t] - rho : rho;
     }
     __syncthreads();
   }
@@ -855,6 +874,8 @@ void PushforwardPlan::setup(const GridDesc& loc, const GridDesc& global, int row
   BFM_CUDA(dmalloc(&large_, (N + 1) * sizeof(int)));
   BFM_CUDA(dmalloc(&nheavy_, 4 * sizeof(unsigned long long)));
   ensure_records(N);
+  BFM_CUDA(cudaFuncSetAttribute(pf_gather_large_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                kLargeSmem));
   BFM_CUDA(cudaFuncSetAttribute(pf_gather_heavy_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 kHeavySmem));
   BFM_CUDA(cudaFuncSetAttribute(pf_gather_medium_kernel<1>,
@@ -977,7 +998,7 @@ void PushforwardPlan::gather(long nrec, const uint32_t* d_keys, const double* d_
   else
     pf_gather_medium_kernel<3><<<med_blocks_, kMedWarps * 32, kMedSmem, stream>>>(G, heavy_, nheavy, hbuf_);
   BFM_LAUNCH_CHECK("pf_gather_medium_kernel");
-  pf_gather_large_kernel<<<large_blocks_, kLargeThreads, 0, stream>>>(G, large_, nheavy, hbuf_);
+  pf_gather_large_kernel<<<large_blocks_, kLargeThreads, kLargeSmem, stream>>>(G, large_, nheavy, hbuf_);
   BFM_LAUNCH_CHECK("pf_gather_large_kernel");
   pf_gather_heavy_kernel<<<2 * 148, 512, kHeavySmem, stream>>>(G, heavy_, nheavy, hbuf_, nheavy_ + 1);
   BFM_LAUNCH_CHECK("pf_gather_heavy_kernel");
