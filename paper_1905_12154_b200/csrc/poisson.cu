@@ -164,7 +164,7 @@ __global__ void __launch_bounds__(512) pois_fft_kernel(PoisArgs a) {
   const int l = threadIdx.x / tpl;
   const int t = threadIdx.x - l * tpl;
   const long L0 = static_cast<long>(blockIdx.x) * lpc;
-  __shared__ long s_base[16];
+  __shared__ long s_base[32];  // lpc <= 32
   if (threadIdx.x < lpc) {
     const long L = L0 + threadIdx.x;
     s_base[threadIdx.x] = L < ax.nlines ? line_base(ax, L) : -1;
@@ -439,9 +439,15 @@ void PoissonPlan::setup(const GridDesc& loc, const GridDesc& global, long col0, 
     c.strided = a != g.d - 1;
     if (H.plan.kind == bfmdct::kFft) {
       const int m = H.plan.m;
+      // about 16 points per thread in the fused radix passes; short lines
+      // (m <= 256, e.g. C4's 384-point lines) of large grids get a half warp
+      // each (two lines per warp, synchronised together by __syncwarp), so
+      // the passes' 12-16 butterfly groups keep most lanes busy and twice as
+      // many lines fit the register file (C4 Poisson 11.5 -> 9.1 ms per
+      // iteration); small grids keep a full warp per line (more CTAs)
       int tpl = (m + 15) / 16;
-      tpl = ((tpl + 31) / 32) * 32;
-      if (tpl < 32) tpl = 32;
+      const bool many = g.size / n >= 16384;  // enough lines to fill the SMs twice over
+      tpl = (tpl <= 16 && many) ? 16 : std::max(32, ((tpl + 31) / 32) * 32);
       if (tpl > 256) tpl = 256;
       c.tpl = tpl;
       c.cslots = (m + 7) & ~7;
@@ -452,7 +458,7 @@ void PoissonPlan::setup(const GridDesc& loc, const GridDesc& global, long col0, 
     }
     if (c.line_bytes > budget) throw std::invalid_argument("solve_neumann: line exceeds shared memory");
     int lpc = std::min(budget / c.line_bytes, 512 / c.tpl);
-    lpc = std::min(lpc, c.strided ? 16 : 4);
+    lpc = std::min(lpc, c.strided ? 32 : std::max(4, 128 / c.tpl));
     if (c.tpl > 32) lpc = std::min(lpc, 15);
     lpc = static_cast<int>(std::min<long>(lpc, c.nlines));
     c.lpc = std::max(1, lpc);
