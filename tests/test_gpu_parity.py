@@ -302,3 +302,31 @@ def test_cpp_facade_driver_runs_on_gpu(tmp_path):
     assert r.returncode == 0, r.stderr
     run = subprocess.run([str(exe)], capture_output=True, text=True, timeout=300)
     assert run.returncode == 0, run.stdout + run.stderr
+
+
+@pytest.mark.parametrize("shape", [(512, 512), (40, 48, 56)])
+def test_pushforward_tier_boundaries(shape):
+    # blocks of consecutive sources sent to one interior point each: its 2^d
+    # corner targets receive exactly K deposits, K straddling every gather
+    # tier boundary (one thread / warp merge / CTA merge / warp fold / exact
+    # parallel fold); the other sources stay put
+    rng = np.random.default_rng(sum(shape))
+    d = len(shape)
+    N = int(np.prod(shape))
+    sizes = [48, 49, 512, 513, 4096, 4097, 16384, 16385]
+    if N < 2 * sum(sizes):
+        sizes = [48, 49, 512, 513, 4096, 4097]
+    coords = np.meshgrid(*[(np.arange(n) + 0.5) / n for n in shape], indexing="ij")
+    disp = [np.zeros(shape) for _ in range(d)]
+    flat = [x.reshape(-1) for x in disp]
+    src = [c.reshape(-1) for c in coords]
+    start = 0
+    for b, K in enumerate(sizes):
+        tgt = rng.uniform(0.1, 0.9, d)
+        for a in range(d):
+            flat[a][start:start + K] = tgt[a] - src[a][start:start + K]
+        start += K + 1000
+    mu = rng.lognormal(0.0, 1.5, shape)
+    got = bfm.pushforward_density(np.stack(disp), mu)
+    want = O.orc_pushforward_density(np.stack(disp), mu)
+    assert O.n_bit_diff(got, want) == 0
