@@ -200,18 +200,10 @@ struct GatherArgs {
   const uint8_t* rmask;
 };
 
-__device__ __forceinline__ double deposit_weight(const GatherArgs& A, int s, int b) {
-  double wt = A.src[s];
-  for (int a = 0; a < A.g.d; ++a) {
-    const double wh = A.w[a * A.nrec + s];
-    wt *= ((b >> a) & 1) ? wh : 1.0 - wh;
-  }
-  return wt;
-}
-
 // Weight of the deposit at sorted position pos into the corner-b target
 // (0 on a clamped axis's upper corner): the same IEEE sequence as
-// deposit_weight, ((m w_0) w_1) w_2, from the packed record.
+// the reference's weight (pushforward.hpp:161-166: m times each axis's upper
+// or lower barycentric weight, in axis order), from the packed record.
 __device__ __forceinline__ double pos_weight(const GatherArgs& A, int pos, int b) {
   if (b & A.rmask[pos]) return 0.0;
   const double4 r = A.rec[pos];
