@@ -81,7 +81,7 @@ __device__ __forceinline__ double g_approx(const CtAxis& A, int k, int j) {
     return 0.5 * dl * dl;
   }
   BFM_DASSERT(k >= 0 && k < A.n && j >= 0 && j < A.n);
-  return A.G[static_cast<long>(k) * A.n + j].x;
+  return __ldg(&A.G[static_cast<long>(k) * A.n + j].x);
 }
 
 __device__ __forceinline__ int g_terms(const CtAxis& A, int k, int j, double* t) {
@@ -91,7 +91,11 @@ __device__ __forceinline__ int g_terms(const CtAxis& A, int k, int j, double* t)
     return 1;
   }
   BFM_DASSERT(k >= 0 && k < A.n && j >= 0 && j < A.n);
-  const double4 v = A.G[static_cast<long>(k) * A.n + j];
+  // read-only for the whole launch: the non-coherent path lets the compiler
+  // issue the loads of several candidates ahead of earlier result stores
+  const double2* row = reinterpret_cast<const double2*>(&A.G[static_cast<long>(k) * A.n + j]);
+  const double2 v01 = __ldg(row), v23 = __ldg(row + 1);
+  const double4 v = make_double4(v01.x, v01.y, v23.x, v23.y);
   int m = 0;
   t[m++] = v.x;
   if (v.y != 0.0) t[m++] = v.y;
@@ -118,7 +122,7 @@ __device__ __forceinline__ long phi_index(const CtPass& p, const LineGeo& g, uin
 __device__ int cand_terms(const CtPass& p, const LineGeo& g, uint32_t chain, int j, int k,
                           double* t) {
   int m = 0;
-  t[m++] = -p.phi[phi_index(p, g, chain, j)];
+  t[m++] = -__ldg(&p.phi[phi_index(p, g, chain, j)]);
   if (p.a >= 1) m += g_terms(p.ax[0], g.k[0], static_cast<int>(chain & 0xFFFFu), t + m);
   if (p.a >= 2) m += g_terms(p.ax[1], g.k[1], static_cast<int>(chain >> 16), t + m);
   m += g_terms(p.ax[p.a], k, j, t + m);
