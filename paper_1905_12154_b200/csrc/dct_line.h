@@ -53,6 +53,24 @@ struct LinePlan {
   const double* cosmat = nullptr;  // [n*n] cos(pi k (2j+1) / 2n) at k*n+j
 };
 
+// Table reads (twiddles, digit reversal): read-only for a whole launch, so
+// the device reads them through the non-coherent path (same values).
+BFM_HD cplx tab_c(const cplx* t, int i) {
+#if defined(__CUDA_ARCH__)
+  const double2 v = __ldg(reinterpret_cast<const double2*>(t) + i);
+  return cplx{v.x, v.y};
+#else
+  return t[i];
+#endif
+}
+BFM_HD int tab_i(const int* t, int i) {
+#if defined(__CUDA_ARCH__)
+  return __ldg(t + i);
+#else
+  return t[i];
+#endif
+}
+
 BFM_HD cplx cmul(cplx a, cplx b) {
   cplx r;
   r.re = a.re * b.re - a.im * b.im;
@@ -82,7 +100,7 @@ BFM_HD void butterfly_regs(const LinePlan& p, int r, cplx* x, int tw, bool inver
     const cplx c = x[1];
     x[0] = cadd(a, c);
     const cplx d = csub(a, c);
-    const cplx w = p.wm[tw];
+    const cplx w = tab_c(p.wm, tw);
     x[1] = inverse ? cmulc(d, w) : cmul(d, w);
   } else if (r == 4) {
     const cplx x0 = x[0], x1 = x[1], x2 = x[2], x3 = x[3];
@@ -99,9 +117,9 @@ BFM_HD void butterfly_regs(const LinePlan& p, int r, cplx* x, int tw, bool inver
     if (t2 >= m) t2 -= m;
     int t3 = t2 + tw;
     if (t3 >= m) t3 -= m;
-    const cplx w1 = p.wm[tw];
-    const cplx w2 = p.wm[t2];
-    const cplx w3 = p.wm[t3];
+    const cplx w1 = tab_c(p.wm, tw);
+    const cplx w2 = tab_c(p.wm, t2);
+    const cplx w3 = tab_c(p.wm, t3);
     if (inverse) {
       x[1] = cmulc(y1, w1);
       x[2] = cmulc(y2, w2);
@@ -126,8 +144,8 @@ BFM_HD void butterfly_regs(const LinePlan& p, int r, cplx* x, int tw, bool inver
     x[0] = y0;
     int t2 = 2 * tw;
     if (t2 >= m) t2 -= m;
-    const cplx w1 = p.wm[tw];
-    const cplx w2 = p.wm[t2];
+    const cplx w1 = tab_c(p.wm, tw);
+    const cplx w2 = tab_c(p.wm, t2);
     if (inverse) {
       x[1] = cmulc(y1, w1);
       x[2] = cmulc(y2, w2);
@@ -175,18 +193,20 @@ BFM_HD void dct2_unpack_vals(const LinePlan& p, cplx zk, cplx zm, int k, double&
   const cplx F{zm.re, -zm.im};
   const cplx S{0.5 * (E.re + F.re), 0.5 * (E.im + F.im)};
   const cplx D{0.5 * (E.re - F.re), 0.5 * (E.im - F.im)};
-  const cplx w{p.wn[k].re, -p.wn[k].im};  // e^{-2 pi i k / n}
+  const cplx wk = tab_c(p.wn, k);
+  const cplx w{wk.re, -wk.im};  // e^{-2 pi i k / n}
   // V = S - i w D
   const double vr = S.re + (w.re * D.im + w.im * D.re);
   const double vi = S.im - (w.re * D.re - w.im * D.im);
-  const double c = p.cs[k].re, s = p.cs[k].im;
+  const cplx csk = tab_c(p.cs, k);
+  const double c = csk.re, s = csk.im;
   yk = 2.0 * (c * vr + s * vi);
   ynk = 2.0 * (s * vr - c * vi);
 }
 BFM_HD void dct2_unpack(const LinePlan& p, const cplx* z, double* y, long stride, int k) {
   const int m = p.m;
-  const cplx zk = z[p.rev[k == m ? 0 : k]];
-  const cplx zm = z[p.rev[k == 0 ? 0 : m - k]];
+  const cplx zk = z[tab_i(p.rev, k == m ? 0 : k)];
+  const cplx zm = z[tab_i(p.rev, k == 0 ? 0 : m - k)];
   double yk, ynk;
   dct2_unpack_vals(p, zk, zm, k, yk, ynk);
   y[static_cast<long>(k) * stride] = yk;
@@ -198,7 +218,8 @@ BFM_HD void dct2_unpack(const LinePlan& p, const cplx* z, double* y, long stride
 // Z_k = (V_k + conj V_{m-k}) + i e^{2 pi i k / n} (V_k - conj V_{m-k}), k < m.
 // V_j from a = x_j and b = x_{n-j} (b = 0 for j = 0).
 BFM_HD cplx dct3_V_vals(const LinePlan& p, double a, double b, int j) {
-  const double c = p.cs[j].re, s = p.cs[j].im;
+  const cplx csj = tab_c(p.cs, j);
+  const double c = csj.re, s = csj.im;
   // (a - i b)(c + i s) = (a c + b s) + i (a s - b c)
   return cplx{a * c + b * s, a * s - b * c};
 }
@@ -212,7 +233,7 @@ BFM_HD cplx dct3_pre_vals(const LinePlan& p, cplx A, cplx Bv, int k) {
   const cplx B{Bv.re, -Bv.im};
   const cplx sum = cadd(A, B);
   const cplx dif = csub(A, B);
-  const cplx w = p.wn[k];  // e^{+2 pi i k / n}
+  const cplx w = tab_c(p.wn, k);  // e^{+2 pi i k / n}
   const cplx wd = cmul(w, dif);
   // + i * wd
   return cplx{sum.re - wd.im, sum.im + wd.re};
@@ -232,7 +253,7 @@ BFM_HD int dct2_vpos(const LinePlan& p, int j) {
 // After the inverse FFT: z_q at slot rev[q] holds (v_{2q}, v_{2q+1});
 // y_{2p} = v_p, y_{2p+1} = v_{n-1-p}.
 BFM_HD void dct3_post(const LinePlan& p, const cplx* z, double* y, long stride, int q) {
-  const cplx v = z[p.rev[q]];
+  const cplx v = z[tab_i(p.rev, q)];
   const int n = p.n;
   const int m = p.m;
   const int p0 = 2 * q, p1 = 2 * q + 1;

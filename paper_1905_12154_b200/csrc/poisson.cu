@@ -229,7 +229,7 @@ __global__ void __launch_bounds__(512) pois_fft_kernel(PoisArgs a) {
     else for (int s = 0; s < a.npass; ++s) gsync(tpl, l);
     if (active)
       for (int q = t; q < m; q += tpl) {
-        const cplx v = cref(zB, P.rev[q]);
+        const cplx v = cref(zB, bfmdct::tab_i(P.rev, q));
         dref(zAd, bfmdct::dct3_ypos(P, 2 * q)) = v.re;
         dref(zAd, bfmdct::dct3_ypos(P, 2 * q + 1)) = v.im;
       }
@@ -241,8 +241,8 @@ __global__ void __launch_bounds__(512) pois_fft_kernel(PoisArgs a) {
       if (active)
         for (int k = t; k <= m; k += tpl) {
           double yk, ynk;
-          bfmdct::dct2_unpack_vals(P, cref(zA, P.rev[k == m ? 0 : k]),
-                                   cref(zA, P.rev[k == 0 ? 0 : m - k]), k, yk, ynk);
+          bfmdct::dct2_unpack_vals(P, cref(zA, bfmdct::tab_i(P.rev, k == m ? 0 : k)),
+                                   cref(zA, bfmdct::tab_i(P.rev, k == 0 ? 0 : m - k)), k, yk, ynk);
           dref(zBd, k) = yk;
           if (k > 0 && k < m) dref(zBd, n - k) = ynk;
         }
@@ -253,10 +253,10 @@ __global__ void __launch_bounds__(512) pois_fft_kernel(PoisArgs a) {
         for (int k = t; k <= half; k += tpl) {
           const int km = m - k;
           double yk, ynk, ykm, ynkm;
-          bfmdct::dct2_unpack_vals(P, cref(zA, P.rev[k == m ? 0 : k]),
-                                   cref(zA, P.rev[k == 0 ? 0 : m - k]), k, yk, ynk);
-          bfmdct::dct2_unpack_vals(P, cref(zA, P.rev[km == m ? 0 : km]),
-                                   cref(zA, P.rev[km == 0 ? 0 : m - km]), km, ykm, ynkm);
+          bfmdct::dct2_unpack_vals(P, cref(zA, bfmdct::tab_i(P.rev, k == m ? 0 : k)),
+                                   cref(zA, bfmdct::tab_i(P.rev, k == 0 ? 0 : m - k)), k, yk, ynk);
+          bfmdct::dct2_unpack_vals(P, cref(zA, bfmdct::tab_i(P.rev, km == m ? 0 : km)),
+                                   cref(zA, bfmdct::tab_i(P.rev, km == 0 ? 0 : m - km)), km, ykm, ynkm);
           const double xk = divide(a, yk, k, l1v, l2v);
           const double xnk = (k > 0 && k < m) ? divide(a, ynk, n - k, l1v, l2v) : 0.0;
           const double xkm = divide(a, ykm, km, l1v, l2v);
@@ -273,7 +273,7 @@ __global__ void __launch_bounds__(512) pois_fft_kernel(PoisArgs a) {
       else for (int s = 0; s < a.npass; ++s) gsync(tpl, l);
       if (active)
         for (int q = t; q < m; q += tpl) {
-          const cplx v = cref(zB, P.rev[q]);
+          const cplx v = cref(zB, bfmdct::tab_i(P.rev, q));
           dref(zAd, bfmdct::dct3_ypos(P, 2 * q)) = v.re;
           dref(zAd, bfmdct::dct3_ypos(P, 2 * q + 1)) = v.im;
         }
