@@ -128,9 +128,9 @@ __global__ void pf_map_kernel(MapArgs A) {
         const double inv_h = static_cast<double>(n);
         const double inv_2h = 0.5 * inv_h;
         double gr;
-        if (j == 0) gr = (A.u[su + st] - A.u[su]) * inv_h;
-        else if (j == n - 1) gr = (A.u[su] - A.u[su - st]) * inv_h;
-        else gr = (A.u[su + st] - A.u[su - st]) * inv_2h;
+        if (j == 0) gr = (__ldg(A.u + su + st) - __ldg(A.u + su)) * inv_h;
+        else if (j == n - 1) gr = (__ldg(A.u + su) - __ldg(A.u + su - st)) * inv_h;
+        else gr = (__ldg(A.u + su + st) - __ldg(A.u + su - st)) * inv_2h;
         double mag = fabs(gr);
         if (!(mag < A.diam)) mag = A.diam;
         const double v = gr < 0.0 ? -mag : mag;
