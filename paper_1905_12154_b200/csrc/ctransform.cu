@@ -129,6 +129,91 @@ __device__ int cand_terms(const CtPass& p, const LineGeo& g, uint32_t chain, int
   return m;
 }
 
+// ---- exact fixed-point candidates (non-dyadic grids with n <= 512) --------
+// Every coordinate y = fl((j+1/2) fl(1/n)) >= 2^-10 is a multiple of 2^-62,
+// hs(y) >= 2^-21 a multiple of 2^-74 and x*y of 2^-124, so g * 2^124 is an
+// exact integer below 2^124. A candidate V = sum_b g_b - phi is then an exact
+// signed 128-bit integer whenever phi is a multiple of 2^-124 below 4 in
+// magnitude (checked per value; otherwise the expansion path is used).
+__device__ __forceinline__ bool to_fixed124(double v, __int128& out) {
+  const long long b = __double_as_longlong(v);
+  const int ex = static_cast<int>((b >> 52) & 0x7ff);
+  long long m = b & 0xFFFFFFFFFFFFFll;
+  if (ex == 0) {
+    if (m == 0) {
+      out = 0;
+      return true;
+    }
+    return false;  // subnormal: far below 2^-124
+  }
+  if (ex == 0x7ff) return false;
+  m |= 1ll << 52;
+  const int sh = ex - 1075 + 124;  // v = m 2^(ex - 1075)
+  if (sh > 73) return false;       // |v| >= 4
+  __int128 r;
+  if (sh >= 0) {
+    r = static_cast<__int128>(m) << sh;
+  } else {
+    if (sh < -52 || (m & ((1ll << -sh) - 1)) != 0) return false;  // not a multiple of 2^-124
+    r = m >> -sh;
+  }
+  out = b < 0 ? -r : r;
+  return true;
+}
+// RD(V * 2^-124) (round toward -inf; V != 0 gives a normal double)
+__device__ __forceinline__ double rd_fixed124(__int128 V) {
+  if (V == 0) return 0.0;
+  const bool neg = V < 0;
+  unsigned __int128 w = neg ? static_cast<unsigned __int128>(-V) : static_cast<unsigned __int128>(V);
+  const unsigned long long hi = static_cast<unsigned long long>(w >> 64);
+  const unsigned long long lo = static_cast<unsigned long long>(w);
+  const int msb = hi ? 127 - __clzll(static_cast<long long>(hi)) : 63 - __clzll(static_cast<long long>(lo));
+  int e2 = -124;  // value = mant * 2^e2
+  unsigned long long mant;
+  if (msb <= 52) {
+    mant = lo;
+  } else {
+    const int drop = msb - 52;
+    mant = static_cast<unsigned long long>(w >> drop);
+    const unsigned __int128 rest = w - (static_cast<unsigned __int128>(mant) << drop);
+    e2 += drop;
+    if (neg && rest != 0) {  // magnitude rounds up for a negative value
+      ++mant;
+      if (mant == (1ull << 53)) {
+        mant >>= 1;
+        ++e2;
+      }
+    }
+  }
+  const double p2 = __longlong_as_double(static_cast<long long>(e2 + 1023) << 52);  // exact power of two
+  const double r = static_cast<double>(mant) * p2;
+  return neg ? -r : r;
+}
+__device__ __forceinline__ bool g_fixed(const CtAxis& A, int k, int j, __int128& out) {
+  if (A.dyadic) return to_fixed124(g_approx(A, k, j), out);  // exact double on dyadic axes
+  out = A.GF[static_cast<long>(k) * A.n + j];
+  return true;
+}
+// Exact candidate value V(k, j) * 2^124, when representable.
+__device__ __forceinline__ bool cand_fixed(const CtPass& p, const LineGeo& g, uint32_t chain, int j, int k,
+                                           __int128& V) {
+  __int128 f;
+  if (!to_fixed124(__ldg(&p.phi[phi_index(p, g, chain, j)]), f)) return false;
+  V = -f;
+  __int128 t;
+  if (p.a >= 1) {
+    if (!g_fixed(p.ax[0], g.k[0], static_cast<int>(chain & 0xFFFFu), t)) return false;
+    V += t;
+  }
+  if (p.a >= 2) {
+    if (!g_fixed(p.ax[1], g.k[1], static_cast<int>(chain >> 16), t)) return false;
+    V += t;
+  }
+  if (!g_fixed(p.ax[p.a], k, j, t)) return false;
+  V += t;
+  return true;
+}
+
 // Certified strict convexity of the middle point (fp64 orientation with a
 // rounding bound; near-collinear counts as NOT convex).
 __device__ __forceinline__ bool convex3(double ya, double fa, double yb, double fb, double yc,
@@ -508,8 +593,10 @@ __global__ void __launch_bounds__(kNdThreads) ct_pass_kernel(CtPass p) {
     };
     // exact value V(k, j) rounded down (last pass)
     auto rd_value = [&](int j, int k) {
-      double tv[12];
       const uint32_t ch = p.a > 0 ? s.chain[j] : 0u;
+      __int128 V;
+      if (p.fixed && cand_fixed(p, geo, ch, j, k, V)) return rd_fixed124(V);
+      double tv[12];
       const int m = cand_terms(p, geo, ch, j, k, tv);
       return bfmx::round_down_sum(tv, m);
     };
@@ -641,8 +728,10 @@ __global__ void __launch_bounds__(kNdThreads) ct_pass_kernel(CtPass p) {
       auto Fhat = [&](int idx, double xk) { return P_f(idx) - xk * P_y(idx); };
       // exact value V(k, j) rounded down (last pass)
       auto rd_value = [&](int j, int k) {
-        double tv[12];
         const uint32_t ch = p.a > 0 ? s.chain[j] : 0u;
+        __int128 V;
+        if (p.fixed && cand_fixed(p, geo, ch, j, k, V)) return rd_fixed124(V);
+        double tv[12];
         const int m = cand_terms(p, geo, ch, j, k, tv);
         return bfmx::round_down_sum(tv, m);
       };
@@ -710,10 +799,29 @@ __global__ void __launch_bounds__(kNdThreads) ct_pass_kernel(CtPass p) {
           outv = best;
           have_out = true;
         } else {
+          // exact argmin: fixed-point values when every candidate is
+          // representable, else the expansion comparison
+          bool fx = p.fixed != 0;
           int bestj = -1;
+          if (fx) {
+            __int128 bv = 0;
+            visit([&](int j) {
+              if (!fx || Fhat(j, xk) > Fbest + Mc) return;
+              __int128 V;
+              if (!cand_fixed(p, geo, p.a > 0 ? s.chain[j] : 0u, j, k, V)) {
+                fx = false;
+                return;
+              }
+              if (bestj < 0 || V < bv) {
+                bestj = j;
+                bv = V;
+              }
+            });
+          }
+          if (!fx) bestj = -1;
           double bt[12];
           int bm = 0;
-          visit([&](int j) {
+          if (!fx) visit([&](int j) {
             if (Fhat(j, xk) > Fbest + Mc) return;
             double ct[12];
             const uint32_t ch = p.a > 0 ? s.chain[j] : 0u;
@@ -756,10 +864,17 @@ __global__ void __launch_bounds__(kNdThreads) ct_pass_kernel(CtPass p) {
       for (int u = 0; u < kB; ++u) {
         const int k = kk + u * tpl;
         if (wv[u] == 0xffff) continue;
-        double tv[12];
         const uint32_t ch = p.a > 0 ? s.chain[wv[u]] : 0u;
-        const int m = cand_terms(p, geo, ch, wv[u], k, tv);
-        p.out[geo.base + static_cast<long>(k) * A.stride] = bfmx::round_down_sum(tv, m);
+        __int128 V;
+        double v;
+        if (p.fixed && cand_fixed(p, geo, ch, wv[u], k, V)) {
+          v = rd_fixed124(V);
+        } else {
+          double tv[12];
+          const int m = cand_terms(p, geo, ch, wv[u], k, tv);
+          v = bfmx::round_down_sum(tv, m);
+        }
+        p.out[geo.base + static_cast<long>(k) * A.stride] = v;
       }
     }
   }
@@ -1462,7 +1577,10 @@ CtPlan::~CtPlan() {
     if (tables_[a]) {
       bool shared = false;
       for (int b = 0; b < a; ++b) shared |= tables_[b] == tables_[a];
-      if (!shared) dfree(tables_[a]);
+      if (!shared) {
+        dfree(tables_[a]);
+        if (ftables_[a]) dfree(ftables_[a]);
+      }
     }
   for (auto* p : state_)
     if (p) dfree(p);
@@ -1544,8 +1662,49 @@ void CtPlan::setup(const GridDesc& loc, const GridDesc& global, int pb, int pe, 
         BFM_CUDA(dmalloc(&tables_[a], host.size() * sizeof(double4)));
         BFM_CUDA(cudaMemcpy(tables_[a], host.data(), host.size() * sizeof(double4),
                             cudaMemcpyHostToDevice));
+        // the same values as exact integers g * 2^124 when every coordinate
+        // is a multiple of 2^-62 (coord(h, 0) >= 2^-10, i.e. n <= 512)
+        if (coord(global.h[a], 0) >= 0x1p-10) {
+          std::vector<__int128> fx(host.size());
+          bool ok = true;
+          auto fixed = [&](double v, int scale) -> __int128 {  // v * 2^scale, must be an integer
+            if (v == 0.0) return 0;
+            int E = 0;
+            const double f = std::frexp(std::fabs(v), &E);  // |v| = f 2^E, f in [0.5, 1)
+            const long long m = static_cast<long long>(std::ldexp(f, 53));  // exact
+            const int sh = E - 53 + scale;
+            __int128 r;
+            if (sh >= 0) {
+              if (sh > 126 - 53) ok = false;
+              r = static_cast<__int128>(m) << (sh > 70 ? 70 : sh);
+            } else {
+              if (sh < -53 || (m & ((1ll << -sh) - 1)) != 0) ok = false;
+              r = sh < -53 ? 0 : (m >> -sh);
+            }
+            return v < 0 ? -r : r;
+          };
+          for (int k = 0; k < n && ok; ++k) {
+            const double x = coord(global.h[a], k);
+            for (int j = 0; j < n; ++j) {
+              const double y = coord(global.h[a], j);
+              const __int128 X = fixed(x, 62), Y = fixed(y, 62);
+              const __int128 g = fixed(0.5 * x * x, 124) + fixed(0.5 * y * y, 124) - X * Y;
+              // must equal the limbs of the expansion table
+              const double4 L = host[static_cast<size_t>(k) * n + j];
+              if (g != fixed(L.x, 124) + fixed(L.y, 124) + fixed(L.z, 124)) ok = false;
+              fx[static_cast<size_t>(k) * n + j] = g;
+            }
+          }
+          if (ok) {
+            BFM_CUDA(dmalloc(&ftables_[a], fx.size() * sizeof(__int128)));
+            BFM_CUDA(cudaMemcpy(ftables_[a], fx.data(), fx.size() * sizeof(__int128), cudaMemcpyHostToDevice));
+          }
+        }
       }
       A.G = tables_[a];
+      for (int b = 0; b < a; ++b)
+        if (tables_[b] == tables_[a]) ftables_[a] = ftables_[b];
+      A.GF = ftables_[a];
     }
   }
   dyadic_ = true;
@@ -1583,6 +1742,9 @@ void CtPlan::setup(const GridDesc& loc, const GridDesc& global, int pb, int pe, 
     const int n = loc.n[a];
     P.nlines = loc.size / n;
     P.strided = a != loc.d - 1;
+    P.fixed = 1;
+    for (int b = 0; b < loc.d; ++b)
+      if (!P.ax[b].dyadic && !P.ax[b].GF) P.fixed = 0;
     const bool dy = dyadic_;
     if (dy) {
       // exact-hull kernel: (s, q) per point in shared memory; about 11 points

@@ -14,6 +14,9 @@ struct CtAxis {
   double h;
   int dyadic;          // 1: g(k,j) = 0.5 (x_k - y_j)^2 is an exact double
   const double4* G;    // else: [n*n] exact limbs (hi, mid, lo, 0) of hs(x_k)+hs(y_j)-x_k*y_j
+  // non-dyadic axes with n <= 512: the same values as exact fixed-point
+  // integers g * 2^124 (every coordinate is then a multiple of 2^-62)
+  const __int128* GF;
 };
 
 struct CtPass {
@@ -36,6 +39,7 @@ struct CtPass {
   double* q_out;  // non-last passes: phi at the winner's chain, per node
   // shared-memory carve-up (bytes, per line)
   int off_fv, off_chain, off_hidx, off_H, off_flag, off_list, off_lohi, off_scal, line_bytes;
+  int fixed;  // non-dyadic kernel: every non-dyadic axis has a fixed-point table
   // statistics (device counters, may be null): lines that needed exact resolution
   unsigned long long* slow_queries;
   unsigned long long* stats;  // optional diagnostics (env BFM_CT_STATS=1)
@@ -76,6 +80,7 @@ class CtPlan {
   GridDesc g_;
   CtAxis ax_[3] = {};
   double4* tables_[3] = {nullptr, nullptr, nullptr};
+  __int128* ftables_[3] = {nullptr, nullptr, nullptr};
   uint32_t* state_[2] = {nullptr, nullptr};
   double* qbuf_[2] = {nullptr, nullptr};  // phi at the argmin chain, per node (pass outputs)
   unsigned long long* slow_ = nullptr;
