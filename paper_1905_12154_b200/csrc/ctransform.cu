@@ -49,6 +49,10 @@ __device__ __forceinline__ void cp_async8(void* smem_dst, const void* gmem_src) 
   const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem_dst));
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gmem_src) : "memory");
 }
+__device__ __forceinline__ void cp_async4(void* smem_dst, const void* gmem_src) {
+  const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem_dst));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(sa), "l"(gmem_src) : "memory");
+}
 __device__ __forceinline__ void cp_async_wait_all() {
   asm volatile("cp.async.wait_all;\n" ::: "memory");
 }
@@ -1176,6 +1180,14 @@ __global__ void __launch_bounds__(kDyThreads) ct_dy_kernel(CtPass p) {
       if (p.a == 0) {
         for (int j = first; j < n; j += step)
           cp_async8(&sm.q[dyi(j)], &p.phi[g.phi_other + static_cast<long>(j) * A.stride]);
+      } else if (p.pregathered) {
+        // q sits at the candidate's own node: chain and q both go straight
+        // to shared memory, every load of the line in flight at once
+        for (int j = first; j < n; j += step) {
+          const long node = g.base + static_cast<long>(j) * A.stride;
+          cp_async4(&sm.ch[j], &p.state_in[node]);
+          cp_async8(&sm.q[dyi(j)], &p.phi[node]);
+        }
       } else {
         constexpr int kBatch = 8;
         for (int j0 = first; j0 < n; j0 += kBatch * step) {
