@@ -330,3 +330,30 @@ def test_pushforward_tier_boundaries(shape):
     got = bfm.pushforward_density(np.stack(disp), mu)
     want = O.orc_pushforward_density(np.stack(disp), mu)
     assert O.n_bit_diff(got, want) == 0
+
+
+def test_solver_c2_until_dual_gap_vs_reference(ref):
+    """C2 (BASELINE configs[1]): 1024^2, run until |dual_n - dual_(n-1)| < 1e-6
+    (capped at 120 steps here). Both solvers step in
+    lockstep: the same stopping iteration, bitwise-equal potentials there,
+    duals within 1e-12 relative throughout."""
+    mu, nu = synthetic.c2()
+    cfg = bfm.SolverConfig(tolerance=-1.0, max_iterations=10 ** 6)
+    a = bfm.Solver(mu, nu, cfg)
+    b = ref.RefSolver(mu, nu, cfg)
+    prev_a = prev_b = None
+    stop_a = stop_b = None
+    for it in range(1, 121):
+        da = a.step().dual_value
+        db = b.step().dual_value
+        assert abs(da - db) <= 1e-12 * max(1.0, abs(db)), it
+        if stop_a is None and prev_a is not None and abs(da - prev_a) < 1e-6:
+            stop_a = it
+        if stop_b is None and prev_b is not None and abs(db - prev_b) < 1e-6:
+            stop_b = it
+        prev_a, prev_b = da, db
+        if stop_a is not None or stop_b is not None:
+            break
+    assert stop_a == stop_b and stop_a is not None
+    print(f"C2: |dual gap| < 1e-6 at iteration {stop_a} (dual {prev_a!r})")
+    assert O.n_bit_diff(a.phi(), b.phi()) == 0 and O.n_bit_diff(a.psi(), b.psi()) == 0
