@@ -84,3 +84,16 @@ def test_ctransform_bfm_iterates_full_size(ref):
         got = bfm.ctransform(phi)
         want = ref.ref_ctransform(phi)
         assert O.n_bit_diff(got, want) == 0
+
+
+def test_ctransform_c4_iterates_full_size(ref):
+    """Both inputs of a C4 iteration at 384^3 (non-dyadic: the fixed-point
+    exact evaluations) after two BFM steps, bitwise vs the reference."""
+    mu, nu = synthetic.c4()
+    s = bfm.Solver(mu, nu, bfm.SolverConfig(tolerance=-1.0, max_iterations=10))
+    s.step()
+    s.step()
+    for phi in (s.phi(), s.psi()):
+        got = bfm.ctransform(phi)
+        want = ref.ref_ctransform(phi)
+        assert O.n_bit_diff(got, want) == 0
