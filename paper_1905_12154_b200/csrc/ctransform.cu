@@ -1825,7 +1825,11 @@ void CtPlan::setup(const GridDesc& loc, const GridDesc& global, int pb, int pe, 
     P.line_bytes = o;
     if (o > budget) throw std::invalid_argument("ctransform: grid line too long for shared memory");
     int lpc = std::min<long>(budget / o, kNdThreads / P.tpl);
-    lpc = std::min(lpc, P.strided ? 16 : 8);
+    // 12 short lines per CTA: two CTAs per SM on C4's 384-lines (measured
+    // best among 4/8/12/16: 49 vs 53 ms of c-transform per C4 iteration at 16)
+    int lcap = 12;
+    if (const char* e = getenv("BFM_ND_LPC")) lcap = std::max(1, atoi(e));  // tuning experiments
+    lpc = std::min(lpc, lcap);
     if (P.tpl > 32) lpc = std::min(lpc, 15);
     lpc = static_cast<int>(std::min<long>(lpc, P.nlines));
     P.lpc = std::max(lpc, 1);
