@@ -458,7 +458,11 @@ void PoissonPlan::setup(const GridDesc& loc, const GridDesc& global, long col0, 
     }
     if (c.line_bytes > budget) throw std::invalid_argument("solve_neumann: line exceeds shared memory");
     int lpc = std::min(budget / c.line_bytes, 512 / c.tpl);
-    lpc = std::min(lpc, c.strided ? 32 : std::max(4, 128 / c.tpl));
+    // strided axes: 8 lines per CTA (64 B row segments) keeps several CTAs
+    // per SM so one CTA's loads overlap another's butterflies (C4: 32 lines,
+    // one 196 KB CTA per SM, 9.4 ms of Poisson per iteration; 16: 8.9; 8:
+    // 7.8; 4: 9.7)
+    lpc = std::min(lpc, c.strided ? 8 : std::max(4, 128 / c.tpl));
     if (c.tpl > 32) lpc = std::min(lpc, 15);
     lpc = static_cast<int>(std::min<long>(lpc, c.nlines));
     c.lpc = std::max(1, lpc);
