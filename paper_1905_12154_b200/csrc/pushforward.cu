@@ -254,7 +254,7 @@ __global__ void pf_pack_kernel(const int* bucket, long nrec, const int* d_n, con
 // and fold in place. Targets with more than kLight deposits are deferred to
 // pf_gather_heavy_kernel.
 template <int D>
-__global__ void __launch_bounds__(256) pf_gather_kernel(GatherArgs A, int* heavy, int* large,
+__global__ void __launch_bounds__(256, 8) pf_gather_kernel(GatherArgs A, int* heavy, int* large,
                                                         int* nheavy) {
   constexpr int NC = 1 << D;  // corner b = bit a set: the target is the upper node on axis a
   const GridDesc& g = A.g;
@@ -545,21 +545,25 @@ __global__ void __launch_bounds__(kMedWarps * 32) pf_gather_medium_kernel(Gather
 // ahead of the chain of adds).
 __global__ void __launch_bounds__(kLargeThreads) pf_gather_large_kernel(GatherArgs A,
                                                                        const int* large,
-                                                                       const int* nheavy,
+                                                                       int* nheavy,
                                                                        double* hbuf) {
   // the target's buckets (source ids) are merged by a merge-path tree in
   // shared memory, as in the warp tier, with 16-bit (run << 12 | index)
   // payloads; the weights then go to the CTA's buffer slice in source order
   extern __shared__ __align__(16) unsigned char large_smem[];
   __shared__ int tab[24];  // run starts, run lengths (merge tree)
-  __shared__ int s_pos[8], s_bits[8], s_nl, s_K;
+  __shared__ int s_pos[8], s_bits[8], s_nl, s_K, s_q;
   int* idsA = reinterpret_cast<int*>(large_smem);
   int* idsB = idsA + kLarge;
   uint16_t* payA = reinterpret_cast<uint16_t*>(idsB + kLarge);
   uint16_t* payB = payA + kLarge;
   const int nl_total = nheavy[4];
   double* buf = hbuf + static_cast<long>(blockIdx.x) * kLarge;
-  for (int q = blockIdx.x; q < nl_total; q += gridDim.x) {
+  for (;;) {  // targets claimed from a counter (nheavy[6], zeroed per call)
+    if (threadIdx.x == 0) s_q = atomicAdd(nheavy + 6, 1);
+    __syncthreads();
+    const int q = s_q;
+    if (q >= nl_total) break;
     const long t = large[q];
     if (threadIdx.x == 0) {
       TargetBuckets tb;
@@ -609,16 +613,23 @@ __global__ void __launch_bounds__(kLargeThreads) pf_gather_large_kernel(GatherAr
 // ids in shared memory when they fit (else ranked against global memory),
 // weights to the global buffer, then the CTA folds them (exact_fold.cuh).
 __global__ void __launch_bounds__(512) pf_gather_heavy_kernel(GatherArgs A, const int* heavy,
-                                                             const int* nheavy, double* hbuf,
+                                                             int* nheavy, double* hbuf,
                                                              unsigned long long* hfill) {
   __shared__ int s_pos[8], s_end[8], s_bits[8], s_cat[8], s_nl, s_K;
   __shared__ unsigned long long s_base;
+  __shared__ int s_q;
   __shared__ FoldTr fold_scr[512 / 32 + 1];
   __shared__ int fold_iscr[512 / 32];
   extern __shared__ int ids[];  // [kHeavyIds]
   const GridDesc& g = A.g;
   const int nh = nheavy[1];
-  for (int q = blockIdx.x; q < nh; q += gridDim.x) {
+  // targets are claimed from a counter (nheavy[5], zeroed per call): their
+  // costs differ by orders of magnitude, so a static stride leaves CTAs idle
+  for (;;) {
+    if (threadIdx.x == 0) s_q = atomicAdd(nheavy + 5, 1);
+    __syncthreads();
+    const int q = s_q;
+    if (q >= nh) break;
     const long t = heavy[g.size - 1 - q];
     if (threadIdx.x == 0) {
       TargetBuckets tb;
