@@ -612,7 +612,7 @@ __global__ void __launch_bounds__(kLargeThreads) pf_gather_large_kernel(GatherAr
 // Heavy targets (K > kLarge): one CTA each, same merge-rank scheme with the
 // ids in shared memory when they fit (else ranked against global memory),
 // weights to the global buffer, then the CTA folds them (exact_fold.cuh).
-__global__ void __launch_bounds__(512) pf_gather_heavy_kernel(GatherArgs A, const int* heavy,
+__global__ void __launch_bounds__(512, 2) pf_gather_heavy_kernel(GatherArgs A, const int* heavy,
                                                              int* nheavy, double* hbuf,
                                                              unsigned long long* hfill) {
   __shared__ int s_pos[8], s_end[8], s_bits[8], s_cat[8], s_nl, s_K;
