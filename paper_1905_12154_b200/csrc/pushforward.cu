@@ -219,34 +219,16 @@ __device__ __forceinline__ double pos_weight(const GatherArgs& A, int pos, int b
 __global__ void pf_pack_kernel(const int* bucket, long nrec, const int* d_n, const double* src, const double* w,
                                const uint8_t* cmask, int d, double4* rec, uint8_t* rmask) {
   const long n = d_n ? *d_n : nrec;
-  const long stride = static_cast<long>(gridDim.x) * blockDim.x;
-  // four records per thread and round: their gathers are in flight together
-  for (long i0 = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; i0 < n; i0 += 4 * stride) {
-    int sv[4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const long i = i0 + u * stride;
-      sv[u] = i < n ? bucket[i] : 0;
-    }
-    double4 r[4];
-    uint8_t mk[4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int s = sv[u];
-      r[u].x = src[s];
-      r[u].y = d > 0 ? w[s] : 0.0;
-      r[u].z = d > 1 ? w[nrec + s] : 0.0;
-      r[u].w = d > 2 ? w[2 * nrec + s] : 0.0;
-      mk[u] = cmask[s];
-    }
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const long i = i0 + u * stride;
-      if (i < n) {
-        rec[i] = r[u];
-        rmask[i] = mk[u];
-      }
-    }
+  for (long i = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<long>(gridDim.x) * blockDim.x) {
+    const int s = bucket[i];
+    double4 r;
+    r.x = src[s];
+    r.y = d > 0 ? w[s] : 0.0;
+    r.z = d > 1 ? w[nrec + s] : 0.0;
+    r.w = d > 2 ? w[2 * nrec + s] : 0.0;
+    rec[i] = r;
+    rmask[i] = cmask[s];
   }
 }
 
@@ -254,7 +236,7 @@ __global__ void pf_pack_kernel(const int* bucket, long nrec, const int* d_n, con
 // and fold in place. Targets with more than kLight deposits are deferred to
 // pf_gather_heavy_kernel.
 template <int D>
-__global__ void __launch_bounds__(256, 8) pf_gather_kernel(GatherArgs A, int* heavy, int* large,
+__global__ void __launch_bounds__(256, D < 3 ? 8 : 1) pf_gather_kernel(GatherArgs A, int* heavy, int* large,
                                                         int* nheavy) {
   constexpr int NC = 1 << D;  // corner b = bit a set: the target is the upper node on axis a
   const GridDesc& g = A.g;

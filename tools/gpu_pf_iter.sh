@@ -11,3 +11,4 @@ python - <<'PY'
 import json; d = json.loads(open("gpurun_out/c4.log").read().strip().splitlines()[-1])
 print("C4 ms/step", d["ms_per_step"], "ops", d.get("op_breakdown_ms_per_step"))
 PY
+[ -n "$C4_LIST" ] && python tools/prof_c3.py c4 1 > /dev/null 2>&1 && ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"pf_|rs_" --csv --log-file gpurun_out/pf_launches_c4.csv python tools/prof_c3.py c4 1 > /dev/null 2>&1; [ -n "$C4_LIST" ] && python tools/launches.py gpurun_out/pf_launches_c4.csv 2>/dev/null | head -8
