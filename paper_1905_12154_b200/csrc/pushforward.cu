@@ -236,7 +236,7 @@ __global__ void pf_pack_kernel(const int* bucket, long nrec, const int* d_n, con
 // and fold in place. Targets with more than kLight deposits are deferred to
 // pf_gather_heavy_kernel.
 template <int D>
-__global__ void __launch_bounds__(256, D < 3 ? 8 : 1) pf_gather_kernel(GatherArgs A, int* heavy, int* large,
+__global__ void __launch_bounds__(256, D < 3 ? 8 : 6) pf_gather_kernel(GatherArgs A, int* heavy, int* large,
                                                         int* nheavy) {
   constexpr int NC = 1 << D;  // corner b = bit a set: the target is the upper node on axis a
   const GridDesc& g = A.g;
