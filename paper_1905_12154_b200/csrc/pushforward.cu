@@ -875,6 +875,9 @@ void PushforwardPlan::setup(const GridDesc& loc, const GridDesc& global, int row
   BFM_CUDA(dmalloc(&end_, (ncells_ + 1) * sizeof(int)));
   BFM_CUDA(dmalloc(&heavy_, (N + 1) * sizeof(int)));
   BFM_CUDA(dmalloc(&large_, (N + 1) * sizeof(int)));
+  // per-call counters, zeroed by gather(); as ints: [0] warp-tier targets,
+  // [1] heavy targets, [2..3] heavy buffer fill (one u64), [4] CTA-tier
+  // targets, [5] / [6] heavy / CTA-tier work claims, [7] unused
   BFM_CUDA(dmalloc(&nheavy_, 4 * sizeof(unsigned long long)));
   ensure_records(N);
   BFM_CUDA(cudaFuncSetAttribute(pf_gather_large_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
