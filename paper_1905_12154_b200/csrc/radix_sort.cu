@@ -115,7 +115,7 @@ __global__ void __launch_bounds__(1024) rs_scan_apply(int* a, long m, const int*
   }
 }
 
-__global__ void __launch_bounds__(kThreads) rs_scatter_kernel(const uint32_t* kin, const int* vin,
+__global__ void __launch_bounds__(kThreads, 6) rs_scatter_kernel(const uint32_t* kin, const int* vin,
                                                             long n_max, const int* d_n, int shift,
                                                             long nblocks, const int* hist, uint32_t* kout,
                                                             int* vout) {
