@@ -185,6 +185,13 @@ int bfm_workspace_last_launches(const bfm_workspace* ws);
  * normalisation to unit mass with the Kahan mass of grid.hpp:151-164. */
 int bfm_builtin_density(int dim, const int* extents, const char* spec, double* out);
 int bfm_normalize(int dim, const int* extents, const double* raw, double* out);
+/* Host-only: the seeded synthetic densities of BASELINE.json configs C1-C4
+ * (SURVEY 8(d) shared generator: std::mt19937_64(seed), u = (rng()>>11)*2^-53,
+ * unit-peak Gaussians, closed indicators, Kahan normalisation). config 1..3
+ * fill n*n samples per density, config 4 n*n*n. Default seeds: C1 1, C2 2,
+ * C3 3, C4 4. The reference has no generator (its fixtures are builtin
+ * shapes, io.hpp:352-476); this is the input side of the benchmark harness. */
+int bfm_synthetic_densities(int config, int n, unsigned long long seed, double* mu, double* nu);
 
 typedef struct bfm_slab bfm_slab;
 /* Host-only: the validation of bfm_solver_create (solver.hpp:105-142,148-167)
@@ -246,6 +253,19 @@ long bfm_solver_launches(const bfm_solver* s);
  * reference also pays, solver.hpp:213) between two CUDA events recorded on the
  * solver's stream; *ms receives the device-timed duration. */
 int bfm_solver_time_steps(bfm_solver* s, int k, double* ms);
+
+/* Iterations run as captured CUDA graphs (one launch per step + probe, a
+ * single host synchronisation per batch of steps); on by default, env
+ * BFM_NO_GRAPHS=1 or this call switches to eager launches (same kernels,
+ * same bits). */
+int bfm_solver_set_graphs(bfm_solver* s, int on);
+/* Test hook: treat iteration `iteration` (1-based) as a near tie — in its
+ * step, or only in its probe when probe_only — so the solver replays it with
+ * every scalar in the reference's sequential Kahan order (the rare path taken
+ * when a sigma / blow-up / stall / stopping decision cannot be certified). */
+int bfm_solver_debug_force_exact(bfm_solver* s, int iteration, int probe_only);
+/* Number of exact replays so far (near ties met, or forced by the hook). */
+long bfm_solver_exact_replays(const bfm_solver* s);
 
 /* Bench helper: per-operator device time (CUDA events on the solver stream
  * around each operator call) accumulated while timing is on; switching it

@@ -203,6 +203,14 @@ def load_library(path: str = LIB_PATH):
     lib.bfm_normalize.restype = C.c_int
     lib.bfm_set_device.argtypes = [C.c_int]
     lib.bfm_set_device.restype = C.c_int
+    lib.bfm_solver_set_graphs.argtypes = [C.c_void_p, C.c_int]
+    lib.bfm_solver_set_graphs.restype = C.c_int
+    lib.bfm_solver_debug_force_exact.argtypes = [C.c_void_p, C.c_int, C.c_int]
+    lib.bfm_solver_debug_force_exact.restype = C.c_int
+    lib.bfm_solver_exact_replays.argtypes = [C.c_void_p]
+    lib.bfm_solver_exact_replays.restype = C.c_long
+    lib.bfm_synthetic_densities.argtypes = [C.c_int, C.c_int, C.c_ulonglong, C.c_void_p, C.c_void_p]
+    lib.bfm_synthetic_densities.restype = C.c_int
     _lib = lib
     return lib
 
@@ -419,6 +427,18 @@ class Solver:
         self._check(self._lib.bfm_solver_op_times(self._h, ms, n))
         return {name: (ms[i], n[i]) for i, name in enumerate(self.OPS)}
 
+    def set_graphs(self, on: bool) -> None:
+        """CUDA-graph iterations (default) or eager launches (same kernels, same bits)."""
+        self._check(self._lib.bfm_solver_set_graphs(self._h, 1 if on else 0))
+
+    def debug_force_exact(self, iteration: int, probe_only: bool = False) -> None:
+        """Test hook: replay `iteration` with reference-order (Kahan) scalars."""
+        self._check(self._lib.bfm_solver_debug_force_exact(self._h, int(iteration),
+                                                           1 if probe_only else 0))
+
+    def exact_replays(self) -> int:
+        return int(self._lib.bfm_solver_exact_replays(self._h))
+
     def time_steps(self, k: int) -> float:
         """Runs k iterations between CUDA events on the solver stream; returns ms."""
         ms = C.c_double()
@@ -535,6 +555,17 @@ def normalize(raw) -> np.ndarray:
     out = np.empty_like(raw)
     _check(lib, lib.bfm_normalize(raw.ndim, _extents(raw.shape), _ptr(raw), _ptr(out)))
     return out
+
+
+def synthetic_densities(config: int, n: int, seed: int):
+    """BASELINE.json configs C1-C4 from the library's shared generator
+    (bfm_synthetic_densities: std::mt19937_64, SURVEY 8(d)); returns (mu, nu)."""
+    lib = load_library()
+    shape = (n, n, n) if config == 4 else (n, n)
+    mu = np.empty(shape, dtype=np.float64)
+    nu = np.empty(shape, dtype=np.float64)
+    _check(lib, lib.bfm_synthetic_densities(int(config), int(n), int(seed), _ptr(mu), _ptr(nu)))
+    return mu, nu
 
 
 def builtin_density(shape: Sequence[int], spec: str) -> np.ndarray:

@@ -7,6 +7,8 @@
 // device through CtPlan / PushforwardPlan / PoissonPlan / Reducer; only
 // scalars cross to the host (one synchronising read per half step).
 #include <cctype>
+#include <cstdlib>
+#include <climits>
 #include <chrono>
 #include <cmath>
 #include <cstring>
@@ -23,8 +25,10 @@
 #include "poisson.cuh"
 #include "pushforward.cuh"
 #include "reduce.cuh"
+#include "solver_ctl.cuh"
 
 namespace bfmgpu {
+int synthetic_densities(int config, int n, uint64_t seed, double* mu, double* nu, std::string& msg);
 void debug_round_down(const double* h_terms, int m, int count, double* h_out);
 void debug_fold(const double* h_w, const long* h_off, int nseq, int mode, double* h_out);
 }
@@ -322,31 +326,51 @@ struct bfm_slab {
 struct bfm_solver {
   GridDesc g;
   bfm_config cfg;
+  CtlConfig kcfg;
   cudaStream_t stream = nullptr;
   bfm_workspace ws;
   DevBuf mu, nu, phi, psi, dir, dir2, r;
   DevBuf rep_phi, rep_psi, rep_map;
-  double sigma = 0.0;
-  double last_pair = 0.0;
-  double prev_dual = std::numeric_limits<double>::quiet_NaN();
-  double probe_dual = 0.0, probe_gn = 0.0;
+  double sigma0 = 0.0;
+  // Scalar state lives on the device (solver_ctl.cuh); h is the pinned mirror
+  // every unit copies back, ring the per-step stats of a batch.
+  SolverCtl* d_ctl = nullptr;
+  SolverCtl* h_ctl = nullptr;
+  CtlStats* d_ring = nullptr;
+  CtlStats* h_ring = nullptr;
+  int iteration = 0;
   bool fresh = false;
-  int iteration = 0, stall = 0;
+  bool probe_blowup = false;  // certified blow-up in a prefetched probe (thrown when consumed)
   bool has_report = false;
+  bool use_graphs = true;
+  int force_near_iter = -1, force_near_probe = 0;  // test hook (bfm_solver_debug_force_exact)
+  long exact_replays = 0;
   std::vector<bfm_iteration_stats> trace;
   std::chrono::steady_clock::time_point start;
 
   // Optional per-operator device timing (bench.py's live roofline): events
-  // recorded on the solver stream around each operator, resolved lazily.
+  // recorded on the solver stream around each operator (external event nodes
+  // inside captured graphs), resolved after the unit's synchronisation.
   bool timing = false;
   struct Pending {
     cudaEvent_t a, b;
     int op;
   };
-  std::vector<Pending> pending;
+  std::vector<Pending> pending;         // eager launches
+  std::vector<Pending>* capture_ev = nullptr;  // set while capturing a graph
+  std::vector<const std::vector<Pending>*> graph_pending;
   std::vector<cudaEvent_t> free_events;
   double op_ms[BFM_OP_COUNT] = {};
   long op_n[BFM_OP_COUNT] = {};
+
+  // One iteration unit as a CUDA graph: kind 0 probe, 1 step, 2 step + probe.
+  struct UnitGraph {
+    cudaGraphExec_t exec = nullptr;
+    long launches = 0;
+    int uses = 0;
+    std::vector<Pending> ev;
+  };
+  UnitGraph graphs[3][2];
 
   cudaEvent_t take_event() {
     if (free_events.empty()) {
@@ -365,22 +389,35 @@ struct bfm_solver {
       return;
     }
     cudaEvent_t a = take_event(), b = take_event();
+    if (capture_ev) {
+      BFM_CUDA(cudaEventRecordWithFlags(a, stream, cudaEventRecordExternal));
+      f();
+      BFM_CUDA(cudaEventRecordWithFlags(b, stream, cudaEventRecordExternal));
+      capture_ev->push_back({a, b, op});
+      return;
+    }
     BFM_CUDA(cudaEventRecord(a, stream));
     f();
     BFM_CUDA(cudaEventRecord(b, stream));
     pending.push_back({a, b, op});
   }
+  void add_time(const Pending& q) {
+    BFM_CUDA(cudaEventSynchronize(q.b));
+    float ms = 0.0f;
+    BFM_CUDA(cudaEventElapsedTime(&ms, q.a, q.b));
+    op_ms[q.op] += ms;
+    op_n[q.op] += 1;
+  }
   void resolve_times() {
     for (const Pending& q : pending) {
-      BFM_CUDA(cudaEventSynchronize(q.b));
-      float ms = 0.0f;
-      BFM_CUDA(cudaEventElapsedTime(&ms, q.a, q.b));
-      op_ms[q.op] += ms;
-      op_n[q.op] += 1;
+      add_time(q);
       free_events.push_back(q.a);
       free_events.push_back(q.b);
     }
     pending.clear();
+    for (const auto* v : graph_pending)
+      for (const Pending& q : *v) add_time(q);
+    graph_pending.clear();
   }
 
   ~bfm_solver() {
@@ -388,16 +425,42 @@ struct bfm_solver {
       cudaEventDestroy(q.a);
       cudaEventDestroy(q.b);
     }
+    for (auto& row : graphs)
+      for (UnitGraph& G : row) {
+        if (G.exec) cudaGraphExecDestroy(G.exec);
+        for (const Pending& q : G.ev) {
+          cudaEventDestroy(q.a);
+          cudaEventDestroy(q.b);
+        }
+      }
     for (cudaEvent_t e : free_events) cudaEventDestroy(e);
+    if (d_ctl) dfree(d_ctl);
+    if (d_ring) dfree(d_ring);
+    if (h_ctl) cudaFreeHost(h_ctl);
+    if (h_ring) cudaFreeHost(h_ring);
     if (stream) cudaStreamDestroy(stream);
   }
 
-  double fetch1(int slot) {
-    double v[4];
-    ws.redp().fetch(v, slot + 1, stream);
-    return v[slot];
+  // ---- scalar state -------------------------------------------------------
+  void init_ctl() {  // solver.hpp:148-167,360-368
+    std::memset(h_ctl, 0, sizeof(SolverCtl));
+    h_ctl->sigma = sigma0;
+    h_ctl->last_pair = 0.0;
+    h_ctl->prev_dual = std::numeric_limits<double>::quiet_NaN();
+    upload_ctl();
+  }
+  void upload_ctl() {
+    BFM_CUDA(cudaMemcpyAsync(d_ctl, h_ctl, sizeof(SolverCtl), cudaMemcpyHostToDevice, stream));
+    BFM_CUDA(cudaStreamSynchronize(stream));
+  }
+  void decide(int stage, int slot) {
+    timed(BFM_OP_REDUCE, [&] {
+      ctl_decide(d_ctl, ws.redp().device_results(), slot, slot >= 0 ? kBoundSlot + slot : 0, stage,
+                 kcfg, d_ring, stream, &ws.lc);
+    });
   }
 
+  // ---- device units (no host synchronisation) ------------------------------
   void pair_value_async() {  // solver.hpp:240
     timed(BFM_OP_REDUCE, [&] {
       ws.redp().dot(phi.p, nu.p, psi.p, mu.p, g.size, g.vol, kSlotPair, stream, &ws.lc);
@@ -406,7 +469,9 @@ struct bfm_solver {
   void ctransform(const double* in, double* out) {
     timed(BFM_OP_CTRANSFORM, [&] { ws.ctp().run(in, out, stream, &ws.lc); });
   }
-
+  void axpy_device(double* u, const double* d) {
+    timed(BFM_OP_REDUCE, [&] { axpy_dev(u, &d_ctl->sigma, d, g.size, stream, &ws.lc); });
+  }
   // solver.hpp:245-260 (result left in d_dir, gn in kSlotGn)
   void ascent_direction_async(const double* u, const double* source, const double* target,
                               double* d_dir) {
@@ -417,95 +482,288 @@ struct bfm_solver {
       ws.redp().dot(r.p, d_dir, nullptr, nullptr, g.size, g.vol, kSlotGn, stream, &ws.lc);
     });
   }
-
-  void ensure_probe() {  // solver.hpp:264-280
-    if (fresh) return;
+  void enqueue_probe() {  // solver.hpp:264-280
     if (cfg.mode == BFM_MODE_BACK_AND_FORTH) {
       ctransform(phi.p, psi.p);
       pair_value_async();
-      const double v = fetch1(kSlotPair);
-      if (v < last_pair - 1e-10)
-        fail(BFM_ERR_NUMERICAL_BLOWUP, "solve: conjugation decreased the dual pair value");
-      last_pair = v;
-      probe_dual = v;
+      decide(kStageProbePair, kSlotPair);
     } else {
-      probe_dual = last_pair;
+      decide(kStageProbeGA, -1);
     }
     ascent_direction_async(psi.p, mu.p, nu.p, dir.p);
-    probe_gn = fetch1(kSlotGn);
-    fresh = true;
+    decide(kStageProbeGn, kSlotGn);
   }
-
-  void step_back_and_forth(bfm_iteration_stats& st) {  // solver.hpp:286-310
-    const double v2 = probe_dual;
-    st.sigma_first = sigma;
-    st.grad_norm_sq_first = probe_gn;
-    timed(BFM_OP_REDUCE, [&] { axpy(phi.p, sigma, dir.p, g.size, stream, &ws.lc); });
+  void enqueue_step() {  // solver.hpp:286-328
+    decide(kStageStepBegin, -1);
+    axpy_device(phi.p, dir.p);
     ctransform(phi.p, psi.p);
     pair_value_async();
-    const double v3 = fetch1(kSlotPair);
-    st.increase_first = v3 - v2;
-    sigma = update_sigma(sigma, st.increase_first, probe_gn, cfg);
-
+    decide(kStageFirst, kSlotPair);
     ctransform(psi.p, phi.p);
     pair_value_async();
-    const double v4 = fetch1(kSlotPair);
-    if (v4 < v3 - 1e-10)
-      fail(BFM_ERR_NUMERICAL_BLOWUP, "solve: conjugation decreased the dual pair value");
+    if (cfg.mode != BFM_MODE_BACK_AND_FORTH) {
+      decide(kStageGAv3, kSlotPair);
+      return;
+    }
+    decide(kStageV4, kSlotPair);
     ascent_direction_async(phi.p, nu.p, mu.p, dir2.p);
-    const double gn2 = fetch1(kSlotGn);
-    st.sigma_second = sigma;
-    st.grad_norm_sq_second = gn2;
-    timed(BFM_OP_REDUCE, [&] { axpy(psi.p, sigma, dir2.p, g.size, stream, &ws.lc); });
+    decide(kStageGn2, kSlotGn);
+    axpy_device(psi.p, dir2.p);
     ctransform(psi.p, phi.p);
     pair_value_async();
-    const double v5 = fetch1(kSlotPair);
-    st.increase_second = v5 - v4;
-    sigma = update_sigma(sigma, st.increase_second, gn2, cfg);
-    st.dual_value = v5;
-    last_pair = v5;
+    decide(kStageV5, kSlotPair);
+  }
+  void enqueue_unit(int kind) {
+    if (kind != 1 && kind != 2) enqueue_probe();
+    if (kind != 0) enqueue_step();
+    if (kind == 2) enqueue_probe();
+    BFM_CUDA(cudaMemcpyAsync(h_ctl, d_ctl, sizeof(SolverCtl), cudaMemcpyDeviceToHost, stream));
+  }
+  // Launches one unit: eagerly the first time (plans allocate lazily), then as
+  // a captured CUDA graph replayed with a single launch.
+  void launch_unit(int kind) {
+    if (!use_graphs) return enqueue_unit(kind);
+    UnitGraph& G = graphs[kind][timing ? 1 : 0];
+    if (G.uses++ == 0) return enqueue_unit(kind);
+    if (!G.exec) {
+      const long before = ws.lc.count;
+      cudaGraph_t graph = nullptr;
+      BFM_CUDA(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal));
+      capture_ev = &G.ev;
+      try {
+        enqueue_unit(kind);
+      } catch (...) {
+        capture_ev = nullptr;
+        cudaStreamEndCapture(stream, &graph);
+        if (graph) cudaGraphDestroy(graph);
+        throw;
+      }
+      capture_ev = nullptr;
+      BFM_CUDA(cudaStreamEndCapture(stream, &graph));
+      const cudaError_t e = cudaGraphInstantiate(&G.exec, graph, 0);
+      cudaGraphDestroy(graph);
+      BFM_CUDA(e);
+      G.launches = ws.lc.count - before;
+      ws.lc.count = before;
+    }
+    BFM_CUDA(cudaGraphLaunch(G.exec, stream));
+    ws.lc.add(G.launches);
+    if (timing) graph_pending.push_back(&G.ev);
+  }
+  void sync() {
+    BFM_CUDA(cudaStreamSynchronize(stream));
+    if (timing) resolve_times();
+  }
+  void clear_flags() {
+    BFM_CUDA(cudaMemsetAsync(&d_ctl->flags, 0, sizeof(int), stream));
   }
 
-  void step_gradient_ascent(bfm_iteration_stats& st) {  // solver.hpp:312-328
-    const double v1 = probe_dual;
-    st.sigma_first = sigma;
-    st.grad_norm_sq_first = probe_gn;
-    timed(BFM_OP_REDUCE, [&] { axpy(phi.p, sigma, dir.p, g.size, stream, &ws.lc); });
-    ctransform(phi.p, psi.p);
-    pair_value_async();
-    const double v2 = fetch1(kSlotPair);
-    st.increase_first = v2 - v1;
-    sigma = update_sigma(sigma, st.increase_first, probe_gn, cfg);
-    ctransform(psi.p, phi.p);
-    pair_value_async();
-    const double v3 = fetch1(kSlotPair);
-    if (v3 < v2 - 1e-10)
-      fail(BFM_ERR_NUMERICAL_BLOWUP, "solve: conjugation decreased the dual pair value");
-    st.dual_value = v3;
-    last_pair = v3;
+  [[noreturn]] void blowup() {
+    fail(BFM_ERR_NUMERICAL_BLOWUP, "solve: conjugation decreased the dual pair value");
   }
 
-  bfm_iteration_stats step() {  // solver.hpp:189-207
-    ensure_probe();
+  // ---- exact scalars (rare path) ------------------------------------------
+  // The reference's sequential Kahan sums (grid.hpp:124-133,171-176) of the
+  // device fields, on the host.
+  std::vector<double> host_field(const double* d) {
+    std::vector<double> h(g.size);
+    copy_d2h(h.data(), d, g.size, stream);
+    return h;
+  }
+  double kahan_dot(const double* da, const double* db) {
+    const std::vector<double> a = host_field(da), b = host_field(db);
+    Kahan k;
+    for (long i = 0; i < g.size; ++i) k.add(a[i] * b[i]);
+    return k.sum * g.vol;
+  }
+  double kahan_pair() { return kahan_dot(phi.p, nu.p) + kahan_dot(psi.p, mu.p); }  // solver.hpp:240
+
+  void exact_probe() {  // solver.hpp:264-280 with reference-order scalars
+    SolverCtl& c = *h_ctl;
+    if (cfg.mode == BFM_MODE_BACK_AND_FORTH) {
+      ctransform(phi.p, psi.p);
+      const double v = kahan_pair();
+      if (v < c.last_pair - 1e-10) blowup();
+      c.last_pair = v;
+      c.last_pair_b = 0.0;
+      c.probe_dual = v;
+    } else {
+      c.probe_dual = c.last_pair;
+    }
+    c.probe_dual_b = 0.0;
+    ascent_direction_async(psi.p, mu.p, nu.p, dir.p);
+    c.probe_gn = kahan_dot(r.p, dir.p);
+    c.probe_gn_b = 0.0;
+  }
+  bfm_iteration_stats exact_step() {  // solver.hpp:189-207,286-328
+    SolverCtl& c = *h_ctl;
     bfm_iteration_stats st;
     std::memset(&st, 0, sizeof(st));
     st.iteration = iteration + 1;
-    st.residual = std::sqrt(std::max(probe_gn, 0.0));
-    if (cfg.mode == BFM_MODE_BACK_AND_FORTH) step_back_and_forth(st);
-    else step_gradient_ascent(st);
-    fresh = false;
-    ++iteration;
-    if (std::abs(st.dual_value - prev_dual) < 1e-12) ++stall;
-    else stall = 0;
-    prev_dual = st.dual_value;
-    trace.push_back(st);
+    st.residual = std::sqrt(std::max(c.probe_gn, 0.0));
+    st.sigma_first = c.sigma;
+    st.grad_norm_sq_first = c.probe_gn;
+    timed(BFM_OP_REDUCE, [&] { axpy(phi.p, c.sigma, dir.p, g.size, stream, &ws.lc); });
+    ctransform(phi.p, psi.p);
+    const double v2 = c.probe_dual, v3 = kahan_pair();
+    st.increase_first = v3 - v2;
+    c.sigma = update_sigma(c.sigma, st.increase_first, c.probe_gn, cfg);
+    ctransform(psi.p, phi.p);
+    const double v4 = kahan_pair();
+    if (v4 < v3 - 1e-10) blowup();
+    if (cfg.mode == BFM_MODE_BACK_AND_FORTH) {
+      ascent_direction_async(phi.p, nu.p, mu.p, dir2.p);
+      const double gn2 = kahan_dot(r.p, dir2.p);
+      st.sigma_second = c.sigma;
+      st.grad_norm_sq_second = gn2;
+      timed(BFM_OP_REDUCE, [&] { axpy(psi.p, c.sigma, dir2.p, g.size, stream, &ws.lc); });
+      ctransform(psi.p, phi.p);
+      const double v5 = kahan_pair();
+      st.increase_second = v5 - v4;
+      c.sigma = update_sigma(c.sigma, st.increase_second, gn2, cfg);
+      st.dual_value = v5;
+    } else {
+      st.dual_value = v4;
+    }
+    c.last_pair = st.dual_value;
+    c.last_pair_b = 0.0;
+    if (std::abs(st.dual_value - c.prev_dual) < 1e-12) ++c.stall;
+    else c.stall = 0;
+    c.prev_dual = st.dual_value;
+    c.prev_dual_b = 0.0;
     return st;
+  }
+
+  // Iteration k's probe (and its step when with_step) could not be certified
+  // to follow the reference's branches: recompute from the initial state —
+  // iterations 1..k-1 on the device (their decisions were certified, so they
+  // reproduce bit for bit), then iteration k with every scalar in the
+  // reference's Kahan order. Leaves iteration = k (or k-1 with a fresh probe).
+  void replay_exact(int k, bool with_step) {
+    ++exact_replays;
+    for (DevBuf* b : {&phi, &psi})
+      BFM_CUDA(cudaMemsetAsync(b->p, 0, g.size * sizeof(double), stream));
+    init_ctl();
+    for (int j = 1; j < k; ++j) {
+      clear_flags();
+      enqueue_unit(0);
+      enqueue_unit(1);
+    }
+    sync();
+    if (k > 1 && (h_ctl->flags & (kCtlNear | kCtlBlowup)))
+      fail(BFM_ERR_ERROR, "internal error: device replay diverged from the certified run");
+    if (h_ctl->done != k - 1) fail(BFM_ERR_ERROR, "internal error: replay iteration count");
+    if (k > 1) {  // the end-of-iteration pair value in the reference's order
+      const double v = kahan_pair();
+      h_ctl->last_pair = h_ctl->prev_dual = v;
+      h_ctl->last_pair_b = h_ctl->prev_dual_b = 0.0;
+    }
+    iteration = k - 1;
+    trace.resize(k - 1);
+    exact_probe();
+    fresh = true;
+    probe_blowup = false;
+    if (with_step) {
+      const bfm_iteration_stats st = exact_step();
+      trace.push_back(st);
+      iteration = k;
+      h_ctl->done = k;
+      fresh = false;
+    }
+    h_ctl->flags = 0;
+    upload_ctl();
+  }
+
+  // ---- host API -----------------------------------------------------------
+  void ensure_probe() {  // solver.hpp:264-280
+    if (fresh) {
+      if (probe_blowup) blowup();
+      return;
+    }
+    clear_flags();
+    launch_unit(0);
+    sync();
+    const int done = h_ctl->done;
+    if ((h_ctl->flags & kCtlNear) || (force_near_iter == done + 1 && force_near_probe)) {
+      force_near_iter = -1;
+      replay_exact(done + 1, false);
+      return;
+    }
+    if (h_ctl->flags & kCtlBlowup) blowup();
+    fresh = true;
+  }
+
+  // n consecutive steps with one synchronisation (prefetch: also the probe
+  // that follows the last step). Stats come back through the device ring.
+  void steps(int n, bool prefetch, cudaEvent_t end_event = nullptr) {
+    ensure_probe();
+    if (n > kCtlRing) n = kCtlRing;
+    const int done0 = h_ctl->done;
+    clear_flags();
+    for (int i = 0; i < n; ++i) launch_unit(i + 1 < n || prefetch ? 2 : 1);
+    if (end_event) BFM_CUDA(cudaEventRecord(end_event, stream));
+    if (n > 1)
+      BFM_CUDA(cudaMemcpyAsync(h_ring, d_ring, kCtlRing * sizeof(CtlStats), cudaMemcpyDeviceToHost,
+                               stream));
+    sync();
+    const SolverCtl c = *h_ctl;
+    // Events of step j+1 (0-based j) and of the probe it consumed carry
+    // near_iter / blowup_iter == j; probe stages order before step stages.
+    auto key = [](int it, int stage) { return static_cast<long>(it) * 16 + stage; };
+    const long near_at = (c.flags & kCtlNear) ? key(c.near_iter, c.near_stage) : LONG_MAX;
+    const long blow_at = (c.flags & kCtlBlowup) ? key(c.blowup_iter, c.blowup_stage) : LONG_MAX;
+    for (int j = done0; j < done0 + n; ++j) {
+      const long end_j = key(j + 1, 0);
+      const bool forced = force_near_iter == j + 1 && !force_near_probe;
+      if (forced || (near_at < end_j && near_at < blow_at)) {
+        // the first uncertified decision belongs to iteration j+1: replay it
+        // with reference-order scalars (the later steps of the batch are redone)
+        force_near_iter = -1;
+        replay_exact(j + 1, true);
+        if (prefetch) ensure_probe();
+        return;
+      }
+      if (blow_at < end_j) {  // certified blow-up inside iteration j+1
+        iteration = j;
+        fresh = false;
+        blowup();
+      }
+      const CtlStats& x = n > 1 ? h_ring[j % kCtlRing] : c.last;
+      bfm_iteration_stats st;
+      st.iteration = j + 1;
+      st.residual = x.residual;
+      st.dual_value = x.dual_value;
+      st.sigma_first = x.sigma_first;
+      st.sigma_second = x.sigma_second;
+      st.grad_norm_sq_first = x.gn_first;
+      st.grad_norm_sq_second = x.gn_second;
+      st.increase_first = x.inc_first;
+      st.increase_second = x.inc_second;
+      trace.push_back(st);
+      iteration = j + 1;
+    }
+    fresh = prefetch;
+    probe_blowup = false;
+    if (!prefetch) return;
+    // the trailing probe belongs to iteration done0 + n + 1
+    const int k = done0 + n + 1;
+    if ((force_near_iter == k && force_near_probe) || (near_at != LONG_MAX && near_at < blow_at)) {
+      force_near_iter = -1;
+      replay_exact(k, false);
+      return;
+    }
+    if (blow_at != LONG_MAX) probe_blowup = true;
+  }
+
+  bfm_iteration_stats step() {  // solver.hpp:189-207
+    steps(1, false);
+    return trace.back();
   }
 
   void finish(int term, double residual, bfm_report* rep) {  // solver.hpp:330-349
     rep->termination = term;
     rep->iterations = iteration;
-    rep->dual_value = probe_dual;
+    rep->dual_value = h_ctl->probe_dual;
     rep->residual = residual;
     rep_phi.alloc(g.size);
     rep_psi.alloc(g.size);
@@ -525,7 +783,9 @@ struct bfm_solver {
     add_scalar(rep_psi.p, shift, g.size, stream, &ws.lc);
     ws.pfp().map_only(rep_psi.p, rep_map.p, stream, &ws.lc);
     ws.redp().primal(rep_map.p, mu.p, g.d, g.size, g.vol, kSlotPrimal, stream, &ws.lc);
-    rep->primal_cost = fetch1(kSlotPrimal);
+    double v[kSlotPrimal + 1];
+    ws.redp().fetch(v, kSlotPrimal + 1, stream);
+    rep->primal_cost = v[kSlotPrimal];
     rep->wall_seconds =
         std::chrono::duration<double>(std::chrono::steady_clock::now() - start).count();
     has_report = true;
@@ -534,16 +794,38 @@ struct bfm_solver {
   void run(bfm_report* rep) {  // solver.hpp:211-226
     while (true) {
       ensure_probe();
-      const double residual = std::sqrt(std::max(probe_gn, 0.0));
+      const SolverCtl& c = *h_ctl;
+      const double residual = std::sqrt(std::max(c.probe_gn, 0.0));
+      // the rules compare certified probe scalars: |sqrt(a) - sqrt(b)| <=
+      // sqrt(|a - b|); a near tie replays the probe with exact scalars
+      const double u4 = 4.0 * 0x1.0p-53;
+      if (cfg.tolerance >= 0.0 &&
+          near_tie(residual, std::sqrt(c.probe_gn_b) + u4 * residual, cfg.tolerance))
+        continue;
       if (cfg.tolerance >= 0.0 && residual <= cfg.tolerance)
         return finish(BFM_TERM_TOLERANCE_MET, residual, rep);
-      if (cfg.has_exact_cost && cfg.exact_tolerance > 0.0 &&
-          std::abs(probe_dual - cfg.exact_cost) <= cfg.exact_tolerance)
-        return finish(BFM_TERM_COST_TARGET_MET, residual, rep);
+      if (cfg.has_exact_cost && cfg.exact_tolerance > 0.0) {
+        const double dev = std::abs(c.probe_dual - cfg.exact_cost);
+        if (near_tie(dev, c.probe_dual_b + u4 * dev, cfg.exact_tolerance)) continue;
+        if (dev <= cfg.exact_tolerance) return finish(BFM_TERM_COST_TARGET_MET, residual, rep);
+      }
       if (iteration >= cfg.max_iterations) return finish(BFM_TERM_MAX_ITERATIONS, residual, rep);
-      if (stall >= 10) return finish(BFM_TERM_DUAL_STALLED, residual, rep);
-      step();
+      if (c.stall >= 10) return finish(BFM_TERM_DUAL_STALLED, residual, rep);
+      // steps no rule can interrupt run back to back with one synchronisation:
+      // only the iteration cap and the stall counter (+1 per step at most) apply
+      int batch = 1;
+      if (cfg.tolerance < 0.0 && !(cfg.has_exact_cost && cfg.exact_tolerance > 0.0) && !timing)
+        batch = std::max(1, std::min(cfg.max_iterations - iteration, 10 - c.stall));
+      steps(batch, true);
     }
+  }
+
+  // A stopping comparison x <= thr whose x is within its bound of thr: replay
+  // the probe with reference-order scalars (then the loop re-evaluates).
+  bool near_tie(double x, double bound, double thr) {
+    if (!(bound > 0.0) || std::abs(x - thr) > 2.0 * bound) return false;
+    replay_exact(iteration + 1, false);
+    return true;
   }
 };
 
@@ -677,8 +959,14 @@ int bfm_solver_create(int dim, const int* extents, const double* mu, const doubl
     if (needs_host(v[5], v[6], v[10]) || std::abs(v[10] - 1.0) > 1e-6) check_density("mu", mu, g);
     if (needs_host(v[8], v[9], v[11]) || std::abs(v[11] - 1.0) > 1e-6) check_density("nu", nu, g);
     const double sup = std::max(v[4], v[7]);  // solver.hpp:160-163
-    s->sigma = c.sigma_init > 0.0 ? c.sigma_init : 8.0 / sup;
-    s->last_pair = 0.0;
+    s->sigma0 = c.sigma_init > 0.0 ? c.sigma_init : 8.0 / sup;
+    s->kcfg = CtlConfig{c.beta_1, c.beta_2, c.alpha_1, c.alpha_2, c.sigma_min};
+    BFM_CUDA(dmalloc(&s->d_ctl, sizeof(SolverCtl)));
+    BFM_CUDA(dmalloc(&s->d_ring, kCtlRing * sizeof(CtlStats)));
+    BFM_CUDA(cudaMallocHost(&s->h_ctl, sizeof(SolverCtl)));
+    BFM_CUDA(cudaMallocHost(&s->h_ring, kCtlRing * sizeof(CtlStats)));
+    s->init_ctl();
+    if (const char* e = std::getenv("BFM_NO_GRAPHS")) s->use_graphs = e[0] == '0';
     s->ws.ctp();
     s->ws.poisp();
     s->ws.pfp();
@@ -689,25 +977,30 @@ int bfm_solver_create(int dim, const int* extents, const double* mu, const doubl
 }
 
 void bfm_solver_destroy(bfm_solver* s) { delete s; }
-int bfm_solver_iteration(const bfm_solver* s) { return s->iteration; }
-double bfm_solver_sigma(const bfm_solver* s) { return s->sigma; }
+int bfm_solver_iteration(const bfm_solver* s) { return s ? s->iteration : -1; }
+double bfm_solver_sigma(const bfm_solver* s) {
+  return s ? s->h_ctl->sigma : std::numeric_limits<double>::quiet_NaN();
+}
 
 int bfm_solver_dual_value(bfm_solver* s, double* out) {
   return guard([&] {
+    if (!s || !out) fail(BFM_ERR_INVALID_ARGUMENT, "bfm_solver_dual_value: null argument");
     s->ensure_probe();
-    *out = s->probe_dual;
+    *out = s->h_ctl->probe_dual;
   });
 }
 
 int bfm_solver_residual(bfm_solver* s, double* out) {
   return guard([&] {
+    if (!s || !out) fail(BFM_ERR_INVALID_ARGUMENT, "bfm_solver_residual: null argument");
     s->ensure_probe();
-    *out = std::sqrt(std::max(s->probe_gn, 0.0));
+    *out = std::sqrt(std::max(s->h_ctl->probe_gn, 0.0));
   });
 }
 
 int bfm_solver_step(bfm_solver* s, bfm_iteration_stats* out) {
   return guard([&] {
+    if (!s) fail(BFM_ERR_INVALID_ARGUMENT, "bfm_solver_step: null handle");
     const bfm_iteration_stats st = s->step();
     if (out) *out = st;
   });
@@ -715,6 +1008,7 @@ int bfm_solver_step(bfm_solver* s, bfm_iteration_stats* out) {
 
 int bfm_solver_run(bfm_solver* s, bfm_report* out) {
   return guard([&] {
+    if (!s) fail(BFM_ERR_INVALID_ARGUMENT, "bfm_solver_run: null handle");
     bfm_report r;
     std::memset(&r, 0, sizeof(r));
     s->run(&r);
@@ -723,13 +1017,17 @@ int bfm_solver_run(bfm_solver* s, bfm_report* out) {
 }
 
 int bfm_solver_trace(const bfm_solver* s, bfm_iteration_stats* out, int cap, int* count) {
-  *count = static_cast<int>(s->trace.size());
-  for (int i = 0; i < cap && i < *count; ++i) out[i] = s->trace[i];
-  return BFM_OK;
+  return guard([&] {
+    if (!s || !count || (cap > 0 && !out))
+      fail(BFM_ERR_INVALID_ARGUMENT, "bfm_solver_trace: null argument");
+    *count = static_cast<int>(s->trace.size());
+    for (int i = 0; i < cap && i < *count; ++i) out[i] = s->trace[i];
+  });
 }
 
 int bfm_solver_field(bfm_solver* s, int which, double* host_out) {
   return guard([&] {
+    if (!s || !host_out) fail(BFM_ERR_INVALID_ARGUMENT, "bfm_solver_field: null argument");
     const double* src = which == BFM_FIELD_PHI ? s->phi.p : which == BFM_FIELD_PSI ? s->psi.p : nullptr;
     if (!src) fail(BFM_ERR_INVALID_ARGUMENT, "bfm_solver_field: PHI or PSI only");
     copy_d2h(host_out, src, s->g.size, s->stream);
@@ -738,6 +1036,7 @@ int bfm_solver_field(bfm_solver* s, int which, double* host_out) {
 
 int bfm_solver_report_field(bfm_solver* s, int which, double* host_out) {
   return guard([&] {
+    if (!s || !host_out) fail(BFM_ERR_INVALID_ARGUMENT, "bfm_solver_report_field: null argument");
     if (!s->has_report) fail(BFM_ERR_ERROR, "no report: call bfm_solver_run first");
     const double* src = nullptr;
     if (which == BFM_FIELD_PHI) src = s->rep_phi.p;
@@ -1024,6 +1323,14 @@ int bfm_normalize(int dim, const int* extents, const double* raw, double* out) {
   });
 }
 
+int bfm_synthetic_densities(int config, int n, unsigned long long seed, double* mu, double* nu) {
+  return guard([&] {
+    std::string msg;
+    const int rc = synthetic_densities(config, n, seed, mu, nu, msg);
+    if (rc != BFM_OK) fail(rc, msg);
+  });
+}
+
 int bfm_validate_inputs(int dim, const int* extents, const double* mu, const double* nu,
                         const bfm_config* cfg) {
   return guard([&] {
@@ -1174,7 +1481,7 @@ int bfm_slab_axpy(bfm_slab* s, double* d_u, double sigma, const double* d_dir, v
 
 int bfm_slab_last_launches(const bfm_slab* s) { return s ? s->last_launches : 0; }
 
-long bfm_solver_launches(const bfm_solver* s) { return s->ws.lc.count; }
+long bfm_solver_launches(const bfm_solver* s) { return s ? s->ws.lc.count : -1; }
 
 int bfm_debug_pf_tiers(bfm_solver* s, int* out3) {
   return guard([&] { s->ws.pfp().tier_counts(out3); });
@@ -1211,15 +1518,20 @@ int bfm_solver_op_times(bfm_solver* s, double* ms, long* calls) {
 
 int bfm_solver_time_steps(bfm_solver* s, int k, double* ms) {
   return guard([&] {
+    if (!s || !ms || k < 0) fail(BFM_ERR_INVALID_ARGUMENT, "bfm_solver_time_steps: bad argument");
     s->ensure_probe();
     cudaEvent_t e0, e1;
     BFM_CUDA(cudaEventCreate(&e0));
     BFM_CUDA(cudaEventCreate(&e1));
-    BFM_CUDA(cudaStreamSynchronize(s->stream));
     BFM_CUDA(cudaEventRecord(e0, s->stream));
-    for (int i = 0; i < k; ++i) s->step();
-    s->ensure_probe();  // the next iteration's probe belongs to this step's work
-    BFM_CUDA(cudaEventRecord(e1, s->stream));
+    // run()'s loop body: k steps, each followed by the next iteration's probe,
+    // in batches with one synchronisation (one per step while timing ops)
+    for (int left = k; left > 0;) {
+      const int b = s->timing ? 1 : std::min(left, kCtlRing);
+      s->steps(b, true, left == b ? e1 : nullptr);
+      left -= b;
+    }
+    if (k == 0) BFM_CUDA(cudaEventRecord(e1, s->stream));
     BFM_CUDA(cudaEventSynchronize(e1));
     float f = 0.0f;
     BFM_CUDA(cudaEventElapsedTime(&f, e0, e1));
@@ -1228,5 +1540,22 @@ int bfm_solver_time_steps(bfm_solver* s, int k, double* ms) {
     *ms = f;
   });
 }
+
+int bfm_solver_set_graphs(bfm_solver* s, int on) {
+  return guard([&] {
+    if (!s) fail(BFM_ERR_INVALID_ARGUMENT, "bfm_solver_set_graphs: null handle");
+    s->use_graphs = on != 0;
+  });
+}
+
+int bfm_solver_debug_force_exact(bfm_solver* s, int iteration, int probe_only) {
+  return guard([&] {
+    if (!s) fail(BFM_ERR_INVALID_ARGUMENT, "bfm_solver_debug_force_exact: null handle");
+    s->force_near_iter = iteration;
+    s->force_near_probe = probe_only ? 1 : 0;
+  });
+}
+
+long bfm_solver_exact_replays(const bfm_solver* s) { return s ? s->exact_replays : -1; }
 
 }  // extern "C"

@@ -83,8 +83,26 @@ __device__ __forceinline__ void red_terms(const RedArgs& A, long i, double& t1, 
   }
 }
 
+__device__ double block_sum_plain(double v) {
+  __shared__ double sa[kRedThreads / 32];
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (lane == 0) sa[w] = v;
+  __syncthreads();
+  double r = 0.0;
+  if (threadIdx.x == 0)
+    for (int i = 0; i < kRedThreads / 32; ++i) r += sa[i];
+  __syncthreads();
+  return r;
+}
+
+// Besides the two double-double sums, every launch accumulates A = sum_i
+// (|t1_i| + |t2_i|) in plain fp64 (a nonnegative sum: relative error <= n*u),
+// from which the final kernel derives a rigorous bound on |our value - the
+// reference's sequential Kahan value| (see red_final_kernel).
 __global__ void __launch_bounds__(kRedThreads) red_partial_kernel(RedArgs A) {
   DD acc1{0.0, 0.0}, acc2{0.0, 0.0};
+  double absum = 0.0;
   const long stride = static_cast<long>(gridDim.x) * kRedThreads;
   long i = blockIdx.x * static_cast<long>(kRedThreads) + threadIdx.x;
   // four elements per round: their loads are in flight together (one load
@@ -97,6 +115,7 @@ __global__ void __launch_bounds__(kRedThreads) red_partial_kernel(RedArgs A) {
     for (int u = 0; u < 4; ++u) {
       dd_add(acc1, t1[u]);
       dd_add(acc2, t2[u]);
+      absum += fabs(t1[u]) + fabs(t2[u]);
     }
   }
   for (; i < A.n; i += stride) {
@@ -104,27 +123,39 @@ __global__ void __launch_bounds__(kRedThreads) red_partial_kernel(RedArgs A) {
     red_terms(A, i, t1, t2);
     dd_add(acc1, t1);
     dd_add(acc2, t2);
+    absum += fabs(t1) + fabs(t2);
   }
   DD r1 = block_reduce(acc1);
   DD r2 = block_reduce(acc2);
+  const double ab = block_sum_plain(absum);
   if (threadIdx.x == 0) {
     A.partials[2 * blockIdx.x] = r1.s;
     A.partials[2 * blockIdx.x + 1] = r1.c;
     A.partials[2 * (gridDim.x + blockIdx.x)] = r2.s;
     A.partials[2 * (gridDim.x + blockIdx.x) + 1] = r2.c;
+    A.partials[4 * gridDim.x + blockIdx.x] = ab;
   }
 }
 
+// results[slot] = value; results[kBoundSlot + slot] = bound with
+//   |value - reference value| <= bound,
+// the reference value being fl(fl(K1*vol) + fl(K2*vol)) of sequential Kahan
+// sums K (grid.hpp:124-133,171-176). Kahan: |K - S| <= (2u + O(n u^2)) A;
+// ours: |D - S| <= u|S| + O(n u^2) A with |S| <= A; the scalings/additions add
+// <= 2u|v| each side. 4u*vol*A + 4u|v| covers all of it (u = 2^-53, n <= 2^30).
 __global__ void __launch_bounds__(kRedThreads) red_final_kernel(const double* partials, int nb,
                                                                 int two, double vol,
                                                                 double* results, int slot) {
   DD acc1{0.0, 0.0}, acc2{0.0, 0.0};
+  double ab = 0.0;
   for (int i = threadIdx.x; i < nb; i += kRedThreads) {
     acc1 = dd_merge(acc1, DD{partials[2 * i], partials[2 * i + 1]});
     acc2 = dd_merge(acc2, DD{partials[2 * (nb + i)], partials[2 * (nb + i) + 1]});
+    ab += partials[4 * nb + i];
   }
   DD r1 = block_reduce(acc1);
   DD r2 = block_reduce(acc2);
+  ab = block_sum_plain(ab);
   if (threadIdx.x == 0 && two < 0) {  // raw double-double partial sums (multi-GPU ranks)
     results[slot] = r1.s;
     results[slot + 1] = r1.c;
@@ -140,6 +171,8 @@ __global__ void __launch_bounds__(kRedThreads) red_final_kernel(const double* pa
       v = v + s2 * vol;
     }
     results[slot] = v;
+    const double u4 = 4.0 * 0x1.0p-53;
+    results[kBoundSlot + slot] = u4 * vol * ab + u4 * fabs(v);
   }
 }
 
@@ -221,7 +254,7 @@ Reducer::~Reducer() {
 
 void Reducer::init() {
   blocks_ = kRedBlocks;
-  BFM_CUDA(dmalloc(&partials_, 4 * blocks_ * sizeof(double)));
+  BFM_CUDA(dmalloc(&partials_, 5 * blocks_ * sizeof(double)));
   BFM_CUDA(dmalloc(&results_, kRedSlots * sizeof(double)));
   BFM_CUDA(cudaMemset(results_, 0, kRedSlots * sizeof(double)));
   BFM_CUDA(cudaMallocHost(&pinned_, kRedSlots * sizeof(double)));
@@ -283,6 +316,20 @@ void Reducer::fetch(double* host, int count, cudaStream_t s) {
   BFM_CUDA(cudaMemcpyAsync(pinned_, results_, count * sizeof(double), cudaMemcpyDeviceToHost, s));
   BFM_CUDA(cudaStreamSynchronize(s));
   for (int i = 0; i < count; ++i) host[i] = pinned_[i];
+}
+
+__global__ void axpy_dev_kernel(double* u, const double* s_ptr, const double* dir, long n) {
+  const double s = *s_ptr;
+  for (long i = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<long>(gridDim.x) * blockDim.x)
+    u[i] = u[i] + s * dir[i];  // solver.hpp:283, no contraction (-fmad=false)
+}
+
+void axpy_dev(double* u, const double* d_s, const double* dir, long n, cudaStream_t st,
+              LaunchCounter* lc) {
+  axpy_dev_kernel<<<ew_grid(n), 256, 0, st>>>(u, d_s, dir, n);
+  BFM_LAUNCH_CHECK("axpy_dev");
+  if (lc) lc->add();
 }
 
 void axpy(double* u, double s, const double* dir, long n, cudaStream_t st, LaunchCounter* lc) {

@@ -10,6 +10,9 @@
 namespace bfmgpu {
 
 constexpr int kRedSlots = 64;
+// results[kBoundSlot + slot]: error bound of results[slot] against the
+// reference's sequential Kahan evaluation (dot / sum only).
+constexpr int kBoundSlot = 32;
 
 class Reducer {
  public:
@@ -49,6 +52,9 @@ class Reducer {
 };
 
 void axpy(double* u, double s, const double* dir, long n, cudaStream_t st, LaunchCounter* lc);
+// u[i] += (*d_s) * dir[i], the step size read from device memory (graph replays)
+void axpy_dev(double* u, const double* d_s, const double* dir, long n, cudaStream_t st,
+              LaunchCounter* lc);
 // u[i] += delta
 void add_scalar(double* u, double delta, long n, cudaStream_t st, LaunchCounter* lc);
 

@@ -2,12 +2,17 @@
 
 No public dataset is involved: the reference's benchmark instances are
 closed-form shapes (benchmark.hpp:27-43), and BASELINE.json's configs are
-seeded random densities. Draws use numpy's default_rng(seed) (PCG64), object
-by object, fields in the listed order. Gaussians are unit-peak
-exp(-|x-c|^2 / (2 s^2)) summed with equal weights, then normalised to unit
-mass (grid.hpp:151-164). Indicators use the reference's closed cell-centre
-membership (io.hpp:407-420). Both the GPU and the CPU reference arm receive
-the identical float64 arrays.
+seeded random densities.
+
+C1-C4 come from the library's shared generator (bfm_synthetic_densities,
+csrc/synthetic.cpp): std::mt19937_64(seed), uniforms (rng()>>11)*2^-53, object
+by object with fields in the listed order, unit-peak Gaussians
+exp(-|x-c|^2 / (2 s^2)) summed with equal weights, closed cell-centre
+indicators (io.hpp:407-420), Kahan normalisation (grid.hpp:151-164) — so a C++
+driver regenerates the identical arrays. Test-sized helpers
+(c1_like) and the C5 operator-sweep potentials use numpy's default_rng
+(PCG64). Both the GPU and the CPU reference arm receive the identical float64
+arrays.
 """
 from __future__ import annotations
 
@@ -17,6 +22,12 @@ from typing import Tuple
 import numpy as np
 
 from . import axis_coords
+
+
+def _shared(config: int, n: int, seed: int) -> Tuple[np.ndarray, np.ndarray]:
+    from . import synthetic_densities
+
+    return synthetic_densities(config, n, seed)
 
 
 def _normalize(raw: np.ndarray) -> np.ndarray:
@@ -56,14 +67,8 @@ def _ball(shape, center, radius) -> np.ndarray:
 
 
 def c1(n: int = 256, seed: int = 1) -> Tuple[np.ndarray, np.ndarray]:
-    rng = np.random.default_rng(seed)
-    cs, ss = [], []
-    for _ in range(3):
-        cs.append(rng.uniform(0.2, 0.8, size=2))
-        ss.append(rng.uniform(0.05, 0.15))
-    mu = _normalize(_gauss((n, n), cs, ss))
-    nu = _normalize(_ball((n, n), (0.5, 0.5), 0.3))
-    return mu, nu
+    """C1: 3 Gaussians (centre ~U[0.2,0.8]^2, s ~U[0.05,0.15]) vs disc:0.5,0.5,0.3."""
+    return _shared(1, n, seed)
 
 
 def c1_like(shape, seed: int = 1) -> Tuple[np.ndarray, np.ndarray]:
@@ -81,28 +86,8 @@ def c1_like(shape, seed: int = 1) -> Tuple[np.ndarray, np.ndarray]:
 
 
 def c2(n: int = 1024, seed: int = 2) -> Tuple[np.ndarray, np.ndarray]:
-    rng = np.random.default_rng(seed)
-    x = axis_coords(n)
-    raw = np.zeros((n, n))
-    for _ in range(5):
-        w = rng.uniform(0.1, 0.4)
-        h = rng.uniform(0.1, 0.4)
-        x0 = rng.uniform(0.0, 1.0 - w)
-        y0 = rng.uniform(0.0, 1.0 - h)
-        m0 = (x >= x0) & (x <= x0 + w)
-        m1 = (x >= y0) & (x <= y0 + h)
-        raw[np.ix_(m0, m1)] = 1.0
-    mu = _normalize(raw)
-    cs, ss = [], []
-    for _ in range(8):
-        cs.append(rng.uniform(0.1, 0.9, size=2))
-        ss.append(rng.uniform(0.02, 0.1))
-    ca = rng.uniform(0.45, 0.55, size=2)
-    g = _gauss((n, n), cs, ss)
-    r = np.sqrt(_dist2((n, n), ca))
-    g[(r < 0.15) | (r > 0.45)] = 0.0
-    nu = _normalize(g)
-    return mu, nu
+    """C2: union of 5 rectangles vs 8 Gaussians masked to an annulus."""
+    return _shared(2, n, seed)
 
 
 def _dist2(shape, c) -> np.ndarray:
@@ -115,41 +100,14 @@ def _dist2(shape, c) -> np.ndarray:
     return d2
 
 
-def _masked_gauss(rng, n: int, k: int, block: int):
-    cs, ss = [], []
-    for _ in range(k):
-        cs.append(rng.uniform(0.0, 1.0, size=2))
-        ss.append(rng.uniform(0.01, 0.1))
-    g = _gauss((n, n), cs, ss)
-    nb = max(1, n // block)
-    keep = rng.uniform(0.0, 1.0, size=(nb, nb)) >= 0.5
-    if not keep.any():
-        keep[0, 0] = True
-    mask = np.kron(keep, np.ones((n // nb, n // nb), dtype=bool))
-    g = np.where(mask, g, 0.0)
-    if not (g > 0).any():
-        g[mask] = 1.0
-    return _normalize(g)
-
-
 def c3(n: int = 4096, seed: int = 3) -> Tuple[np.ndarray, np.ndarray]:
-    """16 Gaussians x Bernoulli(0.5) mask of 64x64-cell blocks, independently for mu, nu."""
-    rng = np.random.default_rng(seed)
-    block = max(1, n // 64)
-    mu = _masked_gauss(rng, n, 16, block)
-    nu = _masked_gauss(rng, n, 16, block)
-    return mu, nu
+    """C3: 16 Gaussians x Bernoulli(0.5) mask of 64x64 blocks, independently for mu, nu."""
+    return _shared(3, n, seed)
 
 
 def c4(n: int = 384, seed: int = 4) -> Tuple[np.ndarray, np.ndarray]:
-    rng = np.random.default_rng(seed)
-    cs, ss = [], []
-    for _ in range(6):
-        cs.append(rng.uniform(0.0, 1.0, size=3))
-        ss.append(rng.uniform(0.03, 0.12))
-    mu = _normalize(_gauss((n, n, n), cs, ss))
-    nu = _normalize(_ball((n, n, n), (0.5, 0.5, 0.5), 0.3))
-    return mu, nu
+    """C4: 6 3-D Gaussians vs ball:0.5,0.5,0.5,0.3."""
+    return _shared(4, n, seed)
 
 
 def c5_potential(shape, seed: int = 5) -> Tuple[np.ndarray, np.ndarray]:

@@ -150,3 +150,32 @@ def test_restatement_vs_reference_random_campaign(ref):
         mism += O.n_bit_diff(a, b)
         tot += a.size
     assert mism == 0, f"{mism} of {tot}"
+
+
+def test_fullrun_goldens_are_self_consistent():
+    """tests/golden/fullrun_*.npz (make_fullrun.py, the reference's own full
+    runs): one record per step, iteration numbers 1..steps, sigma >= sigma_min,
+    a consistent report, and inputs that the shared generator reproduces."""
+    import hashlib
+
+    from paper_1905_12154_b200 import synthetic
+
+    here = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+    found = 0
+    for name in ("c1", "c2", "c3", "c4"):
+        path = os.path.join(here, f"fullrun_{name}.npz")
+        if not os.path.exists(path):
+            continue
+        found += 1
+        g = np.load(path)
+        steps = int(g["steps"])
+        assert g["trace"].shape[0] == steps == len(g["phi_sha"]) == len(g["sigma"])
+        assert list(g["trace"][:, 0]) == list(range(1, steps + 1))
+        assert (g["sigma"] >= 0.01).all()
+        assert int(g["rep_scalars"][0]) == steps and int(g["rep_trace_len"]) == steps
+        if name in ("c1", "c2"):  # cheap enough to regenerate here
+            config, n, seed = (int(v) for v in g["generator"])
+            mu, nu = synthetic._shared(config, n, seed)
+            assert hashlib.sha256(mu.tobytes()).hexdigest() == str(g["mu_sha"])
+            assert hashlib.sha256(nu.tobytes()).hexdigest() == str(g["nu_sha"])
+    assert found >= 2
