@@ -1,19 +1,22 @@
 #!/usr/bin/env python
-"""BFM benchmark: grid-point-iterations/s (float64) on BASELINE.json's C3
-(4096^2, configs[2]) — the headline size the metric is quoted on — or C4
-(384^3) with --config c4.
+"""BFM benchmark: grid-point-iterations/s (float64) at BASELINE.json's two
+headline sizes — C3 (4096^2, configs[2]) is the line's `value`, C4 (384^3,
+configs[3]) is reported in the same line under "c4" (skip with --no-c4);
+--config c4 makes C4 the headline.
 
 A "step" is one steady-state back-and-forth iteration (the reference's
 run() loop body: probe + step(), solver.hpp:211-226, i.e. 4 c-transforms, 2
-ascent directions, 4 pair values, 2 axpys). Inputs are seeded synthetic
-densities of the BASELINE shapes (paper_1905_12154_b200/synthetic.py).
+ascent directions, 4 pair values, 2 axpys). Inputs are the seeded synthetic
+densities of the BASELINE shapes from the library's shared generator
+(bfm_synthetic_densities).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config c1|c2|c3|c4|c5]
   (K defaults to the config's own iteration count: C3 50, C4 30, C1 100)
   python bench.py --impl reference ...   (the reference's own CPU solver,
         oracle/_ref = unmodified headers + FFTW shim, on the host cores)
 
-Prints ONE JSON line (rank 0)."""
+--gpus N > 1 without torchrun re-executes itself under torch.distributed.run
+(one process per GPU). Prints ONE JSON line (rank 0)."""
 import argparse
 import json
 import os
@@ -40,26 +43,40 @@ def peaks():
         return 6650.0, "fallback"
 
 
+ITERATIONS = {"c1": 100, "c2": 50, "c3": 50, "c4": 30}
+
+
 def workload(cfg):
+    """(mu, nu, config dict). The config dict is identical for both arms."""
     from paper_1905_12154_b200 import synthetic
 
-    if cfg == "c3":
-        mu, nu = synthetic.c3()
-        desc = {"workload": "C3: 2D 4096x4096 quadratic BFM, masked Gaussian mixtures (BASELINE configs[2])",
-                "grid": [4096, 4096]}
-    elif cfg == "c4":
-        mu, nu = synthetic.c4()
-        desc = {"workload": "C4: 3D 384^3 quadratic BFM, Gaussian mixture -> ball (BASELINE configs[3])",
-                "grid": [384, 384, 384]}
-    elif cfg == "c1":
-        mu, nu = synthetic.c1()
-        desc = {"workload": "C1: 2D 256x256 quadratic BFM (BASELINE configs[0])", "grid": [256, 256]}
-    elif cfg == "c2":
-        mu, nu = synthetic.c2()
-        desc = {"workload": "C2: 2D 1024x1024 quadratic BFM (BASELINE configs[1])", "grid": [1024, 1024]}
-    else:
+    names = {
+        "c3": ("C3: 2D 4096x4096 quadratic BFM, masked Gaussian mixtures (BASELINE configs[2])", [4096, 4096]),
+        "c4": ("C4: 3D 384^3 quadratic BFM, Gaussian mixture -> ball (BASELINE configs[3])", [384, 384, 384]),
+        "c1": ("C1: 2D 256x256 quadratic BFM, 3 Gaussians -> disc (BASELINE configs[0])", [256, 256]),
+        "c2": ("C2: 2D 1024x1024 quadratic BFM, rectangles -> annulus-masked Gaussians (BASELINE configs[1])",
+               [1024, 1024]),
+    }
+    if cfg not in names:
         raise SystemExit(f"unknown config {cfg}")
+    mu, nu = getattr(synthetic, cfg)()
+    desc = {"workload": names[cfg][0], "grid": names[cfg][1],
+            "inputs": "bfm_synthetic_densities (std::mt19937_64, SURVEY 8(d)), seed %s" % cfg[1],
+            "step": "one BFM iteration: probe + step() (4 c-transforms, 2 ascent directions, 4 pair values, 2 axpys)",
+            "l2": "inputs larger than L2 (about 10 resident float64 fields of the grid)" if cfg in ("c3", "c4")
+            else "fields fit in L2 (small config)"}
     return mu, nu, desc
+
+
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 
 
 class ClockSampler:
@@ -178,12 +195,30 @@ def reference_arm(args):
         "steps": done, "warmup": warm, "ms_per_step": 1e3 * dt / max(1, done),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded, BASELINE shapes)",
-        "config": dict(desc, parallelism="cpu threads", solver="reference bfm::Solver (oracle/_ref)"),
-        "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "reference",
+        "config": desc,
+        "impl_detail": "reference bfm::Solver (oracle/_ref: unmodified headers + FFTW-subset shim) on all host threads",
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "reference", "cpu_model": cpu_model(),
                          "sample": f"{done} full BFM iterations (probe+step) of {desc['workload']} on "
-                                   f"{cores} host threads; Poisson via the FFTW-subset shim"},
+                                   f"{cores} host threads ({cpu_model()}); Poisson via the FFTW-subset shim"},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
+    if args.config == "c3" and not args.no_c4:
+        # the C4 half of the metric: one bounded reference iteration (about a
+        # minute on 16 host threads)
+        mu4, nu4, desc4 = workload("c4")
+        s4 = O.RefSolver(mu4, nu4, SolverConfig(tolerance=-1.0, max_iterations=10 ** 6))
+        s4.dual_value()
+        t4 = time.perf_counter()
+        s4.step()
+        s4.dual_value()
+        dt4 = time.perf_counter() - t4
+        v4 = mu4.size / dt4
+        line["c4"] = {"workload": desc4["workload"], "grid": desc4["grid"], "steps": 1, "value": v4,
+                      "unit": UNIT, "ms_per_step": 1e3 * dt4,
+                      "cpu_baseline": {"value": v4, "unit": UNIT, "cores": cores, "kind": "reference",
+                                       "cpu_model": cpu_model(),
+                                       "sample": f"1 full BFM iteration (probe+step) of {desc4['workload']}"},
+                      "e2e": {"value": v4, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line))
 
 
@@ -203,37 +238,58 @@ def cpu_baseline(mu, nu, desc):
         dt = time.perf_counter() - t0
         cores = os.cpu_count()
         return {"value": mu.size / dt, "unit": UNIT, "cores": cores, "kind": "reference",
+                "cpu_model": cpu_model(),
                 "sample": f"1 full BFM iteration (probe+step) of {desc['workload']} with the reference "
-                          f"bfm::Solver (oracle/_ref, FFTW-subset shim) on {cores} host threads, "
-                          f"{dt:.1f} s"}
+                          f"bfm::Solver (oracle/_ref, FFTW-subset shim) on {cores} host threads "
+                          f"({cpu_model()}), {dt:.1f} s"}
     except Exception as e:  # the baseline is reported, never fatal
         return {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "reference",
                 "sample": f"failed: {e}"}
 
 
-def live_roofline(ops, shape, hbm, hbm_kind):
-    """The dominant kernel (the c-transform, d axis-pass launches per call)
-    timed live in the timed region: CUDA events on the solver stream around
-    every c-transform call of the K steps. Algorithmic bytes 16*d per node
-    per call; traffic = ncu DRAM bytes of one call inside the
-    same C3 iteration (profiles/ctransform_dram_bytes.json)."""
+def traffic_table():
+    """ncu DRAM bytes (read + write) per call of each operator inside the BFM
+    iteration, keyed "<op>@<grid>" (profiles/dram_bytes.json, written from
+    the committed ncu captures by tools/dram_table.py)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "dram_bytes.json")) as f:
+            return json.load(f)
+    except Exception:
+        return {}
+
+
+def op_rooflines(ops, shape, steps, hbm, hbm_kind):
+    """Per-operator rooflines from the live per-operator CUDA events of the
+    timed region (on the solver stream). Algorithmic bytes,
+    per call: c-transform 16 d B/node (d axis-pass launches), pushforward +
+    residual 32 B/node, Neumann solve 16 (2d - 1) B/node; the reductions op
+    (4 pair values x 32 B/node, 2 gn x 16 B/node, 2 axpys x 24 B/node, plus
+    the one-thread decision kernels) is reported per iteration (208 B/node)."""
     d = len(shape)
     N = int(np.prod(shape))
-    ms_total, calls = ops["ctransform"]
-    ms = ms_total / max(calls, 1)
-    bytes_alg = 16.0 * d * N
-    achieved = bytes_alg / (ms * 1e-3) / 1e9
-    traffic = None
-    prof = os.path.join(ROOT, "profiles", "ctransform_dram_bytes.json")
-    if os.path.exists(prof):
-        try:
-            traffic = json.load(open(prof)).get("x".join(map(str, shape)) + "_iteration")
-        except Exception:
-            traffic = None
-    return {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
-            "frac": achieved / hbm, "traffic": traffic,
-            "kernel": f"c-transform ({d} axis-pass launches per call: ct_dy_kernel on dyadic grids, ct_pass_kernel otherwise), {calls} calls in the timed region",
-            "ms_per_call": ms, "algorithmic_bytes_per_call": bytes_alg, "peak_kind": hbm_kind}
+    key = "x".join(map(str, shape))
+    tt = traffic_table()
+    per_node = {"ctransform": 16.0 * d, "pushforward": 32.0, "poisson": 16.0 * (2 * d - 1)}
+    out = {}
+    for op, bpn in per_node.items():
+        ms_total, calls = ops[op]
+        ms = ms_total / max(calls, 1)
+        b = bpn * N
+        ach = b / (ms * 1e-3) / 1e9
+        out[op] = {"bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm,
+                   "traffic": tt.get(f"{op}@{key}"), "ms_per_call": ms, "calls": calls,
+                   "algorithmic_bytes_per_call": b, "algorithmic_bytes_per_node": bpn, "peak_kind": hbm_kind}
+    ms_total, calls = ops["reduce"]
+    ms = ms_total / max(steps, 1)
+    b = 208.0 * N
+    ach = b / (ms * 1e-3) / 1e9
+    out["reductions"] = {"bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm,
+                         "traffic": tt.get(f"reductions@{key}"), "ms_per_iteration": ms,
+                         "algorithmic_bytes_per_iteration": b, "algorithmic_bytes_per_node": 208.0,
+                         "peak_kind": hbm_kind}
+    out["ctransform"]["kernel"] = (f"c-transform: {d} axis-pass launches per call (ct_dy_kernel on dyadic "
+                                   f"grids, ct_pass_kernel otherwise)")
+    return out
 
 
 def ctransform_roofline(lib, shape, torch, hbm, hbm_kind, reps=10):
@@ -422,6 +478,17 @@ def ours_dist(args):
     tdist.barrier()
     ms_max = float(t.item())
     value = N * args.steps / (ms_max * 1e-3)
+
+    # rank-local kernels and all-to-alls, timed with CUDA events on a few
+    # further steps (outside the timed region: the events add host syncs)
+    timer = D.EventTimer()
+    ops.timer = comm.timer = timer
+    k_prof = max(1, min(3, args.steps))
+    for _ in range(k_prof):
+        s.step()
+    s.ensure_probe()
+    prof = timer.resolve()
+    ops.timer = comm.timer = None
     del s
 
     # end to end: pinned host slabs in, K iterations, phi/psi slabs back
@@ -446,15 +513,31 @@ def ours_dist(args):
            "note": "DistSolver from pinned host slabs + K step() + phi/psi slab readback, wall clock, max over ranks"}
     if rank == 0:
         hbm, hbm_kind = peaks()
-        lib = bfm.load_library()
-        roof = ctransform_roofline(lib, desc["grid"], torch, hbm, hbm_kind)
+        d = len(desc["grid"])
+        n_local = nr * (N // L.shape[0])
+        ct_ms, ct_calls, _ = prof.get("ctransform", (0.0, 1, 0))
+        calls = max(1, ct_calls // d)  # d rank-local launches groups per c-transform call
+        ct_call_ms = ct_ms / calls
+        ct_bytes = 16.0 * d * n_local
+        a2a_ms, a2a_calls, a2a_bytes = prof.get("alltoall", (0.0, 1, 0))
+        nvl = a2a_bytes / max(a2a_ms * 1e-3, 1e-12) / 1e9
+        roof = {"bound": "hbm", "achieved": ct_bytes / (ct_call_ms * 1e-3) / 1e9, "peak": hbm, "unit": "GB/s",
+                "frac": ct_bytes / (ct_call_ms * 1e-3) / 1e9 / hbm, "traffic": None,
+                "kernel": f"rank-0 local c-transform kernels ({d} axis passes over its column and row slabs)",
+                "ms_per_call": ct_call_ms, "algorithmic_bytes_per_call": ct_bytes, "peak_kind": hbm_kind,
+                "alltoall": {"bound": "nvlink", "achieved": nvl, "peak": 900.0, "unit": "GB/s",
+                             "frac": nvl / 900.0, "bytes": a2a_bytes, "ms": a2a_ms, "calls": a2a_calls,
+                             "note": f"rank 0: bytes sent to other ranks over {k_prof} profiled steps, "
+                                     "NCCL all_to_all_single time (CUDA events)"},
+                "profiled_steps": k_prof,
+                "op_ms_per_step": {c: v[0] / k_prof for c, v in prof.items()}}
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded, BASELINE shapes; no public dataset)",
-            "config": dict(desc, parallelism=f"axis-0 slabs x{world} (NCCL all-to-all transposes)",
-                           l2="inputs larger than L2 (about 10 resident float64 fields of 128 MiB)"),
+            "config": desc,
+            "impl_detail": f"axis-0 slabs x{world} (NCCL all-to-all transposes and deposit routing)",
             "gpu_launches": int(launches),
             "clocks": ck,
             "roofline": roof,
@@ -464,6 +547,55 @@ def ours_dist(args):
         print(json.dumps(line))
     ops.close()
     tdist.destroy_process_group()
+
+
+def measure(cfg, steps, warmup, local=0):
+    """Our arm on one GPU for one config: device-timed steps (value), live
+    per-operator rooflines, and the end-to-end run through the public API."""
+    import torch
+
+    import paper_1905_12154_b200 as bfm
+
+    mu, nu, desc = workload(cfg)
+    N = mu.size
+    conf = bfm.SolverConfig(tolerance=-1.0, max_iterations=10 ** 6)
+    s = bfm.Solver(mu, nu, conf)
+    for _ in range(warmup):
+        s.step()
+    s.time_steps(1)  # the graphs of the timed loop are captured outside the timed region
+    l0 = s.launches()
+    clocks = ClockSampler(local)
+    torch.cuda.synchronize()
+    clocks.start()
+    s.set_timing(True)  # per-operator CUDA events on the solver stream (live rooflines)
+    ms = s.time_steps(steps)
+    ck = clocks.stop()
+    ops = s.op_times()
+    s.set_timing(False)
+    launches = s.launches() - l0
+    del s
+
+    # end to end through the public API with host buffers: solver creation
+    # from pinned host arrays (H2D of mu, nu), K steps, phi/psi read back (D2H)
+    pin_mu = torch.from_numpy(mu).pin_memory().numpy()
+    pin_nu = torch.from_numpy(nu).pin_memory().numpy()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    s2 = bfm.Solver(pin_mu, pin_nu, conf)
+    for _ in range(steps):
+        s2.step()
+    phi_h = s2.phi()
+    psi_h = s2.psi()
+    e2e_s = time.perf_counter() - t0
+    del s2, phi_h, psi_h
+    e2e = {"value": N * steps / e2e_s, "unit": UNIT,
+           "h2d_bytes_per_step": int(2 * 8 * N / steps),
+           "d2h_bytes_per_step": int(2 * 8 * N / steps),
+           "note": "bfm.Solver(mu, nu) from pinned host arrays + K step() + phi()/psi() readback, wall clock"}
+    hbm, hbm_kind = peaks()
+    roofs = op_rooflines(ops, desc["grid"], steps, hbm, hbm_kind)
+    return {"mu": mu, "nu": nu, "desc": desc, "N": N, "ms": ms, "value": N * steps / (ms * 1e-3),
+            "ops": ops, "rooflines": roofs, "clocks": ck, "launches": launches, "e2e": e2e}
 
 
 def ours(args):
@@ -481,76 +613,65 @@ def ours(args):
         import torch.distributed as dist
 
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    mu, nu, desc = workload(args.config)
-    N = mu.size
-    cfg = bfm.SolverConfig(tolerance=-1.0, max_iterations=10 ** 6)
-    s = bfm.Solver(mu, nu, cfg)
-    for _ in range(args.warmup):
-        s.step()
-    l0 = s.launches()
-    clocks = ClockSampler(local)
-    if dist:
         dist.barrier()
-    torch.cuda.synchronize()
-    clocks.start()
-    s.set_timing(True)  # per-operator CUDA events on the solver stream (live roofline)
-    ms = s.time_steps(args.steps)
-    torch.cuda.synchronize()
-    ck = clocks.stop()
-    ops = s.op_times()
-    s.set_timing(False)
-    launches = s.launches() - l0
-    t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    m = measure(args.config, args.steps, args.warmup, local)
+    t = torch.tensor([m["ms"]], dtype=torch.float64, device="cuda")
     if dist:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         dist.barrier()
     ms_max = float(t.item())
-    value = N * args.steps * world / (ms_max * 1e-3)
-    del s
-
-    # end to end through the public API with host buffers
-    pin_mu = torch.from_numpy(mu).pin_memory().numpy()
-    pin_nu = torch.from_numpy(nu).pin_memory().numpy()
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    s2 = bfm.Solver(pin_mu, pin_nu, cfg)
-    for _ in range(args.steps):
-        s2.step()
-    phi_h = s2.phi()
-    psi_h = s2.psi()
-    e2e_s = time.perf_counter() - t0
-    del s2, phi_h, psi_h
-    e2e = {"value": N * args.steps / e2e_s, "unit": UNIT,
-           "h2d_bytes_per_step": int(2 * 8 * N / args.steps),
-           "d2h_bytes_per_step": int(2 * 8 * N / args.steps),
-           "note": "bfm.Solver(mu, nu) from pinned host arrays + K step() + phi()/psi() readback, wall clock"}
-
+    value = m["N"] * args.steps * world / (ms_max * 1e-3)
+    sub = None
+    if args.config == "c3" and not args.no_c4:
+        c4_steps = ITERATIONS["c4"] if args.c4_steps is None else args.c4_steps
+        m4 = measure("c4", c4_steps, args.warmup, local)
+        sub = {"workload": m4["desc"]["workload"], "grid": m4["desc"]["grid"], "steps": c4_steps,
+               "value": m4["value"] * world, "unit": UNIT, "ms_per_step": m4["ms"] / c4_steps,
+               "roofline": m4["rooflines"]["ctransform"], "rooflines": m4["rooflines"],
+               "op_breakdown_ms_per_step": {k: v[0] / c4_steps for k, v in m4["ops"].items()},
+               "gpu_launches": int(m4["launches"]), "clocks": m4["clocks"], "e2e": m4["e2e"]}
     if rank != 0:
         if dist:
             dist.destroy_process_group()
         return
     hbm, hbm_kind = peaks()
     lib = bfm.load_library()
-    roof = live_roofline(ops, desc["grid"], hbm, hbm_kind)
-    roof["c5_operator"] = ctransform_roofline(lib, desc["grid"], torch, hbm, hbm_kind)
-    cpu = cpu_baseline(mu, nu, desc) if world == 1 and not args.no_cpu_baseline else None
+    roof = dict(m["rooflines"]["ctransform"])
+    roof["c5_operator"] = ctransform_roofline(lib, m["desc"]["grid"], torch, hbm, hbm_kind)
+    cpu = cpu_baseline(m["mu"], m["nu"], m["desc"]) if world == 1 and not args.no_cpu_baseline else None
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded, BASELINE shapes; no public dataset)",
-        "config": dict(desc, parallelism=("independent replicas" if world > 1 else "single GPU"),
-                       l2="inputs larger than L2 (about 10 resident float64 fields of 128 MiB)"),
-        "gpu_launches": int(launches),
-        "clocks": ck,
+        "config": m["desc"],
+        "impl_detail": ("independent single-GPU replicas" if world > 1 else "single B200") +
+                       "; iterations as CUDA graphs, certified device-side scalar decisions",
+        "gpu_launches": int(m["launches"]),
+        "clocks": m["clocks"],
         "roofline": roof,
-        "op_breakdown_ms_per_step": {k: v[0] / args.steps for k, v in ops.items()},
+        "rooflines": m["rooflines"],
+        "op_breakdown_ms_per_step": {k: v[0] / args.steps for k, v in m["ops"].items()},
         "cpu_baseline": cpu,
-        "e2e": e2e,
+        "e2e": m["e2e"],
     }
+    if sub is not None:
+        line["c4"] = sub
     print(json.dumps(line))
     if dist:
         dist.destroy_process_group()
+
+
+def respawn_under_torchrun(args):
+    """--gpus N > 1 outside torchrun: one process per GPU via torch.distributed.run."""
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    os.execv(sys.executable, cmd)
 
 
 def main():
@@ -565,11 +686,18 @@ def main():
     ap.add_argument("--sweep-max", type=int, default=0,
                     help="c5: skip grids with more nodes than this (0: all)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-c4", action="store_true", help="c3: skip the C4 (384^3) sub-object")
+    ap.add_argument("--c4-steps", type=int, default=None, help="c3: timed steps of the C4 sub-object (default 30)")
     ap.add_argument("--slabs", action="store_true",
                     help="use the slab-decomposition driver even at N = 1 (checks the NCCL path)")
     ap.add_argument("--replicas", action="store_true",
                     help="N > 1: independent single-GPU replicas instead of the slab decomposition")
     args = ap.parse_args()
+    world = int(os.environ.get("WORLD_SIZE", "0"))
+    if args.gpus > 1 and world == 0 and args.impl == "ours":
+        respawn_under_torchrun(args)
+    if world and world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
     if args.steps is None:
         args.steps = 5 if args.impl == "reference" else {"c1": 100, "c2": 50, "c3": 50, "c4": 30, "c5": 3}[args.config]
     if args.impl == "reference":

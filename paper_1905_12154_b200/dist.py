@@ -89,6 +89,54 @@ class SlabLayout:
 
 
 # ---------------------------------------------------------------- communicators
+class EventTimer:
+    """Per-category device time (CUDA events on the current stream) and byte
+    counts; bench.py's rank-local kernel and all-to-all rooflines at N > 1."""
+
+    def __init__(self):
+        self.pending = []
+        self.ms = {}
+        self.calls = {}
+        self.bytes = {}
+
+    def span(self, cat: str, nbytes: int = 0):
+        timer = self
+
+        class _Span:
+            def __enter__(self):
+                self.a = torch.cuda.Event(enable_timing=True)
+                self.b = torch.cuda.Event(enable_timing=True)
+                self.a.record()
+
+            def __exit__(self, *exc):
+                self.b.record()
+                timer.pending.append((cat, self.a, self.b))
+                timer.bytes[cat] = timer.bytes.get(cat, 0) + nbytes
+                return False
+
+        return _Span()
+
+    def resolve(self):
+        torch.cuda.synchronize()
+        for cat, a, b in self.pending:
+            self.ms[cat] = self.ms.get(cat, 0.0) + a.elapsed_time(b)
+            self.calls[cat] = self.calls.get(cat, 0) + 1
+        self.pending = []
+        return {c: (self.ms[c], self.calls[c], self.bytes.get(c, 0)) for c in self.ms}
+
+
+class _NoSpan:
+    def __enter__(self):
+        return None
+
+    def __exit__(self, *exc):
+        return False
+
+
+def _span(timer, cat, nbytes=0):
+    return timer.span(cat, nbytes) if timer is not None else _NoSpan()
+
+
 class TorchComm:
     """torch.distributed process group (NCCL between GPUs, gloo on CPU)."""
 
@@ -98,6 +146,7 @@ class TorchComm:
         self.group = group
         self.rank = dist.get_rank(group)
         self.size = dist.get_world_size(group)
+        self.timer = None  # EventTimer: all-to-all time and bytes leaving this rank
 
     def alltoallv(self, sends: List[torch.Tensor],
                   recv_counts: Optional[List[int]] = None) -> List[torch.Tensor]:
@@ -112,8 +161,10 @@ class TorchComm:
             dist.all_to_all_single(rcounts, counts, group=self.group)
             recv_counts = [int(c) for c in rcounts.tolist()]
         out = torch.empty(sum(recv_counts), dtype=ref.dtype, device=ref.device)
-        dist.all_to_all_single(out, torch.cat([x.reshape(-1) for x in sends]), recv_counts, sc,
-                               group=self.group)
+        sent = (sum(sc) - sc[self.rank]) * ref.element_size()
+        with _span(self.timer, "alltoall", sent):
+            dist.all_to_all_single(out, torch.cat([x.reshape(-1) for x in sends]), recv_counts, sc,
+                                   group=self.group)
         return list(torch.split(out, recv_counts))
 
     def alltoall_flat(self, send: torch.Tensor, send_counts: List[int],
@@ -121,7 +172,9 @@ class TorchComm:
         """send is already packed by destination (send_counts elements per
         rank, in rank order); returns the packed receive buffer."""
         out = torch.empty(sum(recv_counts), dtype=send.dtype, device=send.device)
-        self.dist.all_to_all_single(out, send, recv_counts, send_counts, group=self.group)
+        sent = (sum(send_counts) - send_counts[self.rank]) * send.element_size()
+        with _span(self.timer, "alltoall", sent):
+            self.dist.all_to_all_single(out, send, recv_counts, send_counts, group=self.group)
         return out
 
     def allgather(self, values: Sequence[float]) -> np.ndarray:
@@ -221,6 +274,7 @@ class CudaSlabOps:
         _check(lib, lib.bfm_slab_create(layout.d, _extents(layout.shape), r0, nr, c0, nc, C.byref(h)))
         self.h = h
         self.launches = 0
+        self.timer = None  # EventTimer: rank-local operator kernels
         starts = (C.c_int * (layout.P + 1))(*(layout.row0 + [layout.n0]))
         _check(lib, lib.bfm_slab_set_partition(h, layout.P, starts))
 
@@ -255,26 +309,32 @@ class CudaSlabOps:
         n = phi_cols.numel()
         chain = self.empty(n, torch.int32)
         q = self.empty(n)
-        self._run(self.lib.bfm_slab_ct_cols(self.h, self._p(phi_cols), self._p(chain), self._p(q), self._s()))
+        with _span(self.timer, "ctransform"):
+            self._run(self.lib.bfm_slab_ct_cols(self.h, self._p(phi_cols), self._p(chain), self._p(q),
+                                                self._s()))
         return chain, q
 
     def ct_rows(self, chain: torch.Tensor, q: torch.Tensor) -> torch.Tensor:
         out = self.empty(q.numel())
-        self._run(self.lib.bfm_slab_ct_rows(self.h, self._p(chain), self._p(q), self._p(out), self._s()))
+        with _span(self.timer, "ctransform"):
+            self._run(self.lib.bfm_slab_ct_rows(self.h, self._p(chain), self._p(q), self._p(out), self._s()))
         return out
 
     def poisson_rows_forward(self, x: torch.Tensor) -> torch.Tensor:
         out = self.empty(x.numel())
-        self._run(self.lib.bfm_slab_poisson_rows_forward(self.h, self._p(x), self._p(out), self._s()))
+        with _span(self.timer, "poisson"):
+            self._run(self.lib.bfm_slab_poisson_rows_forward(self.h, self._p(x), self._p(out), self._s()))
         return out
 
     def poisson_cols(self, x: torch.Tensor) -> torch.Tensor:
         out = self.empty(x.numel())
-        self._run(self.lib.bfm_slab_poisson_cols(self.h, self._p(x), self._p(out), self._s()))
+        with _span(self.timer, "poisson"):
+            self._run(self.lib.bfm_slab_poisson_cols(self.h, self._p(x), self._p(out), self._s()))
         return out
 
     def poisson_rows_inverse(self, x: torch.Tensor) -> torch.Tensor:
-        self._run(self.lib.bfm_slab_poisson_rows_inverse(self.h, self._p(x), self._s()))
+        with _span(self.timer, "poisson"):
+            self._run(self.lib.bfm_slab_poisson_rows_inverse(self.h, self._p(x), self._s()))
         return x
 
     def pf_map(self, u_halo: torch.Tensor, source: torch.Tensor, want_disp: bool = False):
