@@ -477,11 +477,20 @@ def map_from_conjugate(u, side: int = MU_SIDE) -> np.ndarray:
     return disp
 
 
+def _check_disp(disp: np.ndarray, mu: np.ndarray, what: str) -> None:
+    """The C ABI reads d*N doubles of disp: reject other shapes as the
+    reference's require_same_grid does (pushforward.hpp, GridMismatch)."""
+    if disp.shape != (mu.ndim,) + mu.shape:
+        raise GridMismatch(f"{what}: displacement shape {disp.shape} does not match the grid "
+                           f"{(mu.ndim,) + mu.shape}")
+
+
 def pushforward_density(disp, mu) -> np.ndarray:
     """pushforward.hpp:176-178."""
     lib = load_library()
     mu = _f64(mu)
     disp = _f64(disp)
+    _check_disp(disp, mu, "pushforward_density")
     rho = np.empty_like(mu)
     _check(lib, lib.bfm_pushforward_density(mu.ndim, _extents(mu.shape), _ptr(disp), _ptr(mu),
                                             _ptr(rho)))
@@ -493,6 +502,7 @@ def displacement_interpolant(disp, mu, t: float) -> np.ndarray:
     lib = load_library()
     mu = _f64(mu)
     disp = _f64(disp)
+    _check_disp(disp, mu, "displacement_interpolant")
     rho = np.empty_like(mu)
     _check(lib, lib.bfm_displacement_interpolant(mu.ndim, _extents(mu.shape), _ptr(disp),
                                                  _ptr(mu), float(t), _ptr(rho)))
@@ -535,6 +545,7 @@ def primal_cost(disp, mu) -> float:
     lib = load_library()
     mu = _f64(mu)
     disp = _f64(disp)
+    _check_disp(disp, mu, "primal_cost")
     v = C.c_double()
     _check(lib, lib.bfm_primal_cost(mu.ndim, _extents(mu.shape), _ptr(disp), _ptr(mu),
                                     C.byref(v)))

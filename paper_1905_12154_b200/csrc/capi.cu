@@ -192,9 +192,15 @@ struct Staging {
     }
   }
 };
+// Per thread and device: the pinned chunks and events belong to the device
+// that was current when they were made (bfm_set_device may switch later).
 Staging& staging() {
-  static thread_local Staging st;
-  return st;
+  static thread_local std::unique_ptr<Staging> per_dev[64];
+  int dev = 0;
+  BFM_CUDA(cudaGetDevice(&dev));
+  if (dev < 0 || dev >= 64) throw CudaError("staging: device index out of range");
+  if (!per_dev[dev]) per_dev[dev].reset(new Staging);
+  return *per_dev[dev];
 }
 
 // Host-side copy of a staging chunk split over a few threads: the first touch

@@ -90,3 +90,43 @@ def test_facade_header_compiles():
     r = subprocess.run(["g++", "-std=c++17", "-fsyntax-only", "-I" + os.path.join(ROOT, "include"), src],
                        capture_output=True, text=True)
     assert r.returncode == 0, r.stderr
+
+
+def test_displacement_shape_is_checked():
+    """A wrongly shaped displacement is a GridMismatch (require_same_grid in
+    pushforward.hpp), not an out-of-bounds read of the C ABI."""
+    mu = np.ones((8, 8))
+    for bad in (np.zeros((8, 8)), np.zeros((2, 8, 4)), np.zeros((3, 8, 8))):
+        with pytest.raises(bfm.GridMismatch):
+            bfm.pushforward_density(bad, mu)
+        with pytest.raises(bfm.GridMismatch):
+            bfm.displacement_interpolant(bad, mu, 0.5)
+        with pytest.raises(bfm.GridMismatch):
+            bfm.primal_cost(bad, mu)
+
+
+def test_solver_null_handles_fail_cleanly():
+    lib = bfm.load_library()
+    import ctypes as C
+
+    assert lib.bfm_solver_iteration(None) == -1
+    n = C.c_int()
+    assert lib.bfm_solver_trace(None, None, 0, C.byref(n)) == 2
+    assert lib.bfm_solver_step(None, None) == 2
+    assert lib.bfm_solver_run(None, None) == 2
+    v = C.c_double()
+    assert lib.bfm_solver_dual_value(None, C.byref(v)) == 2
+
+
+def test_synthetic_generator_is_deterministic_and_normalised():
+    """The shared mt19937_64 generator (bfm_synthetic_densities): same bits
+    twice, unit Kahan mass (grid.hpp:151-164), C3's 64x64 block masks."""
+    a = bfm.synthetic_densities(3, 256, 3)
+    b = bfm.synthetic_densities(3, 256, 3)
+    assert all(np.array_equal(x, y) for x, y in zip(a, b))
+    for x in a:
+        assert abs(np.sum(x) / x.size - 1.0) < 1e-12  # (integrate() needs the GPU)
+        blocks = x.reshape(64, 4, 64, 4).max(axis=(1, 3))
+        assert 0.2 < (blocks == 0).mean() < 0.8  # Bernoulli(0.5) blocks
+    with pytest.raises(bfm.InvalidArgument):
+        bfm.synthetic_densities(7, 64, 1)
