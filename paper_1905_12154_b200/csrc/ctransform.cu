@@ -57,6 +57,34 @@ __device__ __forceinline__ void cp_async_wait_all() {
   asm volatile("cp.async.wait_all;\n" ::: "memory");
 }
 
+// ---- TMA bulk copies (cp.async.bulk, sm_90+) with an mbarrier ---------------
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+// global -> shared, `bytes` a multiple of 16, both addresses 16-byte aligned;
+// completion is signalled on bar as transaction bytes
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}\n" ::"r"(
+          smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
 __device__ __forceinline__ void group_sync(int tpl, int l) {
   if (tpl <= 32) {
     __syncwarp();
@@ -1170,6 +1198,29 @@ __global__ void __launch_bounds__(kDyThreads) ct_dy_kernel(CtPass p) {
   };
 
   // ---- load: q_j (cp.async), chain_j; then f~_j = fl(s_j - q_j) ----------
+  // Contiguous pregathered passes (a >= 1 along the last axis) take the TMA
+  // bulk path: per line two cp.async.bulk copies (q: 8n bytes, chain: 4n
+  // bytes) completing on one mbarrier.
+  __shared__ __align__(8) uint64_t tma_bar;
+  const bool tma = p.pregathered && !p.strided && A.stride == 1 && (n & 3) == 0;
+  if (tma) {
+    if (threadIdx.x == 0) {
+      mbar_init(&tma_bar, 1);
+      unsigned bytes = 0;
+      for (int ll = 0; ll < lpc; ++ll)
+        if (dy_carve(p, smem, ll).geo->valid) bytes += 12u * static_cast<unsigned>(n);
+      mbar_expect_tx(&tma_bar, bytes);
+      for (int ll = 0; ll < lpc; ++ll) {
+        const DySmem sm = dy_carve(p, smem, ll);
+        const LineGeo g = *sm.geo;
+        if (!g.valid) continue;
+        bulk_g2s(sm.q, &p.phi[g.base], 8u * n, &tma_bar);
+        bulk_g2s(sm.ch, &p.state_in[g.base], 4u * n, &tma_bar);
+      }
+    }
+    __syncthreads();  // the barrier is initialised before anyone waits on it
+    mbar_wait(&tma_bar, 0);
+  }
   {
     const int ml = p.strided ? static_cast<int>(threadIdx.x % lpc) : l;
     const DySmem sm = dy_carve(p, smem, ml);
@@ -1180,6 +1231,9 @@ __global__ void __launch_bounds__(kDyThreads) ct_dy_kernel(CtPass p) {
       if (p.a == 0) {
         for (int j = first; j < n; j += step)
           cp_async8(&sm.q[dyi(j)], &p.phi[g.phi_other + static_cast<long>(j) * A.stride]);
+      } else if (p.pregathered && tma) {
+        // contiguous line: chain and q are whole rows, moved by TMA bulk
+        // copies issued below (one thread for the CTA)
       } else if (p.pregathered) {
         // q sits at the candidate's own node: chain and q both go straight
         // to shared memory, every load of the line in flight at once
