@@ -170,6 +170,12 @@ int bfm_solve_neumann_device(bfm_workspace* ws, const double* d_rhs, double* d_o
                              void* stream);
 /* Number of device kernels the last *_device call on ws enqueued. */
 int bfm_workspace_last_launches(const bfm_workspace* ws);
+/* Host-pointer operator calls on a workspace: the plans (and their device
+ * tables) are built once and reused across calls — the reference's
+ * TransformWorkspace / SpectralPlan reuse (transforms.hpp:231-283,
+ * poisson.hpp:42-73). N doubles in, N doubles out. */
+int bfm_workspace_ctransform(bfm_workspace* ws, const double* phi, double* out); /* transforms.hpp:396 */
+int bfm_workspace_solve_neumann(bfm_workspace* ws, const double* rhs, double* out); /* poisson.hpp:87 */
 
 /* ---- Multi-GPU building blocks (one process per GPU) ---------
  * The reference has no distributed mode; these are the rank-local halves of

@@ -3,13 +3,16 @@
 // same names, signatures and exception types, so drivers written against the
 // reference (e.g. tools/bfm_ot.cpp's run_solver, benchmark.hpp's
 // run_benchmark_case) compile unchanged against this header and run on the
-// B200. Scope: quadratic cost (the north-star path); power costs throw
-// InvalidArgument. Link with -lbfm_b200 (paper_1905_12154_b200/libbfm_b200.so).
+// B200. Scope: the solver is quadratic-cost (the north-star path); the
+// c-transform also takes power costs (CostModel::power); the solver, map and
+// primal cost throw InvalidArgument for them. Link with -lbfm_b200
+// (paper_1905_12154_b200/libbfm_b200.so).
 #pragma once
 
 #include <array>
 #include <cmath>
 #include <cstddef>
+#include <memory>
 #include <optional>
 #include <stdexcept>
 #include <string>
@@ -123,26 +126,40 @@ struct DensityField : ScalarField {
   explicit DensityField(const Grid& g, double fill = 0.0) : ScalarField(g, fill) {}
 };
 
-// ---- cost.hpp:17-81 (quadratic only on this path) -------------------------------
+// ---- cost.hpp:17-81 ----------------------------------------------------------------
+// Separable costs sum_a |y_a - x_a|^p_a / p_a. The c-transform runs on the B200
+// for every exponent (bfm_ctransform_cost); the solver, the map and the primal
+// cost take the quadratic path only (power costs throw InvalidArgument there).
 class CostModel {
  public:
   static CostModel quadratic(int dim) {
     if (dim < 1 || dim > 3) throw InvalidArgument("cost dimension must be 1..3");
-    CostModel m;
-    m.dim_ = dim;
-    return m;
+    return CostModel(std::vector<double>(dim, 2.0));
   }
   static CostModel power(const std::vector<double>& p) {
+    if (p.empty() || p.size() > 3) throw InvalidArgument("cost dimension must be 1..3");
     for (double q : p)
-      if (q != 2.0) throw InvalidArgument("power costs are outside the B200 path (quadratic only)");
-    return quadratic(static_cast<int>(p.size()));
+      if (!(q > 1.0)) throw InvalidArgument("cost exponents must satisfy p > 1");
+    return CostModel(p);
   }
-  int dim() const { return dim_; }
-  bool is_quadratic() const { return true; }
-  double axis_cost(int, double delta) const { return 0.5 * delta * delta; }
+  int dim() const { return static_cast<int>(p_.size()); }
+  bool is_quadratic() const { return quadratic_; }
+  double exponent(int axis) const { return p_[axis]; }
+  const double* exponents() const { return p_.data(); }
+  double axis_cost(int axis, double delta) const {
+    const double p = p_[axis];
+    if (p == 2.0) return 0.5 * delta * delta;
+    return std::pow(std::fabs(delta), p) / p;
+  }
 
  private:
-  int dim_ = 1;
+  explicit CostModel(std::vector<double> p) : p_(std::move(p)) {
+    quadratic_ = true;
+    for (double q : p_)
+      if (q != 2.0) quadratic_ = false;
+  }
+  std::vector<double> p_;
+  bool quadratic_ = true;
 };
 
 // ---- pushforward.hpp:22-36 ---------------------------------------------------
@@ -171,10 +188,66 @@ inline std::vector<double> flat_disp(const TransportMap& m) {
 }  // namespace detail
 
 // ---- operators -----------------------------------------------------------------
-inline Potential ctransform(const CostModel& model, const Potential& phi) {  // transforms.hpp:396-432
+namespace detail {
+struct WorkspaceDeleter {
+  void operator()(bfm_workspace* w) const { bfm_workspace_destroy(w); }
+};
+inline void require_quadratic(const CostModel& m, const char* what) {
+  if (!m.is_quadratic())
+    throw InvalidArgument(std::string(what) + ": power costs are outside the B200 solver path (quadratic only)");
+}
+}  // namespace detail
+
+// transforms.hpp:231: both paths are exact, so they return the same bits (the
+// reference's automatic quadratic shortcut and its generic divide and
+// conquer agree bitwise; so do ours).
+enum class CtransformPath { automatic, divide_and_conquer };
+
+// transforms.hpp:233-283: a grid's reusable c-transform state. Here it owns a
+// device workspace (bfm_workspace): the per-axis plans, tables and inter-pass
+// buffers are built once and reused by every ctransform on it. `threads` is
+// accepted for API parity (the device ignores it).
+class TransformWorkspace {
+ public:
+  explicit TransformWorkspace(const Grid& grid, int threads = 1)
+      : grid_(grid), threads_(threads < 1 ? 1 : threads) {
+    bfm_workspace* w = nullptr;
+    detail::check(bfm_workspace_create(grid.dim(), grid.extents_ptr(), &w));
+    ws_.reset(w);
+  }
+  const Grid& grid() const { return grid_; }
+  int threads() const { return threads_; }
+  bfm_workspace* handle() const { return ws_.get(); }
+
+ private:
+  Grid grid_;
+  int threads_;
+  std::unique_ptr<bfm_workspace, detail::WorkspaceDeleter> ws_;
+};
+
+inline Potential ctransform(const CostModel& model, const Potential& phi, TransformWorkspace& ws,
+                            CtransformPath path = CtransformPath::automatic) {  // transforms.hpp:396-427
+  (void)path;
+  const Grid& g = phi.grid;
+  if (model.dim() != g.dim()) throw GridMismatch("ctransform: cost dimension does not match grid");
+  if (ws.grid() != g) throw GridMismatch("ctransform: workspace built for a different grid");
+  Potential out(g);
+  if (model.is_quadratic())
+    detail::check(bfm_workspace_ctransform(ws.handle(), phi.values.data(), out.values.data()));
+  else
+    detail::check(bfm_ctransform_cost(g.dim(), g.extents_ptr(), model.exponents(), phi.values.data(),
+                                      out.values.data()));
+  return out;
+}
+
+inline Potential ctransform(const CostModel& model, const Potential& phi) {  // transforms.hpp:429-432
   if (model.dim() != phi.grid.dim()) throw GridMismatch("ctransform: cost dimension does not match grid");
   Potential out(phi.grid);
-  detail::check(bfm_ctransform(phi.grid.dim(), phi.grid.extents_ptr(), phi.values.data(), out.values.data()));
+  if (model.is_quadratic())
+    detail::check(bfm_ctransform(phi.grid.dim(), phi.grid.extents_ptr(), phi.values.data(), out.values.data()));
+  else
+    detail::check(bfm_ctransform_cost(phi.grid.dim(), phi.grid.extents_ptr(), model.exponents(),
+                                      phi.values.data(), out.values.data()));
   return out;
 }
 
@@ -182,6 +255,7 @@ inline TransportMap map_from_conjugate(const CostModel& model, const Potential& 
                                        MapSource source = MapSource::mu_side) {  // pushforward.hpp:70-91
   if (model.dim() != psi.grid.dim())
     throw GridMismatch("map_from_conjugate: cost dimension does not match grid");
+  detail::require_quadratic(model, "map_from_conjugate");
   TransportMap map(psi.grid, source);
   std::vector<double> d(psi.grid.dim() * psi.grid.size());
   detail::check(bfm_map_from_conjugate(psi.grid.dim(), psi.grid.extents_ptr(), psi.values.data(),
@@ -223,6 +297,7 @@ inline std::vector<DensityField> frame_sequence(const TransportMap& map, const D
 inline double primal_cost(const TransportMap& map, const DensityField& mu, const CostModel& model) {
   detail::require_same_grid(map.grid, mu.grid, "primal_cost");
   if (model.dim() != map.grid.dim()) throw GridMismatch("primal_cost: cost dimension does not match grid");
+  detail::require_quadratic(model, "primal_cost");
   const std::vector<double> d = detail::flat_disp(map);
   double v = 0.0;
   detail::check(bfm_primal_cost(mu.grid.dim(), mu.grid.extents_ptr(), d.data(), mu.values.data(), &v));
@@ -266,12 +341,16 @@ inline DensityField builtin_density(const Grid& g, const std::string& spec) {
 }
 
 // poisson.hpp:40-113
-class SpectralPlan {
+class SpectralPlan {  // poisson.hpp:42-113; the device plan is built once per SpectralPlan
  public:
-  explicit SpectralPlan(const Grid& grid) : grid_(grid) {}
+  explicit SpectralPlan(const Grid& grid) : grid_(grid) {
+    bfm_workspace* w = nullptr;
+    detail::check(bfm_workspace_create(grid.dim(), grid.extents_ptr(), &w));
+    ws_.reset(w, detail::WorkspaceDeleter());
+  }
   const Grid& grid() const { return grid_; }
   void solve_neumann(const double* rhs, double* out) const {
-    detail::check(bfm_solve_neumann(grid_.dim(), grid_.extents_ptr(), rhs, out));
+    detail::check(bfm_workspace_solve_neumann(ws_.get(), rhs, out));
   }
   Potential solve_neumann(const ScalarField& rhs) const {
     if (rhs.grid != grid_) throw GridMismatch("field grid does not match plan");
@@ -282,6 +361,7 @@ class SpectralPlan {
 
  private:
   Grid grid_;
+  std::shared_ptr<bfm_workspace> ws_;
 };
 
 // ---- solver.hpp:32-374 -------------------------------------------------------
@@ -371,6 +451,7 @@ class Solver {
       : grid_(mu.grid) {
     detail::require_same_grid(mu.grid, nu.grid, "solve");
     if (model.dim() != mu.grid.dim()) throw GridMismatch("solve: cost dimension does not match grid");
+    detail::require_quadratic(model, "solve");
     const bfm_config c = detail::to_c(config);
     detail::check(bfm_solver_create(grid_.dim(), grid_.extents_ptr(), mu.values.data(), nu.values.data(),
                                     &c, &h_));

@@ -279,6 +279,19 @@ void copy_d2h(double* dst, const double* src, long n, cudaStream_t s) {
 
 struct bfm_workspace {
   GridDesc g;
+  // host-pointer operator calls (bfm_workspace_ctransform / _solve_neumann):
+  // device copies of the operand and result, and a stream, made on first use
+  DevBuf io_in, io_out;
+  cudaStream_t io_stream = nullptr;
+  ~bfm_workspace() {
+    if (io_stream) cudaStreamDestroy(io_stream);
+  }
+  cudaStream_t io() {
+    if (!io_stream) BFM_CUDA(cudaStreamCreateWithFlags(&io_stream, cudaStreamNonBlocking));
+    io_in.alloc(g.size);
+    io_out.alloc(g.size);
+    return io_stream;
+  }
   std::unique_ptr<CtPlan> ct;
   std::unique_ptr<PoissonPlan> pois;
   std::unique_ptr<PushforwardPlan> pf;
@@ -1189,6 +1202,30 @@ int bfm_ctransform_device(bfm_workspace* ws, const double* d_phi, double* d_out,
     const long before = ws->lc.count;
     ws->ctp().run(d_phi, d_out, static_cast<cudaStream_t>(stream), &ws->lc);
     ws->last_launches = static_cast<int>(ws->lc.count - before);
+  });
+}
+
+int bfm_workspace_ctransform(bfm_workspace* ws, const double* phi, double* out) {
+  return guard([&] {
+    if (!ws || !phi || !out) fail(BFM_ERR_INVALID_ARGUMENT, "bfm_workspace_ctransform: null argument");
+    const cudaStream_t st = ws->io();
+    copy_h2d(ws->io_in.p, phi, ws->g.size, st);
+    const long before = ws->lc.count;
+    ws->ctp().run(ws->io_in.p, ws->io_out.p, st, &ws->lc);
+    ws->last_launches = static_cast<int>(ws->lc.count - before);
+    copy_d2h(out, ws->io_out.p, ws->g.size, st);
+  });
+}
+
+int bfm_workspace_solve_neumann(bfm_workspace* ws, const double* rhs, double* out) {
+  return guard([&] {
+    if (!ws || !rhs || !out) fail(BFM_ERR_INVALID_ARGUMENT, "bfm_workspace_solve_neumann: null argument");
+    const cudaStream_t st = ws->io();
+    copy_h2d(ws->io_in.p, rhs, ws->g.size, st);
+    const long before = ws->lc.count;
+    ws->poisp().solve(ws->io_in.p, ws->io_out.p, st, &ws->lc);
+    ws->last_launches = static_cast<int>(ws->lc.count - before);
+    copy_d2h(out, ws->io_out.p, ws->g.size, st);
   });
 }
 

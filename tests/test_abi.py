@@ -130,3 +130,16 @@ def test_synthetic_generator_is_deterministic_and_normalised():
         assert 0.2 < (blocks == 0).mean() < 0.8  # Bernoulli(0.5) blocks
     with pytest.raises(bfm.InvalidArgument):
         bfm.synthetic_densities(7, 64, 1)
+
+
+@pytest.mark.parametrize("driver", ["facade_drive", "workspace_drive"])
+def test_cpp_drivers_compile_against_the_facade(driver, tmp_path):
+    """The reference-API drivers compile and link against the facade and the
+    C ABI library here (they run on the GPU in test_gpu_parity.py)."""
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    libdir = os.path.join(root, "paper_1905_12154_b200")
+    r = subprocess.run(["g++", "-std=c++17", "-O1", "-I" + os.path.join(root, "include"),
+                        os.path.join(root, "tests", "cxx", driver + ".cpp"), "-L" + libdir,
+                        "-l:libbfm_b200.so", "-Wl,-rpath," + libdir, "-o", str(tmp_path / driver)],
+                       capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr

@@ -287,16 +287,18 @@ def test_gradient_ascent_mode_matches_reference(ref):
     assert O.n_bit_diff(a.phi, b.phi) == 0 and O.n_bit_diff(a.psi, b.psi) == 0
 
 
-def test_cpp_facade_driver_runs_on_gpu(tmp_path):
-    """A driver written against the reference's C++ API compiles unchanged
-    against include/bfm_b200/bfm.hpp and passes the reference's own checks."""
+@pytest.mark.parametrize("driver", ["facade_drive", "workspace_drive"])
+def test_cpp_facade_driver_runs_on_gpu(tmp_path, driver):
+    """Drivers written against the reference's C++ API (solver, operators,
+    TransformWorkspace) compile unchanged against include/bfm_b200/bfm.hpp and
+    pass the reference's own checks on the GPU."""
     import subprocess
 
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    exe = tmp_path / "facade_drive"
+    exe = tmp_path / driver
     libdir = os.path.join(root, "paper_1905_12154_b200")
     r = subprocess.run(["g++", "-std=c++17", "-O2", "-I" + os.path.join(root, "include"),
-                        os.path.join(root, "tests", "cxx", "facade_drive.cpp"), "-L" + libdir,
+                        os.path.join(root, "tests", "cxx", driver + ".cpp"), "-L" + libdir,
                         "-l:libbfm_b200.so", "-Wl,-rpath," + libdir, "-o", str(exe)],
                        capture_output=True, text=True)
     assert r.returncode == 0, r.stderr
