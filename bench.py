@@ -431,6 +431,96 @@ def c5_sweep(args):
 
 
 def ours_dist(args):
+    """N > 1: the C++ multi-GPU solver (csrc/dist_solver.cu, bfm_dist_solver_*):
+    one problem split into axis-0 slabs over N GPUs (strong scaling), NCCL
+    send/recv exchanges issued by the library on its own stream, the NCCL
+    unique id broadcast over torch.distributed (plumbing only)."""
+    rank, world, local = dist_env()
+    import torch
+    import torch.distributed as tdist
+
+    import paper_1905_12154_b200 as bfm
+    from paper_1905_12154_b200 import dist_cpp as DC
+
+    torch.cuda.set_device(local)
+    bfm.set_device(local)
+    dev = torch.device("cuda", local)
+    tdist.init_process_group("nccl", device_id=dev)
+    obj = [DC.nccl_unique_id() if rank == 0 else None]
+    tdist.broadcast_object_list(obj, src=0)
+    comm = DC.nccl_comm(obj[0], rank, world)
+    mu, nu, desc = workload(args.config)
+    N = mu.size
+    starts, sizes = DC.split_rows(mu.shape[0], world)
+    r0, nr = starts[rank], sizes[rank]
+    cfg = bfm.SolverConfig(tolerance=-1.0, max_iterations=10 ** 6)
+    s = DC.CppDistSolver(comm, mu.shape, mu[r0:r0 + nr], nu[r0:r0 + nr], cfg)
+    for _ in range(args.warmup):
+        s.step()
+    clocks = ClockSampler(local)
+    tdist.barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    ms = s.time_steps(args.steps)  # CUDA events on the solver stream
+    ck = clocks.stop()
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+    tdist.barrier()
+    ms_max = float(t.item())
+    value = N * args.steps / (ms_max * 1e-3)
+    s.close()
+
+    # end to end: pinned host slabs in, K iterations, phi/psi slabs back
+    pin_mu = torch.from_numpy(np.ascontiguousarray(mu[r0:r0 + nr])).pin_memory().numpy()
+    pin_nu = torch.from_numpy(np.ascontiguousarray(nu[r0:r0 + nr])).pin_memory().numpy()
+    tdist.barrier()
+    t0 = time.perf_counter()
+    s2 = DC.CppDistSolver(comm, mu.shape, pin_mu, pin_nu, cfg)
+    for _ in range(args.steps):
+        s2.step()
+    phi_h = s2.field_rows(0)
+    psi_h = s2.field_rows(1)
+    e2e_local = time.perf_counter() - t0
+    s2.close()
+    te = torch.tensor([e2e_local], dtype=torch.float64, device=dev)
+    tdist.all_reduce(te, op=tdist.ReduceOp.MAX)
+    e2e_s = float(te.item())
+    del phi_h, psi_h
+    e2e = {"value": N * args.steps / e2e_s, "unit": UNIT,
+           "h2d_bytes_per_step": int(2 * 8 * N / args.steps),
+           "d2h_bytes_per_step": int(2 * 8 * N / args.steps),
+           "note": "bfm_dist_solver from pinned host slabs + K steps + phi/psi slab readback, wall clock, "
+                   "max over ranks"}
+    if rank == 0:
+        hbm, hbm_kind = peaks()
+        d = len(desc["grid"])
+        # NVLink bytes per rank and iteration (4 c-transforms x (8 + 12) B/node, 2
+        # Neumann solves x 16 B/node, of which (P-1)/P leave the rank) against
+        # 900 GB/s per direction
+        nvl_bytes = (4 * 20 + 2 * 16) * (N / world) * (world - 1) / world
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded, BASELINE shapes; no public dataset)",
+            "config": desc,
+            "impl_detail": f"C++ multi-GPU solver, axis-0 slabs x{world}, NCCL send/recv exchanges",
+            "gpu_launches": None,
+            "clocks": ck,
+            "roofline": {"bound": "nvlink", "achieved": nvl_bytes / (ms_max / args.steps * 1e-3) / 1e9,
+                         "peak": 900.0, "unit": "GB/s",
+                         "frac": nvl_bytes / (ms_max / args.steps * 1e-3) / 1e9 / 900.0, "traffic": None,
+                         "kernel": "all-to-all exchange volume per iteration per rank over the whole step time",
+                         "hbm_peak": hbm, "peak_kind": hbm_kind},
+            "cpu_baseline": None,
+            "e2e": e2e,
+        }
+        print(json.dumps(line))
+    comm.close()
+    tdist.destroy_process_group()
+
+
+def ours_dist_python(args):
     """N > 1: the axis-0 slab decomposition (paper_1905_12154_b200/dist.py):
     one problem split over N GPUs (strong scaling), NCCL all-to-alls for the
     transposes and deposit records, rank-ordered scalar merges."""
@@ -601,7 +691,7 @@ def measure(cfg, steps, warmup, local=0):
 def ours(args):
     rank, world, local = dist_env()
     if (world > 1 and not args.replicas) or args.slabs:
-        return ours_dist(args)
+        return ours_dist_python(args) if args.py_dist else ours_dist(args)
     import torch
 
     import paper_1905_12154_b200 as bfm
@@ -690,6 +780,8 @@ def main():
     ap.add_argument("--c4-steps", type=int, default=None, help="c3: timed steps of the C4 sub-object (default 30)")
     ap.add_argument("--slabs", action="store_true",
                     help="use the slab-decomposition driver even at N = 1 (checks the NCCL path)")
+    ap.add_argument("--py-dist", action="store_true",
+                    help="N > 1: the Python slab driver (dist.py) instead of the C++ one")
     ap.add_argument("--replicas", action="store_true",
                     help="N > 1: independent single-GPU replicas instead of the slab decomposition")
     args = ap.parse_args()

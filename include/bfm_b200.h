@@ -252,6 +252,44 @@ int bfm_slab_primal(bfm_slab* s, const double* d_disp, const double* d_mu, doubl
 int bfm_slab_axpy(bfm_slab* s, double* d_u, double sigma, const double* d_dir, void* stream);
 int bfm_slab_last_launches(const bfm_slab* s);
 
+/* ---- Multi-GPU solver with a C++ host (one process per GPU) -----------------
+ * bfm::Solver's loop (solver.hpp:146-368) over an axis-0 slab decomposition:
+ * the rank-local kernels above plus NCCL grouped send/recv exchanges issued
+ * by the library (libnccl.so.2, loaded at first use) on the solver's stream.
+ * Results equal the single-GPU solver bit for bit. The caller distributes the
+ * 128-byte NCCL unique id (from rank 0's bfm_nccl_unique_id) however it
+ * likes (MPI, torch.distributed, a file). bfm_comm_create_local_group makes
+ * nranks handles whose ranks run as threads of this process on one device
+ * (host-synchronised exchanges; tests on a single GPU). Errors: the status
+ * codes above, message from bfm_dist_last_error(). */
+typedef struct bfm_comm bfm_comm;
+typedef struct bfm_dist_solver bfm_dist_solver;
+int bfm_nccl_unique_id(unsigned char* out128);
+int bfm_comm_create_nccl(const unsigned char* id128, int rank, int nranks, bfm_comm** out);
+int bfm_comm_create_local_group(int nranks, bfm_comm** out /* nranks handles */);
+void bfm_comm_destroy(bfm_comm* c);
+/* mu_rows, nu_rows: this rank's rows [row0, row0 + nrows) of the densities
+ * (rows split as evenly as possible, lower ranks first; host pointers). The
+ * caller validates the full densities (bfm_validate_inputs) as every rank of
+ * the reference-order check must agree. */
+int bfm_dist_solver_create(bfm_comm* comm, int dim, const int* extents, const double* mu_rows,
+                           const double* nu_rows, const bfm_config* cfg, bfm_dist_solver** out);
+void bfm_dist_solver_destroy(bfm_dist_solver* s);
+int bfm_dist_solver_rows(const bfm_dist_solver* s, int* row0, int* nrows);
+int bfm_dist_solver_step(bfm_dist_solver* s, bfm_iteration_stats* out);        /* :189-207 */
+int bfm_dist_solver_probe(bfm_dist_solver* s, double* dual, double* residual); /* :178-186 */
+int bfm_dist_solver_run(bfm_dist_solver* s, bfm_report* out);                  /* :211-226 */
+int bfm_dist_solver_field(bfm_dist_solver* s, int which, double* host_rows);   /* this rank's rows */
+/* gauge-fixed report fields of the whole grid (every rank holds them) */
+int bfm_dist_solver_report_field(bfm_dist_solver* s, int which, double* host_full);
+int bfm_dist_solver_trace(const bfm_dist_solver* s, bfm_iteration_stats* out, int cap, int* count);
+int bfm_dist_solver_iteration(const bfm_dist_solver* s);
+/* bench helper: k steps + trailing probes between CUDA events on the
+ * solver's stream (device milliseconds) */
+int bfm_dist_solver_time_steps(bfm_dist_solver* s, int k, double* ms);
+double bfm_dist_solver_sigma(const bfm_dist_solver* s);
+const char* bfm_dist_last_error(void);
+
 /* Total device kernels the solver has enqueued so far (launch evidence). */
 long bfm_solver_launches(const bfm_solver* s);
 

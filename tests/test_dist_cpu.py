@@ -151,3 +151,19 @@ def test_dist_solver_gloo(results):
     assert O.n_bit_diff(_full(results, "solve2_psi", shp), psi) == 0
     for r in results:
         np.testing.assert_allclose(r["solve2_dual"], duals, rtol=1e-12, atol=1e-15)
+
+
+def test_cpp_dist_layout_and_comm_handles():
+    """The C++ multi-GPU driver's row partition matches the Python layout, and
+    the in-process communicator group can be made without a device (the
+    solver itself needs the GPU: tests/test_gpu_dist_cpp.py)."""
+    from paper_1905_12154_b200 import dist as D
+    from paper_1905_12154_b200 import dist_cpp as DC
+
+    for n0, parts in [(32, 1), (33, 3), (4096, 8), (384, 8), (10, 4)]:
+        L = D.SlabLayout((n0, 16), parts)
+        assert DC.split_rows(n0, parts) == (L.row0, L.nrows)
+    comms = DC.local_group(3)
+    assert [c.rank for c in comms] == [0, 1, 2] and all(c.size == 3 for c in comms)
+    for c in comms:
+        c.close()
