@@ -113,6 +113,14 @@ double bfm_update_sigma(double sigma, double increase, double grad_norm_sq,
  * checked_solver_inputs (:132-142) and copies mu, nu (host pointers, N each). */
 int bfm_solver_create(int dim, const int* extents, const double* mu, const double* nu,
                       const bfm_config* cfg, bfm_solver** out);
+/* Solver(CostModel::power(exponents), mu, nu, cfg) (cost.hpp:24-30; exponents
+ * p_a > 1 per axis, NULL = quadratic): the exact c-transform on dense axis-cost
+ * tables (extents up to 2048; bitwise the reference's generic path,
+ * transforms.hpp:378-386), the map's inverse gradient |v|^(1/(p-1)) correctly
+ * rounded (glibc's pow, which the reference calls, is not: about 0.1 % of its
+ * results are one ulp off), primal cost with |d|^p / p. */
+int bfm_solver_create_cost(int dim, const int* extents, const double* exponents, const double* mu,
+                           const double* nu, const bfm_config* cfg, bfm_solver** out);
 void bfm_solver_destroy(bfm_solver* s);
 
 int bfm_solver_iteration(const bfm_solver* s);                 /* :169 */
@@ -152,6 +160,11 @@ int bfm_solve_neumann(int dim, const int* extents, const double* rhs, double* ou
 int bfm_integrate(int dim, const int* extents, const double* f, const double* w,
                   double* out);
 /* pushforward.hpp:181-196 primal_cost. */
+/* map_from_conjugate / primal_cost with a power cost (exponents per axis). */
+int bfm_map_from_conjugate_cost(int dim, const int* extents, const double* exponents,
+                                const double* u, int side, double* disp);
+int bfm_primal_cost_cost(int dim, const int* extents, const double* exponents, const double* disp,
+                         const double* mu, double* out);
 int bfm_primal_cost(int dim, const int* extents, const double* disp, const double* mu,
                     double* out);
 
@@ -333,6 +346,9 @@ int bfm_debug_round_down(const double* terms, int m, int count, double* out);
  * rho = ((0 + w_0) + w_1) + ... of each sequence w[offsets[i] .. offsets[i+1])
  * (exact_fold.cuh), by a 512-thread CTA (mode 0) or one warp (mode 1). */
 int bfm_debug_fold(const double* w, const long* offsets, int nseq, int mode, double* out);
+
+/* Test hook: correctly rounded x^y (pow_dd.h) on the host or the device. */
+int bfm_debug_pow(const double* x, const double* y, int n, int on_device, double* out);
 
 const char* bfm_last_error(void);
 /* Selects the CUDA device for subsequent calls on this thread (one process

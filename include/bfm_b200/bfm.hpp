@@ -3,10 +3,10 @@
 // same names, signatures and exception types, so drivers written against the
 // reference (e.g. tools/bfm_ot.cpp's run_solver, benchmark.hpp's
 // run_benchmark_case) compile unchanged against this header and run on the
-// B200. Scope: the solver is quadratic-cost (the north-star path); the
-// c-transform also takes power costs (CostModel::power); the solver, map and
-// primal cost throw InvalidArgument for them. Link with -lbfm_b200
-// (paper_1905_12154_b200/libbfm_b200.so).
+// B200. Quadratic costs (the north-star path) and separable power costs
+// (CostModel::power): the power-cost map uses a correctly rounded pow where the
+// reference calls glibc's (one ulp apart on ~0.1 % of calls). Link with
+// -lbfm_b200 (paper_1905_12154_b200/libbfm_b200.so).
 #pragma once
 
 #include <array>
@@ -127,9 +127,8 @@ struct DensityField : ScalarField {
 };
 
 // ---- cost.hpp:17-81 ----------------------------------------------------------------
-// Separable costs sum_a |y_a - x_a|^p_a / p_a. The c-transform runs on the B200
-// for every exponent (bfm_ctransform_cost); the solver, the map and the primal
-// cost take the quadratic path only (power costs throw InvalidArgument there).
+// Separable costs sum_a |y_a - x_a|^p_a / p_a, every operator and the solver
+// on the B200 (bfm_*_cost entry points for p != 2).
 class CostModel {
  public:
   static CostModel quadratic(int dim) {
@@ -192,10 +191,6 @@ namespace detail {
 struct WorkspaceDeleter {
   void operator()(bfm_workspace* w) const { bfm_workspace_destroy(w); }
 };
-inline void require_quadratic(const CostModel& m, const char* what) {
-  if (!m.is_quadratic())
-    throw InvalidArgument(std::string(what) + ": power costs are outside the B200 solver path (quadratic only)");
-}
 }  // namespace detail
 
 // transforms.hpp:231: both paths are exact, so they return the same bits (the
@@ -255,12 +250,13 @@ inline TransportMap map_from_conjugate(const CostModel& model, const Potential& 
                                        MapSource source = MapSource::mu_side) {  // pushforward.hpp:70-91
   if (model.dim() != psi.grid.dim())
     throw GridMismatch("map_from_conjugate: cost dimension does not match grid");
-  detail::require_quadratic(model, "map_from_conjugate");
   TransportMap map(psi.grid, source);
   std::vector<double> d(psi.grid.dim() * psi.grid.size());
-  detail::check(bfm_map_from_conjugate(psi.grid.dim(), psi.grid.extents_ptr(), psi.values.data(),
-                                       source == MapSource::nu_side ? BFM_MAP_NU_SIDE : BFM_MAP_MU_SIDE,
-                                       d.data()));
+  detail::check(bfm_map_from_conjugate_cost(psi.grid.dim(), psi.grid.extents_ptr(),
+                                            model.is_quadratic() ? nullptr : model.exponents(),
+                                            psi.values.data(),
+                                            source == MapSource::nu_side ? BFM_MAP_NU_SIDE : BFM_MAP_MU_SIDE,
+                                            d.data()));
   for (int a = 0; a < psi.grid.dim(); ++a)
     map.displacement[a].assign(d.begin() + a * psi.grid.size(), d.begin() + (a + 1) * psi.grid.size());
   return map;
@@ -297,10 +293,11 @@ inline std::vector<DensityField> frame_sequence(const TransportMap& map, const D
 inline double primal_cost(const TransportMap& map, const DensityField& mu, const CostModel& model) {
   detail::require_same_grid(map.grid, mu.grid, "primal_cost");
   if (model.dim() != map.grid.dim()) throw GridMismatch("primal_cost: cost dimension does not match grid");
-  detail::require_quadratic(model, "primal_cost");
   const std::vector<double> d = detail::flat_disp(map);
   double v = 0.0;
-  detail::check(bfm_primal_cost(mu.grid.dim(), mu.grid.extents_ptr(), d.data(), mu.values.data(), &v));
+  detail::check(bfm_primal_cost_cost(mu.grid.dim(), mu.grid.extents_ptr(),
+                                     model.is_quadratic() ? nullptr : model.exponents(), d.data(),
+                                     mu.values.data(), &v));
   return v;
 }
 
@@ -451,10 +448,10 @@ class Solver {
       : grid_(mu.grid) {
     detail::require_same_grid(mu.grid, nu.grid, "solve");
     if (model.dim() != mu.grid.dim()) throw GridMismatch("solve: cost dimension does not match grid");
-    detail::require_quadratic(model, "solve");
     const bfm_config c = detail::to_c(config);
-    detail::check(bfm_solver_create(grid_.dim(), grid_.extents_ptr(), mu.values.data(), nu.values.data(),
-                                    &c, &h_));
+    detail::check(bfm_solver_create_cost(grid_.dim(), grid_.extents_ptr(),
+                                         model.is_quadratic() ? nullptr : model.exponents(),
+                                         mu.values.data(), nu.values.data(), &c, &h_));
   }
   ~Solver() {
     if (h_) bfm_solver_destroy(h_);

@@ -314,6 +314,16 @@ int ref_primal_cost(int dim, const int* ext, const double* disp, const double* m
   })
 }
 
+int ref_primal_cost_cost(int dim, const int* ext, const double* exponents, const double* disp,
+                         const double* mu, double* out) {
+  GUARD({
+    const bfm::Grid g = make_grid(dim, ext);
+    bfm::DensityField m(g);
+    std::memcpy(m.values.data(), mu, g.size() * sizeof(double));
+    *out = bfm::primal_cost(make_map(g, disp), m, cost_model(dim, exponents));
+  })
+}
+
 // Fixture helpers (io.hpp:452-476 builtin_density, grid.hpp:151-164 normalize).
 int ref_builtin_density(int dim, const int* ext, const char* spec, double* out) {
   GUARD({

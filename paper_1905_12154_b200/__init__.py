@@ -327,7 +327,10 @@ class Solver:
 
     _prefix = "bfm_"
 
-    def __init__(self, mu, nu, config: Optional[SolverConfig] = None, _lib=None):
+    def __init__(self, mu, nu, config: Optional[SolverConfig] = None, _lib=None,
+                 exponents: Optional[Sequence[float]] = None):
+        """exponents: CostModel::power (cost.hpp:24-30), one p > 1 per axis;
+        None is the quadratic cost."""
         self._lib = _lib or load_library()
         mu = _f64(mu)
         nu = _f64(nu)
@@ -338,8 +341,17 @@ class Solver:
         self._cfg = self.config._c()
         h = C.c_void_p()
         self._h = None
-        rc = self._fn("solver_create")(len(mu.shape), _extents(mu.shape), _ptr(mu), _ptr(nu),
-                                       C.byref(self._cfg), C.byref(h))
+        if exponents is None:
+            rc = self._fn("solver_create")(len(mu.shape), _extents(mu.shape), _ptr(mu), _ptr(nu),
+                                           C.byref(self._cfg), C.byref(h))
+        else:
+            if len(exponents) != mu.ndim:
+                raise GridMismatch("solve: cost dimension does not match grid")
+            ex = (C.c_double * 3)(*([float(e) for e in exponents] + [2.0] * (3 - len(exponents))))
+            f = self._fn("solver_create_cost")
+            f.argtypes = [C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
+            f.restype = C.c_int
+            rc = f(len(mu.shape), _extents(mu.shape), ex, _ptr(mu), _ptr(nu), C.byref(self._cfg), C.byref(h))
         self._check(rc)
         self._h = h
 
@@ -468,13 +480,39 @@ def ctransform(phi, exponents: Optional[Sequence[float]] = None) -> np.ndarray:
     return out
 
 
-def map_from_conjugate(u, side: int = MU_SIDE) -> np.ndarray:
-    """pushforward.hpp:70-91: displacement field, shape (d, *grid)."""
+def _exps(exponents, d):
+    if len(exponents) != d:
+        raise GridMismatch("cost dimension does not match grid")
+    return (C.c_double * 3)(*([float(e) for e in exponents] + [2.0] * (3 - d)))
+
+
+def map_from_conjugate(u, side: int = MU_SIDE, exponents: Optional[Sequence[float]] = None) -> np.ndarray:
+    """pushforward.hpp:70-91: displacement field, shape (d, *grid); exponents:
+    a power cost's p per axis (cost.hpp:58-68 inverse gradient)."""
     lib = load_library()
     u = _f64(u)
     disp = np.empty((u.ndim,) + u.shape, dtype=np.float64)
-    _check(lib, lib.bfm_map_from_conjugate(u.ndim, _extents(u.shape), _ptr(u), side, _ptr(disp)))
+    if exponents is None:
+        _check(lib, lib.bfm_map_from_conjugate(u.ndim, _extents(u.shape), _ptr(u), side, _ptr(disp)))
+    else:
+        f = lib.bfm_map_from_conjugate_cost
+        f.argtypes = [C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_void_p]
+        f.restype = C.c_int
+        _check(lib, f(u.ndim, _extents(u.shape), _exps(exponents, u.ndim), _ptr(u), side, _ptr(disp)))
     return disp
+
+
+def debug_pow(x, y, on_device: bool = True) -> np.ndarray:
+    """Test hook: the library's correctly rounded x^y (pow_dd.h)."""
+    lib = load_library()
+    x = _f64(x).reshape(-1)
+    y = np.broadcast_to(_f64(y), x.shape).copy()
+    out = np.empty_like(x)
+    f = lib.bfm_debug_pow
+    f.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_void_p]
+    f.restype = C.c_int
+    _check(lib, f(_ptr(x), _ptr(y), x.size, 1 if on_device else 0, _ptr(out)))
+    return out
 
 
 def _check_disp(disp: np.ndarray, mu: np.ndarray, what: str) -> None:
@@ -540,15 +578,22 @@ def integrate(f, w=None) -> float:
     return v.value
 
 
-def primal_cost(disp, mu) -> float:
-    """pushforward.hpp:181-196 (quadratic cost)."""
+def primal_cost(disp, mu, exponents: Optional[Sequence[float]] = None) -> float:
+    """pushforward.hpp:181-196 (quadratic, or a power cost's p per axis)."""
     lib = load_library()
     mu = _f64(mu)
     disp = _f64(disp)
     _check_disp(disp, mu, "primal_cost")
     v = C.c_double()
-    _check(lib, lib.bfm_primal_cost(mu.ndim, _extents(mu.shape), _ptr(disp), _ptr(mu),
-                                    C.byref(v)))
+    if exponents is None:
+        _check(lib, lib.bfm_primal_cost(mu.ndim, _extents(mu.shape), _ptr(disp), _ptr(mu),
+                                        C.byref(v)))
+    else:
+        f = lib.bfm_primal_cost_cost
+        f.argtypes = [C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
+        f.restype = C.c_int
+        _check(lib, f(mu.ndim, _extents(mu.shape), _exps(exponents, mu.ndim), _ptr(disp), _ptr(mu),
+                      C.byref(v)))
     return v.value
 
 

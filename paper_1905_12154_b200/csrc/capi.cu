@@ -18,6 +18,8 @@
 #include <thread>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "../../include/bfm_b200.h"
 #include "common.cuh"
 #include "ctransform.cuh"
@@ -25,9 +27,11 @@
 #include "poisson.cuh"
 #include "pushforward.cuh"
 #include "reduce.cuh"
+#include "pow_dd.h"
 #include "solver_ctl.cuh"
 
 namespace bfmgpu {
+void debug_pow_device(const double* h_x, const double* h_y, int n, double* h_out);
 int synthetic_densities(int config, int n, uint64_t seed, double* mu, double* nu, std::string& msg);
 void debug_round_down(const double* h_terms, int m, int count, double* h_out);
 void debug_fold(const double* h_w, const long* h_off, int nseq, int mode, double* h_out);
@@ -351,6 +355,11 @@ struct bfm_solver {
   DevBuf mu, nu, phi, psi, dir, dir2, r;
   DevBuf rep_phi, rep_psi, rep_map;
   double sigma0 = 0.0;
+  // separable power cost (cost.hpp:17-81): exponents per axis, the exact
+  // c-transform on dense axis-cost tables and the pow inverse-gradient map
+  bool power = false;
+  double pexp[3] = {2.0, 2.0, 2.0};
+  std::unique_ptr<CtPowerPlan> ctpow;
   // Scalar state lives on the device (solver_ctl.cuh); h is the pinned mirror
   // every unit copies back, ring the per-step stats of a batch.
   SolverCtl* d_ctl = nullptr;
@@ -401,8 +410,18 @@ struct bfm_solver {
     free_events.pop_back();
     return e;
   }
+  // NVTX range per operator (visible in nsys / ncu --nvtx; free without a tool)
+  static const char* op_name(int op) {
+    static const char* names[BFM_OP_COUNT] = {"bfm.ctransform", "bfm.pushforward", "bfm.poisson",
+                                              "bfm.reduce"};
+    return op >= 0 && op < BFM_OP_COUNT ? names[op] : "bfm.op";
+  }
   template <class F>
   void timed(int op, F&& f) {
+    nvtxRangePushA(op_name(op));
+    struct Pop {
+      ~Pop() { nvtxRangePop(); }
+    } pop;
     if (!timing) {
       f();
       return;
@@ -486,7 +505,10 @@ struct bfm_solver {
     });
   }
   void ctransform(const double* in, double* out) {
-    timed(BFM_OP_CTRANSFORM, [&] { ws.ctp().run(in, out, stream, &ws.lc); });
+    timed(BFM_OP_CTRANSFORM, [&] {
+      if (power) ctpow->run(in, out, stream, &ws.lc);
+      else ws.ctp().run(in, out, stream, &ws.lc);
+    });
   }
   void axpy_device(double* u, const double* d) {
     timed(BFM_OP_REDUCE, [&] { axpy_dev(u, &d_ctl->sigma, d, g.size, stream, &ws.lc); });
@@ -541,6 +563,11 @@ struct bfm_solver {
   // Launches one unit: eagerly the first time (plans allocate lazily), then as
   // a captured CUDA graph replayed with a single launch.
   void launch_unit(int kind) {
+    static const char* unit_names[3] = {"bfm.probe", "bfm.step", "bfm.step+probe"};
+    nvtxRangePushA(unit_names[kind]);
+    struct Pop {
+      ~Pop() { nvtxRangePop(); }
+    } pop;
     if (!use_graphs) return enqueue_unit(kind);
     UnitGraph& G = graphs[kind][timing ? 1 : 0];
     if (G.uses++ == 0) return enqueue_unit(kind);
@@ -801,7 +828,8 @@ struct bfm_solver {
     add_scalar(rep_phi.p, -shift, g.size, stream, &ws.lc);
     add_scalar(rep_psi.p, shift, g.size, stream, &ws.lc);
     ws.pfp().map_only(rep_psi.p, rep_map.p, stream, &ws.lc);
-    ws.redp().primal(rep_map.p, mu.p, g.d, g.size, g.vol, kSlotPrimal, stream, &ws.lc);
+    ws.redp().primal(rep_map.p, mu.p, g.d, g.size, g.vol, kSlotPrimal, stream, &ws.lc,
+                     power ? pexp : nullptr);
     double v[kSlotPrimal + 1];
     ws.redp().fetch(v, kSlotPrimal + 1, stream);
     rep->primal_cost = v[kSlotPrimal];
@@ -903,6 +931,18 @@ int bfm_debug_round_down(const double* terms, int m, int count, double* out) {
   });
 }
 
+int bfm_debug_pow(const double* x, const double* y, int n, int on_device, double* out) {
+  return guard([&] {
+    if (n < 0 || (n > 0 && (!x || !y || !out))) throw std::invalid_argument("debug_pow: bad arguments");
+    if (!on_device) {
+      for (int i = 0; i < n; ++i) out[i] = bfmpow::pow_cr(x[i], y[i]);
+      return;
+    }
+    require_device();
+    bfmgpu::debug_pow_device(x, y, n, out);
+  });
+}
+
 int bfm_debug_fold(const double* w, const long* offsets, int nseq, int mode, double* out) {
   return guard([&] {
     require_device();
@@ -935,6 +975,11 @@ double bfm_update_sigma(double sigma, double increase, double gn, const bfm_conf
 
 int bfm_solver_create(int dim, const int* extents, const double* mu, const double* nu,
                       const bfm_config* cfg, bfm_solver** out) {
+  return bfm_solver_create_cost(dim, extents, nullptr, mu, nu, cfg, out);
+}
+
+int bfm_solver_create_cost(int dim, const int* extents, const double* exponents, const double* mu,
+                           const double* nu, const bfm_config* cfg, bfm_solver** out) {
   return guard([&] {
     *out = nullptr;
     bfm_config c;
@@ -979,6 +1024,18 @@ int bfm_solver_create(int dim, const int* extents, const double* mu, const doubl
     if (needs_host(v[8], v[9], v[11]) || std::abs(v[11] - 1.0) > 1e-6) check_density("nu", nu, g);
     const double sup = std::max(v[4], v[7]);  // solver.hpp:160-163
     s->sigma0 = c.sigma_init > 0.0 ? c.sigma_init : 8.0 / sup;
+    if (exponents) {
+      for (int a = 0; a < dim; ++a) {
+        if (!(exponents[a] > 1.0)) fail(BFM_ERR_INVALID_ARGUMENT, "cost exponents must satisfy p > 1");
+        s->pexp[a] = exponents[a];
+        s->power = s->power || exponents[a] != 2.0;
+      }
+      if (s->power) {
+        s->ctpow.reset(new CtPowerPlan);
+        s->ctpow->init(g, exponents);
+        s->ws.pfp().set_cost(exponents);
+      }
+    }
     s->kcfg = CtlConfig{c.beta_1, c.beta_2, c.alpha_1, c.alpha_2, c.sigma_min};
     BFM_CUDA(dmalloc(&s->d_ctl, sizeof(SolverCtl)));
     BFM_CUDA(dmalloc(&s->d_ring, kCtlRing * sizeof(CtlStats)));
@@ -1172,11 +1229,32 @@ int bfm_integrate(int dim, const int* extents, const double* f, const double* w,
 
 int bfm_primal_cost(int dim, const int* extents, const double* disp, const double* mu,
                     double* out) {
+  return bfm_primal_cost_cost(dim, extents, nullptr, disp, mu, out);
+}
+
+int bfm_map_from_conjugate_cost(int dim, const int* extents, const double* exponents,
+                                const double* u, int /*side*/, double* disp) {
   return guard([&] {
     HostOp op(dim, extents);
+    double* a = op.up(u, op.g.size);
+    double* m = op.up(nullptr, op.g.d * op.g.size);
+    op.ws.pfp().set_cost(exponents);
+    op.ws.pfp().map_only(a, m, nullptr, &op.ws.lc);
+    op.down(disp, m, op.g.d * op.g.size);
+    op.release();
+  });
+}
+
+int bfm_primal_cost_cost(int dim, const int* extents, const double* exponents, const double* disp,
+                         const double* mu, double* out) {
+  return guard([&] {
+    HostOp op(dim, extents);
+    if (exponents)
+      for (int a = 0; a < dim; ++a)
+        if (!(exponents[a] > 1.0)) fail(BFM_ERR_INVALID_ARGUMENT, "cost exponents must satisfy p > 1");
     double* m = op.up(disp, op.g.d * op.g.size);
     double* a = op.up(mu, op.g.size);
-    op.ws.redp().primal(m, a, op.g.d, op.g.size, op.g.vol, 0, nullptr, &op.ws.lc);
+    op.ws.redp().primal(m, a, op.g.d, op.g.size, op.g.vol, 0, nullptr, &op.ws.lc, exponents);
     double v[1];
     op.ws.redp().fetch(v, 1, nullptr);
     *out = v[0];

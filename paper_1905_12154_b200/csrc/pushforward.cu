@@ -24,6 +24,7 @@
 
 #include "exact_fold.cuh"
 #include "pushforward.cuh"
+#include "pow_dd.h"
 
 namespace bfmgpu {
 namespace {
@@ -56,6 +57,7 @@ struct MapArgs {
   double* disp_out;     // optional
   int binning;          // 0: map only
   double diam;          // sqrt(d)
+  double iexp[3];       // power costs: 1/(p_a - 1) per axis (0: quadratic axis)
 };
 
 // Node coordinates of a linear index (grids here have < 2^31 nodes: 32-bit
@@ -131,7 +133,9 @@ __global__ void pf_map_kernel(MapArgs A) {
         if (j == 0) gr = (__ldg(A.u + su + st) - __ldg(A.u + su)) * inv_h;
         else if (j == n - 1) gr = (__ldg(A.u + su) - __ldg(A.u + su - st)) * inv_h;
         else gr = (__ldg(A.u + su + st) - __ldg(A.u + su - st)) * inv_2h;
-        double mag = fabs(gr);
+        // inverse gradient (cost.hpp:59-68): |v| (p = 2) or |v|^(1/(p-1)),
+        // correctly rounded (pow_dd.h), capped at sqrt(d)
+        double mag = A.iexp[a] > 0.0 ? bfmpow::pow_cr(fabs(gr), A.iexp[a]) : fabs(gr);
         if (!(mag < A.diam)) mag = A.diam;
         const double v = gr < 0.0 ? -mag : mag;
         double t = x - v;
@@ -915,8 +919,18 @@ void PushforwardPlan::ensure_records(long nrec) {
   rec_cap_ = cap;
 }
 
+void PushforwardPlan::set_cost(const double* exponents) {
+  for (int a = 0; a < 3; ++a) {
+    iexp_[a] = 0.0;
+    if (exponents && a < g_.d && exponents[a] != 2.0) {
+      if (!(exponents[a] > 1.0)) throw std::invalid_argument("cost exponents must satisfy p > 1");
+      iexp_[a] = 1.0 / (exponents[a] - 1.0);  // cost.hpp:65, the same IEEE expression
+    }
+  }
+}
+
 namespace {
-MapArgs map_args(const GridDesc& g, const GridDesc& gg, int row_off, long cell_shift) {
+MapArgs map_args(const GridDesc& g, const GridDesc& gg, int row_off, long cell_shift, const double* iexp) {
   MapArgs A{};
   A.g = g;
   A.gg = gg;
@@ -924,13 +938,14 @@ MapArgs map_args(const GridDesc& g, const GridDesc& gg, int row_off, long cell_s
   A.u_shift = cell_shift;  // a slab's u carries one halo row on each side
   A.scale = 1.0;
   A.diam = std::sqrt(static_cast<double>(g.d));
+  for (int a = 0; a < 3; ++a) A.iexp[a] = iexp[a];
   return A;
 }
 }  // namespace
 
 void PushforwardPlan::map_only(const double* d_u, double* d_disp, cudaStream_t stream,
                                LaunchCounter* lc) {
-  MapArgs A = map_args(g_, gg_, row_off_, cell_shift_);
+  MapArgs A = map_args(g_, gg_, row_off_, cell_shift_, iexp_);
   A.u = d_u;
   A.disp_out = d_disp;
   pf_map_kernel<<<grid_for(g_.size, 256), 256, 0, stream>>>(A);
@@ -941,7 +956,7 @@ void PushforwardPlan::map_only(const double* d_u, double* d_disp, cudaStream_t s
 void PushforwardPlan::map_records(const double* d_u_ext, const double* d_source, uint32_t* d_key,
                                   double* d_w, uint8_t* d_cmask, double* d_disp_out,
                                   cudaStream_t stream, LaunchCounter* lc) {
-  MapArgs A = map_args(g_, gg_, row_off_, cell_shift_);
+  MapArgs A = map_args(g_, gg_, row_off_, cell_shift_, iexp_);
   A.u = d_u_ext;
   A.src = d_source;
   A.key = d_key;
@@ -1078,7 +1093,7 @@ void PushforwardPlan::from_potential(const double* d_u, const double* d_source,
 void PushforwardPlan::from_displacement(const double* d_disp, double scale,
                                         const double* d_source, double* d_rho,
                                         cudaStream_t stream, LaunchCounter* lc) {
-  MapArgs A = map_args(g_, gg_, row_off_, cell_shift_);
+  MapArgs A = map_args(g_, gg_, row_off_, cell_shift_, iexp_);
   A.disp = d_disp;
   A.scale = scale;
   A.src = d_source;

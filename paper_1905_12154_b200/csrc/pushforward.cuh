@@ -43,6 +43,10 @@ class PushforwardPlan {
               const uint8_t* d_cmask, const double* d_target, double* d_out, cudaStream_t stream,
               LaunchCounter* lc);
   long num_cells() const { return ncells_; }
+  // Separable power cost (cost.hpp:58-68): per axis p_a > 1; the map's inverse
+  // gradient is then sign(v) |v|^(1/(p_a - 1)) (capped at sqrt d); p_a == 2
+  // keeps the quadratic |v|. nullptr restores the quadratic cost.
+  void set_cost(const double* exponents);
   // diagnostics: targets in the warp / CTA / huge tiers of the last gather
   void tier_counts(int* out3) const {
     int v[6] = {};
@@ -68,6 +72,7 @@ class PushforwardPlan {
  private:
   void setup(const GridDesc& loc, const GridDesc& global, int row0, bool slab);
   void ensure_records(long nrec);
+  double iexp_[3] = {0.0, 0.0, 0.0};  // 1/(p_a - 1) per axis, 0 = quadratic axis
   GridDesc g_;    // this plan's nodes
   GridDesc gg_;   // problem grid
   int row_off_ = 0;

@@ -9,6 +9,7 @@
 
 #include "exact.cuh"
 #include "reduce.cuh"
+#include "pow_dd.h"
 
 namespace bfmgpu {
 namespace {
@@ -61,6 +62,7 @@ struct RedArgs {
   int mode;
   int d;
   double* partials;
+  double pexp[3];  // primal: per-axis exponent of a power cost (0: quadratic axis)
 };
 
 // One element's terms (mode 2: 0 for massless nodes, which the sums skip;
@@ -77,7 +79,8 @@ __device__ __forceinline__ void red_terms(const RedArgs& A, long i, double& t1, 
     double c = 0.0;
     for (int a = 0; a < A.d; ++a) {
       const double dl = A.a1[a * A.n + i];
-      c += 0.5 * dl * dl;
+      // axis_cost (cost.hpp:36-40): 0.5 d^2, or |d|^p / p (correctly rounded pow)
+      c += A.pexp[a] == 0.0 ? 0.5 * dl * dl : bfmpow::pow_cr(fabs(dl), A.pexp[a]) / A.pexp[a];
     }
     t1 = m == 0.0 ? 0.0 : c * m;
   }
@@ -297,8 +300,9 @@ void Reducer::sum(const double* a, long n, double vol, int slot, cudaStream_t s,
 }
 
 void Reducer::primal(const double* disp, const double* mu, int d, long n, double vol, int slot,
-                     cudaStream_t s, LaunchCounter* lc) {
-  RedArgs A{disp, mu, nullptr, nullptr, n, 2, d, partials_};
+                     cudaStream_t s, LaunchCounter* lc, const double* exponents) {
+  RedArgs A{disp, mu, nullptr, nullptr, n, 2, d, partials_, {0.0, 0.0, 0.0}};
+  for (int a = 0; a < d && exponents; ++a) A.pexp[a] = exponents[a] == 2.0 ? 0.0 : exponents[a];
   red_partial_kernel<<<blocks_, kRedThreads, 0, s>>>(A);
   red_final_kernel<<<1, kRedThreads, 0, s>>>(partials_, blocks_, 0, vol, results_, slot);
   BFM_LAUNCH_CHECK("reduce primal");
@@ -342,6 +346,30 @@ void add_scalar(double* u, double delta, long n, cudaStream_t st, LaunchCounter*
   add_scalar_kernel<<<ew_grid(n), 256, 0, st>>>(u, delta, n);
   BFM_LAUNCH_CHECK("add_scalar");
   if (lc) lc->add();
+}
+
+namespace {
+__global__ void debug_pow_kernel(const double* x, const double* y, int n, double* out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = bfmpow::pow_cr(x[i], y[i]);
+}
+}  // namespace
+
+// test hook (bfm_debug_pow): the device evaluation of pow_dd.h
+void debug_pow_device(const double* h_x, const double* h_y, int n, double* h_out) {
+  if (n <= 0) return;
+  double *dx = nullptr, *dy = nullptr, *dout = nullptr;
+  BFM_CUDA(dmalloc(&dx, sizeof(double) * n));
+  BFM_CUDA(dmalloc(&dy, sizeof(double) * n));
+  BFM_CUDA(dmalloc(&dout, sizeof(double) * n));
+  BFM_CUDA(cudaMemcpy(dx, h_x, sizeof(double) * n, cudaMemcpyHostToDevice));
+  BFM_CUDA(cudaMemcpy(dy, h_y, sizeof(double) * n, cudaMemcpyHostToDevice));
+  debug_pow_kernel<<<(n + 127) / 128, 128>>>(dx, dy, n, dout);
+  BFM_LAUNCH_CHECK("debug_pow_kernel");
+  BFM_CUDA(cudaMemcpy(h_out, dout, sizeof(double) * n, cudaMemcpyDeviceToHost));
+  dfree(dx);
+  dfree(dy);
+  dfree(dout);
 }
 
 }  // namespace bfmgpu

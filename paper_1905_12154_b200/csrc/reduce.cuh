@@ -38,8 +38,9 @@ class Reducer {
   // non-finite, results[slot+2] = 1 if any negative.
   void scan_density(const double* a, long n, int slot, cudaStream_t s, LaunchCounter* lc);
   // results[slot] = vol * sum_{m != 0} fl(c * m), c = sum_a 0.5*d_a*d_a
+  // exponents (optional): a power cost's p_a per axis (cost.hpp:36-40)
   void primal(const double* disp, const double* mu, int d, long n, double vol, int slot,
-              cudaStream_t s, LaunchCounter* lc);
+              cudaStream_t s, LaunchCounter* lc, const double* exponents = nullptr);
   double* device_results() { return results_; }
   // Copies slots [0, count) to host (synchronises the stream).
   void fetch(double* host, int count, cudaStream_t s);

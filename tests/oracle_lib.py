@@ -75,8 +75,8 @@ def _chk(lib, rc, prefix):
 class RefSolver(bfm.Solver):
     _prefix = "ref_"
 
-    def __init__(self, mu, nu, config=None):
-        super().__init__(mu, nu, config, _lib=ref_lib())
+    def __init__(self, mu, nu, config=None, exponents=None):
+        super().__init__(mu, nu, config, _lib=ref_lib(), exponents=exponents)
 
     def launches(self):
         return 0
@@ -132,6 +132,17 @@ def ref_integrate(f, w=None):
     v = C.c_double()
     wp = None if w is None else _p(np.ascontiguousarray(w, dtype=np.float64))
     _chk(lib, lib.ref_integrate(f.ndim, _ext(f.shape), _p(f), wp, C.byref(v)), "ref_")
+    return v.value
+
+
+def ref_primal_cost_cost(disp, mu, exponents):
+    lib = ref_lib()
+    mu = np.ascontiguousarray(mu, dtype=np.float64)
+    disp = np.ascontiguousarray(disp, dtype=np.float64)
+    ex = (C.c_double * 3)(*([float(e) for e in exponents] + [2.0] * (3 - len(exponents))))
+    lib.ref_primal_cost_cost.argtypes = [C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
+    v = C.c_double()
+    _chk(lib, lib.ref_primal_cost_cost(mu.ndim, _ext(mu.shape), ex, _p(disp), _p(mu), C.byref(v)), "ref_")
     return v.value
 
 

@@ -41,3 +41,101 @@ def test_power_all_quadratic_is_the_shortcut():
 def test_power_rejects_bad_exponents():
     with pytest.raises(bfm.InvalidArgument):
         bfm.ctransform(np.zeros((8, 8)), (1.0, 2.0))
+
+
+# ---- the power-cost map and solver (cost.hpp:58-68, solver.hpp with
+# CostModel::power). glibc's pow, which the reference calls, is not correctly
+# rounded (tests/test_oracle.py measures it); ours is, so results agree with
+# the reference to one ulp per pow call, and trajectories to ~1e-12.
+
+def test_device_pow_equals_host_pow():
+    rng = np.random.default_rng(5)
+    x = rng.uniform(0, 2, 200000) * 10 ** rng.uniform(-8, 2, 200000)
+    y = rng.choice([2.0, 0.5, 1 / 3, 4.0, 1 / (1.1 - 1), 1 / (1.5 - 1), 1 / (2.5 - 1), 1.5, 3.0], x.size)
+    d = bfm.debug_pow(x, y, on_device=True)
+    h = bfm.debug_pow(x, y, on_device=False)
+    assert O.n_bit_diff(d, h) == 0
+
+
+@pytest.mark.parametrize("shape,exps", [((64, 48), (1.5, 2.5)), ((40, 40), (1.1, 3.0)), ((12, 10, 8), (1.2, 2.0, 4.0))])
+def test_power_map_within_one_ulp_of_reference(shape, exps, ref):
+    u = 0.05 * synthetic.c5_potential(shape)[1]
+    got = bfm.map_from_conjugate(u, exponents=exps)
+    want = O.ref_map_from_conjugate_cost(u, exps)
+    diff = np.abs(got.view(np.int64) - want.view(np.int64))
+    # one ulp of the inverse gradient can move t = x - v by at most a couple of
+    # ulps of x after the subtraction and clamp
+    assert np.abs(got - want).max() <= 4e-16
+    assert (diff != 0).mean() < 0.01
+
+
+def test_cubic_cost_inverts_affine_gradient_exactly():
+    """test_pushforward.cpp:168-183: u = 0.25 x gives target max(x - 0.5, 0)."""
+    shape = (32, 24)
+    x = (np.arange(32) + 0.5) * (1.0 / 32)
+    u = np.repeat((0.25 * x)[:, None], 24, 1)
+    disp = bfm.map_from_conjugate(u, exponents=(3.0, 3.0))
+    assert np.array_equal(x[:, None] + disp[0], np.maximum(x - 0.5, 0.0)[:, None] + 0 * disp[0])
+    assert not disp[1].any()
+
+
+def test_power_primal_cost_vs_reference(ref):
+    shape = (48, 40)
+    mu = synthetic.c1_like(shape)[0]
+    disp = O.ref_map_from_conjugate_cost(0.05 * synthetic.c5_potential(shape)[1], (1.5, 2.5))
+    a = bfm.primal_cost(disp, mu, exponents=(1.5, 2.5))
+    b = O.ref_primal_cost_cost(disp, mu, (1.5, 2.5))
+    assert abs(a - b) <= 1e-13 * abs(b)
+
+
+def test_power_solver_rigid_shift_1d(ref):
+    """test_solver.cpp:238-252: a segment shifted by 32 cells under p = 1.5
+    reaches the exact cost |0.5|^1.5 / 1.5 (cost_target_met), in the same
+    number of iterations as the reference."""
+    n = 64
+    x = (np.arange(n) + 0.5) * (1.0 / n)
+    mu = bfm.normalize((np.abs(x - 0.25) <= 0.125).astype(float))
+    nu = bfm.normalize((np.abs(x - 0.75) <= 0.125).astype(float))
+    exact = 0.5 ** 1.5 / 1.5
+    cfg = bfm.SolverConfig(tolerance=-1.0, max_iterations=400, exact_cost=exact, exact_tolerance=1e-4)
+    a = bfm.Solver(mu, nu, cfg, exponents=(1.5,)).run()
+    b = ref.RefSolver(mu, nu, cfg, exponents=(1.5,)).run()
+    assert a.termination == b.termination == "cost_target_met"
+    assert a.iterations == b.iterations
+    assert abs(a.dual_value - exact) <= 1e-4
+    assert abs(a.dual_value - b.dual_value) <= 1e-9 * abs(b.dual_value)
+
+
+@pytest.mark.parametrize("exps", [(1.5, 2.5), (3.0, 1.25)])
+def test_power_solver_tracks_reference_2d(ref, exps):
+    shape = (32, 32)
+    mu, nu = synthetic.c1_like(shape)
+    cfg = bfm.SolverConfig(tolerance=-1.0, max_iterations=10)
+    a = bfm.Solver(mu, nu, cfg, exponents=exps)
+    b = ref.RefSolver(mu, nu, cfg, exponents=exps)
+    for k in range(10):
+        sa, sb = a.step(), b.step()
+        assert sa.sigma_first == sb.sigma_first and sa.sigma_second == sb.sigma_second, k
+        assert abs(sa.dual_value - sb.dual_value) <= 1e-9 * abs(sb.dual_value), k
+    for x, y in [(a.phi(), b.phi()), (a.psi(), b.psi())]:
+        assert np.abs(x - y).max() <= 1e-9 * np.abs(y).max()
+    ra, rb = a.run(), b.run()
+    assert np.abs(ra.map - rb.map).max() <= 1e-9
+    assert abs(ra.primal_cost - rb.primal_cost) <= 1e-9 * abs(rb.primal_cost)
+
+
+def test_acceptance_11_power_cost_moves_discs_vertically():
+    """acceptance_main.cpp:345-370 (criterion 11): p = (1.1, 3) on 256^2 two
+    disc pairs reaches the exact cost 1/24 within 1e-3 and the mean horizontal
+    displacement is <= 0.10 of the vertical (the reference run recorded
+    7.79e-08, test_output.txt)."""
+    g = (256, 256)
+    mu = bfm.normalize(bfm.builtin_density(g, "disc:0.25,0.25,0.125+disc:0.75,0.25,0.125"))
+    nu = bfm.normalize(bfm.builtin_density(g, "disc:0.25,0.75,0.125+disc:0.75,0.75,0.125"))
+    cfg = bfm.SolverConfig(tolerance=-1.0, max_iterations=300, exact_cost=1.0 / 24.0, exact_tolerance=1e-3)
+    rep = bfm.Solver(mu, nu, cfg, exponents=(1.1, 3.0)).run()
+    w = mu != 0
+    wh = float(np.sum(mu[w] * np.abs(rep.map[0][w])))
+    wv = float(np.sum(mu[w] * np.abs(rep.map[1][w])))
+    assert rep.termination == "cost_target_met"
+    assert wh / wv <= 0.10
