@@ -1851,6 +1851,10 @@ void CtPlan::setup(const GridDesc& loc, const GridDesc& global, int pb, int pe, 
       // two CTAs per SM: a CTA's loads overlap the other's hull work
       int lpc = std::min<long>(budget / (2 * o), kDyThreads / (2 * P.tpl));
       lpc = std::min(lpc, P.strided ? 16 : 8);
+      // tiny grids (C1, 256 lines per pass): one line per CTA spreads the
+      // latency-bound passes over the SMs (C1 c-transform 62.6 -> 55.5 us per
+      // call); at 1024 lines (C2) the packed CTAs were faster (119 vs 150 us)
+      if (P.nlines < 1024) lpc = static_cast<int>(std::min<long>(lpc, std::max<long>(1, P.nlines / (2 * 148))));
       lpc = static_cast<int>(std::min<long>(lpc, P.nlines));
       P.lpc = std::max(lpc, 1);
       P.slow_queries = slow_;
