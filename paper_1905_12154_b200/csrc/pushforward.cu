@@ -532,7 +532,9 @@ __global__ void __launch_bounds__(kMedWarps * 32) pf_gather_medium_kernel(Gather
 __global__ void __launch_bounds__(kLargeThreads) pf_gather_large_kernel(GatherArgs A,
                                                                        const int* large,
                                                                        int* nheavy,
-                                                                       double* hbuf) {
+                                                                       double* hbuf,
+                                                                       unsigned long long* hfill,
+                                                                       long long* lmeta) {
   // the target's buckets (source ids) are merged by a merge-path tree in
   // shared memory, as in the warp tier, with 16-bit (run << 12 | index)
   // payloads; the weights then go to the CTA's buffer slice in source order
@@ -544,7 +546,7 @@ __global__ void __launch_bounds__(kLargeThreads) pf_gather_large_kernel(GatherAr
   uint16_t* payA = reinterpret_cast<uint16_t*>(idsB + kLarge);
   uint16_t* payB = payA + kLarge;
   const int nl_total = nheavy[4];
-  double* buf = hbuf + static_cast<long>(blockIdx.x) * kLarge;
+  __shared__ unsigned long long s_base;
   for (;;) {  // targets claimed from a counter (nheavy[6], zeroed per call)
     if (threadIdx.x == 0) s_q = atomicAdd(nheavy + 6, 1);
     __syncthreads();
@@ -563,10 +565,14 @@ __global__ void __launch_bounds__(kLargeThreads) pf_gather_large_kernel(GatherAr
       }
       s_nl = tb.nl;
       s_K = tb.K;
+      // the target's slice of hbuf (shared counter with the heavy tier)
+      s_base = atomicAdd(hfill, static_cast<unsigned long long>(tb.K));
+      lmeta[q] = static_cast<long long>((s_base << 13) | static_cast<unsigned long long>(tb.K));
     }
     __syncthreads();
     const int nl = s_nl;
     const int K = s_K;
+    double* buf = hbuf + s_base;
     for (int qq = 0; qq < nl; ++qq) {
       const int o = tab[qq], len = tab[8 + qq], p0 = s_pos[qq];
       for (int i = threadIdx.x; i < len; i += blockDim.x) {
@@ -586,12 +592,27 @@ __global__ void __launch_bounds__(kLargeThreads) pf_gather_large_kernel(GatherAr
       buf[r] = pos_weight(A, s_pos[qq] + (pl & 4095), s_bits[qq]);
     }
     __syncthreads();
-    // warp 0 folds the weights in order (warp_seq_fold)
-    if (threadIdx.x < 32) {
-      const double rho = warp_seq_fold(buf, K);
-      if (threadIdx.x == 0) A.out[t] = A.target ? A.target[t] - rho : rho;
+    // the sequential fold runs in pf_fold_large_kernel (one warp per target,
+    // many targets in flight per SM) instead of one warp of this CTA
+  }
+}
+
+// Folds of the large tier's weight lists (written in source order by
+// pf_gather_large_kernel): one warp per target, bit for bit the reference's
+// sequential scatter sum (warp_seq_fold).
+__global__ void __launch_bounds__(256) pf_fold_large_kernel(GatherArgs A, const int* large, const int* nheavy,
+                                                          const double* hbuf, const long long* lmeta) {
+  const int nl_total = nheavy[4];
+  const int lane = threadIdx.x & 31;
+  const int nw = static_cast<int>((gridDim.x * blockDim.x) >> 5);
+  for (int q = static_cast<int>((blockIdx.x * blockDim.x + threadIdx.x) >> 5); q < nl_total; q += nw) {
+    const unsigned long long m = static_cast<unsigned long long>(lmeta[q]);
+    const int K = static_cast<int>(m & 8191ull);
+    const double rho = warp_seq_fold(hbuf + (m >> 13), K);
+    if (lane == 0) {
+      const long t = large[q];
+      A.out[t] = A.target ? A.target[t] - rho : rho;
     }
-    __syncthreads();
   }
 }
 
@@ -848,7 +869,8 @@ PushforwardPlan::~PushforwardPlan() {
                   static_cast<void*>(off_), static_cast<void*>(end_), static_cast<void*>(heavy_),
                   static_cast<void*>(nheavy_), static_cast<void*>(hbuf_),
                   static_cast<void*>(row0_), static_cast<void*>(bcount_),
-                  static_cast<void*>(large_), static_cast<void*>(rec_), static_cast<void*>(rmask_)})
+                  static_cast<void*>(large_), static_cast<void*>(rec_), static_cast<void*>(rmask_),
+                  static_cast<void*>(lmeta_)})
     if (p) dfree(p);
   if (hcounts_) cudaFreeHost(hcounts_);
 }
@@ -879,6 +901,8 @@ void PushforwardPlan::setup(const GridDesc& loc, const GridDesc& global, int row
   BFM_CUDA(dmalloc(&end_, (ncells_ + 1) * sizeof(int)));
   BFM_CUDA(dmalloc(&heavy_, (N + 1) * sizeof(int)));
   BFM_CUDA(dmalloc(&large_, (N + 1) * sizeof(int)));
+  // large-tier fold list: fewer than 2^d N / (kMedium + 1) targets
+  BFM_CUDA(dmalloc(&lmeta_, ((8 * N) / (kMedium + 1) + 2) * sizeof(long long)));
   // per-call counters, zeroed by gather(); as ints: [0] warp-tier targets,
   // [1] heavy targets, [2..3] heavy buffer fill (one u64), [4] CTA-tier
   // targets, [5] / [6] heavy / CTA-tier work claims, [7] unused
@@ -1019,11 +1043,14 @@ void PushforwardPlan::gather(long nrec, const uint32_t* d_keys, const double* d_
   else
     pf_gather_medium_kernel<3><<<med_blocks_, kMedWarps * 32, kMedSmem, stream>>>(G, heavy_, nheavy, hbuf_);
   BFM_LAUNCH_CHECK("pf_gather_medium_kernel");
-  pf_gather_large_kernel<<<large_blocks_, kLargeThreads, kLargeSmem, stream>>>(G, large_, nheavy, hbuf_);
+  pf_gather_large_kernel<<<large_blocks_, kLargeThreads, kLargeSmem, stream>>>(G, large_, nheavy, hbuf_,
+                                                                                nheavy_ + 1, lmeta_);
   BFM_LAUNCH_CHECK("pf_gather_large_kernel");
+  pf_fold_large_kernel<<<148 * 8, 256, 0, stream>>>(G, large_, nheavy, hbuf_, lmeta_);
+  BFM_LAUNCH_CHECK("pf_fold_large_kernel");
   pf_gather_heavy_kernel<<<2 * 148, 512, kHeavySmem, stream>>>(G, heavy_, nheavy, hbuf_, nheavy_ + 1);
   BFM_LAUNCH_CHECK("pf_gather_heavy_kernel");
-  if (lc) lc->add(nrec > 0 ? 6 : 4);
+  if (lc) lc->add(nrec > 0 ? 7 : 5);
 }
 
 void PushforwardPlan::set_partition(int P, const int* row_starts) {

@@ -98,6 +98,7 @@ class PushforwardPlan {
   int med_blocks_ = 1;       // medium-gather CTAs (each warp owns a kMedium slice of hbuf_)
   int large_blocks_ = 1;     // large-gather CTAs (each owns a kLarge slice of hbuf_)
   int* large_ = nullptr;     // [N] targets of the CTA-per-target tier
+  long long* lmeta_ = nullptr;  // per large target: hbuf offset << 13 | K
 };
 
 }  // namespace bfmgpu

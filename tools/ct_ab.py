@@ -19,4 +19,5 @@ ms = s.time_steps(steps)
 ops = s.op_times()
 print(f"{name} hull={os.environ.get('BFM_CT_HULL', '0')} B={os.environ.get('BFM_DC_B', '-')} "
       f"lpc={os.environ.get('BFM_DC_LPC', '-')}: {ms / steps:.3f} ms/iter; ctransform "
-      f"{ops['ctransform'][0] / ops['ctransform'][1]:.4f} ms/call; dual {s.dual_value()!r}", flush=True)
+      f"{ops['ctransform'][0] / ops['ctransform'][1]:.4f} ms/call; per iter "
+      + " ".join(f"{k} {v[0] / steps:.3f}" for k, v in ops.items()) + f"; dual {s.dual_value()!r}", flush=True)
