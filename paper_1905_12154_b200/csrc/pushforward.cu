@@ -111,6 +111,9 @@ __device__ __forceinline__ void locate(int n, double h, double x, int& lo, bool&
   whi = (x - clo) / (chi - clo);
 }
 
+// POWER: a power cost's pow inverse gradient (separate instantiation: the
+// pow code would double the quadratic map's registers, 32 -> 62)
+template <bool POWER>
 __global__ void pf_map_kernel(MapArgs A) {
   const GridDesc& g = A.g;
   const GridDesc& gg = A.gg;
@@ -135,7 +138,8 @@ __global__ void pf_map_kernel(MapArgs A) {
         else gr = (__ldg(A.u + su + st) - __ldg(A.u + su - st)) * inv_2h;
         // inverse gradient (cost.hpp:59-68): |v| (p = 2) or |v|^(1/(p-1)),
         // correctly rounded (pow_dd.h), capped at sqrt(d)
-        double mag = A.iexp[a] > 0.0 ? bfmpow::pow_cr(fabs(gr), A.iexp[a]) : fabs(gr);
+        double mag = fabs(gr);
+        if (POWER && A.iexp[a] > 0.0) mag = bfmpow::pow_cr(mag, A.iexp[a]);
         if (!(mag < A.diam)) mag = A.diam;
         const double v = gr < 0.0 ? -mag : mag;
         double t = x - v;
@@ -954,6 +958,12 @@ void PushforwardPlan::set_cost(const double* exponents) {
 }
 
 namespace {
+void launch_map(const MapArgs& A, cudaStream_t stream) {
+  const bool power = A.iexp[0] > 0.0 || A.iexp[1] > 0.0 || A.iexp[2] > 0.0;
+  if (power) pf_map_kernel<true><<<grid_for(A.g.size, 256), 256, 0, stream>>>(A);
+  else pf_map_kernel<false><<<grid_for(A.g.size, 256), 256, 0, stream>>>(A);
+}
+
 MapArgs map_args(const GridDesc& g, const GridDesc& gg, int row_off, long cell_shift, const double* iexp) {
   MapArgs A{};
   A.g = g;
@@ -972,7 +982,7 @@ void PushforwardPlan::map_only(const double* d_u, double* d_disp, cudaStream_t s
   MapArgs A = map_args(g_, gg_, row_off_, cell_shift_, iexp_);
   A.u = d_u;
   A.disp_out = d_disp;
-  pf_map_kernel<<<grid_for(g_.size, 256), 256, 0, stream>>>(A);
+  launch_map(A, stream);
   BFM_LAUNCH_CHECK("pf_map_kernel");
   if (lc) lc->add();
 }
@@ -988,7 +998,7 @@ void PushforwardPlan::map_records(const double* d_u_ext, const double* d_source,
   A.w = d_w;
   A.disp_out = d_disp_out;
   A.binning = 1;
-  pf_map_kernel<<<grid_for(g_.size, 256), 256, 0, stream>>>(A);
+  launch_map(A, stream);
   BFM_LAUNCH_CHECK("pf_map_kernel");
   if (lc) lc->add();
 }
@@ -1128,7 +1138,7 @@ void PushforwardPlan::from_displacement(const double* d_disp, double scale,
   A.cmask = cmask_;
   A.w = w_;
   A.binning = 1;
-  pf_map_kernel<<<grid_for(g_.size, 256), 256, 0, stream>>>(A);
+  launch_map(A, stream);
   BFM_LAUNCH_CHECK("pf_map_kernel");
   if (lc) lc->add();
   gather(g_.size, key_, d_source, w_, cmask_, nullptr, d_rho, stream, lc);

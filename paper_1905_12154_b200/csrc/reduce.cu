@@ -67,12 +67,13 @@ struct RedArgs {
 
 // One element's terms (mode 2: 0 for massless nodes, which the sums skip;
 // adding an exact 0 leaves a double-double unchanged).
+template <int MODE>
 __device__ __forceinline__ void red_terms(const RedArgs& A, long i, double& t1, double& t2) {
   t2 = 0.0;
-  if (A.mode == 0) {
+  if (MODE == 0) {
     t1 = A.a1[i] * A.b1[i];
     if (A.a2) t2 = A.a2[i] * A.b2[i];
-  } else if (A.mode == 1) {
+  } else if (MODE == 1) {
     t1 = A.a1[i];
   } else {
     const double m = A.b1[i];
@@ -103,6 +104,10 @@ __device__ double block_sum_plain(double v) {
 // (|t1_i| + |t2_i|) in plain fp64 (a nonnegative sum: relative error <= n*u),
 // from which the final kernel derives a rigorous bound on |our value - the
 // reference's sequential Kahan value| (see red_final_kernel).
+// One instantiation per mode (dot / sum / primal): the primal's pow path must
+// not inflate the registers of the bandwidth-bound dot (80 regs and spills
+// when they shared one kernel; red_partial 62 -> 165 us per C3 launch).
+template <int MODE>
 __global__ void __launch_bounds__(kRedThreads) red_partial_kernel(RedArgs A) {
   DD acc1{0.0, 0.0}, acc2{0.0, 0.0};
   double absum = 0.0;
@@ -113,7 +118,7 @@ __global__ void __launch_bounds__(kRedThreads) red_partial_kernel(RedArgs A) {
   for (; i + 3 * stride < A.n; i += 4 * stride) {
     double t1[4], t2[4];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) red_terms(A, i + u * stride, t1[u], t2[u]);
+    for (int u = 0; u < 4; ++u) red_terms<MODE>(A, i + u * stride, t1[u], t2[u]);
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
       dd_add(acc1, t1[u]);
@@ -123,7 +128,7 @@ __global__ void __launch_bounds__(kRedThreads) red_partial_kernel(RedArgs A) {
   }
   for (; i < A.n; i += stride) {
     double t1, t2;
-    red_terms(A, i, t1, t2);
+    red_terms<MODE>(A, i, t1, t2);
     dd_add(acc1, t1);
     dd_add(acc2, t2);
     absum += fabs(t1) + fabs(t2);
@@ -266,7 +271,7 @@ void Reducer::init() {
 void Reducer::dot(const double* a1, const double* b1, const double* a2, const double* b2, long n,
                   double vol, int slot, cudaStream_t s, LaunchCounter* lc) {
   RedArgs A{a1, b1, a2, b2, n, 0, 0, partials_};
-  red_partial_kernel<<<blocks_, kRedThreads, 0, s>>>(A);
+  red_partial_kernel<0><<<blocks_, kRedThreads, 0, s>>>(A);
   red_final_kernel<<<1, kRedThreads, 0, s>>>(partials_, blocks_, a2 ? 1 : 0, vol, results_, slot);
   BFM_LAUNCH_CHECK("reduce dot");
   if (lc) lc->add(2);
@@ -275,7 +280,7 @@ void Reducer::dot(const double* a1, const double* b1, const double* a2, const do
 void Reducer::dot_raw(const double* a1, const double* b1, const double* a2, const double* b2,
                       long n, int slot, cudaStream_t s, LaunchCounter* lc) {
   RedArgs A{a1, b1, a2, b2, n, 0, 0, partials_};
-  red_partial_kernel<<<blocks_, kRedThreads, 0, s>>>(A);
+  red_partial_kernel<0><<<blocks_, kRedThreads, 0, s>>>(A);
   red_final_kernel<<<1, kRedThreads, 0, s>>>(partials_, blocks_, -1, 1.0, results_, slot);
   BFM_LAUNCH_CHECK("reduce dot_raw");
   if (lc) lc->add(2);
@@ -284,7 +289,7 @@ void Reducer::dot_raw(const double* a1, const double* b1, const double* a2, cons
 void Reducer::primal_raw(const double* disp, const double* mu, int d, long n, int slot,
                          cudaStream_t s, LaunchCounter* lc) {
   RedArgs A{disp, mu, nullptr, nullptr, n, 2, d, partials_};
-  red_partial_kernel<<<blocks_, kRedThreads, 0, s>>>(A);
+  red_partial_kernel<2><<<blocks_, kRedThreads, 0, s>>>(A);
   red_final_kernel<<<1, kRedThreads, 0, s>>>(partials_, blocks_, -1, 1.0, results_, slot);
   BFM_LAUNCH_CHECK("reduce primal_raw");
   if (lc) lc->add(2);
@@ -293,7 +298,7 @@ void Reducer::primal_raw(const double* disp, const double* mu, int d, long n, in
 void Reducer::sum(const double* a, long n, double vol, int slot, cudaStream_t s,
                   LaunchCounter* lc) {
   RedArgs A{a, nullptr, nullptr, nullptr, n, 1, 0, partials_};
-  red_partial_kernel<<<blocks_, kRedThreads, 0, s>>>(A);
+  red_partial_kernel<1><<<blocks_, kRedThreads, 0, s>>>(A);
   red_final_kernel<<<1, kRedThreads, 0, s>>>(partials_, blocks_, 0, vol, results_, slot);
   BFM_LAUNCH_CHECK("reduce sum");
   if (lc) lc->add(2);
@@ -303,7 +308,7 @@ void Reducer::primal(const double* disp, const double* mu, int d, long n, double
                      cudaStream_t s, LaunchCounter* lc, const double* exponents) {
   RedArgs A{disp, mu, nullptr, nullptr, n, 2, d, partials_, {0.0, 0.0, 0.0}};
   for (int a = 0; a < d && exponents; ++a) A.pexp[a] = exponents[a] == 2.0 ? 0.0 : exponents[a];
-  red_partial_kernel<<<blocks_, kRedThreads, 0, s>>>(A);
+  red_partial_kernel<2><<<blocks_, kRedThreads, 0, s>>>(A);
   red_final_kernel<<<1, kRedThreads, 0, s>>>(partials_, blocks_, 0, vol, results_, slot);
   BFM_LAUNCH_CHECK("reduce primal");
   if (lc) lc->add(2);
