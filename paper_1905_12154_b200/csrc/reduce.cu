@@ -15,7 +15,14 @@ namespace bfmgpu {
 namespace {
 
 constexpr int kRedThreads = 256;
-constexpr int kRedBlocks = 148 * 4;
+#ifndef BFM_RED_BLOCKS_PER_SM
+#define BFM_RED_BLOCKS_PER_SM 4
+#endif
+#ifndef BFM_RED_UNROLL
+#define BFM_RED_UNROLL 8
+#endif
+constexpr int kRedBlocks = 148 * BFM_RED_BLOCKS_PER_SM;
+constexpr int kRedUnroll = BFM_RED_UNROLL;
 
 struct DD {
   double s, c;
@@ -113,14 +120,15 @@ __global__ void __launch_bounds__(kRedThreads) red_partial_kernel(RedArgs A) {
   double absum = 0.0;
   const long stride = static_cast<long>(gridDim.x) * kRedThreads;
   long i = blockIdx.x * static_cast<long>(kRedThreads) + threadIdx.x;
-  // four elements per round: their loads are in flight together (one load
-  // per round left ~8 KB in flight per SM, ~2 TB/s); fixed per-thread order
-  for (; i + 3 * stride < A.n; i += 4 * stride) {
-    double t1[4], t2[4];
+  // kRedUnroll elements per round, their loads in flight together (one per
+  // round: ~2 TB/s; 4: C3 0.79 ms of reductions per iteration; 8: 0.74 ms,
+  // C4 2.19 -> 1.99 ms); fixed per-thread order
+  for (; i + (kRedUnroll - 1) * stride < A.n; i += kRedUnroll * stride) {
+    double t1[kRedUnroll], t2[kRedUnroll];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) red_terms<MODE>(A, i + u * stride, t1[u], t2[u]);
+    for (int u = 0; u < kRedUnroll; ++u) red_terms<MODE>(A, i + u * stride, t1[u], t2[u]);
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
+    for (int u = 0; u < kRedUnroll; ++u) {
       dd_add(acc1, t1[u]);
       dd_add(acc2, t2[u]);
       absum += fabs(t1[u]) + fabs(t2[u]);
