@@ -1850,6 +1850,13 @@ void CtPlan::setup(const GridDesc& loc, const GridDesc& global, int pb, int pe, 
       if (o > budget) throw std::invalid_argument("ctransform: grid line too long for shared memory");
       // two CTAs per SM: a CTA's loads overlap the other's hull work
       int lpc = std::min<long>(budget / (2 * o), kDyThreads / (2 * P.tpl));
+      // strided passes: two adjacent columns per CTA (one CTA per SM) rather
+      // than two one-column CTAs — the column pair shares every 32-byte
+      // sector of its loads and stores (C3 c-transform 1.774 -> 1.697 ms per
+      // call; the contiguous passes are better at one line per CTA)
+      if (P.strided && budget / o >= 2) lpc = std::max(lpc, std::min(2, kDyThreads / P.tpl));
+      if (const char* e = getenv(P.strided ? "BFM_DY_LPC_S" : "BFM_DY_LPC_C"))  // tuning experiments
+        lpc = std::max(1, std::min<int>(std::min<long>(atoi(e), budget / o), kDyThreads / P.tpl));
       lpc = std::min(lpc, P.strided ? 16 : 8);
       // tiny grids (C1, 256 lines per pass): one line per CTA spreads the
       // latency-bound passes over the SMs (C1 c-transform 62.6 -> 55.5 us per
