@@ -334,6 +334,53 @@ __device__ __forceinline__ void target_buckets(const GatherArgs& A, long t, Targ
   }
 }
 
+// target_buckets with the 2^d bucket-bound loads issued by the lanes of one
+// warp in parallel (lane b: corner b), compacted in corner order by ballot.
+// Call from all 32 lanes; every lane returns the same nl, K and, for
+// slot < nl, pos/len/bits of the slot-th non-empty bucket in lane `slot`.
+struct LaneBucket {
+  int nl, K, pos, len, bits;
+};
+__device__ __forceinline__ LaneBucket target_buckets_warp(const GatherArgs& A, long t) {
+  const GridDesc& g = A.g;
+  const int lane = threadIdx.x & 31;
+  int id[3] = {0, 0, 0};
+  node_idx(g, t, id);
+  id[0] += A.row_off;
+  int pos = 0, len = 0;
+  bool ok = lane < (1 << g.d);
+  if (ok) {
+    long c = t + A.cell_shift;
+    for (int a = 0; a < g.d; ++a)
+      if ((lane >> a) & 1) {
+        if (id[a] == 0) ok = false;
+        c -= g.stride[a];
+      }
+    if (ok) {
+      pos = A.off[c];
+      len = A.end[c] - pos;
+      ok = len > 0;
+    }
+  }
+  const unsigned m = __ballot_sync(0xffffffffu, ok);
+  LaneBucket r;
+  r.nl = __popc(m);
+  int K = ok ? len : 0;
+  for (int o = 16; o > 0; o >>= 1) K += __shfl_xor_sync(0xffffffffu, K, o);
+  r.K = K;
+  // the slot-th set bit of m, for slot = lane
+  int src = 0;
+  {
+    unsigned mm = m;
+    for (int i = 0; i < lane && mm; ++i) mm &= mm - 1;
+    src = mm ? __ffs(mm) - 1 : 0;
+  }
+  r.pos = __shfl_sync(0xffffffffu, pos, src);
+  r.len = __shfl_sync(0xffffffffu, len, src);
+  r.bits = src;
+  return r;
+}
+
 __device__ __forceinline__ int lower_bound_ids(const int* v, int len, int key) {
   int lo = 0, hi = len;
   while (lo < hi) {
@@ -557,21 +604,27 @@ __global__ void __launch_bounds__(kLargeThreads) pf_gather_large_kernel(GatherAr
     const int q = s_q;
     if (q >= nl_total) break;
     const long t = large[q];
-    if (threadIdx.x == 0) {
-      TargetBuckets tb;
-      target_buckets(A, t, tb);
-      for (int qq = 0, o = 0; qq < tb.nl; ++qq) {
-        tab[qq] = o;
-        tab[8 + qq] = tb.end[qq] - tb.pos[qq];
-        s_pos[qq] = tb.pos[qq];
-        s_bits[qq] = tb.bits[qq];
-        o += tb.end[qq] - tb.pos[qq];
+    if (threadIdx.x < 32) {  // bucket bounds: one lane per corner, loads in parallel
+      const LaneBucket lb = target_buckets_warp(A, t);
+      int start = lb.len;  // exclusive prefix of the slot lengths (slots < nl)
+      if (threadIdx.x >= lb.nl) start = 0;
+      for (int o = 1; o < 32; o <<= 1) {
+        const int v = __shfl_up_sync(0xffffffffu, start, o);
+        if (static_cast<int>(threadIdx.x) >= o) start += v;
       }
-      s_nl = tb.nl;
-      s_K = tb.K;
-      // the target's slice of hbuf (shared counter with the heavy tier)
-      s_base = atomicAdd(hfill, static_cast<unsigned long long>(tb.K));
-      lmeta[q] = static_cast<long long>((s_base << 13) | static_cast<unsigned long long>(tb.K));
+      if (static_cast<int>(threadIdx.x) < lb.nl) {
+        tab[threadIdx.x] = start - lb.len;
+        tab[8 + threadIdx.x] = lb.len;
+        s_pos[threadIdx.x] = lb.pos;
+        s_bits[threadIdx.x] = lb.bits;
+      }
+      if (threadIdx.x == 0) {
+        s_nl = lb.nl;
+        s_K = lb.K;
+        // the target's slice of hbuf (shared counter with the heavy tier)
+        s_base = atomicAdd(hfill, static_cast<unsigned long long>(lb.K));
+        lmeta[q] = static_cast<long long>((s_base << 13) | static_cast<unsigned long long>(lb.K));
+      }
     }
     __syncthreads();
     const int nl = s_nl;
