@@ -36,6 +36,8 @@ constexpr int kLarge = 4096;   // CTA-per-target tier with a sequential fold: K 
 constexpr int kLargeThreads = 128;
 constexpr int kLargeBlocks = 148 * 8;  // each CTA owns kLarge doubles of hbuf
 constexpr int kLargeSmem = kLarge * 2 * (4 + 2);  // ids + payloads, ping-pong
+constexpr int kLargeA = 2048;                      // the smaller CTA-tier instantiation
+constexpr int kLargeSmemA = kLargeA * 2 * (4 + 2);
 constexpr int kMedWarps = 8;
 constexpr int kHeavyIds = 24576;
 constexpr int kMedSmem = kMedWarps * 2 * kMedium * (4 + 2);  // ids + payloads, ping-pong
@@ -272,7 +274,8 @@ __global__ void __launch_bounds__(256, D < 3 ? 8 : 6) pf_gather_kernel(GatherArg
     }
     if (total > kLight) {
       if (total <= kMedium) heavy[atomicAdd(nheavy, 1)] = static_cast<int>(t);
-      else if (total <= kLarge) large[atomicAdd(nheavy + 4, 1)] = static_cast<int>(t);
+      else if (total <= kLargeA) large[atomicAdd(nheavy + 4, 1)] = static_cast<int>(t);
+      else if (total <= kLarge) large[g.size - 1 - atomicAdd(nheavy + 7, 1)] = static_cast<int>(t);
       else heavy[g.size - 1 - atomicAdd(nheavy + 1, 1)] = static_cast<int>(t);  // huge: from the top
       continue;
     }
@@ -580,12 +583,17 @@ __global__ void __launch_bounds__(kMedWarps * 32) pf_gather_medium_kernel(Gather
 // staged in shared memory, ranks and weights as above into the CTA's slice of
 // the global buffer, then one thread folds them in order (unrolled loads
 // ahead of the chain of adds).
+// Two instantiations: LK = 2048 (24 KB of shared memory, twice the CTAs per
+// SM) for kMedium < K <= 2048 and LK = kLarge for 2048 < K <= kLarge; the
+// second list is stored from the back of `large` / `lmeta` (list = 1).
+template <int LK>
 __global__ void __launch_bounds__(kLargeThreads) pf_gather_large_kernel(GatherArgs A,
                                                                        const int* large,
                                                                        int* nheavy,
                                                                        double* hbuf,
                                                                        unsigned long long* hfill,
-                                                                       long long* lmeta) {
+                                                                       long long* lmeta, long lcap,
+                                                                       int list) {
   // the target's buckets (source ids) are merged by a merge-path tree in
   // shared memory, as in the warp tier, with 16-bit (run << 12 | index)
   // payloads; the weights then go to the CTA's buffer slice in source order
@@ -593,17 +601,18 @@ __global__ void __launch_bounds__(kLargeThreads) pf_gather_large_kernel(GatherAr
   __shared__ int tab[24];  // run starts, run lengths (merge tree)
   __shared__ int s_pos[8], s_bits[8], s_nl, s_K, s_q;
   int* idsA = reinterpret_cast<int*>(large_smem);
-  int* idsB = idsA + kLarge;
-  uint16_t* payA = reinterpret_cast<uint16_t*>(idsB + kLarge);
-  uint16_t* payB = payA + kLarge;
-  const int nl_total = nheavy[4];
+  int* idsB = idsA + LK;
+  uint16_t* payA = reinterpret_cast<uint16_t*>(idsB + LK);
+  uint16_t* payB = payA + LK;
+  const int nl_total = nheavy[list ? 7 : 4];
   __shared__ unsigned long long s_base;
-  for (;;) {  // targets claimed from a counter (nheavy[6], zeroed per call)
-    if (threadIdx.x == 0) s_q = atomicAdd(nheavy + 6, 1);
+  for (;;) {  // targets claimed from a counter (nheavy[6] / [8], zeroed per call)
+    if (threadIdx.x == 0) s_q = atomicAdd(nheavy + (list ? 8 : 6), 1);
     __syncthreads();
     const int q = s_q;
     if (q >= nl_total) break;
-    const long t = large[q];
+    const long t = list ? large[A.g.size - 1 - q] : large[q];
+    const long mq = list ? lcap - 1 - q : q;
     if (threadIdx.x < 32) {  // bucket bounds: one lane per corner, loads in parallel
       const LaneBucket lb = target_buckets_warp(A, t);
       int start = lb.len;  // exclusive prefix of the slot lengths (slots < nl)
@@ -623,7 +632,7 @@ __global__ void __launch_bounds__(kLargeThreads) pf_gather_large_kernel(GatherAr
         s_K = lb.K;
         // the target's slice of hbuf (shared counter with the heavy tier)
         s_base = atomicAdd(hfill, static_cast<unsigned long long>(lb.K));
-        lmeta[q] = static_cast<long long>((s_base << 13) | static_cast<unsigned long long>(lb.K));
+        lmeta[mq] = static_cast<long long>((s_base << 13) | static_cast<unsigned long long>(lb.K));
       }
     }
     __syncthreads();
@@ -658,16 +667,17 @@ __global__ void __launch_bounds__(kLargeThreads) pf_gather_large_kernel(GatherAr
 // pf_gather_large_kernel): one warp per target, bit for bit the reference's
 // sequential scatter sum (warp_seq_fold).
 __global__ void __launch_bounds__(256) pf_fold_large_kernel(GatherArgs A, const int* large, const int* nheavy,
-                                                          const double* hbuf, const long long* lmeta) {
-  const int nl_total = nheavy[4];
+                                                          const double* hbuf, const long long* lmeta, long lcap) {
+  const int na = nheavy[4], nb = nheavy[7];
   const int lane = threadIdx.x & 31;
   const int nw = static_cast<int>((gridDim.x * blockDim.x) >> 5);
-  for (int q = static_cast<int>((blockIdx.x * blockDim.x + threadIdx.x) >> 5); q < nl_total; q += nw) {
-    const unsigned long long m = static_cast<unsigned long long>(lmeta[q]);
+  for (int q = static_cast<int>((blockIdx.x * blockDim.x + threadIdx.x) >> 5); q < na + nb; q += nw) {
+    const bool b = q >= na;
+    const unsigned long long m = static_cast<unsigned long long>(lmeta[b ? lcap - 1 - (q - na) : q]);
     const int K = static_cast<int>(m & 8191ull);
     const double rho = warp_seq_fold(hbuf + (m >> 13), K);
     if (lane == 0) {
-      const long t = large[q];
+      const long t = b ? large[A.g.size - 1 - (q - na)] : large[q];
       A.out[t] = A.target ? A.target[t] - rho : rho;
     }
   }
@@ -959,14 +969,17 @@ void PushforwardPlan::setup(const GridDesc& loc, const GridDesc& global, int row
   BFM_CUDA(dmalloc(&heavy_, (N + 1) * sizeof(int)));
   BFM_CUDA(dmalloc(&large_, (N + 1) * sizeof(int)));
   // large-tier fold list: fewer than 2^d N / (kMedium + 1) targets
-  BFM_CUDA(dmalloc(&lmeta_, ((8 * N) / (kMedium + 1) + 2) * sizeof(long long)));
+  lmeta_cap_ = (8 * N) / (kMedium + 1) + 2;
+  BFM_CUDA(dmalloc(&lmeta_, lmeta_cap_ * sizeof(long long)));
   // per-call counters, zeroed by gather(); as ints: [0] warp-tier targets,
   // [1] heavy targets, [2..3] heavy buffer fill (one u64), [4] CTA-tier
   // targets, [5] / [6] heavy / CTA-tier work claims, [7] unused
-  BFM_CUDA(dmalloc(&nheavy_, 4 * sizeof(unsigned long long)));
+  BFM_CUDA(dmalloc(&nheavy_, 6 * sizeof(unsigned long long)));
   ensure_records(N);
-  BFM_CUDA(cudaFuncSetAttribute(pf_gather_large_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  BFM_CUDA(cudaFuncSetAttribute(pf_gather_large_kernel<kLarge>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 kLargeSmem));
+  BFM_CUDA(cudaFuncSetAttribute(pf_gather_large_kernel<kLargeA>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                kLargeSmemA));
   BFM_CUDA(cudaFuncSetAttribute(pf_gather_heavy_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 kHeavySmem));
   BFM_CUDA(cudaFuncSetAttribute(pf_gather_medium_kernel<1>,
@@ -1063,7 +1076,7 @@ void PushforwardPlan::gather(long nrec, const uint32_t* d_keys, const double* d_
   const long N = g_.size;
   BFM_CUDA(cudaMemsetAsync(off_, 0, (ncells_ + 1) * sizeof(int), stream));
   BFM_CUDA(cudaMemsetAsync(end_, 0, (ncells_ + 1) * sizeof(int), stream));
-  BFM_CUDA(cudaMemsetAsync(nheavy_, 0, 4 * sizeof(unsigned long long), stream));
+  BFM_CUDA(cudaMemsetAsync(nheavy_, 0, 6 * sizeof(unsigned long long), stream));
   const int* svals = nullptr;
   if (nrec > 0) {
     const uint32_t* skeys = nullptr;
@@ -1106,14 +1119,18 @@ void PushforwardPlan::gather(long nrec, const uint32_t* d_keys, const double* d_
   else
     pf_gather_medium_kernel<3><<<med_blocks_, kMedWarps * 32, kMedSmem, stream>>>(G, heavy_, nheavy, hbuf_);
   BFM_LAUNCH_CHECK("pf_gather_medium_kernel");
-  pf_gather_large_kernel<<<large_blocks_, kLargeThreads, kLargeSmem, stream>>>(G, large_, nheavy, hbuf_,
-                                                                                nheavy_ + 1, lmeta_);
-  BFM_LAUNCH_CHECK("pf_gather_large_kernel");
-  pf_fold_large_kernel<<<148 * 8, 256, 0, stream>>>(G, large_, nheavy, hbuf_, lmeta_);
+  const long lcap = lmeta_cap_;
+  pf_gather_large_kernel<kLargeA><<<2 * large_blocks_, kLargeThreads, kLargeSmemA, stream>>>(
+      G, large_, nheavy, hbuf_, nheavy_ + 1, lmeta_, lcap, 0);
+  BFM_LAUNCH_CHECK("pf_gather_large_kernel<2048>");
+  pf_gather_large_kernel<kLarge><<<large_blocks_, kLargeThreads, kLargeSmem, stream>>>(
+      G, large_, nheavy, hbuf_, nheavy_ + 1, lmeta_, lcap, 1);
+  BFM_LAUNCH_CHECK("pf_gather_large_kernel<4096>");
+  pf_fold_large_kernel<<<148 * 8, 256, 0, stream>>>(G, large_, nheavy, hbuf_, lmeta_, lcap);
   BFM_LAUNCH_CHECK("pf_fold_large_kernel");
   pf_gather_heavy_kernel<<<2 * 148, 512, kHeavySmem, stream>>>(G, heavy_, nheavy, hbuf_, nheavy_ + 1);
   BFM_LAUNCH_CHECK("pf_gather_heavy_kernel");
-  if (lc) lc->add(nrec > 0 ? 7 : 5);
+  if (lc) lc->add(nrec > 0 ? 8 : 6);
 }
 
 void PushforwardPlan::set_partition(int P, const int* row_starts) {

@@ -99,6 +99,7 @@ class PushforwardPlan {
   int large_blocks_ = 1;     // large-gather CTAs (each owns a kLarge slice of hbuf_)
   int* large_ = nullptr;     // [N] targets of the CTA-per-target tier
   long long* lmeta_ = nullptr;  // per large target: hbuf offset << 13 | K
+  long lmeta_cap_ = 0;
 };
 
 }  // namespace bfmgpu
