@@ -669,17 +669,42 @@ __global__ void __launch_bounds__(kLargeThreads) pf_gather_large_kernel(GatherAr
 __global__ void __launch_bounds__(256) pf_fold_large_kernel(GatherArgs A, const int* large, const int* nheavy,
                                                           const double* hbuf, const long long* lmeta, long lcap) {
   const int na = nheavy[4], nb = nheavy[7];
-  const int lane = threadIdx.x & 31;
-  const int nw = static_cast<int>((gridDim.x * blockDim.x) >> 5);
-  for (int q = static_cast<int>((blockIdx.x * blockDim.x + threadIdx.x) >> 5); q < na + nb; q += nw) {
+  const int nt = static_cast<int>(gridDim.x * blockDim.x);
+  if (na + nb < nt) {
+    // few targets (C3): one warp per target, coalesced loads a round ahead of
+    // the chain (a lone thread would wait on every sector)
+    const int lane = threadIdx.x & 31;
+    const int nw = nt >> 5;
+    for (int q = static_cast<int>((blockIdx.x * blockDim.x + threadIdx.x) >> 5); q < na + nb; q += nw) {
+      const bool b = q >= na;
+      const unsigned long long m = static_cast<unsigned long long>(lmeta[b ? lcap - 1 - (q - na) : q]);
+      const double rho = warp_seq_fold(hbuf + (m >> 13), static_cast<int>(m & 8191ull));
+      if (lane == 0) {
+        const long t = b ? large[A.g.size - 1 - (q - na)] : large[q];
+        A.out[t] = A.target ? A.target[t] - rho : rho;
+      }
+    }
+    return;
+  }
+  // many targets (C4: ~10^5 per call): one target per THREAD, 32 independent
+  // add chains per warp (the chains, not the loads, bound the warp version)
+  for (int q = static_cast<int>(blockIdx.x * blockDim.x + threadIdx.x); q < na + nb; q += nt) {
     const bool b = q >= na;
     const unsigned long long m = static_cast<unsigned long long>(lmeta[b ? lcap - 1 - (q - na) : q]);
     const int K = static_cast<int>(m & 8191ull);
-    const double rho = warp_seq_fold(hbuf + (m >> 13), K);
-    if (lane == 0) {
-      const long t = b ? large[A.g.size - 1 - (q - na)] : large[q];
-      A.out[t] = A.target ? A.target[t] - rho : rho;
+    const double* w = hbuf + (m >> 13);
+    double rho = 0.0;
+    int i = 0;
+    for (; i + 8 <= K; i += 8) {
+      double v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = w[i + u];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) rho += v[u];
     }
+    for (; i < K; ++i) rho += w[i];
+    const long t = b ? large[A.g.size - 1 - (q - na)] : large[q];
+    A.out[t] = A.target ? A.target[t] - rho : rho;
   }
 }
 
@@ -1126,7 +1151,7 @@ void PushforwardPlan::gather(long nrec, const uint32_t* d_keys, const double* d_
   pf_gather_large_kernel<kLarge><<<large_blocks_, kLargeThreads, kLargeSmem, stream>>>(
       G, large_, nheavy, hbuf_, nheavy_ + 1, lmeta_, lcap, 1);
   BFM_LAUNCH_CHECK("pf_gather_large_kernel<4096>");
-  pf_fold_large_kernel<<<148 * 8, 256, 0, stream>>>(G, large_, nheavy, hbuf_, lmeta_, lcap);
+  pf_fold_large_kernel<<<148 * 4, 128, 0, stream>>>(G, large_, nheavy, hbuf_, lmeta_, lcap);
   BFM_LAUNCH_CHECK("pf_fold_large_kernel");
   pf_gather_heavy_kernel<<<2 * 148, 512, kHeavySmem, stream>>>(G, heavy_, nheavy, hbuf_, nheavy_ + 1);
   BFM_LAUNCH_CHECK("pf_gather_heavy_kernel");
