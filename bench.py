@@ -121,6 +121,21 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.samples)}
 
 
+def quiet_stdout(fn):
+    """Runs fn with file descriptor 1 pointed at stderr (native libraries that
+    print banners at initialisation would otherwise break the one-JSON-line
+    stdout contract)."""
+    sys.stdout.flush()
+    saved = os.dup(1)
+    os.dup2(2, 1)
+    try:
+        return fn()
+    finally:
+        sys.stdout.flush()
+        os.dup2(saved, 1)
+        os.close(saved)
+
+
 def dist_env():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -445,10 +460,14 @@ def ours_dist(args):
     torch.cuda.set_device(local)
     bfm.set_device(local)
     dev = torch.device("cuda", local)
-    tdist.init_process_group("nccl", device_id=dev)
-    obj = [DC.nccl_unique_id() if rank == 0 else None]
-    tdist.broadcast_object_list(obj, src=0)
-    comm = DC.nccl_comm(obj[0], rank, world)
+
+    def setup():
+        tdist.init_process_group("nccl", device_id=dev)
+        obj = [DC.nccl_unique_id() if rank == 0 else None]
+        tdist.broadcast_object_list(obj, src=0)
+        return DC.nccl_comm(obj[0], rank, world)
+
+    comm = quiet_stdout(setup)  # NCCL's init banner must not precede the JSON line
     mu, nu, desc = workload(args.config)
     N = mu.size
     starts, sizes = DC.split_rows(mu.shape[0], world)
