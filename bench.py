@@ -553,7 +553,7 @@ def ours_dist_python(args):
     torch.cuda.set_device(local)
     bfm.set_device(local)
     dev = torch.device("cuda", local)
-    tdist.init_process_group("nccl", device_id=dev)
+    quiet_stdout(lambda: (tdist.init_process_group("nccl", device_id=dev), tdist.barrier()))
     comm = D.TorchComm()
     mu, nu, desc = workload(args.config)
     N = mu.size
@@ -721,8 +721,8 @@ def ours(args):
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-        dist.barrier()
+        quiet_stdout(lambda: (dist.init_process_group("nccl", device_id=torch.device("cuda", local)),
+                              dist.barrier()))
     m = measure(args.config, args.steps, args.warmup, local)
     t = torch.tensor([m["ms"]], dtype=torch.float64, device="cuda")
     if dist:
