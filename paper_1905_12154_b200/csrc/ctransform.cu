@@ -325,7 +325,7 @@ __device__ __forceinline__ void slack_max(uint8_t* dlt, int e, uint8_t c) {
 
 // Threads per CTA (lpc * tpl) at most for the non-dyadic kernel (its exact
 // path lives in local memory anyway; 1024 measured fastest).
-constexpr int kNdThreads = 1024;
+constexpr int kNdThreads = 768;
 
 __global__ void __launch_bounds__(kNdThreads) ct_pass_kernel(CtPass p) {
   extern __shared__ __align__(16) unsigned char smem[];
