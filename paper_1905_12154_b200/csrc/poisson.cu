@@ -8,6 +8,7 @@
 // in shared memory, and runs the shared line algorithm of dct_line.h with the
 // butterflies of a stage spread over the line's threads. Every value goes
 // through the same IEEE operations as the CPU shim (bitwise-equal results).
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -464,6 +465,11 @@ void PoissonPlan::setup(const GridDesc& loc, const GridDesc& global, long col0, 
     // 7.8; 4: 9.7)
     lpc = std::min(lpc, c.strided ? 8 : std::max(4, 128 / c.tpl));
     if (c.tpl > 32) lpc = std::min(lpc, 15);
+    // long contiguous lines (C3: 64 KB each): one line per CTA, three CTAs
+    // per SM that drift out of phase (C3 Poisson 2.20 -> 2.09 ms per iteration)
+    if (!c.strided && c.line_bytes >= 32768) lpc = 1;
+    if (const char* e = getenv(c.strided ? "BFM_POIS_LPC_S" : "BFM_POIS_LPC_C"))  // tuning experiments
+      lpc = std::max(1, std::min(atoi(e), std::min(budget / c.line_bytes, 512 / c.tpl)));
     lpc = static_cast<int>(std::min<long>(lpc, c.nlines));
     c.lpc = std::max(1, lpc);
   }
