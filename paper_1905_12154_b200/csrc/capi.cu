@@ -166,7 +166,7 @@ struct DevBuf {
   }
 };
 
-enum { kSlotPair = 0, kSlotGn = 1, kSlotShift = 2, kSlotPrimal = 3 };
+enum { kSlotPair = 0, kSlotGn = 1, kSlotShift = 2, kSlotPrimal = 3, kSlotGn2 = 4 };
 
 bool is_pinned(const void* p) {
   cudaPointerAttributes a;
@@ -355,6 +355,14 @@ struct bfm_solver {
   DevBuf mu, nu, phi, psi, dir, dir2, r;
   DevBuf rep_phi, rep_psi, rep_map;
   double sigma0 = 0.0;
+  // Side stream: the pair-value reductions and every decision kernel run on
+  // it, overlapping the bandwidth-bound reductions with the issue-bound
+  // c-transform / pushforward kernels of the main stream (events order the
+  // hazards; see enqueue_step). Its reductions use their own Reducer.
+  cudaStream_t side = nullptr;
+  Reducer side_red;
+  cudaEvent_t xev[16] = {};
+  int xev_i = 0;
   // separable power cost (cost.hpp:17-81): exponents per axis, the exact
   // c-transform on dense axis-cost tables and the pow inverse-gradient map
   bool power = false;
@@ -417,7 +425,7 @@ struct bfm_solver {
     return op >= 0 && op < BFM_OP_COUNT ? names[op] : "bfm.op";
   }
   template <class F>
-  void timed(int op, F&& f) {
+  void timed(int op, F&& f, cudaStream_t on = nullptr) {
     nvtxRangePushA(op_name(op));
     struct Pop {
       ~Pop() { nvtxRangePop(); }
@@ -426,18 +434,39 @@ struct bfm_solver {
       f();
       return;
     }
+    const cudaStream_t st = on ? on : stream;
     cudaEvent_t a = take_event(), b = take_event();
     if (capture_ev) {
-      BFM_CUDA(cudaEventRecordWithFlags(a, stream, cudaEventRecordExternal));
+      BFM_CUDA(cudaEventRecordWithFlags(a, st, cudaEventRecordExternal));
       f();
-      BFM_CUDA(cudaEventRecordWithFlags(b, stream, cudaEventRecordExternal));
+      BFM_CUDA(cudaEventRecordWithFlags(b, st, cudaEventRecordExternal));
       capture_ev->push_back({a, b, op});
       return;
     }
-    BFM_CUDA(cudaEventRecord(a, stream));
+    BFM_CUDA(cudaEventRecord(a, st));
     f();
-    BFM_CUDA(cudaEventRecord(b, stream));
+    BFM_CUDA(cudaEventRecord(b, st));
     pending.push_back({a, b, op});
+  }
+  // cross-stream ordering (dependency edges inside a captured graph)
+  cudaEvent_t next_xev() {
+    cudaEvent_t& e = xev[xev_i++ & 15];
+    if (!e) BFM_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    return e;
+  }
+  cudaEvent_t mark(cudaStream_t st) {
+    const cudaEvent_t e = next_xev();
+    BFM_CUDA(cudaEventRecord(e, st));
+    return e;
+  }
+  // With per-operator timing on, the side work runs on the main stream
+  // (serialised: each operator's events then time that operator alone).
+  cudaStream_t sd() const { return timing ? stream : side; }
+  void side_after_main() {
+    if (!timing) BFM_CUDA(cudaStreamWaitEvent(side, mark(stream), 0));
+  }
+  void main_after_side() {
+    if (!timing) BFM_CUDA(cudaStreamWaitEvent(stream, mark(side), 0));
   }
   void add_time(const Pending& q) {
     BFM_CUDA(cudaEventSynchronize(q.b));
@@ -459,6 +488,9 @@ struct bfm_solver {
   }
 
   ~bfm_solver() {
+    for (cudaEvent_t e : xev)
+      if (e) cudaEventDestroy(e);
+    if (side) cudaStreamDestroy(side);
     for (const Pending& q : pending) {
       cudaEventDestroy(q.a);
       cudaEventDestroy(q.b);
@@ -491,73 +523,105 @@ struct bfm_solver {
     BFM_CUDA(cudaMemcpyAsync(d_ctl, h_ctl, sizeof(SolverCtl), cudaMemcpyHostToDevice, stream));
     BFM_CUDA(cudaStreamSynchronize(stream));
   }
+  // decisions run on the side stream in program order (they share ctl);
+  // pair values come from the side Reducer, gn values from the main one
   void decide(int stage, int slot) {
+    const double* res = (slot == kSlotGn || slot == kSlotGn2) ? ws.redp().device_results()
+                                                              : side_red.device_results();
     timed(BFM_OP_REDUCE, [&] {
-      ctl_decide(d_ctl, ws.redp().device_results(), slot, slot >= 0 ? kBoundSlot + slot : 0, stage,
-                 kcfg, d_ring, stream, &ws.lc);
-    });
+      ctl_decide(d_ctl, res, slot, slot >= 0 ? kBoundSlot + slot : 0, stage, kcfg, d_ring, sd(), &ws.lc);
+    }, sd());
   }
 
   // ---- device units (no host synchronisation) ------------------------------
+  // pair value on the side stream, after the main stream's pending work
   void pair_value_async() {  // solver.hpp:240
+    side_after_main();
     timed(BFM_OP_REDUCE, [&] {
-      ws.redp().dot(phi.p, nu.p, psi.p, mu.p, g.size, g.vol, kSlotPair, stream, &ws.lc);
-    });
+      side_red.dot(phi.p, nu.p, psi.p, mu.p, g.size, g.vol, kSlotPair, sd(), &ws.lc);
+    }, sd());
   }
-  void ctransform(const double* in, double* out) {
+  // before_last: the output's readers on the side stream (the last pass waits)
+  void ctransform(const double* in, double* out, cudaEvent_t before_last = nullptr) {
     timed(BFM_OP_CTRANSFORM, [&] {
-      if (power) ctpow->run(in, out, stream, &ws.lc);
-      else ws.ctp().run(in, out, stream, &ws.lc);
+      if (power) {
+        if (before_last) BFM_CUDA(cudaStreamWaitEvent(stream, before_last, 0));
+        ctpow->run(in, out, stream, &ws.lc);
+      } else {
+        ws.ctp().run(in, out, stream, &ws.lc, before_last);
+      }
     });
   }
   void axpy_device(double* u, const double* d) {
     timed(BFM_OP_REDUCE, [&] { axpy_dev(u, &d_ctl->sigma, d, g.size, stream, &ws.lc); });
   }
-  // solver.hpp:245-260 (result left in d_dir, gn in kSlotGn)
+  // solver.hpp:245-260 (result left in d_dir, gn in gn_slot of the main Reducer)
   void ascent_direction_async(const double* u, const double* source, const double* target,
-                              double* d_dir) {
+                              double* d_dir, int gn_slot = kSlotGn) {
     timed(BFM_OP_PUSHFORWARD,
           [&] { ws.pfp().from_potential(u, source, target, r.p, nullptr, stream, &ws.lc); });
     timed(BFM_OP_POISSON, [&] { ws.poisp().solve(r.p, d_dir, stream, &ws.lc); });
     timed(BFM_OP_REDUCE, [&] {
-      ws.redp().dot(r.p, d_dir, nullptr, nullptr, g.size, g.vol, kSlotGn, stream, &ws.lc);
+      ws.redp().dot(r.p, d_dir, nullptr, nullptr, g.size, g.vol, gn_slot, stream, &ws.lc);
     });
   }
+  // Stream layout of a unit. Main: axpys, c-transforms, ascents (gn). Side:
+  // pair values and decisions. A pair value reads phi and psi while the next
+  // c-transform's early passes run; that c-transform's LAST pass (which
+  // overwrites one of them) waits for it (pending_read). An axpy waits for
+  // the decision that produced its sigma.
+  cudaEvent_t pending_read = nullptr;  // side-stream reads of phi/psi not yet fenced
   void enqueue_probe() {  // solver.hpp:264-280
     if (cfg.mode == BFM_MODE_BACK_AND_FORTH) {
-      ctransform(phi.p, psi.p);
+      ctransform(phi.p, psi.p, pending_read);
+      pending_read = nullptr;
       pair_value_async();
+      pending_read = timing ? nullptr : mark(side);
       decide(kStageProbePair, kSlotPair);
     } else {
       decide(kStageProbeGA, -1);
     }
-    ascent_direction_async(psi.p, mu.p, nu.p, dir.p);
+    ascent_direction_async(psi.p, mu.p, nu.p, dir.p, kSlotGn);
+    side_after_main();
     decide(kStageProbeGn, kSlotGn);
   }
   void enqueue_step() {  // solver.hpp:286-328
     decide(kStageStepBegin, -1);
+    main_after_side();  // sigma, and the side stream's reads of phi/psi
+    pending_read = nullptr;
     axpy_device(phi.p, dir.p);
     ctransform(phi.p, psi.p);
     pair_value_async();
+    pending_read = timing ? nullptr : mark(side);
     decide(kStageFirst, kSlotPair);
-    ctransform(psi.p, phi.p);
+    ctransform(psi.p, phi.p, pending_read);
+    pending_read = nullptr;
     pair_value_async();
+    pending_read = timing ? nullptr : mark(side);
     if (cfg.mode != BFM_MODE_BACK_AND_FORTH) {
       decide(kStageGAv3, kSlotPair);
       return;
     }
     decide(kStageV4, kSlotPair);
-    ascent_direction_async(phi.p, nu.p, mu.p, dir2.p);
-    decide(kStageGn2, kSlotGn);
+    ascent_direction_async(phi.p, nu.p, mu.p, dir2.p, kSlotGn2);
+    side_after_main();
+    decide(kStageGn2, kSlotGn2);
+    main_after_side();  // sigma (kStageFirst) and the pair value's read of psi
+    pending_read = nullptr;
     axpy_device(psi.p, dir2.p);
     ctransform(psi.p, phi.p);
     pair_value_async();
+    pending_read = timing ? nullptr : mark(side);
     decide(kStageV5, kSlotPair);
   }
   void enqueue_unit(int kind) {
+    pending_read = nullptr;
+    side_after_main();  // forks the side stream into a capture; orders it after main's prior work
     if (kind != 1 && kind != 2) enqueue_probe();
     if (kind != 0) enqueue_step();
     if (kind == 2) enqueue_probe();
+    main_after_side();  // every decision is in ctl before the copy back
+    pending_read = nullptr;
     BFM_CUDA(cudaMemcpyAsync(h_ctl, d_ctl, sizeof(SolverCtl), cudaMemcpyDeviceToHost, stream));
   }
   // Launches one unit: eagerly the first time (plans allocate lazily), then as
@@ -1000,6 +1064,8 @@ int bfm_solver_create_cost(int dim, const int* extents, const double* exponents,
     s->cfg = c;
     s->ws.g = g;
     BFM_CUDA(cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking));
+    BFM_CUDA(cudaStreamCreateWithFlags(&s->side, cudaStreamNonBlocking));
+    s->side_red.init();
     const long N = g.size;
     for (DevBuf* b : {&s->mu, &s->nu, &s->phi, &s->psi, &s->dir, &s->dir2, &s->r}) b->alloc(N);
     copy_h2d(s->mu.p, mu, N, s->stream);

@@ -1941,9 +1941,11 @@ void CtPlan::run_rows(const uint32_t* d_chain0, const double* d_q, double* d_out
 
 // Pass a >= 1 reads phi(chain*, y) at its own nodes from the previous pass's
 // q output (written next to the argmin chain) instead of gathering phi.
-void CtPlan::run(const double* d_phi, double* d_out, cudaStream_t stream, LaunchCounter* lc) {
+void CtPlan::run(const double* d_phi, double* d_out, cudaStream_t stream, LaunchCounter* lc,
+                 cudaEvent_t before_last) {
   for (int a = 0; a < g_.d; ++a) {
     CtPass P = pass_[a];
+    if (P.last && before_last) BFM_CUDA(cudaStreamWaitEvent(stream, before_last, 0));
     P.phi = a == 0 ? d_phi : qbuf_[(a - 1) & 1];
     P.pregathered = a > 0 ? 1 : 0;
     P.state_in = a > 0 ? state_[(a - 1) & 1] : nullptr;

@@ -55,7 +55,11 @@ class CtPlan {
   void init(const GridDesc& g);
   // out = phi^c (exactly rounded toward -inf). phi and out are device pointers
   // (may not alias). Enqueues g.d kernels on stream.
-  void run(const double* d_phi, double* d_out, cudaStream_t stream, LaunchCounter* lc);
+  // before_last (optional): an event the last pass waits for — the pass that
+  // writes d_out — so readers of d_out on another stream can overlap the
+  // earlier passes.
+  void run(const double* d_phi, double* d_out, cudaStream_t stream, LaunchCounter* lc,
+           cudaEvent_t before_last = nullptr);
 
   // Multi-GPU slab decomposition along axis 0. Column slab:
   // the (n0 x ncols) block of the flattened non-axis-0 columns; pass 0 writes
