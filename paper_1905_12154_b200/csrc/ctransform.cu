@@ -1350,9 +1350,15 @@ __global__ void __launch_bounds__(kDyThreads) ct_dy_kernel(CtPass p) {
   PH(1);
   const bool convex_line = s.scal[4] == 0ull;
 
+  // kept_convex: every chunk's monotone chain ran without a pop and every
+  // join between consecutive chunks is a strict corner, so the kept points
+  // are a convex sequence and are the hull (phase 1b); the hull then lives in
+  // the res buffer and the per-query results in H (line flag: scal[7])
+  bool kept_convex = false;
   if (!convex_line) {
     // ---- 1. chunk hulls (monotone chain, exact strict corners) at H[t*C..)
     uint16_t* st = s.H + t * C;
+    bool popped = false;
     if (active) {
       int sz = 0;
       double fa = 0, fb = 0;
@@ -1362,6 +1368,7 @@ __global__ void __launch_bounds__(kDyThreads) ct_dy_kernel(CtPass p) {
         const double fj = P_f(j);
         while (sz >= 2) {
           if (convex_x(ia, fa, ib, fb, j, fj)) break;
+          popped = true;
           --sz;
           ib = ia;
           fb = fa;
@@ -1378,126 +1385,172 @@ __global__ void __launch_bounds__(kDyThreads) ct_dy_kernel(CtPass p) {
       }
       s.gsz[t] = sz;
     }
+    if (popped) atomicOr(reinterpret_cast<unsigned int*>(&s.scal[5]), 1u);
+    group_sync(tpl, l);
     PH(2);
-    in_merge = 1;
-    // ---- 2. tree merge: bridge by galloping searches, then B's surviving
-    //         corners are moved next to A's (register-staged, in place)
     auto cvx3 = [&](int i0, int i1, int i2) { return convex_x(i0, P_f(i0), i1, P_f(i1), i2, P_f(i2)); };
-    uint16_t* Hh = s.H;
-    for (int lvl = 1, li = 0; lvl < tpl; lvl <<= 1, ++li) {
-      if (2 * lvl <= 32) __syncwarp();
-      else group_sync(tpl, l);
-      if (p.stats && t == 0) {  // per-level clocks of thread 0 (diagnostics)
-        const long long now = clock64();
-        if (li > 0) atomicAdd(p.stats + 18 + li - 1, static_cast<unsigned long long>(now - tph));
-        tph = now;
-      }
-      if (active && (t % (2 * lvl)) == 0) {
-        const int gB = t + lvl;
-        const int szA = s.gsz[t];
-        const int szB = gB < tpl ? s.gsz[gB] : 0;
-        const uint16_t* HA = Hh + t * C;
-        const uint16_t* HB = Hh + gB * C;
-        int ia = szA - 1, ib = 0;
-        if (szA > 0 && szB > 0) {
-          while (true) {
-            bool moved = false;
-            // retreat: P(a) = (a == 0 || cvx(A[a-1], A[a], B[ib])) holds up to
-            // the tangent from B[ib] and fails after it
-            const int qb = HB[ib];
-            if (ia > 0 && !cvx3(HA[ia - 1], HA[ia], qb)) {
-              int bad = ia, good = 0, step = 1;
-              while (true) {
-                const int c = bad - step;
-                if (c <= 0) break;
-                if (cvx3(HA[c - 1], HA[c], qb)) {
-                  good = c;
-                  break;
-                }
-                bad = c;
-                step <<= 1;
-              }
-              while (bad - good > 1) {
-                const int mid = (bad + good) >> 1;
-                if (cvx3(HA[mid - 1], HA[mid], qb)) good = mid;
-                else bad = mid;
-              }
-              ia = good;
-              moved = true;
-            }
-            // advance: Q(b) = (b == last || cvx(A[ia], B[b], B[b+1])) fails
-            // before the tangent from A[ia] and holds from it on
-            const int pa = HA[ia];
-            if (ib < szB - 1 && !cvx3(pa, HB[ib], HB[ib + 1])) {
-              int bad = ib, good = szB - 1, step = 1;
-              while (true) {
-                const int c = bad + step;
-                if (c >= szB - 1) break;
-                if (cvx3(pa, HB[c], HB[c + 1])) {
-                  good = c;
-                  break;
-                }
-                bad = c;
-                step <<= 1;
-              }
-              while (good - bad > 1) {
-                const int mid = (bad + good) >> 1;
-                if (cvx3(pa, HB[mid], HB[mid + 1])) good = mid;
-                else bad = mid;
-              }
-              ib = good;
-              moved = true;
-            }
-            if (!moved) break;
-          }
+    // ---- 1b. no pops anywhere (typical of c-concave input on the first
+    //          pass): check the chunk joins, then compact the chunk hulls
+    if (active && s.scal[5] == 0ull) {
+      const int m = s.gsz[t];
+      bool bad = false;
+      if (m > 0) {
+        int tp = t - 1;
+        while (tp >= 0 && s.gsz[tp] == 0) --tp;
+        int tn = t + 1;
+        while (tn < tpl && s.gsz[tn] == 0) ++tn;
+        if (tp >= 0) {  // (last kept before, first, second or next chunk's first)
+          const int c = m >= 2 ? st[1] : (tn < tpl ? s.H[tn * C] : -1);
+          if (c >= 0 && !cvx3(s.H[tp * C + s.gsz[tp] - 1], st[0], c)) bad = true;
         }
-        s.bA[t] = ia;
-        s.bB[t] = ib;
-        s.gsz[t] = (ia + 1) + (szB - ib);
+        if (!bad && m >= 2 && tn < tpl && !cvx3(st[m - 2], st[m - 1], s.H[tn * C])) bad = true;
       }
-      if (2 * lvl <= 32) __syncwarp();
-      else group_sync(tpl, l);
-      // move B[ib..szB) to A's end (a left move): each round reads its corners
-      // before any is written; at most lvl*C corners over 2*lvl threads, so
-      // ceil(C / (2 kDyStage)) rounds (uniform over the line) suffice
-      const int g = t & ~(2 * lvl - 1);
-      const int gthreads = min(2 * lvl, tpl - g);
-      int nmv = 0, dst0 = 0;
-      const uint16_t* src = Hh;
-      if (active && g + lvl < tpl) {
-        const int ia = s.bA[g], ib = s.bB[g];
-        nmv = s.gsz[g] - (ia + 1);
-        src = Hh + (g + lvl) * C + ib;
-        dst0 = g * C + ia + 1;
-      }
-      const int rounds = (C + 2 * kDyStage - 1) / (2 * kDyStage);
-      for (int rd = 0; rd < rounds; ++rd) {
-        const int base = rd * kDyStage * gthreads + (t - g);
-        uint16_t v[kDyStage];
-#pragma unroll
-        for (int r = 0; r < kDyStage; ++r) {
-          const int i = base + r * gthreads;
-          if (i < nmv) v[r] = src[i];
+      if (bad) atomicOr(reinterpret_cast<unsigned int*>(&s.scal[6]), 1u);
+      group_sync(tpl, l);
+      if (s.scal[6] == 0ull) {
+        kept_convex = true;
+        // exclusive prefix of the chunk sizes (warps never straddle lines:
+        // tpl is a multiple of 32), then every chunk moves to res
+        const int lane = threadIdx.x & 31;
+        int inc = m;
+        for (int o = 1; o < 32; o <<= 1) {
+          const int u = __shfl_up_sync(0xffffffffu, inc, o);
+          if (lane >= o) inc += u;
         }
-        if (2 * lvl <= 32) __syncwarp();
-        else group_sync(tpl, l);
-#pragma unroll
-        for (int r = 0; r < kDyStage; ++r) {
-          const int i = base + r * gthreads;
-          if (i < nmv) Hh[dst0 + i] = v[r];
+        if (lane == 31) s.bA[t >> 5] = inc;
+        group_sync(tpl, l);
+        int base = 0;
+        for (int w = 0; w < (t >> 5); ++w) base += s.bA[w];
+        uint16_t* R = s.res;
+        for (int i = 0, o = base + inc - m; i < m; ++i) R[o + i] = st[i];
+        if (t == tpl - 1) {
+          s.scal[3] = static_cast<unsigned long long>(base + inc);
+          s.scal[7] = 1ull;
+          if (p.stats) atomicAdd(p.stats + 28, 1ull);  // lines on the kept-convex path
         }
       }
     }
-    group_sync(tpl, l);
-    if (p.stats && t == 0) atomicAdd(p.stats + 27, static_cast<unsigned long long>(clock64() - tph));
-    if (t == 0) s.scal[3] = static_cast<unsigned long long>(s.gsz[0]);
+    if (!kept_convex) {
+      if (p.stats && t == 0 && active) atomicAdd(p.stats + 29, 1ull);  // lines merged
+      in_merge = 1;
+      // ---- 2. tree merge: bridge by galloping searches, then B's surviving
+      //         corners are moved next to A's (register-staged, in place)
+      uint16_t* Hh = s.H;
+      for (int lvl = 1, li = 0; lvl < tpl; lvl <<= 1, ++li) {
+        if (2 * lvl <= 32) __syncwarp();
+        else group_sync(tpl, l);
+        if (p.stats && t == 0) {  // per-level clocks of thread 0 (diagnostics)
+          const long long now = clock64();
+          if (li > 0) atomicAdd(p.stats + 18 + li - 1, static_cast<unsigned long long>(now - tph));
+          tph = now;
+        }
+        if (active && (t % (2 * lvl)) == 0) {
+          const int gB = t + lvl;
+          const int szA = s.gsz[t];
+          const int szB = gB < tpl ? s.gsz[gB] : 0;
+          const uint16_t* HA = Hh + t * C;
+          const uint16_t* HB = Hh + gB * C;
+          int ia = szA - 1, ib = 0;
+          if (szA > 0 && szB > 0) {
+            while (true) {
+              bool moved = false;
+              // retreat: P(a) = (a == 0 || cvx(A[a-1], A[a], B[ib])) holds up to
+              // the tangent from B[ib] and fails after it
+              const int qb = HB[ib];
+              if (ia > 0 && !cvx3(HA[ia - 1], HA[ia], qb)) {
+                int bad = ia, good = 0, step = 1;
+                while (true) {
+                  const int c = bad - step;
+                  if (c <= 0) break;
+                  if (cvx3(HA[c - 1], HA[c], qb)) {
+                    good = c;
+                    break;
+                  }
+                  bad = c;
+                  step <<= 1;
+                }
+                while (bad - good > 1) {
+                  const int mid = (bad + good) >> 1;
+                  if (cvx3(HA[mid - 1], HA[mid], qb)) good = mid;
+                  else bad = mid;
+                }
+                ia = good;
+                moved = true;
+              }
+              // advance: Q(b) = (b == last || cvx(A[ia], B[b], B[b+1])) fails
+              // before the tangent from A[ia] and holds from it on
+              const int pa = HA[ia];
+              if (ib < szB - 1 && !cvx3(pa, HB[ib], HB[ib + 1])) {
+                int bad = ib, good = szB - 1, step = 1;
+                while (true) {
+                  const int c = bad + step;
+                  if (c >= szB - 1) break;
+                  if (cvx3(pa, HB[c], HB[c + 1])) {
+                    good = c;
+                    break;
+                  }
+                  bad = c;
+                  step <<= 1;
+                }
+                while (good - bad > 1) {
+                  const int mid = (bad + good) >> 1;
+                  if (cvx3(pa, HB[mid], HB[mid + 1])) good = mid;
+                  else bad = mid;
+                }
+                ib = good;
+                moved = true;
+              }
+              if (!moved) break;
+            }
+          }
+          s.bA[t] = ia;
+          s.bB[t] = ib;
+          s.gsz[t] = (ia + 1) + (szB - ib);
+        }
+        if (2 * lvl <= 32) __syncwarp();
+        else group_sync(tpl, l);
+        // move B[ib..szB) to A's end (a left move): each round reads its corners
+        // before any is written; at most lvl*C corners over 2*lvl threads, so
+        // ceil(C / (2 kDyStage)) rounds (uniform over the line) suffice
+        const int g = t & ~(2 * lvl - 1);
+        const int gthreads = min(2 * lvl, tpl - g);
+        int nmv = 0, dst0 = 0;
+        const uint16_t* src = Hh;
+        if (active && g + lvl < tpl) {
+          const int ia = s.bA[g], ib = s.bB[g];
+          nmv = s.gsz[g] - (ia + 1);
+          src = Hh + (g + lvl) * C + ib;
+          dst0 = g * C + ia + 1;
+        }
+        const int rounds = (C + 2 * kDyStage - 1) / (2 * kDyStage);
+        for (int rd = 0; rd < rounds; ++rd) {
+          const int base = rd * kDyStage * gthreads + (t - g);
+          uint16_t v[kDyStage];
+  #pragma unroll
+          for (int r = 0; r < kDyStage; ++r) {
+            const int i = base + r * gthreads;
+            if (i < nmv) v[r] = src[i];
+          }
+          if (2 * lvl <= 32) __syncwarp();
+          else group_sync(tpl, l);
+  #pragma unroll
+          for (int r = 0; r < kDyStage; ++r) {
+            const int i = base + r * gthreads;
+            if (i < nmv) Hh[dst0 + i] = v[r];
+          }
+        }
+      }
+      group_sync(tpl, l);
+      if (p.stats && t == 0) atomicAdd(p.stats + 27, static_cast<unsigned long long>(clock64() - tph));
+      if (t == 0) s.scal[3] = static_cast<unsigned long long>(s.gsz[0]);
+    }  // !kept_convex
     PH(3);
   }
   group_sync(tpl, l);
   const int hsz = convex_line ? n : static_cast<int>(s.scal[3]);
   BFM_DASSERT(!active || (hsz >= 1 && hsz <= n));
-  const uint16_t* Hf = s.H;
-  uint16_t* res = s.res;
+  const uint16_t* Hf = kept_convex ? s.res : s.H;
+  uint16_t* res = kept_convex ? s.H : s.res;
   auto HH = [&](int i) { return convex_line ? i : static_cast<int>(Hf[i]); };
 
   // ---- 4. tangent corner of every query: balanced merge path of the query
@@ -1623,7 +1676,7 @@ __global__ void __launch_bounds__(kDyThreads) ct_dy_kernel(CtPass p) {
     if (g.valid)
       for (int k = first; k < n; k += step) {
         const long node = g.base + static_cast<long>(k) * A.stride;
-        const int win = sm.res[k];
+        const int win = (sm.scal[7] ? sm.H : sm.res)[k];
         const uint32_t packed = p.a == 0 ? static_cast<uint32_t>(win)
                                          : (sm.ch[win] | (static_cast<uint32_t>(win) << 16));
         p.state_out[node] = packed;
