@@ -246,6 +246,44 @@ __device__ __forceinline__ bool cand_fixed(const CtPass& p, const LineGeo& g, ui
   return true;
 }
 
+// Exact fixed-point values of two candidates at once (jb < 0: only ja). Every
+// global load of both candidates (phi at the chain, the table entries of the
+// chain's axes and of the pass axis) is issued before the first conversion,
+// so a flagged query pays one memory round trip instead of one per load.
+__device__ __forceinline__ bool cand_fixed2(const CtPass& p, const LineGeo& g, const uint32_t* chain_s,
+                                            int k, int ja, int jb, __int128& Va, __int128& Vb) {
+  const int jb2 = jb >= 0 ? jb : ja;
+  const uint32_t cha = p.a > 0 ? chain_s[ja] : 0u;
+  const uint32_t chb = p.a > 0 ? chain_s[jb2] : 0u;
+  const double pha = __ldg(&p.phi[phi_index(p, g, cha, ja)]);
+  const double phb = __ldg(&p.phi[phi_index(p, g, chb, jb2)]);
+  __int128 ta[3] = {0, 0, 0}, tb[3] = {0, 0, 0};
+  bool ok = true;
+#pragma unroll
+  for (int b = 0; b < 3; ++b) {
+    const bool chain_axis = b < 2;
+    if (chain_axis && p.a <= b) continue;
+    const CtAxis& A = chain_axis ? p.ax[b] : p.ax[p.a];
+    const int kk = chain_axis ? g.k[b] : k;
+    const int j0 = !chain_axis ? ja : (b == 0 ? static_cast<int>(cha & 0xFFFFu) : static_cast<int>(cha >> 16));
+    const int j1 = !chain_axis ? jb2 : (b == 0 ? static_cast<int>(chb & 0xFFFFu) : static_cast<int>(chb >> 16));
+    if (A.dyadic) {
+      ok = to_fixed124(g_approx(A, kk, j0), ta[b]) && ok;
+      ok = to_fixed124(g_approx(A, kk, j1), tb[b]) && ok;
+    } else {
+      const __int128* row = A.GF + static_cast<long>(kk) * A.n;
+      ta[b] = row[j0];
+      tb[b] = row[j1];
+    }
+  }
+  __int128 fa, fb;
+  ok = to_fixed124(pha, fa) && ok;
+  ok = to_fixed124(phb, fb) && ok;
+  Va = ((ta[0] + ta[1]) + ta[2]) - fa;
+  Vb = ((tb[0] + tb[1]) + tb[2]) - fb;
+  return ok;
+}
+
 // Certified strict convexity of the middle point (fp64 orientation with a
 // rounding bound; near-collinear counts as NOT convex).
 __device__ __forceinline__ bool convex3(double ya, double fa, double yb, double fb, double yc,
@@ -801,72 +839,101 @@ __global__ void __launch_bounds__(kNdThreads) ct_pass_kernel(CtPass p) {
       if (!lone) {
         const int e0 = L > 0 ? L - 1 : 0;
         const int e1 = R < hsz - 1 ? R : hsz - 2;
-        auto visit = [&](auto&& fn) {
-          for (int c = L; c <= R; ++c) fn(HH(c));
-          if (convex_line) return;
-          for (int e = e0; e <= e1; ++e) {
-            const uint8_t code = s.dlt[e];
-            if (p.stats) atomicAdd(p.stats + 3, 1ull);
-            if (code == 0) continue;
-            const int a = HH(e), b = HH(e + 1);
-            const double Fa = Fhat(a, xk), Fb = Fhat(b, xk);
-            const double slack = slack_value(code, sref) + Mc;
-            if (fmin(Fa, Fb) > Fmin + slack) continue;
-            if (fabs(Fa - Fb) > slack * (1.000001 * (b - a)) + Mc) continue;
-            if (p.stats) {
-              atomicAdd(p.stats + 4, 1ull);
-              atomicAdd(p.stats + 5, static_cast<unsigned long long>(b - a - 1));
-            }
-            for (int j = a + 1; j < b; ++j) fn(j);
-          }
-        };
-        double Fbest = INFINITY;
-        visit([&](int j) { Fbest = fmin(Fbest, Fhat(j, xk)); });
-        if (p.last) {
-          // RD is monotone: RD(min_j V_j) = min_j RD(V_j); no exact argmin needed.
-          double best = INFINITY;
-          visit([&](int j) {
-            if (Fhat(j, xk) <= Fbest + Mc) best = fmin(best, rd_value(j, k));
-          });
-          outv = best;
-          have_out = true;
-        } else {
-          // exact argmin: fixed-point values when every candidate is
-          // representable, else the expansion comparison
-          bool fx = p.fixed != 0;
+        // One traversal of the candidates: the corners L..R, then the
+        // suspects of the adjacent edges that pass the relevance tests. A
+        // candidate is evaluated exactly when its F^ is within the margin of
+        // the running minimum (a superset of those within the margin of the
+        // final minimum, which contain the exact argmin). Fixed-point grids
+        // (mode 0) evaluate candidates in pairs with all their loads in
+        // flight together; a value outside the fixed-point range restarts
+        // the traversal on the expansion path (mode 1). The loop body exists
+        // once: this path is instruction-cache bound.
+        for (int mode = p.fixed ? 0 : 1;; mode = 1) {
+          double Fbest = Fmin;  // min over the corners L..R
           int bestj = -1;
-          if (fx) {
-            __int128 bv = 0;
-            visit([&](int j) {
-              if (!fx || Fhat(j, xk) > Fbest + Mc) return;
-              __int128 V;
-              if (!cand_fixed(p, geo, p.a > 0 ? s.chain[j] : 0u, j, k, V)) {
-                fx = false;
-                return;
-              }
-              if (bestj < 0 || V < bv) {
-                bestj = j;
-                bv = V;
-              }
-            });
-          }
-          if (!fx) bestj = -1;
-          double bt[12];
+          __int128 bv = 0;      // mode 0: exact best value
+          double bt[12];        // mode 1: exact best terms / best round-down
           int bm = 0;
-          if (!fx) visit([&](int j) {
-            if (Fhat(j, xk) > Fbest + Mc) return;
-            double ct[12];
-            const uint32_t ch = p.a > 0 ? s.chain[j] : 0u;
-            const int cm = cand_terms(p, geo, ch, j, k, ct);
-            if (bestj >= 0) {
-              if (p.slow_queries) atomicAdd(p.slow_queries, 1ull);
-              if (bfmx::sign_diff(ct, cm, bt, bm) >= 0) return;
+          double brd = INFINITY;
+          bool fail = false;
+          int pend = -1;  // mode 0: first candidate of an unfinished pair
+          int c = L, e = e0 - 1, js = 0, jend = 0;
+          while (true) {
+            int j = -1;
+            bool flush = false;
+            if (c <= R) {
+              j = HH(c++);
+            } else if (js < jend) {
+              j = js++;
+            } else if (!convex_line && e < e1) {
+              ++e;
+              const uint8_t code = s.dlt[e];
+              if (p.stats) atomicAdd(p.stats + 3, 1ull);
+              if (code == 0) continue;
+              const int a = HH(e), b = HH(e + 1);
+              const double Fa = Fhat(a, xk), Fb = Fhat(b, xk);
+              const double slack = slack_value(code, sref) + Mc;
+              if (fmin(Fa, Fb) > Fmin + slack) continue;
+              if (fabs(Fa - Fb) > slack * (1.000001 * (b - a)) + Mc) continue;
+              js = a + 1;
+              jend = b;
+              continue;
+            } else {
+              if (pend < 0) break;
+              flush = true;  // an odd candidate is left
             }
-            bestj = j;
-            for (int q = 0; q < cm; ++q) bt[q] = ct[q];
-            bm = cm;
-          });
+            if (!flush) {
+              const double F = Fhat(j, xk);
+              const bool in = F <= Fbest + Mc;
+              Fbest = fmin(Fbest, F);
+              if (!in) continue;
+            }
+            if (mode == 0) {
+              if (!flush && pend < 0) {
+                pend = j;
+                continue;
+              }
+              __int128 Va, Vb;
+              if (!cand_fixed2(p, geo, s.chain, k, pend, j, Va, Vb)) {
+                fail = true;
+                break;
+              }
+              if (bestj < 0 || Va < bv) {
+                bestj = pend;
+                bv = Va;
+              }
+              if (j >= 0 && Vb < bv) {
+                bestj = j;
+                bv = Vb;
+              }
+              pend = -1;
+              if (flush) break;
+            } else {
+              double ct[12];
+              const uint32_t ch = p.a > 0 ? s.chain[j] : 0u;
+              const int cm = cand_terms(p, geo, ch, j, k, ct);
+              if (p.last) {
+                // RD is monotone: RD(min_j V_j) = min_j RD(V_j)
+                brd = fmin(brd, bfmx::round_down_sum(ct, cm));
+                bestj = j;
+              } else {
+                if (bestj >= 0) {
+                  if (p.slow_queries) atomicAdd(p.slow_queries, 1ull);
+                  if (bfmx::sign_diff(ct, cm, bt, bm) >= 0) continue;
+                }
+                bestj = j;
+                for (int q = 0; q < cm; ++q) bt[q] = ct[q];
+                bm = cm;
+              }
+            }
+          }
+          if (fail) continue;  // (mode 0 only)
           win = bestj;
+          if (p.last) {
+            outv = mode == 0 ? rd_fixed124(bv) : brd;
+            have_out = true;
+          }
+          break;
         }
       }
       BFM_DASSERT(win >= 0 && win < n);
