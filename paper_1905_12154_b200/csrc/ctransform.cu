@@ -246,12 +246,15 @@ __device__ __forceinline__ bool cand_fixed(const CtPass& p, const LineGeo& g, ui
   return true;
 }
 
-// Exact fixed-point values of two candidates at once (jb < 0: only ja). Every
+__device__ __forceinline__ bool g_fixed_dyadic(const CtAxis& A, int k, int j, __int128& out) {
+  return to_fixed124(g_approx(A, k, j), out);  // exact double on dyadic axes
+}
+// Exact fixed-point values of two candidates (ka, ja), (kb, jb) at once (jb < 0: only the first). Every
 // global load of both candidates (phi at the chain, the table entries of the
 // chain's axes and of the pass axis) is issued before the first conversion,
 // so a flagged query pays one memory round trip instead of one per load.
 __device__ __forceinline__ bool cand_fixed2(const CtPass& p, const LineGeo& g, const uint32_t* chain_s,
-                                            int k, int ja, int jb, __int128& Va, __int128& Vb) {
+                                            int ka, int ja, int kb, int jb, __int128& Va, __int128& Vb) {
   const int jb2 = jb >= 0 ? jb : ja;
   const uint32_t cha = p.a > 0 ? chain_s[ja] : 0u;
   const uint32_t chb = p.a > 0 ? chain_s[jb2] : 0u;
@@ -264,16 +267,16 @@ __device__ __forceinline__ bool cand_fixed2(const CtPass& p, const LineGeo& g, c
     const bool chain_axis = b < 2;
     if (chain_axis && p.a <= b) continue;
     const CtAxis& A = chain_axis ? p.ax[b] : p.ax[p.a];
-    const int kk = chain_axis ? g.k[b] : k;
+    const int kk = chain_axis ? g.k[b] : ka;
+    const int kk2 = chain_axis ? g.k[b] : kb;
     const int j0 = !chain_axis ? ja : (b == 0 ? static_cast<int>(cha & 0xFFFFu) : static_cast<int>(cha >> 16));
     const int j1 = !chain_axis ? jb2 : (b == 0 ? static_cast<int>(chb & 0xFFFFu) : static_cast<int>(chb >> 16));
-    if (A.dyadic) {
-      ok = to_fixed124(g_approx(A, kk, j0), ta[b]) && ok;
-      ok = to_fixed124(g_approx(A, kk, j1), tb[b]) && ok;
+    if (A.dyadic) {  // (mixed grids only: rare, kept out of line)
+      ok = g_fixed_dyadic(A, kk, j0, ta[b]) && ok;
+      ok = g_fixed_dyadic(A, kk2, j1, tb[b]) && ok;
     } else {
-      const __int128* row = A.GF + static_cast<long>(kk) * A.n;
-      ta[b] = row[j0];
-      tb[b] = row[j1];
+      ta[b] = A.GF[static_cast<long>(kk) * A.n + j0];
+      tb[b] = A.GF[static_cast<long>(kk2) * A.n + j1];
     }
   }
   __int128 fa, fb;
@@ -661,15 +664,6 @@ __global__ void __launch_bounds__(kNdThreads) ct_pass_kernel(CtPass p) {
       const int a = HH(i), b = HH(i + 1);
       return (P_f(b) - P_f(a)) >= xk * (P_y(b) - P_y(a));
     };
-    // exact value V(k, j) rounded down (last pass)
-    auto rd_value = [&](int j, int k) {
-      const uint32_t ch = p.a > 0 ? s.chain[j] : 0u;
-      __int128 V;
-      if (p.fixed && cand_fixed(p, geo, ch, j, k, V)) return rd_fixed124(V);
-      double tv[12];
-      const int m = cand_terms(p, geo, ch, j, k, tv);
-      return bfmx::round_down_sum(tv, m);
-    };
     // ---- 5a. tangent corner of every query: balanced merge path of the
     //          query slopes x_k against the hull-edge slopes (ties: query first)
     {
@@ -796,15 +790,6 @@ __global__ void __launch_bounds__(kNdThreads) ct_pass_kernel(CtPass p) {
       auto P_f = [&](int idx) { return s.fh[padj(idx)]; };
       auto HH = [&](int i) { return convex_line ? i : static_cast<int>(s.H[i]); };
       auto Fhat = [&](int idx, double xk) { return P_f(idx) - xk * P_y(idx); };
-      // exact value V(k, j) rounded down (last pass)
-      auto rd_value = [&](int j, int k) {
-        const uint32_t ch = p.a > 0 ? s.chain[j] : 0u;
-        __int128 V;
-        if (p.fixed && cand_fixed(p, geo, ch, j, k, V)) return rd_fixed124(V);
-        double tv[12];
-        const int m = cand_terms(p, geo, ch, j, k, tv);
-        return bfmx::round_down_sum(tv, m);
-      };
       const int k = s.flist[fi];
       const int rv = res[k];
       const int i = rv & 0x7fff;
@@ -894,7 +879,7 @@ __global__ void __launch_bounds__(kNdThreads) ct_pass_kernel(CtPass p) {
                 continue;
               }
               __int128 Va, Vb;
-              if (!cand_fixed2(p, geo, s.chain, k, pend, j, Va, Vb)) {
+              if (!cand_fixed2(p, geo, s.chain, k, pend, k, j, Va, Vb)) {
                 fail = true;
                 break;
               }
@@ -937,11 +922,11 @@ __global__ void __launch_bounds__(kNdThreads) ct_pass_kernel(CtPass p) {
         }
       }
       BFM_DASSERT(win >= 0 && win < n);
-      if (p.last) {
-        if (!have_out) outv = rd_value(win, k);
+      if (p.last && have_out) {
         p.out[geo.base + static_cast<long>(k) * A.stride] = outv;
         res[k] = 0xffffu;  // done
       } else {
+        // (last pass: the final round-down loop below evaluates the winner)
         res[k] = static_cast<uint16_t>(win);
       }
     }
@@ -950,27 +935,28 @@ __global__ void __launch_bounds__(kNdThreads) ct_pass_kernel(CtPass p) {
   else group_sync(tpl, l);
   PH(8);  // flagged queries
   if (p.last && active) {
-    // lone queries: final round-downs
-    constexpr int kB = 8;
-    for (int kk = t; kk < n; kk += kB * tpl) {
-      int wv[kB];
-#pragma unroll
-      for (int u = 0; u < kB; ++u) {
-        const int k = kk + u * tpl;
-        wv[u] = (k < n) ? static_cast<int>(res[k]) : 0xffff;
-      }
-#pragma unroll
-      for (int u = 0; u < kB; ++u) {
-        const int k = kk + u * tpl;
-        if (wv[u] == 0xffff) continue;
-        const uint32_t ch = p.a > 0 ? s.chain[wv[u]] : 0u;
-        __int128 V;
+    // final round-downs of the queries not written by the flagged path: two
+    // queries per round (their loads in flight together); the body is kept
+    // rolled, the kernel is instruction-cache bound
+    for (int kk = t; kk < n; kk += 2 * tpl) {
+      const int k2 = kk + tpl;
+      const int w1 = res[kk];
+      const int w2 = k2 < n ? static_cast<int>(res[k2]) : 0xffff;
+      const bool v1 = w1 != 0xffff, v2 = w2 != 0xffff;
+      if (!v1 && !v2) continue;
+      const int ka = v1 ? kk : k2, ja = v1 ? w1 : w2;
+      const int jb = (v1 && v2) ? w2 : -1;
+      __int128 Va, Vb;
+      const bool fx = p.fixed && cand_fixed2(p, geo, s.chain, ka, ja, k2, jb, Va, Vb);
+      for (int u = 0; u < 2; ++u) {
+        if (u == 1 && jb < 0) break;
+        const int k = u == 0 ? ka : k2, j = u == 0 ? ja : jb;
         double v;
-        if (p.fixed && cand_fixed(p, geo, ch, wv[u], k, V)) {
-          v = rd_fixed124(V);
+        if (fx) {
+          v = rd_fixed124(u == 0 ? Va : Vb);
         } else {
           double tv[12];
-          const int m = cand_terms(p, geo, ch, wv[u], k, tv);
+          const int m = cand_terms(p, geo, p.a > 0 ? s.chain[j] : 0u, j, k, tv);
           v = bfmx::round_down_sum(tv, m);
         }
         p.out[geo.base + static_cast<long>(k) * A.stride] = v;

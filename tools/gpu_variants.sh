@@ -1,0 +1,8 @@
+# A/B of variant libraries (tools/build_variant.sh): gpu_variants.sh CONFIG STEPS NAME...
+cd $GRAFT_REPO_ROOT
+export PYTHONPATH=.
+cfg=$1; steps=$2; shift 2
+for v in "$@"; do
+  echo "== $v"
+  BFM_LIB_OVERRIDE=$GRAFT_REPO_ROOT/paper_1905_12154_b200/variants/libbfm_$v.so timeout 300 python tools/ct_ab.py $cfg $steps
+done
