@@ -18,6 +18,7 @@
 //      reference adds them — then writes target - rho.
 #include <algorithm>
 #include <climits>
+#include <cstdlib>
 
 #include <cmath>
 #include <vector>
@@ -1108,14 +1109,35 @@ void PushforwardPlan::gather(long nrec, const uint32_t* d_keys, const double* d_
     // massless sources (sentinel keys) deposit nothing: a stable compaction
     // drops them before the sort (their count stays on the device)
     const uint32_t sentinel = static_cast<uint32_t>(ncells_);
-    const uint32_t* ckeys = nullptr;
-    const int* cvals = nullptr;
-    const int* d_n = sorter_.compact(d_keys, nrec, sentinel, stream, lc, &ckeys, &cvals);
-    sorter_.sort(ckeys, cvals, nrec, key_bits_, stream, lc, &skeys, &svals, d_n);
-    pf_bounds_kernel<<<grid_for(nrec, 256), 256, 0, stream>>>(skeys, nrec, d_n, sentinel, off_, end_);
-    pf_pack_kernel<<<grid_for(nrec, 256), 256, 0, stream>>>(svals, nrec, d_n, d_mass, d_w, d_cmask, g_.d, rec_,
-                                                             rmask_);
-    BFM_LAUNCH_CHECK("pf_pack_kernel");
+    // One-sweep up to 2^24 records (C1: pushforward 0.33 -> 0.25 ms per
+    // iteration, C2 0.56 -> 0.48, C3 3.83 -> 3.77); above that the look-back
+    // chain over the many tiles costs more than the per-pass histogram and
+    // scan kernels it replaces (C4: 24.9 vs 24.4 ms), so the multi-kernel
+    // passes stay. BFM_PF_SORT=legacy|onesweep overrides (A/B).
+    static const char* sort_mode = getenv("BFM_PF_SORT");
+    const bool onesweep = sort_mode ? sort_mode[0] == 'o' : nrec <= (1L << 24);
+    if (onesweep) {
+      // one-sweep: digit histograms in one read of the keys, one scatter
+      // kernel per digit (decoupled look-back), sentinels dropped by the
+      // first pass, the packed records written by the last
+      // (the records are packed after the sort: in sorted order the source
+      // ids of neighbouring positions are close, so the gathers coalesce;
+      // fused into the last scatter they cost 4x the separate kernel)
+      const int* d_n = sorter_.sort_onesweep(d_keys, nrec, sentinel, key_bits_, nullptr, stream, lc, &skeys, &svals);
+      pf_bounds_kernel<<<grid_for(nrec, 256), 256, 0, stream>>>(skeys, nrec, d_n, sentinel, off_, end_);
+      pf_pack_kernel<<<grid_for(nrec, 256), 256, 0, stream>>>(svals, nrec, d_n, d_mass, d_w, d_cmask, g_.d, rec_,
+                                                               rmask_);
+      BFM_LAUNCH_CHECK("pf_pack_kernel");
+    } else {
+      const uint32_t* ckeys = nullptr;
+      const int* cvals = nullptr;
+      const int* d_n = sorter_.compact(d_keys, nrec, sentinel, stream, lc, &ckeys, &cvals);
+      sorter_.sort(ckeys, cvals, nrec, key_bits_, stream, lc, &skeys, &svals, d_n);
+      pf_bounds_kernel<<<grid_for(nrec, 256), 256, 0, stream>>>(skeys, nrec, d_n, sentinel, off_, end_);
+      pf_pack_kernel<<<grid_for(nrec, 256), 256, 0, stream>>>(svals, nrec, d_n, d_mass, d_w, d_cmask, g_.d, rec_,
+                                                               rmask_);
+      BFM_LAUNCH_CHECK("pf_pack_kernel");
+    }
   }
   GatherArgs G{};
   G.g = g_;
