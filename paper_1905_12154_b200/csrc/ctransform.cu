@@ -1232,6 +1232,7 @@ __global__ void __launch_bounds__(kDyThreads) ct_dy_kernel(CtPass p) {
       }
     }
     g.k[0] += p.k0_off;
+    if (p.t0) g.phi_other = g.base;  // transposed pass 0: line L is row L of phi^T
     *s.geo = g;
     for (int q = 0; q < 8; ++q) s.scal[q] = 0ull;
   }
@@ -1738,6 +1739,30 @@ __global__ void __launch_bounds__(kDyThreads) ct_dy_kernel(CtPass p) {
   }
 }
 
+// Tiled transposes for the transposed pass 0: in (rows x cols) -> out (cols x
+// rows), 32 x 32 tiles through padded shared memory, both sides coalesced.
+template <class T>
+__device__ __forceinline__ void transpose_tile(const T* in, T* out, int rows, int cols, T (*tile)[33]) {
+  const int c0 = blockIdx.x * 32, r0 = blockIdx.y * 32;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
+  for (int i = ty; i < 32; i += 8)
+    if (r0 + i < rows && c0 + tx < cols) tile[i][tx] = in[static_cast<long>(r0 + i) * cols + c0 + tx];
+  __syncthreads();
+  for (int i = ty; i < 32; i += 8)
+    if (c0 + i < cols && r0 + tx < rows) out[static_cast<long>(c0 + i) * rows + r0 + tx] = tile[tx][i];
+}
+__global__ void __launch_bounds__(256) ct_transpose_f64(const double* in, double* out, int rows, int cols) {
+  __shared__ double tile[32][33];
+  transpose_tile(in, out, rows, cols, tile);
+}
+__global__ void __launch_bounds__(256) ct_transpose_state(const uint32_t* sin, const double* qin, uint32_t* sout,
+                                                          double* qout, int rows, int cols) {
+  __shared__ double tq[32][33];
+  __shared__ uint32_t ts[32][33];
+  transpose_tile(qin, qout, rows, cols, tq);
+  transpose_tile(sin, sout, rows, cols, ts);
+}
+
 int align16(int v) { return (v + 15) & ~15; }
 
 bool is_dyadic(int n) { return n > 0 && (n & (n - 1)) == 0 && n <= (1 << 25); }
@@ -1760,6 +1785,9 @@ CtPlan::~CtPlan() {
     if (p) dfree(p);
   if (slow_) dfree(slow_);
   if (stats_) dfree(stats_);
+  if (phit_) dfree(phit_);
+  if (statet_) dfree(statet_);
+  if (qt_) dfree(qt_);
 }
 
 void CtPlan::init(const GridDesc& g) { setup(g, g, 0, g.d, 0, false, false); }
@@ -2007,6 +2035,33 @@ void CtPlan::setup(const GridDesc& loc, const GridDesc& global, int pb, int pe, 
     P.slow_queries = slow_;
     P.stats = stats_;
   }
+  // Transposed pass 0 (2-D dyadic grids, whole-grid plans): pass 0's lines are
+  // the columns of phi — two per CTA at best, every row a separate sector.
+  // On phi^T they are contiguous rows like the last pass's (one line per CTA,
+  // coalesced loads and stores); the two tiled transposes (phi in; chain and q
+  // out) cost less than the strided pass loses. BFM_CT_T0=0/1 overrides.
+  t0_ = dyadic_ && loc.d == 2 && pb == 0 && pe == 2 && !virtual_cols && !pregathered && k0_off == 0 &&
+        loc.size >= (1L << 22);
+  if (const char* e = getenv("BFM_CT_T0"))
+    t0_ = atoi(e) != 0 && dyadic_ && loc.d == 2 && pb == 0 && pe == 2 && !virtual_cols && !pregathered;
+  if (t0_) {
+    BFM_CUDA(dmalloc(&phit_, loc.size * sizeof(double)));
+    BFM_CUDA(dmalloc(&statet_, loc.size * sizeof(uint32_t)));
+    BFM_CUDA(dmalloc(&qt_, loc.size * sizeof(double)));
+    CtPass& T = pass0t_;
+    T = pass_[0];
+    T.t0 = 1;
+    T.strided = 0;
+    T.ax[0].stride = 1;
+    T.ax[1].stride = loc.n[0];
+    // lines per CTA as for a contiguous pass
+    int lpc = std::min<long>(budget / (2 * T.line_bytes), kDyThreads / (2 * T.tpl));
+    if (const char* e = getenv("BFM_DY_LPC_C"))
+      lpc = std::max(1, std::min<int>(std::min<long>(atoi(e), budget / T.line_bytes), kDyThreads / T.tpl));
+    lpc = std::min(lpc, 8);
+    lpc = static_cast<int>(std::min<long>(lpc, T.nlines));
+    T.lpc = std::max(lpc, 1);
+  }
   BFM_CUDA(cudaFuncSetAttribute(ct_dy_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, budget));
   BFM_CUDA(cudaFuncSetAttribute(ct_pass_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, budget));
   ready_ = true;
@@ -2050,6 +2105,23 @@ void CtPlan::run_rows(const uint32_t* d_chain0, const double* d_q, double* d_out
 void CtPlan::run(const double* d_phi, double* d_out, cudaStream_t stream, LaunchCounter* lc,
                  cudaEvent_t before_last) {
   for (int a = 0; a < g_.d; ++a) {
+    if (a == 0 && t0_) {
+      const int n0 = g_.n[0], n1 = g_.n[1];
+      const dim3 gin((n1 + 31) / 32, (n0 + 31) / 32), gout((n0 + 31) / 32, (n1 + 31) / 32);
+      ct_transpose_f64<<<gin, 256, 0, stream>>>(d_phi, phit_, n0, n1);
+      CtPass P = pass0t_;
+      P.phi = phit_;
+      P.pregathered = 0;
+      P.state_in = nullptr;
+      P.state_out = statet_;
+      P.q_out = qt_;
+      P.out = d_out;
+      launch(P, stream, lc);
+      ct_transpose_state<<<gout, 256, 0, stream>>>(statet_, qt_, state_[0], qbuf_[0], n1, n0);
+      BFM_LAUNCH_CHECK("ct transposes");
+      if (lc) lc->add(2);
+      continue;
+    }
     CtPass P = pass_[a];
     if (P.last && before_last) BFM_CUDA(cudaStreamWaitEvent(stream, before_last, 0));
     P.phi = a == 0 ? d_phi : qbuf_[(a - 1) & 1];

@@ -40,6 +40,9 @@ struct CtPass {
   // shared-memory carve-up (bytes, per line)
   int off_fv, off_chain, off_hidx, off_H, off_flag, off_list, off_lohi, off_scal, line_bytes;
   int fixed;  // non-dyadic kernel: every non-dyadic axis has a fixed-point table
+  // pass 0 on the transposed potential (2-D dyadic grids): its lines are the
+  // rows of phi^T, contiguous like the last pass's
+  int t0;
   // statistics (device counters, may be null): lines that needed exact resolution
   unsigned long long* slow_queries;
   unsigned long long* stats;  // optional diagnostics (env BFM_CT_STATS=1)
@@ -90,6 +93,13 @@ class CtPlan {
   unsigned long long* slow_ = nullptr;
   unsigned long long* stats_ = nullptr;
   CtPass pass_[3] = {};
+  // transposed pass 0 (2-D dyadic single-GPU plans): phi^T, and pass 0's
+  // chain and q in transposed layout before they are transposed back
+  CtPass pass0t_ = {};
+  bool t0_ = false;
+  double* phit_ = nullptr;
+  uint32_t* statet_ = nullptr;
+  double* qt_ = nullptr;
   bool ready_ = false;
   bool dyadic_ = false;
 };
