@@ -1256,20 +1256,20 @@ __global__ void __launch_bounds__(kDyThreads) ct_dy_kernel(CtPass p) {
   // bulk path: per line two cp.async.bulk copies (q: 8n bytes, chain: 4n
   // bytes) completing on one mbarrier.
   __shared__ __align__(8) uint64_t tma_bar;
-  const bool tma = p.pregathered && !p.strided && A.stride == 1 && (n & 3) == 0;
+  const bool tma = (p.pregathered || p.t0) && !p.strided && A.stride == 1 && (n & 3) == 0;
   if (tma) {
     if (threadIdx.x == 0) {
       mbar_init(&tma_bar, 1);
       unsigned bytes = 0;
       for (int ll = 0; ll < lpc; ++ll)
-        if (dy_carve(p, smem, ll).geo->valid) bytes += 12u * static_cast<unsigned>(n);
+        if (dy_carve(p, smem, ll).geo->valid) bytes += (p.a > 0 ? 12u : 8u) * static_cast<unsigned>(n);
       mbar_expect_tx(&tma_bar, bytes);
       for (int ll = 0; ll < lpc; ++ll) {
         const DySmem sm = dy_carve(p, smem, ll);
         const LineGeo g = *sm.geo;
         if (!g.valid) continue;
         bulk_g2s(sm.q, &p.phi[g.base], 8u * n, &tma_bar);
-        bulk_g2s(sm.ch, &p.state_in[g.base], 4u * n, &tma_bar);
+        if (p.a > 0) bulk_g2s(sm.ch, &p.state_in[g.base], 4u * n, &tma_bar);
       }
     }
     __syncthreads();  // the barrier is initialised before anyone waits on it
@@ -1282,7 +1282,10 @@ __global__ void __launch_bounds__(kDyThreads) ct_dy_kernel(CtPass p) {
     const int step = p.strided ? blockDim.x / lpc : tpl;
     const int first = p.strided ? static_cast<int>(threadIdx.x / lpc) : t;
     if (g.valid) {
-      if (p.a == 0) {
+      if (tma) {
+        // contiguous line: q (and the chain) are whole rows, moved by the
+        // TMA bulk copies issued above (one thread for the CTA)
+      } else if (p.a == 0) {
         for (int j = first; j < n; j += step)
           cp_async8(&sm.q[dyi(j)], &p.phi[g.phi_other + static_cast<long>(j) * A.stride]);
       } else if (p.pregathered && tma) {
