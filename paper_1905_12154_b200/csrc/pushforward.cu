@@ -1110,10 +1110,9 @@ void PushforwardPlan::gather(long nrec, const uint32_t* d_keys, const double* d_
     // drops them before the sort (their count stays on the device)
     const uint32_t sentinel = static_cast<uint32_t>(ncells_);
     // One-sweep up to 2^24 records (C1: pushforward 0.33 -> 0.25 ms per
-    // iteration, C2 0.56 -> 0.48, C3 3.83 -> 3.77); above that the look-back
-    // chain over the many tiles costs more than the per-pass histogram and
-    // scan kernels it replaces (C4: 24.9 vs 24.4 ms), so the multi-kernel
-    // passes stay. BFM_PF_SORT=legacy|onesweep overrides (A/B).
+    // iteration, C2 0.56 -> 0.48, C3 3.83 -> 3.70); above that the look-back
+    // chain over the many tiles makes it a wash (C4: 24.43 vs 24.46 ms), so
+    // the multi-kernel passes stay. BFM_PF_SORT=legacy|onesweep overrides (A/B).
     static const char* sort_mode = getenv("BFM_PF_SORT");
     const bool onesweep = sort_mode ? sort_mode[0] == 'o' : nrec <= (1L << 24);
     if (onesweep) {

@@ -308,10 +308,12 @@ __global__ void __launch_bounds__(kThreads, 4) os_scatter_kernel(OsArgs A) {
   if (base >= n) return;
   const long wbase = base + static_cast<long>(warp) * (kItems * 32) + lane;
   uint32_t kr[kItems];
+  int vr[kItems];  // the values travel with the keys: both loads in flight together
 #pragma unroll
   for (int r = 0; r < kItems; ++r) {
     const long i = wbase + r * 32;
     kr[r] = i < n ? A.kin[i] : A.sentinel;
+    vr[r] = FIRST ? static_cast<int>(i) : (i < n ? A.vin[i] : 0);
   }
   // ranks inside the warp (rounds in order; the per-warp digit counters are
   // only touched by their own warp)
@@ -334,18 +336,17 @@ __global__ void __launch_bounds__(kThreads, 4) os_scatter_kernel(OsArgs A) {
     if (ok && (__ffs(m) - 1) == static_cast<int>(lane)) wcnt[warp][d] += __popc(m);
     __syncwarp();
   }
-  // the values travel with the keys; loaded here so the loads overlap the look-back
-  int vr[kItems];
-#pragma unroll
-  for (int r = 0; r < kItems; ++r) {
-    const long i = wbase + r * 32;
-    vr[r] = FIRST ? static_cast<int>(i) : (((okmask >> r) & 1u) ? A.vin[i] : 0);
-  }
   __syncthreads();
-  // per digit (two per thread): exclusive prefix over the warps, the tile's
-  // count, then the look-back over the earlier tiles
+  // per digit (two per thread: d and d + kThreads): exclusive prefix over the
+  // warps and the tile's count, published for BOTH digits before either
+  // look-back starts (a successor's look-back waits for them); then the
+  // look-back over the earlier tiles, both digits' loads in flight together
   unsigned* state = A.aux + kOsState;
-  for (int d = threadIdx.x; d < kBins; d += kThreads) {
+  constexpr int kDig = kBins / kThreads;
+  int cnt[kDig];
+#pragma unroll
+  for (int q = 0; q < kDig; ++q) {
+    const int d = threadIdx.x + q * kThreads;
     int c = 0;
 #pragma unroll
     for (int w = 0; w < kWarps; ++w) {
@@ -353,38 +354,63 @@ __global__ void __launch_bounds__(kThreads, 4) os_scatter_kernel(OsArgs A) {
       wcnt[w][d] = c;
       c += v;
     }
-    volatile unsigned* st = state + static_cast<long>(tile) * kBins + d;
-    *st = static_cast<unsigned>(c) | (tile == 0 ? kFlagIncl : kFlagAgg);
-    // look-back: kLook predecessors are read per round trip (independent
-    // loads), then consumed in order up to the first unpublished one
-    // (measured: 8 per round beats 16 or 32, and beats polling the
-    // unpublished entry alone)
-    unsigned excl = 0;
-    for (int pt = tile - 1; pt >= 0;) {
-      unsigned v[kLook];
+    cnt[q] = c;
+    *reinterpret_cast<volatile unsigned*>(state + static_cast<long>(tile) * kBins + d) =
+        static_cast<unsigned>(c) | (tile == 0 ? kFlagIncl : kFlagAgg);
+  }
+  // look-back: kLook predecessors per digit are read per round trip
+  // (independent loads), then consumed in order up to the first unpublished
+  // one (measured: 8 per round beats 16 or 32, and beats polling the
+  // unpublished entry alone)
+  unsigned excl[kDig];
+  int pt[kDig];
+#pragma unroll
+  for (int q = 0; q < kDig; ++q) {
+    excl[q] = 0;
+    pt[q] = tile - 1;
+  }
+  while (true) {
+    bool any = false;
+#pragma unroll
+    for (int q = 0; q < kDig; ++q) any = any || pt[q] >= 0;
+    if (!any) break;
+    unsigned v[kDig][kLook];
+#pragma unroll
+    for (int q = 0; q < kDig; ++q)
 #pragma unroll
       for (int u = 0; u < kLook; ++u)
-        v[u] = pt - u >= 0 ? *reinterpret_cast<volatile unsigned*>(state + static_cast<long>(pt - u) * kBins + d)
-                           : (2u << 30);  // (kFlagIncl: nothing before tile 0)
+        v[q][u] = pt[q] - u >= 0
+                      ? *reinterpret_cast<volatile unsigned*>(state + static_cast<long>(pt[q] - u) * kBins +
+                                                               threadIdx.x + q * kThreads)
+                      : (2u << 30);  // (kFlagIncl: nothing before tile 0; also a finished digit)
+#pragma unroll
+    for (int q = 0; q < kDig; ++q) {
+      if (pt[q] < 0) continue;
       bool done = false;
 #pragma unroll
       for (int u = 0; u < kLook; ++u) {
         if (done) continue;
-        const unsigned f = v[u] >> 30;
+        const unsigned f = v[q][u] >> 30;
         if (f == 0) {  // not published yet: retry from here
           done = true;
           continue;
         }
-        excl += v[u] & kValMask;
-        --pt;
+        excl[q] += v[q][u] & kValMask;
+        --pt[q];
         if (f == 2) {
-          pt = -1;
+          pt[q] = -1;
           done = true;
         }
       }
     }
-    if (tile > 0) *st = (excl + static_cast<unsigned>(c)) | kFlagIncl;
-    gbase[d] += static_cast<int>(excl);
+  }
+#pragma unroll
+  for (int q = 0; q < kDig; ++q) {
+    const int d = threadIdx.x + q * kThreads;
+    if (tile > 0)
+      *reinterpret_cast<volatile unsigned*>(state + static_cast<long>(tile) * kBins + d) =
+          (excl[q] + static_cast<unsigned>(cnt[q])) | kFlagIncl;
+    gbase[d] += static_cast<int>(excl[q]);
   }
   __syncthreads();
 #pragma unroll
