@@ -13,6 +13,7 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 OPS = {  # kernel -> operator of bench.py's rooflines
     "ct_dy_kernel": "ctransform", "ct_pass_kernel": "ctransform",
+    "ct_transpose_f64": "ctransform", "ct_transpose_state": "ctransform",
     "pois_fft_kernel": "poisson", "pois_naive_kernel": "poisson",
     "red_partial_kernel": "reductions", "red_final_kernel": "reductions", "axpy_dev_kernel": "reductions",
     "ctl_decide_kernel": "reductions",
@@ -60,7 +61,7 @@ def main():
             t[0] += d.get("gpu__time_duration.sum", 0)
             t[1] += 1
             t[2] += b
-            per_op[OPS.get(k, "pushforward" if k.startswith(("pf_", "rs_")) else "other")] += b
+            per_op[OPS.get(k, "pushforward" if k.startswith(("pf_", "rs_", "os_")) else "other")] += b
         T = sum(v[0] for v in per_kernel.values())
         lines = [f"# one steady-state {cfg.upper()} iteration ({grid}) after 8 warm-up iterations, "
                  f"eager launches (ncu --profile-from-start off, --clock-control none; serialised, cold-cache "
