@@ -37,7 +37,14 @@ x = [(np.arange(n) + 0.5) / n for n in shape]
 X = np.meshgrid(*x, indexing="ij")
 u2 = sum(0.5 * Xi * Xi - 0.5 * Xi for Xi in X) * 0.97
 rho2 = bfm.pushforward_density(bfm.map_from_conjugate(u2), mu)
-print(hashlib.sha256(rho.tobytes()).hexdigest(), hashlib.sha256(rho2.tobytes()).hexdigest())
+# no mass at all (every key is the sentinel), and a single massive source
+rho3 = bfm.pushforward_density(disp, np.zeros(shape))
+one = np.zeros(shape)
+one.flat[one.size // 3] = 2.5
+rho4 = bfm.pushforward_density(disp, one)
+assert not rho3.any() and abs(rho4.sum() - 2.5) < 1e-12
+print(hashlib.sha256(rho.tobytes()).hexdigest(), hashlib.sha256(rho2.tobytes()).hexdigest(),
+      hashlib.sha256(rho4.tobytes()).hexdigest())
 """
 
 
