@@ -542,13 +542,14 @@ struct bfm_solver {
     }, sd());
   }
   // before_last: the output's readers on the side stream (the last pass waits)
-  void ctransform(const double* in, double* out, cudaEvent_t before_last = nullptr) {
+  // concave: the input is itself a c-transform (a speed hint for the plan, see CtPlan::run)
+  void ctransform(const double* in, double* out, cudaEvent_t before_last = nullptr, bool concave = false) {
     timed(BFM_OP_CTRANSFORM, [&] {
       if (power) {
         if (before_last) BFM_CUDA(cudaStreamWaitEvent(stream, before_last, 0));
         ctpow->run(in, out, stream, &ws.lc);
       } else {
-        ws.ctp().run(in, out, stream, &ws.lc, before_last);
+        ws.ctp().run(in, out, stream, &ws.lc, before_last, concave);
       }
     });
   }
@@ -573,7 +574,7 @@ struct bfm_solver {
   cudaEvent_t pending_read = nullptr;  // side-stream reads of phi/psi not yet fenced
   void enqueue_probe() {  // solver.hpp:264-280
     if (cfg.mode == BFM_MODE_BACK_AND_FORTH) {
-      ctransform(phi.p, psi.p, pending_read);
+      ctransform(phi.p, psi.p, pending_read, true);  // phi = psi^c from the last step
       pending_read = nullptr;
       pair_value_async();
       pending_read = timing ? nullptr : mark(side);
@@ -594,7 +595,7 @@ struct bfm_solver {
     pair_value_async();
     pending_read = timing ? nullptr : mark(side);
     decide(kStageFirst, kSlotPair);
-    ctransform(psi.p, phi.p, pending_read);
+    ctransform(psi.p, phi.p, pending_read, true);  // psi = phi^c
     pending_read = nullptr;
     pair_value_async();
     pending_read = timing ? nullptr : mark(side);

@@ -1201,6 +1201,11 @@ __device__ __noinline__ int dy_orient_exact(const CtPass& p, const LineGeo& g, c
   return dy_sign_slow(x);
 }
 
+// QG: the small-state form (p.qglobal): contiguous lines only; q and the chain
+// are not staged in shared memory but read from global memory (L1/L2: the
+// line's rows were just streamed) by the f~ phase, the rare exact tests, the
+// flagged queries and the output gather.
+template <bool QG>
 __global__ void __launch_bounds__(kDyThreads) ct_dy_kernel(CtPass p) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int tpl = p.tpl;
@@ -1255,6 +1260,7 @@ __global__ void __launch_bounds__(kDyThreads) ct_dy_kernel(CtPass p) {
   // Contiguous pregathered passes (a >= 1 along the last axis) take the TMA
   // bulk path: per line two cp.async.bulk copies (q: 8n bytes, chain: 4n
   // bytes) completing on one mbarrier.
+  if (!QG) {
   __shared__ __align__(8) uint64_t tma_bar;
   const bool tma = (p.pregathered || p.t0) && !p.strided && A.stride == 1 && (n & 3) == 0;
   if (tma) {
@@ -1321,12 +1327,14 @@ __global__ void __launch_bounds__(kDyThreads) ct_dy_kernel(CtPass p) {
     cp_async_wait_all();
   }
   __syncthreads();
+  }
 
   const LineGeo geo = *s.geo;
   const bool active = geo.valid;
   const double* F = s.f;
-  const double* Q = s.q;
-  const uint32_t* CH = s.ch;
+  // QG: the line's own rows in global memory (contiguous: element j at [j])
+  const double* Q = QG ? p.phi + (p.a == 0 ? geo.phi_other : geo.base) : s.q;
+  const uint32_t* CH = QG ? (p.a > 0 ? p.state_in + geo.base : nullptr) : s.ch;
   auto P_f = [&](int j) { return F[dyi(j)]; };
   const double hh = 0.5 * h;
   auto P_y = [&](int j) { return dy_coord(hh, j); };
@@ -1734,10 +1742,12 @@ __global__ void __launch_bounds__(kDyThreads) ct_dy_kernel(CtPass p) {
       for (int k = first; k < n; k += step) {
         const long node = g.base + static_cast<long>(k) * A.stride;
         const int win = (sm.scal[7] ? sm.H : sm.res)[k];
+        const uint32_t* chp = QG ? CH : sm.ch;  // (QG: one line per thread group, ml == l)
+        const double* qp = QG ? Q : sm.q;
         const uint32_t packed = p.a == 0 ? static_cast<uint32_t>(win)
-                                         : (sm.ch[win] | (static_cast<uint32_t>(win) << 16));
+                                         : (chp[win] | (static_cast<uint32_t>(win) << 16));
         p.state_out[node] = packed;
-        if (p.q_out) p.q_out[node] = sm.q[dyi(win)];
+        if (p.q_out) p.q_out[node] = qp[dyi(win)];
       }
   }
 }
@@ -1949,17 +1959,26 @@ void CtPlan::setup(const GridDesc& loc, const GridDesc& global, int pb, int pe, 
     for (int b = 0; b < loc.d; ++b)
       if (!P.ax[b].dyadic && !P.ax[b].GF) P.fixed = 0;
     const bool dy = dyadic_;
-    if (dy) {
+    auto dy_layout = [&](CtPass& P, int a, int n, bool qg) {
       // exact-hull kernel: (s, q) per point in shared memory; about 11 points
       // per thread, up to kDyThreads threads per line
       // about cpt points per thread, and an ODD count C (the unpadded
       // per-thread chunk walks are then bank-conflict free)
       int cpt = 11;
       if (const char* e = getenv("BFM_CT_C")) cpt = std::max(2, atoi(e));  // tuning experiments
+      // Small-state form (qg) for long contiguous lines: q and the chain stay
+      // in global memory, so four 4096-lines of 192 threads fit one SM
+      // instead of two of 384. On a generic potential that is 24-29 % faster
+      // (C5 4096^2: 1.91 -> 1.44 ms per call, 8192^2: 8.44 -> 6.00); on a
+      // c-concave input it is 1-7 % slower (its exactly collinear runs send
+      // 16 % of the points through the exact local test, which then reads q
+      // and the chain from L2), so the caller's hint picks the form per call.
+      if (qg) cpt = 22;
+      if (const char* e = getenv("BFM_CT_QG_C")) { if (qg) cpt = std::max(2, atoi(e)); }
       int best_tpl = 32, best_err = 1 << 30;
       for (int tp = 32; tp <= kDyThreads; tp += 32) {
         const int c = (n + tp - 1) / tp;
-        const int err = std::abs(c - cpt) + ((c & 1) ? 0 : 3) + (tp > n ? 2000 : 0);
+        const int err = std::abs(c - cpt) + ((c & 1) || qg ? 0 : 3) + (tp > n ? 2000 : 0);
         if (err < best_err) {
           best_err = err;
           best_tpl = tp;
@@ -1970,10 +1989,11 @@ void CtPlan::setup(const GridDesc& loc, const GridDesc& global, int pb, int pe, 
       int o = 0;
       P.off_fv = o;
       o = align16(o + 8 * n);
+      P.qglobal = qg ? 1 : 0;
       P.off_chain = o;
-      o = align16(o + 8 * n);
+      if (!qg) o = align16(o + 8 * n);
       P.off_flag = o;  // chain (uint32, passes a >= 1)
-      if (a > 0) o = align16(o + 4 * n);
+      if (a > 0 && !qg) o = align16(o + 4 * n);
       P.off_hidx = o;  // hull
       o = align16(o + 2 * P.tpl * P.C);
       P.off_H = o;  // per-query tangent / winner
@@ -1987,6 +2007,7 @@ void CtPlan::setup(const GridDesc& loc, const GridDesc& global, int pb, int pe, 
       if (o > budget) throw std::invalid_argument("ctransform: grid line too long for shared memory");
       // two CTAs per SM: a CTA's loads overlap the other's hull work
       int lpc = std::min<long>(budget / (2 * o), kDyThreads / (2 * P.tpl));
+      if (qg) lpc = 1;  // independent CTAs, as many as fit
       // strided passes: two adjacent columns per CTA (one CTA per SM) rather
       // than two one-column CTAs — the column pair shares every 32-byte
       // sector of its loads and stores (C3 c-transform 1.774 -> 1.697 ms per
@@ -2003,6 +2024,15 @@ void CtPlan::setup(const GridDesc& loc, const GridDesc& global, int pb, int pe, 
       P.lpc = std::max(lpc, 1);
       P.slow_queries = slow_;
       P.stats = stats_;
+    };
+    if (dy) {
+      dy_layout(P, a, n, false);
+      // the small-state form of the last (contiguous) pass, for lines of 4096 points and more
+      if (a == loc.d - 1 && n >= 4096 && !virtual_cols) {
+        passq_ = P;
+        dy_layout(passq_, a, n, true);
+        have_q_ = true;
+      }
       continue;
     }
     P.tpl = n <= 512 ? 32 : (n <= 1024 ? 64 : (n <= 2048 ? 128 : 256));
@@ -2064,8 +2094,32 @@ void CtPlan::setup(const GridDesc& loc, const GridDesc& global, int pb, int pe, 
     lpc = std::min(lpc, 8);
     lpc = static_cast<int>(std::min<long>(lpc, T.nlines));
     T.lpc = std::max(lpc, 1);
+    // (the transposed pass 0 is contiguous: on a square grid it can take the
+    // last pass's small-state layout)
+    have_qt_ = have_q_ && loc.n[0] == loc.n[1];
+    if (have_qt_) {
+      const CtPass& L = passq_;
+      CtPass& Q = pass0tq_;
+      Q = T;
+      Q.qglobal = 1;
+      Q.tpl = L.tpl;
+      Q.C = L.C;
+      Q.lpc = 1;
+      Q.off_fv = L.off_fv;
+      Q.off_chain = L.off_chain;
+      Q.off_flag = L.off_flag;
+      Q.off_hidx = L.off_hidx;
+      Q.off_H = L.off_H;
+      Q.off_list = L.off_list;
+      Q.off_lohi = L.off_lohi;
+      Q.off_scal = L.off_scal;
+      Q.line_bytes = L.line_bytes;
+    }
   }
-  BFM_CUDA(cudaFuncSetAttribute(ct_dy_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, budget));
+  qg_mode_ = 2;  // 0: never, 1: whenever available, 2: by the caller's hint (default)
+  if (const char* e = getenv("BFM_CT_QG")) qg_mode_ = atoi(e);
+  BFM_CUDA(cudaFuncSetAttribute(ct_dy_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, budget));
+  BFM_CUDA(cudaFuncSetAttribute(ct_dy_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, budget));
   BFM_CUDA(cudaFuncSetAttribute(ct_pass_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, budget));
   ready_ = true;
 }
@@ -2073,7 +2127,10 @@ void CtPlan::setup(const GridDesc& loc, const GridDesc& global, int pb, int pe, 
 void CtPlan::launch(const CtPass& P, cudaStream_t stream, LaunchCounter* lc) {
   const long blocks = (P.nlines + P.lpc - 1) / P.lpc;
   if (dyadic_)
-    ct_dy_kernel<<<static_cast<unsigned>(blocks), P.lpc * P.tpl, P.lpc * P.line_bytes, stream>>>(P);
+    if (P.qglobal)
+      ct_dy_kernel<true><<<static_cast<unsigned>(blocks), P.lpc * P.tpl, P.lpc * P.line_bytes, stream>>>(P);
+    else
+      ct_dy_kernel<false><<<static_cast<unsigned>(blocks), P.lpc * P.tpl, P.lpc * P.line_bytes, stream>>>(P);
   else
     ct_pass_kernel<<<static_cast<unsigned>(blocks), P.lpc * P.tpl, P.lpc * P.line_bytes, stream>>>(P);
   BFM_LAUNCH_CHECK("ct_pass_kernel");
@@ -2106,13 +2163,14 @@ void CtPlan::run_rows(const uint32_t* d_chain0, const double* d_q, double* d_out
 // Pass a >= 1 reads phi(chain*, y) at its own nodes from the previous pass's
 // q output (written next to the argmin chain) instead of gathering phi.
 void CtPlan::run(const double* d_phi, double* d_out, cudaStream_t stream, LaunchCounter* lc,
-                 cudaEvent_t before_last) {
+                 cudaEvent_t before_last, bool concave_input) {
+  const bool qg = qg_mode_ == 1 || (qg_mode_ == 2 && !concave_input);
   for (int a = 0; a < g_.d; ++a) {
     if (a == 0 && t0_) {
       const int n0 = g_.n[0], n1 = g_.n[1];
       const dim3 gin((n1 + 31) / 32, (n0 + 31) / 32), gout((n0 + 31) / 32, (n1 + 31) / 32);
       ct_transpose_f64<<<gin, 256, 0, stream>>>(d_phi, phit_, n0, n1);
-      CtPass P = pass0t_;
+      CtPass P = (qg && have_qt_) ? pass0tq_ : pass0t_;
       P.phi = phit_;
       P.pregathered = 0;
       P.state_in = nullptr;
@@ -2125,7 +2183,7 @@ void CtPlan::run(const double* d_phi, double* d_out, cudaStream_t stream, Launch
       if (lc) lc->add(2);
       continue;
     }
-    CtPass P = pass_[a];
+    CtPass P = (qg && have_q_ && a == g_.d - 1) ? passq_ : pass_[a];
     if (P.last && before_last) BFM_CUDA(cudaStreamWaitEvent(stream, before_last, 0));
     P.phi = a == 0 ? d_phi : qbuf_[(a - 1) & 1];
     P.pregathered = a > 0 ? 1 : 0;

@@ -43,6 +43,10 @@ struct CtPass {
   // pass 0 on the transposed potential (2-D dyadic grids): its lines are the
   // rows of phi^T, contiguous like the last pass's
   int t0;
+  // small line state (contiguous dyadic passes of long lines): q and the chain
+  // are read from global memory where needed instead of being staged, so four
+  // lines fit one SM's shared memory
+  int qglobal;
   // statistics (device counters, may be null): lines that needed exact resolution
   unsigned long long* slow_queries;
   unsigned long long* stats;  // optional diagnostics (env BFM_CT_STATS=1)
@@ -61,8 +65,11 @@ class CtPlan {
   // before_last (optional): an event the last pass waits for — the pass that
   // writes d_out — so readers of d_out on another stream can overlap the
   // earlier passes.
+  // concave_input: a hint that phi is itself a c-transform (exactly collinear
+  // runs); picks the staged form of the long contiguous passes over the
+  // small-state one (see setup). The result does not depend on it.
   void run(const double* d_phi, double* d_out, cudaStream_t stream, LaunchCounter* lc,
-           cudaEvent_t before_last = nullptr);
+           cudaEvent_t before_last = nullptr, bool concave_input = false);
 
   // Multi-GPU slab decomposition along axis 0. Column slab:
   // the (n0 x ncols) block of the flattened non-axis-0 columns; pass 0 writes
@@ -97,6 +104,11 @@ class CtPlan {
   // chain and q in transposed layout before they are transposed back
   CtPass pass0t_ = {};
   bool t0_ = false;
+  // small-state forms of the last pass and of the transposed pass 0
+  CtPass passq_ = {};
+  CtPass pass0tq_ = {};
+  bool have_q_ = false, have_qt_ = false;
+  int qg_mode_ = 2;
   double* phit_ = nullptr;
   uint32_t* statet_ = nullptr;
   double* qt_ = nullptr;
