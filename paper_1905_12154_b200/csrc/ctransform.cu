@@ -1066,6 +1066,15 @@ __device__ __forceinline__ DySmem dy_carve(const CtPass& p, unsigned char* base,
 }
 
 // Exact s_j = G_j + hs(y_j) of element j (G from the chain; exact on dyadic grids).
+__device__ __forceinline__ double dy_s_c(const CtPass& p, const LineGeo& g, uint32_t c, int j) {
+  const double y = dy_coord(0.5 * p.ax[p.a].h, j);
+  double G = 0.0;
+  if (p.a >= 1) {
+    G = g_approx(p.ax[0], g.k[0], static_cast<int>(c & 0xFFFFu));
+    if (p.a >= 2) G += g_approx(p.ax[1], g.k[1], static_cast<int>(c >> 16));
+  }
+  return G + 0.5 * y * y;
+}
 __device__ __forceinline__ double dy_s(const CtPass& p, const LineGeo& g, const uint32_t* ch, int j) {
   const double y = dy_coord(0.5 * p.ax[p.a].h, j);
   double G = 0.0;
@@ -1120,19 +1129,8 @@ __device__ __noinline__ int dy_sign_slow(const double* x) {
   return e.sign();
 }
 
-// Exact sign of (c-a) f_b - (c-b) f_a - (b-a) f_c with f = s - q (a < b < c):
-// negative iff b is a strict lower-hull corner of (a, b, c).
-// Exact sign of 2 f_b - f_a - f_c for consecutive a = b-1, c = b+1 (the
-// local-corner test): (2 s_b - s_a - s_c) is exact in fp64 and 2 q_b is
-// exact, so the value is an exact sum of four doubles, distilled by
-// error-free cascades (usually one pass decides).
-__device__ __forceinline__ int dy_orient_local(const CtPass& p, const LineGeo& g, const uint32_t* ch,
-                                               const double* Q, int b) {
-  const double sa = dy_s(p, g, ch, b - 1), sb = dy_s(p, g, ch, b), sc = dy_s(p, g, ch, b + 1);
-  double x0 = (2.0 * sb - sa) - sc;
-  double x1 = -2.0 * Q[dyi(b)];
-  double x2 = Q[dyi(b - 1)];
-  double x3 = Q[dyi(b + 1)];
+// Exact sign of x0 + x1 + x2 + x3: error-free cascades (usually one pass decides).
+__device__ __forceinline__ int dy_sign_sum4(double x0, double x1, double x2, double x3) {
   for (int pass = 0; pass < 16; ++pass) {
     double sm, er;
     bfmx::two_sum(x1, x0, sm, er);
@@ -1155,6 +1153,18 @@ __device__ __forceinline__ int dy_orient_local(const CtPass& p, const LineGeo& g
   e.grow(x2);
   e.grow(x3);
   return e.sign();
+}
+
+// Exact sign of (c-a) f_b - (c-b) f_a - (b-a) f_c with f = s - q (a < b < c):
+// negative iff b is a strict lower-hull corner of (a, b, c).
+// Exact sign of 2 f_b - f_a - f_c for consecutive a = b-1, c = b+1 (the
+// local-corner test): (2 s_b - s_a - s_c) is exact in fp64 and 2 q_b is
+// exact, so the value is an exact sum of four doubles, distilled by
+// error-free cascades (usually one pass decides).
+__device__ __forceinline__ int dy_orient_local(const CtPass& p, const LineGeo& g, const uint32_t* ch,
+                                               const double* Q, int b) {
+  const double sa = dy_s(p, g, ch, b - 1), sb = dy_s(p, g, ch, b), sc = dy_s(p, g, ch, b + 1);
+  return dy_sign_sum4((2.0 * sb - sa) - sc, -2.0 * Q[dyi(b)], Q[dyi(b - 1)], Q[dyi(b + 1)]);
 }
 
 __device__ __noinline__ int dy_orient_exact(const CtPass& p, const LineGeo& g, const uint32_t* ch,
@@ -1342,10 +1352,41 @@ __global__ void __launch_bounds__(kDyThreads) ct_dy_kernel(CtPass p) {
   {
     double amax = 0.0;
     if (active)
-      for (int j = t; j < n; j += tpl) {
-        const double f = dy_s(p, geo, CH, j) - Q[dyi(j)];
-        s.f[dyi(j)] = f;
-        amax = fmax(amax, fabs(f));
+      if (QG) {
+        // q and the chain straight from global memory, eight coalesced loads
+        // of each in flight per thread. The small-state form also remembers
+        // which f~ are exact (no rounding in s - q): three exact neighbours
+        // decide a local corner from shared memory alone, without reading q
+        // and the chain back from L2.
+        constexpr int kB = 8;
+        // (flags in the second half of the res buffer, free until the hull is compacted)
+        uint8_t* fx = reinterpret_cast<uint8_t*>(s.res) + n;
+        for (int jb = t; jb < n; jb += kB * tpl) {
+          double qv[kB];
+          uint32_t cv[kB];
+#pragma unroll
+          for (int u = 0; u < kB; ++u) {
+            const int j = jb + u * tpl;
+            qv[u] = j < n ? __ldg(Q + j) : 0.0;
+            cv[u] = (p.a > 0 && j < n) ? __ldg(CH + j) : 0u;
+          }
+#pragma unroll
+          for (int u = 0; u < kB; ++u) {
+            const int j = jb + u * tpl;
+            if (j >= n) continue;
+            double f, er;
+            bfmx::two_sum(dy_s_c(p, geo, cv[u], j), -qv[u], f, er);
+            fx[j] = er == 0.0 ? 1 : 0;
+            s.f[dyi(j)] = f;
+            amax = fmax(amax, fabs(f));
+          }
+        }
+      } else {
+        for (int j = t; j < n; j += tpl) {
+          const double f = dy_s(p, geo, CH, j) - Q[dyi(j)];
+          s.f[dyi(j)] = f;
+          amax = fmax(amax, fabs(f));
+        }
       }
     for (int o = 16; o > 0; o >>= 1) amax = fmax(amax, __shfl_xor_sync(0xffffffffu, amax, o));
     if ((threadIdx.x & 31) == 0) atomicMax(&s.scal[0], dbits(amax));
@@ -1400,7 +1441,15 @@ __global__ void __launch_bounds__(kDyThreads) ct_dy_kernel(CtPass p) {
           k = filt(j - 1, fa, j, fb, j + 1, fc, und);
           if (und) {
             if (p.stats) ++c_xchunk;
-            k = dy_orient_local(p, geo, CH, Q, j) < 0;
+            if (QG && keep[n + j - 1] && keep[n + j] && keep[n + j + 1]) {
+              // 2 f_b - f_a - f_c from exact f~ values
+              double h1, l1, h2, l2;
+              bfmx::two_sum(fb, -fa, h1, l1);
+              bfmx::two_sum(fb, -fc, h2, l2);
+              k = dy_sign_sum4(l1, l2, h1, h2) < 0;
+            } else {
+              k = dy_orient_local(p, geo, CH, Q, j) < 0;
+            }
           }
         }
         keep[j] = static_cast<uint8_t>(k);
