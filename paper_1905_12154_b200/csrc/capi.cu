@@ -572,9 +572,12 @@ struct bfm_solver {
   // overwrites one of them) waits for it (pending_read). An axpy waits for
   // the decision that produced its sigma.
   cudaEvent_t pending_read = nullptr;  // side-stream reads of phi/psi not yet fenced
+  // which c-concave-input calls ask for the staged c-transform kernel (bit 0:
+  // the probe's phi -> psi, bit 1: the step's psi -> phi); BFM_CT_HINTS overrides
+  int ct_hints = getenv("BFM_CT_HINTS") ? atoi(getenv("BFM_CT_HINTS")) : 3;
   void enqueue_probe() {  // solver.hpp:264-280
     if (cfg.mode == BFM_MODE_BACK_AND_FORTH) {
-      ctransform(phi.p, psi.p, pending_read, true);  // phi = psi^c from the last step
+      ctransform(phi.p, psi.p, pending_read, (ct_hints & 1) != 0);  // phi = psi^c from the last step
       pending_read = nullptr;
       pair_value_async();
       pending_read = timing ? nullptr : mark(side);
@@ -595,7 +598,7 @@ struct bfm_solver {
     pair_value_async();
     pending_read = timing ? nullptr : mark(side);
     decide(kStageFirst, kSlotPair);
-    ctransform(psi.p, phi.p, pending_read, true);  // psi = phi^c
+    ctransform(psi.p, phi.p, pending_read, (ct_hints & 2) != 0);  // psi = phi^c
     pending_read = nullptr;
     pair_value_async();
     pending_read = timing ? nullptr : mark(side);
