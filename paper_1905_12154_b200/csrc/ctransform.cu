@@ -2014,6 +2014,11 @@ void CtPlan::setup(const GridDesc& loc, const GridDesc& global, int pb, int pe, 
       // about cpt points per thread, and an ODD count C (the unpadded
       // per-thread chunk walks are then bank-conflict free)
       int cpt = 11;
+      // tiny grids (C1: 256 lines of 256 points, one line per CTA): three points
+      // per thread shorten the per-thread loops of a latency-bound line (C1
+      // c-transform 55 -> 45 us per call); with many lines (128^3) or longer
+      // ones (512^2) eleven stay better
+      if (n <= 256 && P.nlines < 1024) cpt = 3;
       if (const char* e = getenv("BFM_CT_C")) cpt = std::max(2, atoi(e));  // tuning experiments
       // Small-state form (qg) for long contiguous lines: q and the chain stay
       // in global memory, so four 4096-lines of 192 threads fit one SM
