@@ -1,0 +1,32 @@
+"""Small dyadic grids through the exact-hull c-transform: every thread /
+chunk layout the plan can pick for short lines (one to eight points per
+thread, lines shorter than a warp, one-point axes' neighbours) against the
+CPU restatement, on a generic potential and on its c-transform (exactly
+collinear runs). Reference: transforms.hpp:396-432."""
+import numpy as np
+import pytest
+
+import oracle_lib as O
+import paper_1905_12154_b200 as bfm
+from paper_1905_12154_b200 import synthetic
+
+pytestmark = pytest.mark.gpu
+
+SHAPES = [(2, 2), (4, 4), (8, 8), (16, 16), (32, 32), (64, 64), (128, 128), (256, 256), (8, 256), (256, 8),
+          (2, 256), (128, 2), (256,), (64,), (4, 4, 4), (8, 8, 8), (16, 16, 4)]
+
+
+@pytest.fixture(scope="module", autouse=True)
+def need_gpu():
+    if not bfm.device_available():
+        pytest.skip("no CUDA device")
+
+
+@pytest.mark.parametrize("shape", SHAPES)
+def test_small_dyadic_grids_bitwise(shape):
+    rng = np.random.default_rng(sum(shape))
+    phi = synthetic.c5_potential(shape)[0] + 0.01 * rng.standard_normal(shape)
+    psi = bfm.ctransform(phi)
+    want = O.orc_ctransform(phi)
+    assert O.n_bit_diff(psi, want) == 0
+    assert O.n_bit_diff(bfm.ctransform(psi), O.orc_ctransform(want)) == 0
