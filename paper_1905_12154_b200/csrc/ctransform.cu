@@ -2172,6 +2172,7 @@ void CtPlan::setup(const GridDesc& loc, const GridDesc& global, int pb, int pe, 
   }
   qg_mode_ = 2;  // 0: never, 1: whenever available, 2: by the caller's hint (default)
   if (const char* e = getenv("BFM_CT_QG")) qg_mode_ = atoi(e);
+  if (const char* e = getenv("BFM_CT_QG_MIX")) qg_mix_ = atoi(e);
   BFM_CUDA(cudaFuncSetAttribute(ct_dy_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, budget));
   BFM_CUDA(cudaFuncSetAttribute(ct_dy_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, budget));
   BFM_CUDA(cudaFuncSetAttribute(ct_pass_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, budget));
@@ -2219,12 +2220,15 @@ void CtPlan::run_rows(const uint32_t* d_chain0, const double* d_q, double* d_out
 void CtPlan::run(const double* d_phi, double* d_out, cudaStream_t stream, LaunchCounter* lc,
                  cudaEvent_t before_last, bool concave_input) {
   const bool qg = qg_mode_ == 1 || (qg_mode_ == 2 && !concave_input);
+  // hinted calls: per-pass choice of the form (bit 0: transposed pass 0, bit 1: last pass)
+  const bool qg_first = qg || (qg_mode_ == 2 && concave_input && (qg_mix_ & 1));
+  const bool qg_last = qg || (qg_mode_ == 2 && concave_input && (qg_mix_ & 2));
   for (int a = 0; a < g_.d; ++a) {
     if (a == 0 && t0_) {
       const int n0 = g_.n[0], n1 = g_.n[1];
       const dim3 gin((n1 + 31) / 32, (n0 + 31) / 32), gout((n0 + 31) / 32, (n1 + 31) / 32);
       ct_transpose_f64<<<gin, 256, 0, stream>>>(d_phi, phit_, n0, n1);
-      CtPass P = (qg && have_qt_) ? pass0tq_ : pass0t_;
+      CtPass P = (qg_first && have_qt_) ? pass0tq_ : pass0t_;
       P.phi = phit_;
       P.pregathered = 0;
       P.state_in = nullptr;
@@ -2237,7 +2241,7 @@ void CtPlan::run(const double* d_phi, double* d_out, cudaStream_t stream, Launch
       if (lc) lc->add(2);
       continue;
     }
-    CtPass P = (qg && have_q_ && a == g_.d - 1) ? passq_ : pass_[a];
+    CtPass P = (qg_last && have_q_ && a == g_.d - 1) ? passq_ : pass_[a];
     if (P.last && before_last) BFM_CUDA(cudaStreamWaitEvent(stream, before_last, 0));
     P.phi = a == 0 ? d_phi : qbuf_[(a - 1) & 1];
     P.pregathered = a > 0 ? 1 : 0;

@@ -109,6 +109,7 @@ class CtPlan {
   CtPass pass0tq_ = {};
   bool have_q_ = false, have_qt_ = false;
   int qg_mode_ = 2;
+  int qg_mix_ = 0;  // hinted calls: passes that still take the small-state form (bit 0: pass 0, bit 1: last)
   double* phit_ = nullptr;
   uint32_t* statet_ = nullptr;
   double* qt_ = nullptr;
