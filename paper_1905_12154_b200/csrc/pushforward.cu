@@ -204,11 +204,9 @@ struct GatherArgs {
   const double* src;  // record mass
   const double* target;  // may be null: output rho
   double* out;
-  // records in sorted (bucket) order, packed by pf_pack_kernel: (mass,
-  // upper weights per axis) and the clamp mask of the record at each sorted
-  // position — one contiguous read per deposit instead of 2 + d scattered ones
-  const double4* rec;
-  const uint8_t* rmask;
+  // every deposit's weight for each of its 2^d corners, in sorted (bucket)
+  // order and corner-major (pf_pack_kernel): wts[b * nrec + position]
+  const double* wts;
 };
 
 // Weight of the deposit at sorted position pos into the corner-b target
@@ -216,30 +214,32 @@ struct GatherArgs {
 // the reference's weight (pushforward.hpp:161-166: m times each axis's upper
 // or lower barycentric weight, in axis order), from the packed record.
 __device__ __forceinline__ double pos_weight(const GatherArgs& A, int pos, int b) {
-  if (b & A.rmask[pos]) return 0.0;
-  const double4 r = A.rec[pos];
-  double wt = r.x;
-  const double wa[3] = {r.y, r.z, r.w};
-#pragma unroll
-  for (int a = 0; a < 3; ++a)
-    if (a < A.g.d) wt *= ((b >> a) & 1) ? wa[a] : 1.0 - wa[a];
-  return wt;
+  // packed per corner by pf_pack_kernel: corner-major, so a bucket's deposits
+  // are consecutive doubles for the corner that reads them
+  return A.wts[static_cast<long>(b) * A.nrec + pos];
 }
 
 // records -> sorted order (one pass after the sort)
 __global__ void pf_pack_kernel(const int* bucket, long nrec, const int* d_n, const double* src, const double* w,
-                               const uint8_t* cmask, int d, double4* rec, uint8_t* rmask) {
+                               const uint8_t* cmask, int d, double* wts) {
+  // the weight of every deposit for each of its 2^d corners (the reference's
+  // expression, pushforward.hpp:161-166: m times each axis's upper or lower
+  // barycentric weight, in axis order; 0 on a clamped axis's upper corner),
+  // corner-major: wts[b * nrec + sorted position]
   const long n = d_n ? *d_n : nrec;
   for (long i = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<long>(gridDim.x) * blockDim.x) {
     const int s = bucket[i];
-    double4 r;
-    r.x = src[s];
-    r.y = d > 0 ? w[s] : 0.0;
-    r.z = d > 1 ? w[nrec + s] : 0.0;
-    r.w = d > 2 ? w[2 * nrec + s] : 0.0;
-    rec[i] = r;
-    rmask[i] = cmask[s];
+    const double m = src[s];
+    double wa[3] = {0.0, 0.0, 0.0};
+    for (int a = 0; a < d; ++a) wa[a] = w[a * nrec + s];
+    const int mask = cmask[s];
+    for (int b = 0; b < (1 << d); ++b) {
+      double wt = m;
+      for (int a = 0; a < d; ++a) wt *= ((b >> a) & 1) ? wa[a] : 1.0 - wa[a];
+      if (b & mask) wt = 0.0;
+      wts[static_cast<long>(b) * nrec + i] = wt;
+    }
   }
 }
 
@@ -962,7 +962,7 @@ PushforwardPlan::~PushforwardPlan() {
                   static_cast<void*>(off_), static_cast<void*>(end_), static_cast<void*>(heavy_),
                   static_cast<void*>(nheavy_), static_cast<void*>(hbuf_),
                   static_cast<void*>(row0_), static_cast<void*>(bcount_),
-                  static_cast<void*>(large_), static_cast<void*>(rec_), static_cast<void*>(rmask_),
+                  static_cast<void*>(large_), static_cast<void*>(wts_),
                   static_cast<void*>(lmeta_)})
     if (p) dfree(p);
   if (hcounts_) cudaFreeHost(hcounts_);
@@ -1031,10 +1031,8 @@ void PushforwardPlan::ensure_records(long nrec) {
   const long hcap = std::max<long>(deposits, std::max<long>(static_cast<long>(med_blocks_) * kMedWarps * kMedium,
                                                             static_cast<long>(large_blocks_) * kLarge));
   BFM_CUDA(dmalloc(&hbuf_, hcap * sizeof(double)));
-  if (rec_) dfree(rec_);
-  if (rmask_) dfree(rmask_);
-  BFM_CUDA(dmalloc(&rec_, cap * sizeof(double4)));
-  BFM_CUDA(dmalloc(&rmask_, cap * sizeof(uint8_t)));
+  if (wts_) dfree(wts_);
+  BFM_CUDA(dmalloc(&wts_, cap * sizeof(double) * (1L << g_.d)));  // 2^d corner weights per record
   sorter_.init(cap);
   rec_cap_ = cap;
 }
@@ -1122,10 +1120,9 @@ void PushforwardPlan::gather(long nrec, const uint32_t* d_keys, const double* d_
       // (the records are packed after the sort: in sorted order the source
       // ids of neighbouring positions are close, so the gathers coalesce;
       // fused into the last scatter they cost 4x the separate kernel)
-      const int* d_n = sorter_.sort_onesweep(d_keys, nrec, sentinel, key_bits_, nullptr, stream, lc, &skeys, &svals);
+      const int* d_n = sorter_.sort_onesweep(d_keys, nrec, sentinel, key_bits_, stream, lc, &skeys, &svals);
       pf_bounds_kernel<<<grid_for(nrec, 256), 256, 0, stream>>>(skeys, nrec, d_n, sentinel, off_, end_);
-      pf_pack_kernel<<<grid_for(nrec, 256), 256, 0, stream>>>(svals, nrec, d_n, d_mass, d_w, d_cmask, g_.d, rec_,
-                                                               rmask_);
+      pf_pack_kernel<<<grid_for(nrec, 256), 256, 0, stream>>>(svals, nrec, d_n, d_mass, d_w, d_cmask, g_.d, wts_);
       BFM_LAUNCH_CHECK("pf_pack_kernel");
     } else {
       const uint32_t* ckeys = nullptr;
@@ -1133,8 +1130,7 @@ void PushforwardPlan::gather(long nrec, const uint32_t* d_keys, const double* d_
       const int* d_n = sorter_.compact(d_keys, nrec, sentinel, stream, lc, &ckeys, &cvals);
       sorter_.sort(ckeys, cvals, nrec, key_bits_, stream, lc, &skeys, &svals, d_n);
       pf_bounds_kernel<<<grid_for(nrec, 256), 256, 0, stream>>>(skeys, nrec, d_n, sentinel, off_, end_);
-      pf_pack_kernel<<<grid_for(nrec, 256), 256, 0, stream>>>(svals, nrec, d_n, d_mass, d_w, d_cmask, g_.d, rec_,
-                                                               rmask_);
+      pf_pack_kernel<<<grid_for(nrec, 256), 256, 0, stream>>>(svals, nrec, d_n, d_mass, d_w, d_cmask, g_.d, wts_);
       BFM_LAUNCH_CHECK("pf_pack_kernel");
     }
   }
@@ -1151,8 +1147,7 @@ void PushforwardPlan::gather(long nrec, const uint32_t* d_keys, const double* d_
   G.src = d_mass;
   G.target = d_target;
   G.out = d_out;
-  G.rec = rec_;
-  G.rmask = rmask_;
+  G.wts = wts_;
   int* nheavy = reinterpret_cast<int*>(nheavy_);
   if (g_.d == 1) pf_gather_kernel<1><<<grid_for(N, 256), 256, 0, stream>>>(G, heavy_, large_, nheavy);
   else if (g_.d == 2) pf_gather_kernel<2><<<grid_for(N, 256), 256, 0, stream>>>(G, heavy_, large_, nheavy);

@@ -91,8 +91,7 @@ class PushforwardPlan {
   int* heavy_ = nullptr;     // [N] medium targets (bottom) and huge targets (top)
   unsigned long long* nheavy_ = nullptr;  // [0] heavy count, [1] buffer fill
   double* hbuf_ = nullptr;   // [2^d * N] merged heavy deposits
-  double4* rec_ = nullptr;   // [N] records in sorted order: mass, upper weights per axis
-  uint8_t* rmask_ = nullptr; // [N] clamp masks in sorted order
+  double* wts_ = nullptr;    // [2^d][N] deposit weights per corner, in sorted order (corner-major)
   RadixSorter sorter_;
   int key_bits_ = 0;
   int med_blocks_ = 1;       // medium-gather CTAs (each warp owns a kMedium slice of hbuf_)

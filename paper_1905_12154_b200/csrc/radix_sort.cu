@@ -273,7 +273,6 @@ struct OsArgs {
   unsigned* aux;
   uint32_t* kout;
   int* vout;
-  SortPack pack;
 };
 
 // One digit pass. Tiles take their ids from a counter in launch order, so a
@@ -281,8 +280,9 @@ struct OsArgs {
 // elements are ordered (warp, round, lane); equal digits keep that order:
 // rank = (the digit's count in the warp's earlier rounds) + (lower lanes of
 // the round, __match_any_sync) + (the digit's count in lower warps) + (the
-// tiles before, by look-back) + (the digit's global base).
-template <bool FIRST, bool PACK>
+// tiles before, by look-back) + (the digit's global base). (Packing the
+// pushforward's records here was measured 4x slower than a separate pass.)
+template <bool FIRST>
 __global__ void __launch_bounds__(kThreads, 4) os_scatter_kernel(OsArgs A) {
   __shared__ int s_tile, s_tot;
   __shared__ int gbase[kBins];
@@ -422,16 +422,6 @@ __global__ void __launch_bounds__(kThreads, 4) os_scatter_kernel(OsArgs A) {
     const long pos = static_cast<long>(gbase[d]) + wcnt[warp][d] + rk[r];
     A.kout[pos] = k;
     A.vout[pos] = v;
-    if (PACK) {
-      const SortPack& P = A.pack;
-      double4 rc;
-      rc.x = __ldg(P.src + v);
-      rc.y = P.d > 0 ? __ldg(P.w + v) : 0.0;
-      rc.z = P.d > 1 ? __ldg(P.w + P.nrec + v) : 0.0;
-      rc.w = P.d > 2 ? __ldg(P.w + 2 * P.nrec + v) : 0.0;
-      P.rec[pos] = rc;
-      P.rmask[pos] = __ldg(P.cmask + v);
-    }
   }
 }
 
@@ -504,8 +494,8 @@ void RadixSorter::sort(const uint32_t* keys_in, const int* vals_in, long n, int 
 
 
 const int* RadixSorter::sort_onesweep(const uint32_t* keys_in, long n, uint32_t sentinel, int bits,
-                                      const SortPack* pack, cudaStream_t s, LaunchCounter* lc,
-                                      const uint32_t** keys_out, const int** vals_out) {
+                                      cudaStream_t s, LaunchCounter* lc, const uint32_t** keys_out,
+                                      const int** vals_out) {
   const int npass = (bits + kBits - 1) / kBits;
   if (npass < 1 || npass > kMaxPass) throw std::invalid_argument("radix sort: 1..36 key bits supported");
   const long nb = (n + kTile - 1) / kTile;
@@ -528,12 +518,8 @@ const int* RadixSorter::sort_onesweep(const uint32_t* keys_in, long n, uint32_t 
     A.aux = aux_;
     A.kout = kbuf_[cur];
     A.vout = vbuf_[cur];
-    const bool last = p == npass - 1;
-    if (pack && last) A.pack = *pack;
-    if (p == 0 && last && pack) os_scatter_kernel<true, true><<<static_cast<unsigned>(nb), kThreads, 0, s>>>(A);
-    else if (p == 0) os_scatter_kernel<true, false><<<static_cast<unsigned>(nb), kThreads, 0, s>>>(A);
-    else if (last && pack) os_scatter_kernel<false, true><<<static_cast<unsigned>(nb), kThreads, 0, s>>>(A);
-    else os_scatter_kernel<false, false><<<static_cast<unsigned>(nb), kThreads, 0, s>>>(A);
+    if (p == 0) os_scatter_kernel<true><<<static_cast<unsigned>(nb), kThreads, 0, s>>>(A);
+    else os_scatter_kernel<false><<<static_cast<unsigned>(nb), kThreads, 0, s>>>(A);
     BFM_LAUNCH_CHECK("one-sweep scatter");
     kin = kbuf_[cur];
     vin = vbuf_[cur];

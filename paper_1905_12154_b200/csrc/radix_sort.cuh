@@ -11,18 +11,6 @@
 
 namespace bfmgpu {
 
-// Optional fused gather of the pushforward's deposit records into sorted
-// order by the last pass of sort_onesweep (what pf_pack_kernel does).
-struct SortPack {
-  const double* src = nullptr;   // record mass
-  const double* w = nullptr;     // upper weights, axis-major (stride nrec)
-  const uint8_t* cmask = nullptr;
-  long nrec = 0;
-  int d = 0;
-  double4* rec = nullptr;
-  uint8_t* rmask = nullptr;
-};
-
 class RadixSorter {
  public:
   RadixSorter() = default;
@@ -42,11 +30,10 @@ class RadixSorter {
   // One-sweep form of compact + sort (+ pack): one histogram kernel over the
   // raw keys (all digit positions at once, sentinel keys skipped), then one
   // scatter kernel per digit whose tiles chain their digit offsets by
-  // decoupled look-back; the first pass drops the sentinel keys, the last
-  // can write the packed records. Returns the device pointer of the number
-  // of sorted pairs.
-  const int* sort_onesweep(const uint32_t* keys_in, long n, uint32_t sentinel, int bits, const SortPack* pack,
-                           cudaStream_t s, LaunchCounter* lc, const uint32_t** keys_out, const int** vals_out);
+  // decoupled look-back; the first pass drops the sentinel keys. Returns the
+  // device pointer of the number of sorted pairs.
+  const int* sort_onesweep(const uint32_t* keys_in, long n, uint32_t sentinel, int bits, cudaStream_t s,
+                           LaunchCounter* lc, const uint32_t** keys_out, const int** vals_out);
 
  private:
   long cap_ = 0;
