@@ -178,19 +178,6 @@ __global__ void pf_map_kernel(MapArgs A) {
   }
 }
 
-// Bucket boundaries of the sorted (cell, source) pairs: off[c] = first, end[c] = one past last.
-__global__ void pf_bounds_kernel(const uint32_t* keys, long n_max, const int* d_n, uint32_t sentinel, int* off,
-                                 int* end) {
-  const long n = d_n ? *d_n : n_max;
-  for (long i = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; i < n;
-       i += static_cast<long>(gridDim.x) * blockDim.x) {
-    const uint32_t k = keys[i];
-    if (k == sentinel) continue;
-    if (i == 0 || keys[i - 1] != k) off[k] = static_cast<int>(i);
-    if (i == n - 1 || keys[i + 1] != k) end[k] = static_cast<int>(i + 1);
-  }
-}
-
 struct GatherArgs {
   GridDesc g;        // target nodes (whole grid or a row slab)
   int row_off;       // global row of local target row 0
@@ -219,8 +206,9 @@ __device__ __forceinline__ double pos_weight(const GatherArgs& A, int pos, int b
   return A.wts[static_cast<long>(b) * A.nrec + pos];
 }
 
-// records -> sorted order (one pass after the sort)
-__global__ void pf_pack_kernel(const int* bucket, long nrec, const int* d_n, const double* src, const double* w,
+// bucket bounds and per-corner weights in sorted order (one pass after the sort)
+__global__ void pf_pack_kernel(const uint32_t* keys, uint32_t sentinel, int* off, int* end, const int* bucket,
+                               long nrec, const int* d_n, const double* src, const double* w,
                                const uint8_t* cmask, int d, double* wts) {
   // the weight of every deposit for each of its 2^d corners (the reference's
   // expression, pushforward.hpp:161-166: m times each axis's upper or lower
@@ -229,6 +217,13 @@ __global__ void pf_pack_kernel(const int* bucket, long nrec, const int* d_n, con
   const long n = d_n ? *d_n : nrec;
   for (long i = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<long>(gridDim.x) * blockDim.x) {
+    // bucket boundaries of the sorted (cell, source) pairs: off[c] = first,
+    // end[c] = one past the last
+    const uint32_t k = keys[i];
+    if (k != sentinel) {
+      if (i == 0 || keys[i - 1] != k) off[k] = static_cast<int>(i);
+      if (i == n - 1 || keys[i + 1] != k) end[k] = static_cast<int>(i + 1);
+    }
     const int s = bucket[i];
     const double m = src[s];
     double wa[3] = {0.0, 0.0, 0.0};
@@ -959,8 +954,8 @@ __global__ void route_unpack_kernel(const double* packed, long nrec, int d, uint
 
 PushforwardPlan::~PushforwardPlan() {
   for (void* p : {static_cast<void*>(key_), static_cast<void*>(cmask_), static_cast<void*>(w_),
-                  static_cast<void*>(off_), static_cast<void*>(end_), static_cast<void*>(heavy_),
-                  static_cast<void*>(nheavy_), static_cast<void*>(hbuf_),
+                  static_cast<void*>(heavy_), static_cast<void*>(nheavy_) /* with off_, end_ */,
+                  static_cast<void*>(hbuf_),
                   static_cast<void*>(row0_), static_cast<void*>(bcount_),
                   static_cast<void*>(large_), static_cast<void*>(wts_),
                   static_cast<void*>(lmeta_)})
@@ -990,8 +985,15 @@ void PushforwardPlan::setup(const GridDesc& loc, const GridDesc& global, int row
   BFM_CUDA(dmalloc(&key_, N * sizeof(uint32_t)));
   BFM_CUDA(dmalloc(&cmask_, N));
   BFM_CUDA(dmalloc(&w_, g_.d * N * sizeof(double)));
-  BFM_CUDA(dmalloc(&off_, (ncells_ + 1) * sizeof(int)));
-  BFM_CUDA(dmalloc(&end_, (ncells_ + 1) * sizeof(int)));
+  // the per-call counters and the bucket bounds share one allocation so one
+  // memset clears them: [64 bytes of counters][off][end]
+  {
+    unsigned char* pool = nullptr;
+    BFM_CUDA(dmalloc(&pool, 64 + 2 * (ncells_ + 1) * sizeof(int)));
+    nheavy_ = reinterpret_cast<unsigned long long*>(pool);
+    off_ = reinterpret_cast<int*>(pool + 64);
+    end_ = off_ + ncells_ + 1;
+  }
   BFM_CUDA(dmalloc(&heavy_, (N + 1) * sizeof(int)));
   BFM_CUDA(dmalloc(&large_, (N + 1) * sizeof(int)));
   // large-tier fold list: fewer than 2^d N / (kMedium + 1) targets
@@ -1000,7 +1002,6 @@ void PushforwardPlan::setup(const GridDesc& loc, const GridDesc& global, int row
   // per-call counters, zeroed by gather(); as ints: [0] warp-tier targets,
   // [1] heavy targets, [2..3] heavy buffer fill (one u64), [4] CTA-tier
   // targets, [5] / [6] heavy / CTA-tier work claims, [7] unused
-  BFM_CUDA(dmalloc(&nheavy_, 6 * sizeof(unsigned long long)));
   ensure_records(N);
   BFM_CUDA(cudaFuncSetAttribute(pf_gather_large_kernel<kLarge>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 kLargeSmem));
@@ -1098,9 +1099,7 @@ void PushforwardPlan::gather(long nrec, const uint32_t* d_keys, const double* d_
                              double* d_out, cudaStream_t stream, LaunchCounter* lc) {
   ensure_records(nrec);
   const long N = g_.size;
-  BFM_CUDA(cudaMemsetAsync(off_, 0, (ncells_ + 1) * sizeof(int), stream));
-  BFM_CUDA(cudaMemsetAsync(end_, 0, (ncells_ + 1) * sizeof(int), stream));
-  BFM_CUDA(cudaMemsetAsync(nheavy_, 0, 6 * sizeof(unsigned long long), stream));
+  BFM_CUDA(cudaMemsetAsync(nheavy_, 0, 64 + 2 * (ncells_ + 1) * sizeof(int), stream));  // counters, off, end
   const int* svals = nullptr;
   if (nrec > 0) {
     const uint32_t* skeys = nullptr;
@@ -1121,16 +1120,16 @@ void PushforwardPlan::gather(long nrec, const uint32_t* d_keys, const double* d_
       // ids of neighbouring positions are close, so the gathers coalesce;
       // fused into the last scatter they cost 4x the separate kernel)
       const int* d_n = sorter_.sort_onesweep(d_keys, nrec, sentinel, key_bits_, stream, lc, &skeys, &svals);
-      pf_bounds_kernel<<<grid_for(nrec, 256), 256, 0, stream>>>(skeys, nrec, d_n, sentinel, off_, end_);
-      pf_pack_kernel<<<grid_for(nrec, 256), 256, 0, stream>>>(svals, nrec, d_n, d_mass, d_w, d_cmask, g_.d, wts_);
+      pf_pack_kernel<<<grid_for(nrec, 256), 256, 0, stream>>>(skeys, sentinel, off_, end_, svals, nrec, d_n, d_mass,
+                                                               d_w, d_cmask, g_.d, wts_);
       BFM_LAUNCH_CHECK("pf_pack_kernel");
     } else {
       const uint32_t* ckeys = nullptr;
       const int* cvals = nullptr;
       const int* d_n = sorter_.compact(d_keys, nrec, sentinel, stream, lc, &ckeys, &cvals);
       sorter_.sort(ckeys, cvals, nrec, key_bits_, stream, lc, &skeys, &svals, d_n);
-      pf_bounds_kernel<<<grid_for(nrec, 256), 256, 0, stream>>>(skeys, nrec, d_n, sentinel, off_, end_);
-      pf_pack_kernel<<<grid_for(nrec, 256), 256, 0, stream>>>(svals, nrec, d_n, d_mass, d_w, d_cmask, g_.d, wts_);
+      pf_pack_kernel<<<grid_for(nrec, 256), 256, 0, stream>>>(skeys, sentinel, off_, end_, svals, nrec, d_n, d_mass,
+                                                               d_w, d_cmask, g_.d, wts_);
       BFM_LAUNCH_CHECK("pf_pack_kernel");
     }
   }
@@ -1171,7 +1170,7 @@ void PushforwardPlan::gather(long nrec, const uint32_t* d_keys, const double* d_
   BFM_LAUNCH_CHECK("pf_fold_large_kernel");
   pf_gather_heavy_kernel<<<2 * 148, 512, kHeavySmem, stream>>>(G, heavy_, nheavy, hbuf_, nheavy_ + 1);
   BFM_LAUNCH_CHECK("pf_gather_heavy_kernel");
-  if (lc) lc->add(nrec > 0 ? 8 : 6);
+  if (lc) lc->add(nrec > 0 ? 7 : 6);
 }
 
 void PushforwardPlan::set_partition(int P, const int* row_starts) {
