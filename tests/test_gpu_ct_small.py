@@ -1,4 +1,4 @@
-"""Small dyadic grids through the exact-hull c-transform: every thread /
+"""Small and oddly shaped dyadic grids through the exact-hull c-transform: every thread /
 chunk layout the plan can pick for short lines (one to eight points per
 thread, lines shorter than a warp, one-point axes' neighbours) against the
 CPU restatement, on a generic potential and on its c-transform (exactly
@@ -13,7 +13,9 @@ from paper_1905_12154_b200 import synthetic
 pytestmark = pytest.mark.gpu
 
 SHAPES = [(2, 2), (4, 4), (8, 8), (16, 16), (32, 32), (64, 64), (128, 128), (256, 256), (8, 256), (256, 8),
-          (2, 256), (128, 2), (256,), (64,), (4, 4, 4), (8, 8, 8), (16, 16, 4)]
+          (2, 256), (128, 2), (256,), (64,), (4, 4, 4), (8, 8, 8), (16, 16, 4),
+          # long lines: the small-state form (lines of 4096 points and more) in 1-D, thin 2-D and 3-D grids
+          (4096,), (8192,), (8, 4096), (4096, 8), (2, 8192), (512, 4096), (4096, 512), (16, 16, 4096)]
 
 
 @pytest.fixture(scope="module", autouse=True)
