@@ -1992,22 +1992,7 @@ void CtPlan::setup(const GridDesc& loc, const GridDesc& global, int pb, int pe, 
   BFM_CUDA(cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
   const int budget = max_optin - 1024;
 
-  for (int a = pb; a < pe; ++a) {
-    CtPass& P = pass_[a];
-    std::memset(&P, 0, sizeof(P));
-    P.d = loc.d;
-    P.a = a;
-    P.last = a == global.d - 1;
-    P.k0_off = k0_off;
-    P.pregathered = pregathered ? 1 : 0;
-    for (int b = 0; b < loc.d; ++b) P.ax[b] = ax_[b];
-    const int n = loc.n[a];
-    P.nlines = loc.size / n;
-    P.strided = a != loc.d - 1;
-    P.fixed = 1;
-    for (int b = 0; b < loc.d; ++b)
-      if (!P.ax[b].dyadic && !P.ax[b].GF) P.fixed = 0;
-    const bool dy = dyadic_;
+  // shared-memory layout, threads and lines per CTA of a dyadic pass (qg: the small-state form)
     auto dy_layout = [&](CtPass& P, int a, int n, bool qg) {
       // exact-hull kernel: (s, q) per point in shared memory; about 11 points
       // per thread, up to kDyThreads threads per line
@@ -2079,13 +2064,46 @@ void CtPlan::setup(const GridDesc& loc, const GridDesc& global, int pb, int pe, 
       P.slow_queries = slow_;
       P.stats = stats_;
     };
+  for (int a = pb; a < pe; ++a) {
+    CtPass& P = pass_[a];
+    std::memset(&P, 0, sizeof(P));
+    P.d = loc.d;
+    P.a = a;
+    P.last = a == global.d - 1;
+    P.k0_off = k0_off;
+    P.pregathered = pregathered ? 1 : 0;
+    for (int b = 0; b < loc.d; ++b) P.ax[b] = ax_[b];
+    const int n = loc.n[a];
+    P.nlines = loc.size / n;
+    P.strided = a != loc.d - 1;
+    P.fixed = 1;
+    for (int b = 0; b < loc.d; ++b)
+      if (!P.ax[b].dyadic && !P.ax[b].GF) P.fixed = 0;
+    const bool dy = dyadic_;
     if (dy) {
-      dy_layout(P, a, n, false);
       // the small-state form of the last (contiguous) pass, for lines of 4096 points and more
-      if (a == loc.d - 1 && n >= 4096 && !virtual_cols) {
+      const bool want_q = a == loc.d - 1 && n >= 4096 && !virtual_cols;
+      bool staged_ok = true;
+      try {
+        dy_layout(P, a, n, false);
+      } catch (const std::invalid_argument&) {
+        // the staged line state (24 bytes per point) does not fit: the last
+        // pass can still run in the small-state form alone (12 bytes per
+        // point: lines of up to ~17 k points), and so can pass 0 of a 2-D
+        // grid on the transposed potential (checked below)
+        const bool t0_can = a == 0 && loc.d == 2 && pb == 0 && pe == 2 && !virtual_cols && !pregathered && k0_off == 0;
+        if (!want_q && !t0_can) throw;
+        staged_ok = false;
+        if (t0_can && !want_q) pass0_needs_t0_ = true;
+      }
+      if (want_q) {
         passq_ = P;
         dy_layout(passq_, a, n, true);
         have_q_ = true;
+        if (!staged_ok) {
+          P = passq_;
+          q_only_ = true;
+        }
       }
       continue;
     }
@@ -2131,6 +2149,7 @@ void CtPlan::setup(const GridDesc& loc, const GridDesc& global, int pb, int pe, 
         loc.size >= (1L << 22);
   if (const char* e = getenv("BFM_CT_T0"))
     t0_ = atoi(e) != 0 && dyadic_ && loc.d == 2 && pb == 0 && pe == 2 && !virtual_cols && !pregathered;
+  if (pass0_needs_t0_) t0_ = true;
   if (t0_) {
     BFM_CUDA(dmalloc(&phit_, loc.size * sizeof(double)));
     BFM_CUDA(dmalloc(&statet_, loc.size * sizeof(uint32_t)));
@@ -2141,33 +2160,23 @@ void CtPlan::setup(const GridDesc& loc, const GridDesc& global, int pb, int pe, 
     T.strided = 0;
     T.ax[0].stride = 1;
     T.ax[1].stride = loc.n[0];
-    // lines per CTA as for a contiguous pass
-    int lpc = std::min<long>(budget / (2 * T.line_bytes), kDyThreads / (2 * T.tpl));
-    if (const char* e = getenv("BFM_DY_LPC_C"))
-      lpc = std::max(1, std::min<int>(std::min<long>(atoi(e), budget / T.line_bytes), kDyThreads / T.tpl));
-    lpc = std::min(lpc, 8);
-    lpc = static_cast<int>(std::min<long>(lpc, T.nlines));
-    T.lpc = std::max(lpc, 1);
-    // (the transposed pass 0 is contiguous: on a square grid it can take the
-    // last pass's small-state layout)
-    have_qt_ = have_q_ && loc.n[0] == loc.n[1];
+    if (!pass0_needs_t0_) {
+      // lines per CTA as for a contiguous pass
+      int lpc = std::min<long>(budget / (2 * T.line_bytes), kDyThreads / (2 * T.tpl));
+      if (const char* e = getenv("BFM_DY_LPC_C"))
+        lpc = std::max(1, std::min<int>(std::min<long>(atoi(e), budget / T.line_bytes), kDyThreads / T.tpl));
+      lpc = std::min(lpc, 8);
+      lpc = static_cast<int>(std::min<long>(lpc, T.nlines));
+      T.lpc = std::max(lpc, 1);
+    }
+    // the transposed pass 0 is contiguous: with lines of 4096 points and more
+    // it has a small-state twin (its only form when the staged state does not fit)
+    have_qt_ = loc.n[0] >= 4096;
     if (have_qt_) {
-      const CtPass& L = passq_;
-      CtPass& Q = pass0tq_;
-      Q = T;
-      Q.qglobal = 1;
-      Q.tpl = L.tpl;
-      Q.C = L.C;
-      Q.lpc = 1;
-      Q.off_fv = L.off_fv;
-      Q.off_chain = L.off_chain;
-      Q.off_flag = L.off_flag;
-      Q.off_hidx = L.off_hidx;
-      Q.off_H = L.off_H;
-      Q.off_list = L.off_list;
-      Q.off_lohi = L.off_lohi;
-      Q.off_scal = L.off_scal;
-      Q.line_bytes = L.line_bytes;
+      pass0tq_ = T;
+      dy_layout(pass0tq_, 0, loc.n[0], true);
+    } else if (pass0_needs_t0_) {
+      throw std::invalid_argument("ctransform: grid line too long for shared memory");
     }
   }
   qg_mode_ = 2;  // 0: never, 1: whenever available, 2: by the caller's hint (default)
@@ -2228,7 +2237,7 @@ void CtPlan::run(const double* d_phi, double* d_out, cudaStream_t stream, Launch
       const int n0 = g_.n[0], n1 = g_.n[1];
       const dim3 gin((n1 + 31) / 32, (n0 + 31) / 32), gout((n0 + 31) / 32, (n1 + 31) / 32);
       ct_transpose_f64<<<gin, 256, 0, stream>>>(d_phi, phit_, n0, n1);
-      CtPass P = (qg_first && have_qt_) ? pass0tq_ : pass0t_;
+      CtPass P = ((qg_first || pass0_needs_t0_) && have_qt_) ? pass0tq_ : pass0t_;
       P.phi = phit_;
       P.pregathered = 0;
       P.state_in = nullptr;
@@ -2241,7 +2250,7 @@ void CtPlan::run(const double* d_phi, double* d_out, cudaStream_t stream, Launch
       if (lc) lc->add(2);
       continue;
     }
-    CtPass P = (qg_last && have_q_ && a == g_.d - 1) ? passq_ : pass_[a];
+    CtPass P = ((qg_last || q_only_) && have_q_ && a == g_.d - 1) ? passq_ : pass_[a];
     if (P.last && before_last) BFM_CUDA(cudaStreamWaitEvent(stream, before_last, 0));
     P.phi = a == 0 ? d_phi : qbuf_[(a - 1) & 1];
     P.pregathered = a > 0 ? 1 : 0;

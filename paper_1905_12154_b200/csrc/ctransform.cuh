@@ -108,6 +108,8 @@ class CtPlan {
   CtPass passq_ = {};
   CtPass pass0tq_ = {};
   bool have_q_ = false, have_qt_ = false;
+  bool pass0_needs_t0_ = false;  // pass 0's lines are too long for the staged form: transposed small-state pass only
+  bool q_only_ = false;  // the last pass's line is too long for the staged form (pass_[d-1] is the small-state one)
   int qg_mode_ = 2;
   int qg_mix_ = 0;  // hinted calls: passes that still take the small-state form (bit 0: pass 0, bit 1: last)
   double* phit_ = nullptr;
